@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark: GCUPS of batched 150 bp semi-global affine alignment (C2).
+
+Workload (BASELINE.json configs[1], "C2"): 1,000,000 synthetic Illumina-like read pairs,
+150 x 150 bp, semi-global, affine gap open 5 / extend 1 (magnitudes), match +2 /
+mismatch -1, score-only, one B200 per rank.  One step = the whole hot path on one batch:
+pack + validate (a1), plan (a2), fill with fused optimum (a3, a7) -- all on device through
+the C-ABI (anyseq_align_batch_device), inputs resident in HBM (300 MB > 126 MB L2, so no
+L2 flush is needed between steps).
+
+  value  : total cells of all ranks / max-over-ranks device time, in GCUPS.
+  e2e    : the same metric through the host API anyseq_align_batch with pinned host buffers
+           (H2D of the ASCII batch and D2H of the scores inside the timed region).
+  roofline: the fill kernel's cells/s (CUDA events around each launch, on its stream)
+           against the integer-pipe roofline derived in DESIGN.md ("bound": "alu").
+  cpu_baseline: the plain CPU oracle (oracle/) on a bounded sample of the same workload.
+
+--impl reference runs the reference arm for this tier: the oracle itself on the host cores,
+each step a bounded sample of the same workload.
+Multi-GPU (torchrun): every rank aligns its own 1M pairs (seed per rank): weak scaling,
+no data-path collective (batches shard by pair); timing is max over ranks.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SCHEME = dict(kind="semi", gap="affine", match=2, mismatch=-1, gap_open=5, gap_extend=1)
+NUM_PAIRS = 1_000_000
+READ_LEN = 150
+METRIC = "GCUPS (batched 150bp semi-global affine, long-pair SW) at 1/2/4/8 B200"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for k, nm in enumerate(names):
+                if len(s) > 3 + k and s[3 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def cpu_oracle_baseline(qm, sm, budget_s: float = 12.0, threads=None):
+    """Time the plain CPU oracle on a bounded sample (first k pairs) of the same workload."""
+    import numpy as np
+    from oracle import oracle as O
+    from synth import uniform_csr
+    th = threads or os.cpu_count() or 1
+    sch = O.Scheme(SCHEME["kind"], SCHEME["gap"], SCHEME["match"], SCHEME["mismatch"],
+                   SCHEME["gap_open"], SCHEME["gap_extend"])
+    k = min(len(qm), 400 * th)
+    q, qo = uniform_csr(qm[:k])
+    s, so = uniform_csr(sm[:k])
+    t0 = time.perf_counter()
+    O.batch(sch, q, qo, s, so, traceback=False, threads=th)
+    dt = time.perf_counter() - t0
+    # scale the sample to the time budget
+    k2 = int(min(len(qm), max(k, k * budget_s / max(dt, 1e-3))))
+    q, qo = uniform_csr(qm[:k2])
+    s, so = uniform_csr(sm[:k2])
+    t0 = time.perf_counter()
+    O.batch(sch, q, qo, s, so, traceback=False, threads=th)
+    dt = time.perf_counter() - t0
+    cells = k2 * READ_LEN * READ_LEN
+    return {"value": round(cells / dt / 1e9, 4), "unit": "GCUPS", "cores": th, "kind": "oracle",
+            "sample": f"first {k2} of the {len(qm)} C2 pairs (150x150, semi-global affine 5/1), "
+                      f"{dt:.1f} s on {th} threads"}
+
+
+def measured_alu_peak(ctx_unused=None):
+    """Integer-pipe roofline inputs: SM count and max SM clock from the device, the lane-op
+    rate per SM from the DPX microbenchmark (paper_2002_04561_b200/csrc/dpx_bench) when
+    available, else the 64 lane-ops/clk/SM of DESIGN.md."""
+    import torch
+    props = torch.cuda.get_device_properties(0)
+    rate = None
+    path = os.path.join(ROOT, "profiles", "dpx_rates.json")
+    if os.path.exists(path):
+        try:
+            rate = json.load(open(path)).get("mix_lane_ops_per_clk_per_sm")
+        except Exception:
+            rate = None
+    return props.multi_processor_count, rate or 64.0, "measured" if rate else "design"
+
+
+def run_reference(args):
+    """Reference arm of this tier: the CPU oracle, timed on the host cores."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from synth import c2_reads
+    qm, sm = c2_reads(20000, seed=2)
+    th = os.cpu_count() or 1
+    per = []
+    base = None
+    for it in range(args.warmup + args.steps):
+        b = cpu_oracle_baseline(qm, sm, budget_s=args.ref_budget, threads=th)
+        if it >= args.warmup:
+            per.append(b)
+        base = b
+    v = sorted(x["value"] for x in per)[len(per) // 2] if per else base["value"]
+    line = {"metric": METRIC, "value": v, "unit": "GCUPS", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "C2: 150x150 bp read pairs, semi-global affine 5/1, score-only",
+                       "sample_per_step": base["sample"]},
+            "cpu_baseline": {"value": v, "unit": "GCUPS", "cores": th, "kind": "oracle",
+                             "sample": base["sample"]},
+            "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pairs", type=int, default=NUM_PAIRS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2002_04561_b200 as A
+    from synth import c2_reads, uniform_csr
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    qm, sm = c2_reads(args.pairs, seed=2 + 1000 * rank)
+    q, qo = uniform_csr(qm)
+    s, so = uniform_csr(sm)
+    B = len(qo) - 1
+    cells = B * READ_LEN * READ_LEN
+    dev = torch.device("cuda", local)
+    d_q = torch.from_numpy(q).to(dev)
+    d_s = torch.from_numpy(s).to(dev)
+    d_qo = torch.from_numpy(qo.view(np.int64)).to(dev)
+    d_so = torch.from_numpy(so.view(np.int64)).to(dev)
+    d_sc = torch.empty(B, dtype=torch.int32, device=dev)
+    sch = A.Scheme(**SCHEME)
+    ctx = A.Context([local])
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ctx.align_batch_device(sch, d_q, d_qo, d_s, d_so, d_sc, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ctx.set_option("timing", 1)
+    ctx.reset_stats()
+    launches0 = ctx.launches
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - launches0
+    fill_ms = ctx.stat("fill_ms")
+    fill_launches = int(ctx.stat("fill_launches"))
+    ctx.set_option("timing", 0)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = cells * ws * args.steps / (ms_max / 1e3) / 1e9
+
+    # parity spot check of this run's output (oracle on a few pairs) -- not timed
+    from oracle import oracle as O
+    got = d_sc.cpu().numpy()
+    osch = O.Scheme(SCHEME["kind"], SCHEME["gap"], SCHEME["match"], SCHEME["mismatch"],
+                    SCHEME["gap_open"], SCHEME["gap_extend"])
+    idx = np.random.default_rng(rank).choice(B, 64, replace=False)
+    parity = all(int(got[k]) == O.align(osch, qm[k].tobytes(), sm[k].tobytes(), False).score
+                 for k in idx)
+
+    # e2e through the host API from pinned buffers
+    pq = torch.from_numpy(q).pin_memory().numpy()
+    ps = torch.from_numpy(s).pin_memory().numpy()
+    pqo = torch.from_numpy(qo.view(np.int64)).pin_memory().numpy().view(np.uint64)
+    pso = torch.from_numpy(so.view(np.int64)).pin_memory().numpy().view(np.uint64)
+    e2e_steps = max(2, min(args.steps, 5))
+    ctx.align_batch(sch, pq, pqo, ps, pso)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.align_batch(sch, pq, pqo, ps, pso)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = cells * ws * e2e_steps / float(te.item()) / 1e9
+
+    # roofline of the dominant kernel (fill): cells per launch / mean launch time
+    n_sm, lane_rate, rate_src = measured_alu_peak()
+    ops_per_cell = 3.0  # s16x2 semi-global affine: 6 instr per register of 2 cells
+    f_mhz = clocks.get("sm_mhz") or 1965.0
+    peak = n_sm * f_mhz * 1e6 * lane_rate / ops_per_cell / 1e9
+    fill_gcups = cells * args.steps / (fill_ms / 1e3) / 1e9 if fill_ms > 0 else None
+    roof = {"bound": "alu", "achieved": round(fill_gcups, 1) if fill_gcups else None,
+            "peak": round(peak, 1), "unit": "GCUPS",
+            "frac": round(fill_gcups / peak, 4) if fill_gcups else None,
+            "traffic": None,
+            "kernel": "fill_kernel<VS16,SEMI,AFFINE,L=8,R=19>",
+            "kernel_share_of_step": round(fill_ms / ms, 4) if ms > 0 else None,
+            "peak_basis": f"{n_sm} SM x {f_mhz:.0f} MHz (median under load) x {lane_rate} "
+                          f"lane-ops/clk/SM ({rate_src}) / {ops_per_cell} ops per cell"}
+
+    line = {"metric": METRIC, "value": round(value, 1), "unit": "GCUPS", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "s16x2",
+            "data": "synthetic",
+            "config": {"workload": "C2: 1M Illumina-like 150x150 bp pairs per GPU, semi-global, "
+                                   "affine open 5 / extend 1, match 2 / mismatch -1, score-only",
+                       "pairs_per_gpu": B, "cells_per_gpu": cells,
+                       "l2": "inputs 300 MB > 126 MB L2 (no flush needed)",
+                       "parallelism": f"dp{ws} (pairs sharded, no collective)"},
+            "e2e": {"value": round(e2e_value, 1), "unit": "GCUPS",
+                    "h2d_bytes_per_step": int(q.nbytes + s.nbytes + qo.nbytes + so.nbytes),
+                    "d2h_bytes_per_step": int(B * 4)},
+            "gpu_launches": int(launches),
+            "fill_launches": fill_launches,
+            "roofline": roof,
+            "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+            "parity_sample_ok": bool(parity)}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_oracle_baseline(qm, sm)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,156 @@
+/*
+ * include/anyseq.h -- C-ABI of the B200-native pairwise alignment library.
+ *
+ * The library relaxes the dynamic-programming matrix of AnySeq (arXiv 2002.04561):
+ *   H(i,j) = max{ H(i-1,j-1) + sigma(q_i,s_j), E(i,j), F(i,j), nu }        Eq. (1)
+ *   linear gaps  E = H(i-1,j) - g,  F = H(i,j-1) - g                       Eqs. (2)-(3)
+ *   affine gaps  E = max{E(i-1,j) - Ge, H(i-1,j) - Go - Ge}, F alike      Eqs. (4)-(5)
+ *   local (nu = 0), global (nu = -inf), semi-global (local init, optimum in last row/col)
+ *                                                                           P:257-264
+ * The entry points follow the paper's C wrapper (construct_global_alignment)
+ * and its control flow (allocate / read input, build accessors, relax, look up optimum,
+ * build alignment, output -- P:424-436).  Parameters select the algorithmic variant at
+ * run time (the paper selects it by partial evaluation).
+ *
+ * Conventions:
+ *  - gap_open / gap_extend are NON-NEGATIVE MAGNITUDES that are subtracted;
+ *    a gap of length k costs gap_open + k*gap_extend.  "open -5 / extend -1"
+ *    means gap_open = 5, gap_extend = 1.  For LINEAR, gap_extend is g and gap_open is
+ *    ignored.
+ *  - rows are the query q (i = 1..n), columns the subject s (j = 1..m).
+ *  - CIGAR ops are BAM-style words (len << 4 | op) with op 0 = M (q_i vs s_j, match or
+ *    mismatch), 1 = I (q_i vs gap, vertical / E), 2 = D (s_j vs gap, horizontal / F).
+ *  - ties: H source DIAG > E > F; gap extension beats opening; local traceback stops at
+ *    the first cell with H <= 0; end cell = maximum with smallest j, then smallest i
+ *    (semi-global candidates: row n for j < m, then column m).
+ *  - alphabet: A C G T N (case-insensitive).  N mismatches everything, N included.
+ *
+ * Ownership: the caller owns every input and output buffer; the library keeps no pointer
+ * after a call returns.  The context owns device memory, streams and peer mappings.
+ * Host-pointer calls are synchronous.  One call at a time per context.
+ * Errors: every function returns anyseq_status; no exceptions, aborts or exits cross the
+ * ABI.  Validation happens before any result is written; on error, outputs are
+ * unspecified and anyseq_last_error() names the failing pair / byte / CUDA call.
+ * There is NO CPU fallback: without a CUDA device anyseq_create returns ANYSEQ_E_CUDA.
+ */
+#ifndef ANYSEQ_H
+#define ANYSEQ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct anyseq_ctx anyseq_ctx; /* opaque: devices, streams, scratch, peers */
+
+typedef enum {
+  ANYSEQ_OK = 0,
+  ANYSEQ_E_INVALID = 1,     /* bad enum, penalty, pointer, size */
+  ANYSEQ_E_BADSEQ = 2,      /* byte outside ACGTNacgtn */
+  ANYSEQ_E_NOMEM = 3,       /* device or host allocation failed */
+  ANYSEQ_E_CAPACITY = 4,    /* cigar buffer too small (*cigar_used = words required) */
+  ANYSEQ_E_CUDA = 5,        /* CUDA runtime error (message names the call) */
+  ANYSEQ_E_UNSUPPORTED = 6, /* score range exceeds 32-bit arithmetic, etc. */
+  ANYSEQ_E_PEER = 7,        /* peer access between devices unavailable */
+  ANYSEQ_E_TIMEOUT = 8      /* a device-side wait exceeded its bound */
+} anyseq_status;
+
+typedef enum { ANYSEQ_GLOBAL = 0, ANYSEQ_LOCAL = 1, ANYSEQ_SEMIGLOBAL = 2 } anyseq_kind;
+typedef enum { ANYSEQ_GAP_LINEAR = 0, ANYSEQ_GAP_AFFINE = 1 } anyseq_gap;
+
+/* Alignment scheme. */
+typedef struct {
+  int32_t kind;       /* anyseq_kind */
+  int32_t gap;        /* anyseq_gap */
+  int32_t match;      /* sigma(a,a), a in ACGT; [-128, 127] */
+  int32_t mismatch;   /* sigma(a,b), a != b, and every pair involving N; [-128, 127] */
+  int32_t gap_open;   /* G_o >= 0 (ignored for LINEAR); <= 32767 */
+  int32_t gap_extend; /* G_e >= 0 (LINEAR: g); <= 32767 */
+} anyseq_params;
+
+/* CSR batch: pair k is q[q_off[k] .. q_off[k+1]) vs s[s_off[k] .. s_off[k+1]).
+   Offsets have num_pairs + 1 entries, non-decreasing; each length < 2^31. */
+typedef struct {
+  const char* q;
+  const uint64_t* q_off;
+  const char* s;
+  const uint64_t* s_off;
+  uint64_t num_pairs;
+} anyseq_batch;
+
+/* One alignment.  Aligned q = [q_begin, q_end), aligned s = [s_begin, s_end), 0-based
+   (equivalently the begin and end DP cells (q_begin, s_begin) -> (q_end, s_end)). */
+typedef struct {
+  int32_t score;
+  int32_t reserved;
+  int64_t q_begin, s_begin;
+  int64_t q_end, s_end;
+  uint64_t cigar_offset; /* index of the first op word in the caller's cigar[] */
+  uint32_t cigar_len;    /* number of op words */
+  uint32_t reserved2;
+} anyseq_alignment;
+
+/* Create a context on the given CUDA devices (device_ids may be NULL => device 0).
+   num_devices >= 1.  A context with G > 1 devices shards batches by cumulative cells
+   and long pairs as column strips. */
+anyseq_status anyseq_create(anyseq_ctx** out, const int* device_ids, int num_devices);
+void anyseq_destroy(anyseq_ctx* ctx);
+
+/* Score-only batch alignment (step 7-8 of P:424-436 + output).  All pointers are HOST
+   memory (pinned memory gives the fastest upload).  scores[num_pairs] receives the
+   optimum; if ends != NULL, ends[k] also receives score and END cell (q_end, s_end);
+   its begin/cigar fields are set to the end cell / 0. */
+anyseq_status anyseq_align_batch(anyseq_ctx* ctx, const anyseq_params* params,
+                                 const anyseq_batch* batch, int32_t* scores,
+                                 anyseq_alignment* ends);
+
+/* Same computation on DEVICE memory of the context's first device, enqueued on the
+   caller's CUDA stream (cudaStream_t passed as void*; NULL = legacy default stream).
+   d_batch points to a HOST struct whose q, q_off, s, s_off are DEVICE pointers.
+   d_scores / d_ends are DEVICE pointers (d_ends may be NULL).  Asynchronous: returns
+   after enqueueing; validation errors in the sequence bytes are reported by the NEXT
+   call to anyseq_sync(ctx) (returns ANYSEQ_E_BADSEQ) or by the host API. */
+anyseq_status anyseq_align_batch_device(anyseq_ctx* ctx, const anyseq_params* params,
+                                        const anyseq_batch* d_batch, int32_t* d_scores,
+                                        anyseq_alignment* d_ends, void* stream);
+
+/* Full alignment with traceback (predecessor walk) for a batch.
+   out[num_pairs] (host), cigar[cigar_capacity] (host).  cigar_capacity >= sum(n_k + m_k)
+   always suffices; if smaller, returns ANYSEQ_E_CAPACITY with *cigar_used = words
+   required.  Otherwise *cigar_used = words written. */
+anyseq_status anyseq_traceback(anyseq_ctx* ctx, const anyseq_params* params,
+                               const anyseq_batch* batch, anyseq_alignment* out,
+                               uint32_t* cigar, uint64_t cigar_capacity, uint64_t* cigar_used);
+
+/* Long-pair score-only alignment (tiled wavefront) of host
+   sequences q[0..n) and s[0..m).  out receives score and end cell (cigar_len = 0). */
+anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, const char* q,
+                                uint64_t n, const char* s, uint64_t m, anyseq_alignment* out);
+
+/* Wait for all device work of the context; reports deferred device-side errors. */
+anyseq_status anyseq_sync(anyseq_ctx* ctx);
+
+/* Number of kernels the context launched since creation (instrumentation). */
+uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx);
+
+/* Instrumentation: with option "timing" = 1 the context brackets every fill (relaxation)
+   kernel launch with CUDA events on its stream.  anyseq_get_stat reads
+   "fill_ms" (summed device time of fill kernels), "fill_launches", "walk_ms";
+   anyseq_reset_stats clears them.  Returns ANYSEQ_E_INVALID for unknown names. */
+anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value);
+anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
+
+/* Tunables (benchmarking): name = "long_band_rows", "long_blocks", ...; returns
+   ANYSEQ_E_INVALID for unknown names. */
+anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value);
+
+const char* anyseq_status_str(anyseq_status st);
+const char* anyseq_last_error(const anyseq_ctx* ctx);
+/* Library version string. */
+const char* anyseq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ANYSEQ_H */

@@ -1,0 +1,835 @@
+// csrc/api.cu -- the anyseq_* C-ABI (include/anyseq.h): context, validation, planner
+// orchestration, host <-> device staging, multi-GPU sharding of batches.
+//
+// Control flow per call follows the paper's ten steps: allocate/read input
+// (H2D of the caller's ASCII CSR), allocate output, build accessors (pack kernel -> byte
+// codes), allocate temporaries (context-owned device buffers), relax (fill kernels),
+// look up the optimum (fused into the fill epilogue), build alignments if needed (walk +
+// compaction kernels), output (D2H).
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/anyseq.h"
+#include "kernels.h"
+#include "long.h"
+
+using namespace anyseq;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct Device {
+  int id = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  DevBuf q_ascii, s_ascii, q_code, s_code, q_off, s_off, flags, keys, keys2, vals, vals2, slots;
+  DevBuf scores, end_i, end_j, beg_i, beg_j, n_ops, cig_off, ops, dirs, tb, strip, aln, cigar;
+  DevBuf temp, sum, long_ws;
+  PlanSummary* h_sum = nullptr;  // pinned
+  uint64_t* h_small = nullptr;   // pinned scratch
+};
+
+}  // namespace
+
+struct anyseq_ctx {
+  std::vector<Device> devs;
+  std::string err;
+  std::atomic<uint64_t> launches{0};
+  int64_t tb_scratch_bytes = 4ll << 30;
+  int64_t force_variant = -1;
+  int64_t allow16 = 1;
+  LongOptions long_opt;
+  int timing = 0;
+  std::mutex ev_mu;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> fill_ev, walk_ev, pool;
+  double fill_ms = 0, walk_ms = 0;
+  uint64_t fill_launches = 0;
+};
+
+namespace {
+
+const char* kStatus[] = {"ok",          "invalid argument", "invalid sequence byte",
+                         "out of memory", "cigar capacity too small", "CUDA error",
+                         "unsupported",  "peer access unavailable", "timeout"};
+
+anyseq_status fail(anyseq_ctx* c, anyseq_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      if (e_ == cudaErrorMemoryAllocation)                                              \
+        return fail(ctx, ANYSEQ_E_NOMEM, "%s: %s", #call, cudaGetErrorString(e_));      \
+      return fail(ctx, ANYSEQ_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_));         \
+    }                                                                                   \
+  } while (0)
+
+std::pair<cudaEvent_t, cudaEvent_t> take_events(anyseq_ctx* c) {
+  std::lock_guard<std::mutex> lk(c->ev_mu);
+  if (!c->pool.empty()) {
+    auto e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
+  cudaEventCreate(&e.first);
+  cudaEventCreate(&e.second);
+  return e;
+}
+
+void resolve_events(anyseq_ctx* c) {
+  std::lock_guard<std::mutex> lk(c->ev_mu);
+  for (int w = 0; w < 2; ++w) {
+    auto& v = w == 0 ? c->fill_ev : c->walk_ev;
+    for (auto& e : v) {
+      cudaEventSynchronize(e.second);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e.first, e.second);
+      (w == 0 ? c->fill_ms : c->walk_ms) += ms;
+      c->pool.push_back(e);
+    }
+    v.clear();
+  }
+}
+
+anyseq_status validate_params(anyseq_ctx* ctx, const anyseq_params* p) {
+  if (!p) return fail(ctx, ANYSEQ_E_INVALID, "params is NULL");
+  if (p->kind < 0 || p->kind > 2) return fail(ctx, ANYSEQ_E_INVALID, "kind %d invalid", p->kind);
+  if (p->gap < 0 || p->gap > 1) return fail(ctx, ANYSEQ_E_INVALID, "gap %d invalid", p->gap);
+  if (p->match < -128 || p->match > 127 || p->mismatch < -128 || p->mismatch > 127)
+    return fail(ctx, ANYSEQ_E_INVALID, "match/mismatch must be in [-128,127]");
+  if (p->gap_extend < 0 || p->gap_extend > 32767)
+    return fail(ctx, ANYSEQ_E_INVALID, "gap_extend must be in [0,32767]");
+  if (p->gap == ANYSEQ_GAP_AFFINE && (p->gap_open < 0 || p->gap_open > 32767))
+    return fail(ctx, ANYSEQ_E_INVALID, "gap_open must be in [0,32767]");
+  return ANYSEQ_OK;
+}
+
+DevParams dev_params(const anyseq_params* p) {
+  DevParams d;
+  d.kind = p->kind;
+  d.gap = p->gap;
+  d.match = p->match;
+  d.mismatch = p->mismatch;
+  d.go = p->gap == ANYSEQ_GAP_AFFINE ? p->gap_open : 0;
+  d.ge = p->gap_extend;
+  d.mism4 = ((uint32_t)(p->mismatch & 0xff)) * 0x01010101u;
+  d.xm = ((uint32_t)(p->match ^ p->mismatch)) & 0xffu;
+  return d;
+}
+
+void init_summary(PlanSummary* s) {
+  memset(s, 0, sizeof(*s));
+  s->err_pos = ~0ull;
+  for (int v = 0; v < NV; ++v) {
+    s->kmin[v] = ~0ull;
+    s->kmax[v] = 0;
+  }
+}
+
+// Device-side batch job: offsets and sequences are already in device memory.
+struct DeviceJob {
+  const char* d_q;
+  const uint64_t* d_qoff;
+  const char* d_s;
+  const uint64_t* d_soff;
+  uint64_t B;
+  uint64_t q_end, s_end;      // q_off[B], s_off[B] (absolute ends; codes are indexed absolutely)
+  int tb;                     // traceback mode
+  int want_ends;              // score mode: fill end cells + alignment structs
+  int32_t* d_scores_out;      // score mode output (device) or null => ctx buffer
+  anyseq_alignment* d_aln_out;  // alignment structs (device) or null => ctx buffer
+  // traceback: cigar sizing results
+  uint64_t cigar_total = 0;
+};
+
+anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, DeviceJob& J,
+                         uint32_t* d_cigar_out_or_null, uint64_t cigar_cap) {
+  cudaStream_t st = D.stream;
+  const uint64_t B = J.B;
+  const DevParams P = dev_params(prm);
+  auto L = [&](uint64_t n) { ctx->launches += n; };
+
+  CK(D.q_code.ensure(J.q_end + 16));
+  CK(D.s_code.ensure(J.s_end + 16));
+  CK(D.flags.ensure(B * 4 + 4));
+  CK(D.keys.ensure(B * 8 + 8));
+  CK(D.keys2.ensure(B * 8 + 8));
+  CK(D.vals.ensure(B * 4 + 4));
+  CK(D.vals2.ensure(B * 4 + 4));
+  CK(D.slots.ensure(B * sizeof(Slot) + 16));
+  CK(D.sum.ensure(sizeof(PlanSummary)));
+  CK(D.end_i.ensure(B * 4 + 4));
+  CK(D.end_j.ensure(B * 4 + 4));
+  int32_t* d_scores = J.d_scores_out;
+  if (!d_scores) {
+    CK(D.scores.ensure(B * 4 + 4));
+    d_scores = D.scores.as<int32_t>();
+  }
+  if (J.tb) {
+    CK(D.beg_i.ensure(B * 4 + 4));
+    CK(D.beg_j.ensure(B * 4 + 4));
+    CK(D.n_ops.ensure(B * 4 + 4));
+    CK(D.cig_off.ensure(B * 8 + 16));
+    CK(D.ops.ensure((J.q_end + J.s_end + B + 1) * 4));
+    CK(D.tb.ensure(B * sizeof(TbInfo) + 16));
+  }
+
+  // ---- a1: pack + validate ----
+  init_summary(D.h_sum);
+  CK(cudaMemcpyAsync(D.sum.p, D.h_sum, sizeof(PlanSummary), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(D.flags.p, 0, B * 4 + 4, st));
+  // byte codes are indexed by absolute CSR position; pack the whole [0, end) range the
+  // caller's offsets cover (bytes before off[0] are never read by a pair)
+  CK(launch_pack(J.d_q, J.q_end, D.q_code.as<uint8_t>(), 0, J.d_qoff, B, D.flags.as<uint32_t>(),
+                 D.sum.as<PlanSummary>(), st, D.num_sms));
+  CK(launch_pack(J.d_s, J.s_end, D.s_code.as<uint8_t>(), 1ull << 62, J.d_soff, B,
+                 D.flags.as<uint32_t>(), D.sum.as<PlanSummary>(), st, D.num_sms));
+  L(2);
+
+  // ---- a2: classify ----
+  ClassifyArgs ca;
+  memset(&ca, 0, sizeof(ca));
+  ca.P = P;
+  ca.cfg.tb = J.tb;
+  ca.cfg.allow16 = (int32_t)ctx->allow16;
+  ca.cfg.force_variant = (int32_t)ctx->force_variant;
+  ca.cfg.bound_go = P.go;
+  ca.cfg.bound_ge = P.ge;
+  ca.cfg.bound_match = std::max(P.match, P.mismatch);
+  ca.q_off = J.d_qoff;
+  ca.s_off = J.d_soff;
+  ca.num_pairs = B;
+  ca.flags = D.flags.as<uint32_t>();
+  ca.sum = D.sum.as<PlanSummary>();
+  ca.keys = D.keys.as<unsigned long long>();
+  ca.vals = D.vals.as<int32_t>();
+  ca.scores = d_scores;
+  ca.end_i = D.end_i.as<int32_t>();
+  ca.end_j = D.end_j.as<int32_t>();
+  if (J.tb) {
+    ca.ops = D.ops.as<uint32_t>();
+    ca.n_ops = D.n_ops.as<int32_t>();
+    ca.beg_i = D.beg_i.as<int32_t>();
+    ca.beg_j = D.beg_j.as<int32_t>();
+  }
+  CK(launch_classify(ca, st, D.num_sms));
+  L(1);
+  CK(cudaMemcpyAsync(D.h_sum, D.sum.p, sizeof(PlanSummary), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const PlanSummary S = *D.h_sum;
+  if (S.err_pos != ~0ull) {
+    const bool in_s = S.err_pos >= (1ull << 62);
+    return fail(ctx, ANYSEQ_E_BADSEQ, "invalid symbol at %s byte offset %llu", in_s ? "s" : "q",
+                (unsigned long long)(in_s ? S.err_pos - (1ull << 62) : S.err_pos));
+  }
+  if (S.range_err)
+    return fail(ctx, ANYSEQ_E_UNSUPPORTED, "score range exceeds 32-bit arithmetic");
+
+  // ---- a2: order pairs by (variant, m, n) and form slots ----
+  int32_t voff[NV + 1], sbase[NV], nslot[NV];
+  int64_t nontriv = 0, total_slots = 0;
+  int used = 0, used_v = -1;
+  for (int v = 0; v < NV; ++v) {
+    voff[v] = (int32_t)nontriv;
+    nontriv += S.count[v];
+    sbase[v] = (int32_t)total_slots;
+    const int pp = variant_desc(v).pairs;
+    nslot[v] = pp == 2 ? (S.count[v] + 1) / 2 : S.count[v];
+    total_slots += nslot[v];
+    if (S.count[v]) { ++used; used_v = v; }
+  }
+  voff[NV] = (int32_t)nontriv;
+  const int32_t* order = D.vals.as<int32_t>();
+  const bool uniform = used == 1 && (uint64_t)S.count[used_v] == B && S.kmin[used_v] == S.kmax[used_v];
+  if (nontriv > 0 && !uniform) {
+    size_t tb = 0;
+    CK(sort_pairs(nullptr, tb, nullptr, nullptr, nullptr, nullptr, (int64_t)B, st));
+    CK(D.temp.ensure(tb + 256));
+    tb = D.temp.cap;
+    CK(sort_pairs(D.temp.p, tb, D.keys.as<unsigned long long>(), D.keys2.as<unsigned long long>(),
+                  D.vals.as<int32_t>(), D.vals2.as<int32_t>(), (int64_t)B, st));
+    L(4);
+    order = D.vals2.as<int32_t>();
+  }
+  if (nontriv > 0) {
+    CK(launch_slots(order, nontriv, voff, S.count, sbase, D.slots.as<Slot>(), st, D.num_sms));
+    L(1);
+  }
+
+  // ---- a3/a4: fill (+ a5 walk) per variant ----
+  for (int v = 0; v < NV; ++v) {
+    if (!S.count[v]) continue;
+    const VariantDesc d = variant_desc(v);
+    FillArgs fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.P = P;
+    fa.qcode = D.q_code.as<uint8_t>();
+    fa.scode = D.s_code.as<uint8_t>();
+    fa.q_off = J.d_qoff;
+    fa.s_off = J.d_soff;
+    fa.slots = D.slots.as<Slot>();
+    fa.nslots_dev = nullptr;
+    fa.pos = J.want_ends || J.tb;
+    fa.scores = d_scores;
+    fa.end_i = D.end_i.as<int32_t>();
+    fa.end_j = D.end_j.as<int32_t>();
+    const int HS = d.L * d.R;
+    const int G = 32 / d.L;
+    // strip row buffer only when some pair needs more than one strip
+    int grid_est = D.num_sms * 16;  // upper bound of resident blocks (128 threads each)
+    if (S.maxn[v] > HS) {
+      fa.strip_stride = S.maxm[v] + 1;
+      const int64_t groups = (int64_t)grid_est * 4 * G;
+      CK(D.strip.ensure((size_t)groups * fa.strip_stride * sizeof(uint2)));
+      fa.strip_scratch = D.strip.as<uint2>();
+    } else {
+      fa.strip_stride = 0;
+      CK(D.strip.ensure(256));
+      fa.strip_scratch = D.strip.as<uint2>();
+    }
+    if (!d.tb) {
+      fa.slot_lo = sbase[v];
+      fa.slot_hi = sbase[v] + nslot[v];
+      int grid = 0;
+      std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+      if (ctx->timing) { ev = take_events(ctx); CK(cudaEventRecord(ev.first, st)); }
+      CK(launch_fill(v, prm->kind, prm->gap, fa, st, D.num_sms, &grid));
+      if (ctx->timing) {
+        CK(cudaEventRecord(ev.second, st));
+        std::lock_guard<std::mutex> lk(ctx->ev_mu);
+        ctx->fill_ev.push_back(ev);
+        ctx->fill_launches++;
+      }
+      if (grid > grid_est) return fail(ctx, ANYSEQ_E_CUDA, "occupancy above scratch estimate");
+      L(1);
+    } else {
+      const int64_t ns = (S.maxn[v] + HS - 1) / HS;
+      const int64_t s8 = (S.maxm[v] + d.L - 1 + 7) / 8;
+      const int64_t block_words = ns * s8 * d.R * d.L * d.pairs;
+      const int64_t cap_words = std::max<int64_t>(ctx->tb_scratch_bytes / 4, block_words);
+      int64_t chunk = std::max<int64_t>(1, cap_words / block_words);
+      chunk = std::min<int64_t>(chunk, nslot[v]);
+      CK(D.dirs.ensure((size_t)(chunk * block_words) * 4));
+      fa.dirs = D.dirs.as<uint32_t>();
+      fa.dir_block_words = block_words;
+      fa.tb = D.tb.as<TbInfo>();
+      for (int64_t lo = 0; lo < nslot[v]; lo += chunk) {
+        const int64_t hi = std::min<int64_t>(nslot[v], lo + chunk);
+        fa.slot_lo = (int32_t)(sbase[v] + lo);
+        fa.slot_hi = (int32_t)(sbase[v] + hi);
+        int grid = 0;
+        std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+        if (ctx->timing) { ev = take_events(ctx); CK(cudaEventRecord(ev.first, st)); }
+        CK(launch_fill(v, prm->kind, prm->gap, fa, st, D.num_sms, &grid));
+        if (ctx->timing) {
+          CK(cudaEventRecord(ev.second, st));
+          std::lock_guard<std::mutex> lk(ctx->ev_mu);
+          ctx->fill_ev.push_back(ev);
+          ctx->fill_launches++;
+        }
+        if (grid > grid_est) return fail(ctx, ANYSEQ_E_CUDA, "occupancy above scratch estimate");
+        WalkArgs wa;
+        wa.kind = prm->kind;
+        wa.gap = prm->gap;
+        wa.slots = D.slots.as<Slot>();
+        wa.slot_lo = fa.slot_lo;
+        wa.slot_hi = fa.slot_hi;
+        wa.pairs_per_slot = d.pairs;
+        wa.tb = D.tb.as<TbInfo>();
+        wa.dirs = D.dirs.as<uint32_t>();
+        wa.q_off = J.d_qoff;
+        wa.s_off = J.d_soff;
+        wa.ops = D.ops.as<uint32_t>();
+        wa.n_ops = D.n_ops.as<int32_t>();
+        wa.beg_i = D.beg_i.as<int32_t>();
+        wa.beg_j = D.beg_j.as<int32_t>();
+        std::pair<cudaEvent_t, cudaEvent_t> ew{nullptr, nullptr};
+        if (ctx->timing) { ew = take_events(ctx); CK(cudaEventRecord(ew.first, st)); }
+        CK(launch_walk(wa, st, D.num_sms));
+        if (ctx->timing) {
+          CK(cudaEventRecord(ew.second, st));
+          std::lock_guard<std::mutex> lk(ctx->ev_mu);
+          ctx->walk_ev.push_back(ew);
+        }
+        L(2);
+      }
+    }
+  }
+
+  // ---- output assembly ----
+  FinalizeArgs fz;
+  memset(&fz, 0, sizeof(fz));
+  fz.num_pairs = B;
+  fz.scores = d_scores;
+  fz.end_i = D.end_i.as<int32_t>();
+  fz.end_j = D.end_j.as<int32_t>();
+  fz.q_off = J.d_qoff;
+  fz.s_off = J.d_soff;
+  if (J.tb) {
+    size_t tbytes = 0;
+    CK(exclusive_scan_i32_to_u64(nullptr, tbytes, nullptr, nullptr, (int64_t)B + 1, st));
+    CK(D.temp.ensure(tbytes + 256));
+    tbytes = D.temp.cap;
+    // n_ops[B] is a zero sentinel so cig_off[B] is the total
+    CK(cudaMemsetAsync(D.n_ops.as<int32_t>() + B, 0, 4, st));
+    CK(exclusive_scan_i32_to_u64(D.temp.p, tbytes, D.n_ops.as<int32_t>(), D.cig_off.as<uint64_t>(),
+                                 (int64_t)B + 1, st));
+    L(1);
+    CK(cudaMemcpyAsync(D.h_small, D.cig_off.as<uint64_t>() + B, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    J.cigar_total = D.h_small[0];
+    fz.beg_i = D.beg_i.as<int32_t>();
+    fz.beg_j = D.beg_j.as<int32_t>();
+    fz.n_ops = D.n_ops.as<int32_t>();
+    fz.cig_off = D.cig_off.as<uint64_t>();
+    fz.ops = D.ops.as<uint32_t>();
+    fz.cigar = d_cigar_out_or_null;
+    fz.cigar_cap = cigar_cap;
+  }
+  if (J.tb || J.want_ends) {
+    anyseq_alignment* out = J.d_aln_out;
+    if (!out) {
+      CK(D.aln.ensure(B * sizeof(anyseq_alignment) + 64));
+      out = D.aln.as<anyseq_alignment>();
+    }
+    fz.out_aln = out;
+    CK(launch_finalize(fz, st, D.num_sms));
+    L(1);
+  }
+  return ANYSEQ_OK;
+}
+
+anyseq_status check_batch_host(anyseq_ctx* ctx, const anyseq_batch* b) {
+  if (!b) return fail(ctx, ANYSEQ_E_INVALID, "batch is NULL");
+  if (b->num_pairs == 0) return ANYSEQ_OK;
+  if (!b->q_off || !b->s_off) return fail(ctx, ANYSEQ_E_INVALID, "offsets are NULL");
+  if (b->num_pairs >= (1ull << 31)) return fail(ctx, ANYSEQ_E_INVALID, "too many pairs");
+  for (uint64_t k = 0; k < b->num_pairs; ++k) {
+    if (b->q_off[k + 1] < b->q_off[k] || b->s_off[k + 1] < b->s_off[k])
+      return fail(ctx, ANYSEQ_E_INVALID, "pair %llu: offsets decrease", (unsigned long long)k);
+    if (b->q_off[k + 1] - b->q_off[k] >= (1ull << 31) || b->s_off[k + 1] - b->s_off[k] >= (1ull << 31))
+      return fail(ctx, ANYSEQ_E_INVALID, "pair %llu: sequence longer than 2^31-1",
+                  (unsigned long long)k);
+  }
+  if ((b->q_off[b->num_pairs] > 0 && !b->q) || (b->s_off[b->num_pairs] > 0 && !b->s))
+    return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
+  return ANYSEQ_OK;
+}
+
+// Map an error byte position back to (pair, offset) for the message.
+void describe_badseq(anyseq_ctx* ctx, const anyseq_batch* b, uint64_t k0) {
+  // ctx->err holds "invalid symbol at q byte offset X" relative to the shard
+  unsigned long long pos = 0;
+  char which = 0;
+  if (sscanf(ctx->err.c_str(), "invalid symbol at %c byte offset %llu", &which, &pos) != 2) return;
+  const uint64_t* off = which == 'q' ? b->q_off : b->s_off;
+  const char* seq = which == 'q' ? b->q : b->s;
+  const uint64_t abs = pos + off[k0];
+  const uint64_t* it = std::upper_bound(off, off + b->num_pairs + 1, abs);
+  const uint64_t k = (uint64_t)(it - off) - 1;
+  char buf[256];
+  snprintf(buf, sizeof(buf), "pair %llu: byte 0x%02x at %c offset %llu",
+           (unsigned long long)k, (unsigned)(unsigned char)seq[abs], which,
+           (unsigned long long)(abs - off[k]));
+  ctx->err = buf;
+}
+
+// Host-memory batch on one device, pairs [k0, k1).
+anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* prm,
+                             const anyseq_batch* b, uint64_t k0, uint64_t k1, int tb,
+                             int32_t* scores, anyseq_alignment* aln, std::vector<uint32_t>* cig) {
+  CK(cudaSetDevice(D.id));
+  cudaStream_t st = D.stream;
+  const uint64_t B = k1 - k0;
+  const uint64_t q0 = b->q_off[k0], qN = b->q_off[k1], s0 = b->s_off[k0], sN = b->s_off[k1];
+  const uint64_t qlen = qN - q0, slen = sN - s0;
+  CK(D.q_ascii.ensure(qlen + 16));
+  CK(D.s_ascii.ensure(slen + 16));
+  CK(D.q_off.ensure((B + 1) * 8));
+  CK(D.s_off.ensure((B + 1) * 8));
+  // rebased offsets (host staging in pinned scratch would avoid the pageable path; the
+  // offsets are small compared to the sequences)
+  std::vector<uint64_t> qo(B + 1), so(B + 1);
+  for (uint64_t k = 0; k <= B; ++k) {
+    qo[k] = b->q_off[k0 + k] - q0;
+    so[k] = b->s_off[k0 + k] - s0;
+  }
+  if (qlen) CK(cudaMemcpyAsync(D.q_ascii.p, b->q + q0, qlen, cudaMemcpyHostToDevice, st));
+  if (slen) CK(cudaMemcpyAsync(D.s_ascii.p, b->s + s0, slen, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(D.q_off.p, qo.data(), (B + 1) * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(D.s_off.p, so.data(), (B + 1) * 8, cudaMemcpyHostToDevice, st));
+  DeviceJob J;
+  J.d_q = D.q_ascii.as<char>();
+  J.d_qoff = D.q_off.as<uint64_t>();
+  J.d_s = D.s_ascii.as<char>();
+  J.d_soff = D.s_off.as<uint64_t>();
+  J.B = B;
+  J.q_end = qlen;
+  J.s_end = slen;
+  J.tb = tb;
+  J.want_ends = aln != nullptr;
+  J.d_scores_out = nullptr;
+  J.d_aln_out = nullptr;
+  uint64_t cap_words = 0;
+  if (tb) {
+    // worst case sum(n+m) words; the exact total is known after the walk
+    cap_words = qlen + slen + 1;
+    CK(D.cigar.ensure(cap_words * 4));
+  }
+  anyseq_status s = run_device(ctx, D, prm, J, tb ? D.cigar.as<uint32_t>() : nullptr, cap_words);
+  if (s != ANYSEQ_OK) {
+    if (s == ANYSEQ_E_BADSEQ) {
+      // rebase the message to absolute batch coordinates
+      unsigned long long pos = 0;
+      char which = 0;
+      if (sscanf(ctx->err.c_str(), "invalid symbol at %c byte offset %llu", &which, &pos) == 2) {
+        char buf[128];
+        snprintf(buf, sizeof(buf), "invalid symbol at %c byte offset %llu", which,
+                 (unsigned long long)(pos - (which == 'q' ? 0 : 0)));
+        ctx->err = buf;
+        describe_badseq(ctx, b, k0);
+      }
+    }
+    return s;
+  }
+  if (!tb) {
+    CK(cudaMemcpyAsync(scores + k0, D.scores.p, B * 4, cudaMemcpyDeviceToHost, st));
+    if (aln) CK(cudaMemcpyAsync(aln + k0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(aln + k0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
+    cig->resize(J.cigar_total);
+    if (J.cigar_total)
+      CK(cudaMemcpyAsync(cig->data(), D.cigar.p, J.cigar_total * 4, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return ANYSEQ_OK;
+}
+
+// Split [0, B) into G contiguous shards of ~equal cell count.
+std::vector<uint64_t> shard_bounds(const anyseq_batch* b, int G) {
+  std::vector<uint64_t> bounds(G + 1, b->num_pairs);
+  bounds[0] = 0;
+  if (G == 1) return bounds;
+  long double total = 0;
+  for (uint64_t k = 0; k < b->num_pairs; ++k)
+    total += (long double)(b->q_off[k + 1] - b->q_off[k] + 1) * (b->s_off[k + 1] - b->s_off[k] + 1);
+  long double acc = 0;
+  int g = 1;
+  for (uint64_t k = 0; k < b->num_pairs && g < G; ++k) {
+    acc += (long double)(b->q_off[k + 1] - b->q_off[k] + 1) * (b->s_off[k + 1] - b->s_off[k] + 1);
+    while (g < G && acc >= total * g / G) bounds[g++] = k + 1;
+  }
+  for (; g < G; ++g) bounds[g] = b->num_pairs;
+  return bounds;
+}
+
+anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const anyseq_batch* b,
+                             int tb, int32_t* scores, anyseq_alignment* aln, uint32_t* cigar,
+                             uint64_t cap, uint64_t* used) {
+  const int G = (int)ctx->devs.size();
+  std::vector<uint64_t> bounds = shard_bounds(b, G);
+  std::vector<anyseq_status> st(G, ANYSEQ_OK);
+  std::vector<std::string> errs(G);
+  std::vector<std::vector<uint32_t>> cigs(G);
+  if (G == 1) {
+    st[0] = run_host_shard(ctx, ctx->devs[0], prm, b, 0, b->num_pairs, tb, scores, aln, &cigs[0]);
+  } else {
+    std::vector<anyseq_ctx*> sub(G);
+    std::vector<std::thread> th;
+    std::mutex mu;
+    for (int g = 0; g < G; ++g) {
+      th.emplace_back([&, g] {
+        anyseq_ctx local;  // per-thread error string
+        local.tb_scratch_bytes = ctx->tb_scratch_bytes;
+        local.force_variant = ctx->force_variant;
+        local.allow16 = ctx->allow16;
+        anyseq_status s = ANYSEQ_OK;
+        if (bounds[g + 1] > bounds[g])
+          s = run_host_shard(&local, ctx->devs[g], prm, b, bounds[g], bounds[g + 1], tb, scores,
+                             aln, &cigs[g]);
+        std::lock_guard<std::mutex> lk(mu);
+        st[g] = s;
+        errs[g] = local.err;
+        ctx->launches += local.launches.load();
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int g = 0; g < G; ++g)
+      if (st[g] != ANYSEQ_OK) {
+        ctx->err = "device " + std::to_string(ctx->devs[g].id) + ": " + errs[g];
+        return st[g];
+      }
+  }
+  if (st[0] != ANYSEQ_OK) return st[0];
+  if (tb) {
+    uint64_t total = 0;
+    for (int g = 0; g < G; ++g) total += cigs[g].size();
+    if (used) *used = total;
+    if (total > cap) return fail(ctx, ANYSEQ_E_CAPACITY, "cigar needs %llu words, capacity %llu",
+                                 (unsigned long long)total, (unsigned long long)cap);
+    uint64_t base = 0;
+    for (int g = 0; g < G; ++g) {
+      if (!cigs[g].empty()) memcpy(cigar + base, cigs[g].data(), cigs[g].size() * 4);
+      if (base)
+        for (uint64_t k = bounds[g]; k < bounds[g + 1]; ++k) aln[k].cigar_offset += base;
+      base += cigs[g].size();
+    }
+  }
+  return ANYSEQ_OK;
+}
+
+}  // namespace
+
+// =========================================================================== C-ABI
+extern "C" {
+
+anyseq_status anyseq_create(anyseq_ctx** out, const int* device_ids, int num_devices) {
+  if (!out) return ANYSEQ_E_INVALID;
+  *out = nullptr;
+  if (num_devices < 1) return ANYSEQ_E_INVALID;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return ANYSEQ_E_CUDA;
+  }
+  anyseq_ctx* c = new (std::nothrow) anyseq_ctx();
+  if (!c) return ANYSEQ_E_NOMEM;
+  for (int g = 0; g < num_devices; ++g) {
+    const int id = device_ids ? device_ids[g] : g;
+    if (id < 0 || id >= ndev) {
+      anyseq_destroy(c);
+      return ANYSEQ_E_INVALID;
+    }
+    Device D;
+    D.id = id;
+    if (cudaSetDevice(id) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaDeviceGetAttribute(&D.num_sms, cudaDevAttrMultiProcessorCount, id) != cudaSuccess ||
+        cudaMallocHost(&D.h_sum, sizeof(PlanSummary)) != cudaSuccess ||
+        cudaMallocHost(&D.h_small, 64) != cudaSuccess) {
+      c->devs.push_back(D);
+      anyseq_destroy(c);
+      return ANYSEQ_E_CUDA;
+    }
+    c->devs.push_back(D);
+  }
+  cudaSetDevice(c->devs[0].id);
+  *out = c;
+  return ANYSEQ_OK;
+}
+
+void anyseq_destroy(anyseq_ctx* c) {
+  if (!c) return;
+  resolve_events(c);
+  for (auto& e : c->pool) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (auto& D : c->devs) {
+    cudaSetDevice(D.id);
+    DevBuf* bufs[] = {&D.q_ascii, &D.s_ascii, &D.q_code, &D.s_code, &D.q_off, &D.s_off,
+                      &D.flags,   &D.keys,    &D.keys2,  &D.vals,   &D.vals2, &D.slots,
+                      &D.scores,  &D.end_i,   &D.end_j,  &D.beg_i,  &D.beg_j, &D.n_ops,
+                      &D.cig_off, &D.ops,     &D.dirs,   &D.tb,     &D.strip, &D.aln,
+                      &D.cigar,   &D.temp,    &D.sum,    &D.long_ws};
+    for (DevBuf* b : bufs) b->release();
+    if (D.h_sum) cudaFreeHost(D.h_sum);
+    if (D.h_small) cudaFreeHost(D.h_small);
+    if (D.stream) cudaStreamDestroy(D.stream);
+  }
+  delete c;
+}
+
+anyseq_status anyseq_align_batch(anyseq_ctx* ctx, const anyseq_params* params,
+                                 const anyseq_batch* batch, int32_t* scores,
+                                 anyseq_alignment* ends) {
+  if (!ctx) return ANYSEQ_E_INVALID;
+  anyseq_status s = validate_params(ctx, params);
+  if (s != ANYSEQ_OK) return s;
+  if ((s = check_batch_host(ctx, batch)) != ANYSEQ_OK) return s;
+  if (batch->num_pairs == 0) return ANYSEQ_OK;
+  if (!scores) return fail(ctx, ANYSEQ_E_INVALID, "scores is NULL");
+  return run_host_batch(ctx, params, batch, 0, scores, ends, nullptr, 0, nullptr);
+}
+
+anyseq_status anyseq_traceback(anyseq_ctx* ctx, const anyseq_params* params,
+                               const anyseq_batch* batch, anyseq_alignment* out, uint32_t* cigar,
+                               uint64_t cigar_capacity, uint64_t* cigar_used) {
+  if (!ctx) return ANYSEQ_E_INVALID;
+  anyseq_status s = validate_params(ctx, params);
+  if (s != ANYSEQ_OK) return s;
+  if ((s = check_batch_host(ctx, batch)) != ANYSEQ_OK) return s;
+  if (cigar_used) *cigar_used = 0;
+  if (batch->num_pairs == 0) return ANYSEQ_OK;
+  if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
+  if (!cigar && cigar_capacity) return fail(ctx, ANYSEQ_E_INVALID, "cigar is NULL");
+  std::vector<int32_t> scores(batch->num_pairs);
+  return run_host_batch(ctx, params, batch, 1, scores.data(), out, cigar, cigar_capacity,
+                        cigar_used);
+}
+
+anyseq_status anyseq_align_batch_device(anyseq_ctx* ctx, const anyseq_params* params,
+                                        const anyseq_batch* d_batch, int32_t* d_scores,
+                                        anyseq_alignment* d_ends, void* stream) {
+  if (!ctx) return ANYSEQ_E_INVALID;
+  anyseq_status s = validate_params(ctx, params);
+  if (s != ANYSEQ_OK) return s;
+  if (!d_batch) return fail(ctx, ANYSEQ_E_INVALID, "batch is NULL");
+  if (d_batch->num_pairs == 0) return ANYSEQ_OK;
+  if (!d_batch->q_off || !d_batch->s_off || !d_scores)
+    return fail(ctx, ANYSEQ_E_INVALID, "NULL device pointer");
+  if (d_batch->num_pairs >= (1ull << 31)) return fail(ctx, ANYSEQ_E_INVALID, "too many pairs");
+  Device& D = ctx->devs[0];
+  CK(cudaSetDevice(D.id));
+  cudaStream_t user = (cudaStream_t)stream;
+  // order the context stream after the caller's stream, run, then order the caller after us
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, user));
+  CK(cudaStreamWaitEvent(D.stream, ev, 0));
+  // absolute ends of the CSR ranges
+  CK(cudaMemcpyAsync(D.h_small, d_batch->q_off + d_batch->num_pairs, 8, cudaMemcpyDeviceToHost, D.stream));
+  CK(cudaMemcpyAsync(D.h_small + 1, d_batch->s_off + d_batch->num_pairs, 8, cudaMemcpyDeviceToHost, D.stream));
+  CK(cudaStreamSynchronize(D.stream));
+  DeviceJob J;
+  J.d_q = d_batch->q;
+  J.d_qoff = d_batch->q_off;
+  J.d_s = d_batch->s;
+  J.d_soff = d_batch->s_off;
+  J.B = d_batch->num_pairs;
+  J.q_end = D.h_small[0];
+  J.s_end = D.h_small[1];
+  J.tb = 0;
+  J.want_ends = d_ends != nullptr;
+  J.d_scores_out = d_scores;
+  J.d_aln_out = d_ends;
+  s = run_device(ctx, D, params, J, nullptr, 0);
+  CK(cudaEventRecord(ev, D.stream));
+  CK(cudaStreamWaitEvent(user, ev, 0));
+  cudaEventDestroy(ev);
+  return s;
+}
+
+anyseq_status anyseq_sync(anyseq_ctx* ctx) {
+  if (!ctx) return ANYSEQ_E_INVALID;
+  for (auto& D : ctx->devs) {
+    CK(cudaSetDevice(D.id));
+    CK(cudaStreamSynchronize(D.stream));
+  }
+  return ANYSEQ_OK;
+}
+
+uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value) {
+  if (!ctx || !name) return ANYSEQ_E_INVALID;
+  std::string n(name);
+  if (n == "tb_scratch_bytes") { ctx->tb_scratch_bytes = std::max<int64_t>(value, 1 << 20); return ANYSEQ_OK; }
+  if (n == "timing") { ctx->timing = value ? 1 : 0; return ANYSEQ_OK; }
+  if (n == "force_variant") { ctx->force_variant = value; return ANYSEQ_OK; }
+  if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }
+  if (n == "long_band_rows") { ctx->long_opt.band_rows = (int)value; return ANYSEQ_OK; }
+  if (n == "long_blocks") { ctx->long_opt.blocks = (int)value; return ANYSEQ_OK; }
+  if (n == "long_strips") { ctx->long_opt.virtual_strips = (int)value; return ANYSEQ_OK; }
+  if (n == "long_chunk_cols") { ctx->long_opt.chunk_cols = (int)value; return ANYSEQ_OK; }
+  return fail(ctx, ANYSEQ_E_INVALID, "unknown option %s", name);
+}
+
+anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, const char* q,
+                                uint64_t n, const char* s, uint64_t m, anyseq_alignment* out) {
+  if (!ctx) return ANYSEQ_E_INVALID;
+  anyseq_status st = validate_params(ctx, params);
+  if (st != ANYSEQ_OK) return st;
+  if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
+  if ((n && !q) || (m && !s)) return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
+  if (n >= (1ull << 31) || m >= (1ull << 31))
+    return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long sequences must be shorter than 2^31");
+  std::vector<LongDevice> ld;
+  for (auto& D : ctx->devs) {
+    LongDevice x;
+    x.id = D.id;
+    x.stream = D.stream;
+    x.num_sms = D.num_sms;
+    ld.push_back(x);
+  }
+  std::string err;
+  uint64_t launches = 0;
+  LongResult r;
+  const int rc = run_long(ld, dev_params(params), q, n, s, m, ctx->long_opt, &r, &err, &launches);
+  ctx->launches += launches;
+  if (rc != 0) return fail(ctx, (anyseq_status)rc, "%s", err.c_str());
+  memset(out, 0, sizeof(*out));
+  out->score = r.score;
+  out->q_end = out->q_begin = r.end_i;
+  out->s_end = out->s_begin = r.end_j;
+  return ANYSEQ_OK;
+}
+
+anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) {
+  if (!ctx || !name || !value) return ANYSEQ_E_INVALID;
+  for (auto& D : ctx->devs) {
+    cudaSetDevice(D.id);
+  }
+  resolve_events(ctx);
+  std::string n(name);
+  if (n == "fill_ms") { *value = ctx->fill_ms; return ANYSEQ_OK; }
+  if (n == "walk_ms") { *value = ctx->walk_ms; return ANYSEQ_OK; }
+  if (n == "fill_launches") { *value = (double)ctx->fill_launches; return ANYSEQ_OK; }
+  return fail(ctx, ANYSEQ_E_INVALID, "unknown stat %s", name);
+}
+
+anyseq_status anyseq_reset_stats(anyseq_ctx* ctx) {
+  if (!ctx) return ANYSEQ_E_INVALID;
+  resolve_events(ctx);
+  ctx->fill_ms = ctx->walk_ms = 0;
+  ctx->fill_launches = 0;
+  return ANYSEQ_OK;
+}
+
+const char* anyseq_status_str(anyseq_status s) {
+  const int i = (int)s;
+  return (i >= 0 && i < (int)(sizeof(kStatus) / sizeof(kStatus[0]))) ? kStatus[i] : "unknown status";
+}
+
+const char* anyseq_last_error(const anyseq_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+const char* anyseq_version(void) { return "anyseq-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

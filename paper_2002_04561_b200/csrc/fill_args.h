@@ -1,0 +1,29 @@
+// csrc/fill_args.h -- argument block of the fill kernel (host + device).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace anyseq {
+
+struct FillArgs {
+  DevParams P;
+  const uint8_t* qcode;
+  const uint8_t* scode;
+  const uint64_t* q_off;
+  const uint64_t* s_off;
+  const Slot* slots;          // this variant's slot array
+  const int32_t* nslots_dev;  // if non-null: slot range is [0, *nslots_dev)
+  int32_t slot_lo, slot_hi;   // otherwise [slot_lo, slot_hi)
+  int32_t pos;                // also produce end cells
+  int32_t* scores;            // [num_pairs]
+  int32_t* end_i;             // [num_pairs] (pos)
+  int32_t* end_j;
+  uint2* strip_scratch;       // per resident lane group: strip_stride entries (H, E)
+  int64_t strip_stride;
+  uint32_t* dirs;             // TB: direction nibbles
+  int64_t dir_block_words;    // TB: words per slot block (fixed per launch)
+  TbInfo* tb;                 // TB: per pair
+};
+
+}  // namespace anyseq

@@ -1,0 +1,358 @@
+// csrc/kernels.cu -- pack (a1), plan (a2), traceback walk (a5), output assembly.
+//
+//  * pack: "Sequence" accessor storage of the paper as byte codes on the device;
+//    validation of the alphabet (reading R12).
+//  * classify/slots: per-pair variant choice (register width by the 16-bit range guard,
+//    the paper's narrow differential-score argument P:498 applied to absolute scores --
+//    reading R11), sort by (variant, m, n) so that pairs sharing a warp have similar shape.
+//  * walk: the predecessor walk of the traceback.
+#include <cub/cub.cuh>
+#include "kernels.h"
+#include "../../include/anyseq.h"
+
+namespace anyseq {
+
+static inline int grid_for(int64_t work, int threads, int num_sms, int per_sm = 8) {
+  int64_t g = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ------------------------------------------------------------------------------- pack
+__device__ __forceinline__ uint32_t code_of(uint32_t c) {
+  const uint32_t x = c | 0x20u;  // lower case
+  return x == 'a' ? 0u : x == 'c' ? 1u : x == 'g' ? 2u : x == 't' ? 3u : x == 'n' ? 4u : 0xFFu;
+}
+
+__device__ int64_t find_pair(const uint64_t* off, uint64_t num_pairs, uint64_t pos) {
+  // largest k with off[k] <= pos
+  int64_t lo = 0, hi = (int64_t)num_pairs;  // off[hi] > pos for pos < off[num]
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (off[mid] <= pos) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void pack_kernel(const uint8_t* __restrict__ in, uint64_t len, uint8_t* __restrict__ out,
+                            uint64_t pos_base, const uint64_t* __restrict__ off, uint64_t num_pairs,
+                            uint32_t* flags, PlanSummary* sum) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 16;
+  for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; b < len; b += stride) {
+    const bool vec = (b + 16 <= len) && ((((uintptr_t)(in + b)) & 15) == 0) &&
+                     ((((uintptr_t)(out + b)) & 15) == 0);
+    uint8_t c[16];
+    int cnt = 16;
+    if (vec) {
+      const uint4 v = *reinterpret_cast<const uint4*>(in + b);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 16; ++k) c[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+    } else {
+      cnt = (int)((len - b) < 16 ? (len - b) : 16);
+      for (int k = 0; k < cnt; ++k) c[k] = in[b + k];
+    }
+    uint8_t o[16];
+    bool hasN = false;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t x = code_of(c[k]);
+      o[k] = (uint8_t)x;
+      if (k < cnt) {
+        if (x == 0xFFu) atomicMin(&sum->err_pos, (unsigned long long)(pos_base + b + k));
+        if (x == 4u) hasN = true;
+      }
+    }
+    if (vec) {
+      uint4 v;
+      v.x = o[0] | (o[1] << 8) | (o[2] << 16) | ((uint32_t)o[3] << 24);
+      v.y = o[4] | (o[5] << 8) | (o[6] << 16) | ((uint32_t)o[7] << 24);
+      v.z = o[8] | (o[9] << 8) | (o[10] << 16) | ((uint32_t)o[11] << 24);
+      v.w = o[12] | (o[13] << 8) | (o[14] << 16) | ((uint32_t)o[15] << 24);
+      *reinterpret_cast<uint4*>(out + b) = v;
+    } else {
+      for (int k = 0; k < cnt; ++k) out[b + k] = o[k];
+    }
+    if (hasN) {  // rare: mark every pair that owns an N in this chunk
+      for (int k = 0; k < cnt; ++k)
+        if (o[k] == 4u) atomicOr(&flags[find_pair(off, num_pairs, b + k)], 1u);
+    }
+  }
+}
+
+cudaError_t launch_pack(const char* d_ascii, uint64_t len, uint8_t* d_code, uint64_t pos_base,
+                        const uint64_t* d_off, uint64_t num_pairs, uint32_t* d_flags,
+                        PlanSummary* d_sum, cudaStream_t st, int num_sms) {
+  if (len == 0) return cudaSuccess;
+  const int threads = 256;
+  const int grid = grid_for((int64_t)((len + 15) / 16), threads, num_sms, 16);
+  pack_kernel<<<grid, threads, 0, st>>>((const uint8_t*)d_ascii, len, d_code, pos_base, d_off,
+                                        num_pairs, d_flags, d_sum);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------- classify
+__global__ void classify_kernel(ClassifyArgs a) {
+  const DevParams& P = a.P;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.num_pairs;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t n = (int64_t)(a.q_off[k + 1] - a.q_off[k]);
+    const int64_t m = (int64_t)(a.s_off[k + 1] - a.s_off[k]);
+    if (n == 0 || m == 0) {
+      // empty sequences (SURVEY 8(b) "Empty sequences"): global = one gap run, else 0
+      int32_t sc = 0, ei = 0, ej = 0;
+      if (P.kind == KGLOBAL) {
+        const int64_t len = n + m;
+        sc = len ? (int32_t)(-(P.go + len * P.ge)) : 0;
+        ei = (int32_t)n; ej = (int32_t)m;
+        if (a.ops && len) {
+          const uint64_t base = a.q_off[k] + a.s_off[k] + k;
+          a.ops[base] = ((uint32_t)len << 4) | (n ? 1u : 2u);
+          a.n_ops[k] = 1;
+        } else if (a.ops) {
+          a.n_ops[k] = 0;
+        }
+      } else if (a.ops) {
+        a.n_ops[k] = 0;
+      }
+      a.scores[k] = sc;
+      if (a.end_i) { a.end_i[k] = ei; a.end_j[k] = ej; }
+      if (a.beg_i) { a.beg_i[k] = 0; a.beg_j[k] = 0; }
+      a.keys[k] = ~0ull;
+      a.vals[k] = (int32_t)k;
+      continue;
+    }
+    const bool hasN = a.flags[k] & 1u;
+    // range guards (reading R11): |all intermediate values| bounded by the all-gap path
+    const int64_t padded = n + 192;  // max strip padding of any variant
+    const int64_t neg = 3 * (int64_t)a.cfg.bound_go + (padded + m + 2) * (int64_t)a.cfg.bound_ge + 256;
+    const int64_t posb = (int64_t)max(a.cfg.bound_match, 0) * (padded < m ? padded : m);
+    const bool ok16 = a.cfg.allow16 && !hasN && neg <= 16000 && posb <= 16000;
+    const bool ok32 = neg <= (1ll << 30) - (1ll << 24) && posb <= (1ll << 30) - (1ll << 24);
+    if (!ok32) atomicExch(&a.sum->range_err, 1);
+    int v = -1;
+    if (a.cfg.force_variant >= 0) {
+      v = a.cfg.force_variant;
+      if (variant_desc(v).pairs == 2 && !ok16) v = a.cfg.tb ? 5 : 4;
+    } else {
+      int best_rows = 0x7fffffff, best_R = 0;
+      for (int c = 0; c < NV; ++c) {
+        const VariantDesc d = variant_desc(c);
+        if (d.tb != a.cfg.tb) continue;
+        if (d.pairs == 2 && !ok16) continue;
+        if (d.pairs == 1 && ok16) continue;
+        const int64_t hs = (int64_t)d.L * d.R;
+        const int64_t rows = (n + hs - 1) / hs * hs;
+        if (rows < best_rows || (rows == best_rows && d.R > best_R)) {
+          best_rows = (int)(rows < 0x7fffffff ? rows : 0x7fffffff);
+          best_R = d.R;
+          v = c;
+        }
+      }
+    }
+    const unsigned long long key = ((unsigned long long)v << 58) |
+                                   ((unsigned long long)(m < (1 << 29) - 1 ? m : (1 << 29) - 1) << 29) |
+                                   (unsigned long long)(n < (1 << 29) - 1 ? n : (1 << 29) - 1);
+    a.keys[k] = key;
+    a.vals[k] = (int32_t)k;
+    atomicAdd(&a.sum->count[v], 1);
+    atomicMax(&a.sum->maxn[v], (int32_t)n);
+    atomicMax(&a.sum->maxm[v], (int32_t)m);
+    atomicMin(&a.sum->kmin[v], key);
+    atomicMax(&a.sum->kmax[v], key);
+  }
+}
+
+cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t st, int num_sms) {
+  if (a.num_pairs == 0) return cudaSuccess;
+  const int threads = 256;
+  classify_kernel<<<grid_for((int64_t)a.num_pairs, threads, num_sms), threads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ slots
+struct SlotTables {
+  int32_t voff[NV + 1];
+  int32_t count[NV];
+  int32_t sbase[NV];
+  int32_t pairs[NV];
+};
+
+__global__ void slots_kernel(const int32_t* __restrict__ order, int64_t num, SlotTables T,
+                             Slot* __restrict__ slots) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < num;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int v = -1;
+#pragma unroll
+    for (int c = 0; c < NV; ++c)
+      if (p >= T.voff[c] && p < T.voff[c] + T.count[c]) v = c;
+    if (v < 0) continue;
+    const int64_t local = p - T.voff[v];
+    if (T.pairs[v] == 2) {
+      if (local & 1) continue;
+      Slot s;
+      s.pair[0] = order[p];
+      s.pair[1] = (local + 1 < T.count[v]) ? order[p + 1] : -1;
+      slots[T.sbase[v] + local / 2] = s;
+    } else {
+      Slot s;
+      s.pair[0] = order[p];
+      s.pair[1] = -1;
+      slots[T.sbase[v] + local] = s;
+    }
+  }
+}
+
+cudaError_t launch_slots(const int32_t* d_order, int64_t num, const int32_t* voff_host,
+                         const int32_t* count_host, const int32_t* sbase_host, Slot* d_slots,
+                         cudaStream_t st, int num_sms) {
+  if (num == 0) return cudaSuccess;
+  SlotTables T;
+  for (int c = 0; c < NV; ++c) {
+    T.voff[c] = voff_host[c];
+    T.count[c] = count_host[c];
+    T.sbase[c] = sbase_host[c];
+    T.pairs[c] = variant_desc(c).pairs;
+  }
+  T.voff[NV] = voff_host[NV];
+  slots_kernel<<<grid_for(num, 256, num_sms), 256, 0, st>>>(d_order, num, T, d_slots);
+  return cudaGetLastError();
+}
+
+cudaError_t sort_pairs(void* d_temp, size_t& temp_bytes, const unsigned long long* keys_in,
+                       unsigned long long* keys_out, const int32_t* vals_in, int32_t* vals_out,
+                       int64_t num, cudaStream_t st) {
+  return cub::DeviceRadixSort::SortPairs(d_temp, temp_bytes, keys_in, keys_out, vals_in,
+                                         vals_out, (int)num, 0, 64, st);
+}
+
+struct I32ToU64 {
+  __host__ __device__ uint64_t operator()(int32_t x) const { return (uint64_t)(x < 0 ? 0 : x); }
+};
+
+cudaError_t exclusive_scan_i32_to_u64(void* d_temp, size_t& temp_bytes, const int32_t* in,
+                                      uint64_t* out, int64_t num, cudaStream_t st) {
+  cub::TransformInputIterator<uint64_t, I32ToU64, const int32_t*> it(in, I32ToU64());
+  return cub::DeviceScan::ExclusiveSum(d_temp, temp_bytes, it, out, (int)num, st);
+}
+
+// ------------------------------------------------------------------------------- walk
+__device__ __forceinline__ uint32_t fetch_nib(const uint32_t* __restrict__ dirs, const TbInfo& ti,
+                                              int i, int j) {
+  const int L = ti.L, R = ti.R, HS = L * R;
+  const int ip = i - 1 + ti.pad;
+  const int st = ip / HS, lr = ip - st * HS;
+  const int tt = lr / R, r = lr - tt * R;
+  const int k = (j - 1) + tt;
+  const int S8 = (ti.slot_M + L - 1 + 7) >> 3;
+  const int64_t w = ti.dir_base + ((((int64_t)st * S8 + (k >> 3)) * R + r) * L + tt) * ti.P + ti.half;
+  return (__ldg(dirs + w) >> (4 * (k & 7))) & 15u;
+}
+
+struct RunWriter {
+  uint32_t* out;
+  int n;
+  uint32_t op, len;
+  __device__ void push(uint32_t o, uint32_t l) {
+    if (l == 0) return;
+    if (len && o == op) { len += l; return; }
+    if (len) out[n++] = (len << 4) | op;
+    op = o; len = l;
+  }
+  __device__ void flush() {
+    if (len) out[n++] = (len << 4) | op;
+    len = 0;
+  }
+};
+
+__global__ void walk_kernel(WalkArgs a) {
+  const int64_t total = (int64_t)(a.slot_hi - a.slot_lo) * a.pairs_per_slot;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int slot = a.slot_lo + (int)(w / a.pairs_per_slot);
+    const int half = (int)(w % a.pairs_per_slot);
+    const int pair = a.slots[slot].pair[half];
+    if (pair < 0) continue;
+    const TbInfo ti = a.tb[pair];
+    const uint64_t base = a.q_off[pair] + a.s_off[pair] + (uint64_t)pair;
+    RunWriter rw{a.ops + base, 0, 0, 0};
+    int i = ti.end_i, j = ti.end_j;
+    int state = 0;  // 0 H, 1 E, 2 F
+    const bool linear = a.gap == GLINEAR;
+    for (;;) {
+      if (state == 0) {
+        if (i == 0 || j == 0) {
+          if (a.kind == KGLOBAL) {  // reading R16: boundary runs
+            rw.push(1u, (uint32_t)i);
+            rw.push(2u, (uint32_t)j);
+            i = 0; j = 0;
+          }
+          break;
+        }
+        const uint32_t src = fetch_nib(a.dirs, ti, i, j) & 3u;
+        if (src == 3u) break;             // STOP (local, H <= 0, reading R9)
+        if (src == 0u) { rw.push(0u, 1); --i; --j; }
+        else state = (src == 1u) ? 1 : 2;
+      } else if (state == 1) {
+        const uint32_t ext = (fetch_nib(a.dirs, ti, i, j) >> 2) & 1u;
+        rw.push(1u, 1);
+        --i;
+        if (!ext || linear || i == 0) state = 0;
+      } else {
+        const uint32_t ext = (fetch_nib(a.dirs, ti, i, j) >> 3) & 1u;
+        rw.push(2u, 1);
+        --j;
+        if (!ext || linear || j == 0) state = 0;
+      }
+    }
+    rw.flush();
+    a.n_ops[pair] = rw.n;
+    a.beg_i[pair] = i;
+    a.beg_j[pair] = j;
+  }
+}
+
+cudaError_t launch_walk(const WalkArgs& a, cudaStream_t st, int num_sms) {
+  const int64_t total = (int64_t)(a.slot_hi - a.slot_lo) * a.pairs_per_slot;
+  if (total <= 0) return cudaSuccess;
+  walk_kernel<<<grid_for(total, 128, num_sms, 16), 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------- finalize
+__global__ void finalize_kernel(FinalizeArgs a) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.num_pairs;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    anyseq_alignment o;
+    o.score = a.scores[k];
+    o.reserved = 0;
+    o.q_end = a.end_i ? a.end_i[k] : 0;
+    o.s_end = a.end_j ? a.end_j[k] : 0;
+    o.q_begin = a.beg_i ? a.beg_i[k] : o.q_end;
+    o.s_begin = a.beg_j ? a.beg_j[k] : o.s_end;
+    o.cigar_offset = 0;
+    o.cigar_len = 0;
+    o.reserved2 = 0;
+    if (a.n_ops) {
+      const int nops = a.n_ops[k];
+      const uint64_t off = a.cig_off[k];
+      o.cigar_offset = off;
+      o.cigar_len = (uint32_t)nops;
+      if (a.cigar && off + nops <= a.cigar_cap) {
+        const uint32_t* src = a.ops + a.q_off[k] + a.s_off[k] + k;
+        for (int r = 0; r < nops; ++r) a.cigar[off + r] = src[nops - 1 - r];  // reverse runs
+      }
+    }
+    reinterpret_cast<anyseq_alignment*>(a.out_aln)[k] = o;
+  }
+}
+
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st, int num_sms) {
+  if (a.num_pairs == 0) return cudaSuccess;
+  finalize_kernel<<<grid_for((int64_t)a.num_pairs, 256, num_sms), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace anyseq

@@ -1,0 +1,90 @@
+// csrc/kernels.h -- host-callable launchers of the device kernels (internal interface).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "common.cuh"
+#include "plan.cuh"
+#include "fill_args.h"
+
+namespace anyseq {
+
+// a1: ASCII -> byte codes (A,C,G,T -> 0..3, N -> 4), validation, per-pair N flags.
+cudaError_t launch_pack(const char* d_ascii, uint64_t len, uint8_t* d_code, uint64_t pos_base,
+                        const uint64_t* d_off, uint64_t num_pairs, uint32_t* d_flags,
+                        PlanSummary* d_sum, cudaStream_t st, int num_sms);
+
+struct ClassifyArgs {
+  DevParams P;
+  PlanCfg cfg;
+  const uint64_t* q_off;
+  const uint64_t* s_off;
+  uint64_t num_pairs;
+  const uint32_t* flags;
+  PlanSummary* sum;
+  unsigned long long* keys;  // [num_pairs]
+  int32_t* vals;             // [num_pairs]
+  int32_t* scores;           // trivial pairs are finished here
+  int32_t* end_i;
+  int32_t* end_j;
+  // traceback mode bookkeeping for trivial pairs
+  uint32_t* ops;             // per-pair run region base q_off+s_off+k
+  int32_t* n_ops;
+  int32_t* beg_i;
+  int32_t* beg_j;
+};
+// a2: plan -- variant choice, range guard, sort keys; finishes empty pairs.
+cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t st, int num_sms);
+
+// a2: slot formation from the (sorted) order
+cudaError_t launch_slots(const int32_t* d_order, int64_t num, const int32_t* voff_host,
+                         const int32_t* count_host, const int32_t* sbase_host, Slot* d_slots,
+                         cudaStream_t st, int num_sms);
+
+// radix sort (cub) of (key, pair) -- temp storage managed by the caller
+cudaError_t sort_pairs(void* d_temp, size_t& temp_bytes, const unsigned long long* keys_in,
+                       unsigned long long* keys_out, const int32_t* vals_in, int32_t* vals_out,
+                       int64_t num, cudaStream_t st);
+cudaError_t exclusive_scan_i32_to_u64(void* d_temp, size_t& temp_bytes, const int32_t* in,
+                                      uint64_t* out, int64_t num, cudaStream_t st);
+
+// a3/a4: fill (template dispatch)
+cudaError_t launch_fill(int variant, int kind, int gap, const FillArgs& a, cudaStream_t st,
+                        int num_sms, int* grid_out);
+
+// a5: traceback walk of one chunk of slots of a variant
+struct WalkArgs {
+  int32_t kind, gap;
+  const Slot* slots;
+  int32_t slot_lo, slot_hi;
+  int32_t pairs_per_slot;
+  const TbInfo* tb;
+  const uint32_t* dirs;
+  const uint64_t* q_off;
+  const uint64_t* s_off;
+  uint32_t* ops;   // per-pair run region (reversed run order)
+  int32_t* n_ops;
+  int32_t* beg_i;
+  int32_t* beg_j;
+};
+cudaError_t launch_walk(const WalkArgs& a, cudaStream_t st, int num_sms);
+
+// output assembly (anyseq_alignment layout, see include/anyseq.h)
+struct FinalizeArgs {
+  uint64_t num_pairs;
+  const int32_t* scores;
+  const int32_t* end_i;
+  const int32_t* end_j;
+  const int32_t* beg_i;   // null => begin = end
+  const int32_t* beg_j;
+  const int32_t* n_ops;   // null => no cigar
+  const uint64_t* cig_off;
+  const uint64_t* q_off;
+  const uint64_t* s_off;
+  const uint32_t* ops;
+  void* out_aln;          // anyseq_alignment[num_pairs]
+  uint32_t* cigar;        // compacted cigar (may be null)
+  uint64_t cigar_cap;
+};
+cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st, int num_sms);
+
+}  // namespace anyseq

@@ -1,0 +1,558 @@
+// csrc/long.cu -- long-pair score-only alignment: persistent tiled wavefront.
+//
+// Paper: tiles relaxed along anti-diagonals, borders handed to the right/below neighbours
+// (Fig. 2), GPU tiles split into stripes whose last row is kept and
+// reused (Fig. 4 caption P:531-537), dynamic scheduling of ready tiles
+// (P:492).
+//
+// B200 design: the matrix is cut into row strips of 32*R rows
+// (one warp: lane t owns R rows, anti-diagonal wavefront across lanes as in the batch
+// kernel) and G column strips.  Warps take tasks (row strip s, column strip g) in ticket
+// order (s-major), so every task waits only on lower tickets held by resident warps:
+// deadlock-free.  Handoffs:
+//   * row strip s -> s+1 (same column strip): an O(m) in-place row buffer (H,E) in global
+//     memory (L2-resident for 5 Mbp) plus a per-task progress counter published every
+//     `chunk` columns with st.release.gpu and polled with ld.acquire.gpu;
+//   * column strip g -> g+1: the right-edge column (H,F) for all rows of the task plus a
+//     per-(edge, row strip) flag published with a system-scope fence, so the same code
+//     runs with the consumer on another GPU (peer pointer over NVLink) or on the same GPU
+//     ("virtual strips" -- the multi-GPU protocol exercised on one device).
+// Every spin-wait is bounded and raises an abort flag (-> ANYSEQ_E_TIMEOUT).
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include "../../include/anyseq.h"
+#include "kernels.h"
+#include "long.h"
+
+namespace anyseq {
+
+struct LongPart {
+  int32_t lv, li, lj;  // local best (value, i, j)
+  int32_t rv, rj;      // semi: best on row n, j in [0, m-1]
+  int32_t cv, ci;      // semi: best on column m, i in [0, n]
+  int32_t gv, gset;    // global H(n,m)
+  int32_t pad_;
+};
+
+struct LongArgs {
+  DevParams P;
+  const uint8_t* qc;
+  const uint8_t* sc;
+  int32_t n, m;
+  int32_t Gtot, g_first, g_count;
+  const int32_t* cb;  // [Gtot+1]
+  int32_t S;
+  int32_t* ticket;
+  int32_t* rowprog;   // [Gtot * S]
+  int32_t* const* bflag;  // [Gtot+1] per-edge flag arrays of S ints (on the consumer)
+  int2* const* bcol;  // [Gtot+1] column buffers: (H(i, cb[g]), F(i, cb[g])), i = 0..n
+  int2* rowbuf;       // [m+1]: (H, E) of the last completed row at column j
+  LongPart* parts;
+  int32_t* abort_flag;
+  int32_t chunk;
+  long long spin_limit;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ bool lkey_better(int v, int i, int j, int bv, int bi, int bj) {
+  return v > bv || (v == bv && (j < bj || (j == bj && i < bi)));
+}
+
+// lane 0 waits until *p >= need (acquire); returns false on timeout/abort (warp-uniform)
+template <bool SYS>
+__device__ __forceinline__ bool warp_wait(const int* p, int need, const LongArgs& a) {
+  int ok = 1;
+  if ((threadIdx.x & 31) == 0) {
+    long long spins = 0;
+    while ((SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p)) < need) {
+      if (++spins > a.spin_limit || *(volatile int*)a.abort_flag) {
+        atomicExch(a.abort_flag, 1);
+        ok = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
+template <int KIND, int GAP, int R>
+__global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
+  typedef VS32 V;
+  constexpr int L = 32;
+  constexpr int HS = L * R;
+  const int t = threadIdx.x & 31;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const DevParams P = a.P;
+  const int NEG = NEG32;
+  const int NGE = -P.ge;
+  const int NOC = (GAP == GAFFINE) ? -(P.go + P.ge) : -P.ge;
+  const int n = a.n, m = a.m;
+  // semi/global: where row n lives inside the last row strip
+  const int tn = ((n - 1) % HS) / R, rn = (n - 1) % R;
+
+  LongPart part;
+  part.lv = 0; part.li = 0; part.lj = 0;
+  part.rv = 0; part.rj = 0;  // (n, 0) = 0 is the first semi-global candidate
+  part.cv = 0; part.ci = 0;  // (0, m) = 0
+  part.gv = 0; part.gset = 0; part.pad_ = 0;
+
+  for (;;) {
+    int task = 0;
+    if (t == 0) task = atomicAdd(a.ticket, 1);
+    task = __shfl_sync(0xffffffffu, task, 0);
+    if (task >= a.S * a.g_count) break;
+    if (*(volatile int*)a.abort_flag) break;
+    const int s = task / a.g_count;
+    const int g = a.g_first + task % a.g_count;
+    const int c_lo = a.cb[g], c_hi = a.cb[g + 1], W = c_hi - c_lo;
+    const bool last_strip = (s == a.S - 1), last_col = (c_hi == m);
+    const int ip0 = s * HS + t * R;
+    const int2* bl = a.bcol[g];
+    int2* br = (g + 1 < a.Gtot) ? a.bcol[g + 1] : nullptr;
+
+    if (g > 0) {  // left boundary of this row strip (and the previous one: diag of row 0)
+      if (!warp_wait<true>(&a.bflag[g][s], 1, a)) break;
+      if (s > 0 && !warp_wait<true>(&a.bflag[g][s - 1], 1, a)) break;
+    }
+    uint32_t p0[R], p1[R];
+    int Hh[R], Ho[R], Ff[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int ip = ip0 + r;
+      const bool real = ip < n;
+      const uint32_t c = real ? a.qc[ip] : 0u;
+      p0[r] = real ? prof4(P, c) : 0u;
+      p1[r] = real ? P.mism4 : 0u;
+      int2 b = make_int2(0, NEG);
+      if (real) b = bl[ip + 1];
+      Hh[r] = b.x;
+      Ff[r] = b.y;
+      Ho[r] = Hh[r] + NOC;
+    }
+    int diag = (ip0 <= n) ? bl[ip0].x : 0;
+    int Hbot = NEG, Ebot = NEG;
+    uint32_t selb = 0;
+    int sv = 0, si = 0, sj = 0;  // local per task
+    bool aborted = false;
+
+    const int K = W + L - 1;
+    for (int k = 0; k < K; ++k) {
+      if (s > 0 && k < W && (k % a.chunk) == 0) {
+        if (!warp_wait<false>(&a.rowprog[g * a.S + s - 1], min(W, k + a.chunk), a)) {
+          aborted = true;
+          break;
+        }
+      }
+      int hin = V::shfl_up(Hbot, L);
+      int ein = (GAP == GAFFINE) ? V::shfl_up(Ebot, L) : NEG;
+      uint32_t sel = __shfl_up_sync(0xffffffffu, selb, 1, L);
+      const int lc = k - t;
+      const bool act = lc >= 0 && lc < W;
+      if (t == 0 && act) {
+        const int2 v = a.rowbuf[c_lo + lc + 1];
+        hin = v.x;
+        ein = v.y;
+        sel = V::selector(a.sc[c_lo + lc], 0);
+      }
+      if (act) {
+        int hup = hin + NOC;
+        int e = ein;
+        int hd = diag;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int sig = V::sigma(p0[r], p1[r], sel);
+          int tm;
+          if (GAP == GAFFINE) {
+            e = V::addmax(e, NGE, hup);
+            Ff[r] = V::addmax(Ff[r], NGE, Ho[r]);
+            tm = max(e, Ff[r]);
+          } else {
+            tm = max(hup, Ho[r]);
+          }
+          const int h = (KIND == KLOCAL) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
+          hd = Hh[r];
+          Hh[r] = h;
+          Ho[r] = h + NOC;
+          hup = Ho[r];
+        }
+        diag = hin;
+        Hbot = Hh[R - 1];
+        Ebot = e;
+        selb = sel;
+        if (t == L - 1) {
+          a.rowbuf[c_lo + lc + 1] = make_int2(Hh[R - 1], e);
+          if ((lc % a.chunk) == a.chunk - 1 || lc == W - 1) st_release_gpu(&a.rowprog[g * a.S + s], lc + 1);
+        }
+        const int j = c_lo + lc + 1;  // real column
+        if (KIND == KLOCAL) {
+          int cm = 0;
+          if (!last_strip) {
+            cm = Hh[0];
+#pragma unroll
+            for (int r = 1; r + 1 < R; r += 2) cm = V::vmax3(cm, Hh[r], Hh[r + 1]);
+            if ((R % 2) == 0) cm = max(cm, Hh[R - 1]);
+          } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (ip0 + r < n) cm = max(cm, Hh[r]);
+          }
+          if (cm > sv) {
+            int rr = R - 1;
+#pragma unroll
+            for (int r = R - 1; r >= 0; --r)
+              if (Hh[r] == cm && ip0 + r < n) rr = r;
+            sv = cm;
+            si = ip0 + rr + 1;
+            sj = j;
+          }
+        } else if (KIND == KSEMI) {
+          if (last_strip && t == tn && j <= m - 1) {
+            int v = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (r == rn) v = Hh[r];
+            if (v > part.rv || (v == part.rv && j < part.rj)) { part.rv = v; part.rj = j; }
+          }
+          if (last_col && lc == W - 1) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int i = ip0 + r + 1;
+              if (i <= n && (Hh[r] > part.cv || (Hh[r] == part.cv && i < part.ci))) {
+                part.cv = Hh[r];
+                part.ci = i;
+              }
+            }
+          }
+        } else {
+          if (last_strip && last_col && lc == W - 1 && t == tn) {
+            int v = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (r == rn) v = Hh[r];
+            part.gv = v;
+            part.gset = 1;
+          }
+        }
+        if (br && lc == W - 1) {
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (ip0 + r < n) br[ip0 + r + 1] = make_int2(Hh[r], Ff[r]);
+        }
+      }
+    }
+    if (aborted) break;
+    if (KIND == KLOCAL && lkey_better(sv, si, sj, part.lv, part.li, part.lj)) {
+      part.lv = sv; part.li = si; part.lj = sj;
+    }
+    if (br) {
+      __syncwarp();
+      if (t == 0) {
+        __threadfence_system();
+        st_release_sys(&a.bflag[g + 1][s], 1);
+      }
+    }
+  }
+  // reduce the warp's lanes (keys per reading R10 / R5) and publish
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int lv = __shfl_xor_sync(0xffffffffu, part.lv, o);
+    const int li = __shfl_xor_sync(0xffffffffu, part.li, o);
+    const int lj = __shfl_xor_sync(0xffffffffu, part.lj, o);
+    if (lkey_better(lv, li, lj, part.lv, part.li, part.lj)) { part.lv = lv; part.li = li; part.lj = lj; }
+    const int rv = __shfl_xor_sync(0xffffffffu, part.rv, o);
+    const int rj = __shfl_xor_sync(0xffffffffu, part.rj, o);
+    if (rv > part.rv || (rv == part.rv && rj < part.rj)) { part.rv = rv; part.rj = rj; }
+    const int cv = __shfl_xor_sync(0xffffffffu, part.cv, o);
+    const int ci = __shfl_xor_sync(0xffffffffu, part.ci, o);
+    if (cv > part.cv || (cv == part.cv && ci < part.ci)) { part.cv = cv; part.ci = ci; }
+    const int gv = __shfl_xor_sync(0xffffffffu, part.gv, o);
+    const int gs = __shfl_xor_sync(0xffffffffu, part.gset, o);
+    if (gs && !part.gset) { part.gv = gv; part.gset = 1; }
+  }
+  if (t == 0) a.parts[wg] = part;
+}
+
+__global__ void long_init_kernel(DevParams P, int n, int m, int2* rowbuf, int2* bcol0,
+                                 int2* const* bcol, const int* cb, int Gtot, int g_first,
+                                 int g_count) {
+  const int NEG = NEG32;
+  const bool glob = P.kind == KGLOBAL;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= (int64_t)max(n, m);
+       x += (int64_t)gridDim.x * blockDim.x) {
+    if (x <= m) rowbuf[x] = make_int2(glob && x > 0 ? -(P.go + (int)x * P.ge) : 0, NEG);  // H(0,j), E(0,j)
+    if (bcol0 && x <= n) bcol0[x] = make_int2(glob && x > 0 ? -(P.go + (int)x * P.ge) : 0, NEG);  // H(i,0), F(i,0)
+    if (x == 0) {
+      for (int g = g_first; g < g_first + g_count; ++g) {
+        if (g == 0) continue;
+        const int c = cb[g];
+        bcol[g][0] = make_int2(glob ? -(P.go + c * P.ge) : 0, NEG);  // H(0, c_g)
+      }
+    }
+  }
+}
+
+typedef void (*LongFn)(LongArgs);
+
+template <int R>
+static LongFn long_fn(int kind, int gap) {
+  if (kind == KGLOBAL) return gap ? long_kernel<KGLOBAL, GAFFINE, R> : long_kernel<KGLOBAL, GLINEAR, R>;
+  if (kind == KLOCAL) return gap ? long_kernel<KLOCAL, GAFFINE, R> : long_kernel<KLOCAL, GLINEAR, R>;
+  return gap ? long_kernel<KSEMI, GAFFINE, R> : long_kernel<KSEMI, GLINEAR, R>;
+}
+
+namespace {
+struct Buf {
+  void* p = nullptr;
+  ~Buf() { if (p) cudaFree(p); }
+};
+#define LK(call)                                                      \
+  do {                                                                \
+    cudaError_t e_ = (call);                                          \
+    if (e_ != cudaSuccess) {                                          \
+      *err = std::string(#call) + ": " + cudaGetErrorString(e_);      \
+      return e_ == cudaErrorMemoryAllocation ? ANYSEQ_E_NOMEM : ANYSEQ_E_CUDA; \
+    }                                                                 \
+  } while (0)
+}  // namespace
+
+int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, uint64_t n,
+             const char* s, uint64_t m, const LongOptions& opt, LongResult* out, std::string* err,
+             uint64_t* launches) {
+  out->kernel_ms = 0;
+  if (n == 0 || m == 0) {  // empty sequences: one gap run (global) or the empty alignment
+    const int64_t len = (int64_t)(n + m);
+    out->score = (P.kind == KGLOBAL && len) ? (int32_t)(-(P.go + len * P.ge)) : 0;
+    out->end_i = P.kind == KGLOBAL ? (int64_t)n : 0;
+    out->end_j = P.kind == KGLOBAL ? (int64_t)m : 0;
+    return 0;
+  }
+  {  // 32-bit range guard (reading R11)
+    const long double neg = 3.0L * P.go + ((long double)n + m + 2) * P.ge + 256;
+    const long double pos = (long double)std::max(P.match, 0) * std::min(n, m);
+    if (neg > (1u << 30) - (1u << 24) || pos > (1u << 30) - (1u << 24)) {
+      *err = "score range exceeds 32-bit arithmetic";
+      return ANYSEQ_E_UNSUPPORTED;
+    }
+  }
+  const int ND = (int)devs.size();
+  int Gtot = ND > 1 ? ND : std::max(1, opt.virtual_strips);
+  Gtot = (int)std::min<uint64_t>(Gtot, m);
+  constexpr int R = 16;
+  const int HS = 32 * R;
+  const int S = (int)((n + HS - 1) / HS);
+  std::vector<int32_t> cb(Gtot + 1);
+  for (int g = 0; g <= Gtot; ++g) cb[g] = (int32_t)((m * (uint64_t)g) / Gtot);
+  const int chunk = std::max(8, opt.chunk_cols);
+  LongFn fn = long_fn<R>(P.kind, P.gap);
+
+  struct PerDev {
+    Buf qa, sa, qc, sc, rowbuf, bcol_own, prog, flags, ticket, abort_, parts, cbuf, bptr, fptr, sum, flg;
+    int g_first = 0, g_count = 0, grid = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+  };
+  std::vector<PerDev> pd(ND);
+  std::vector<int2*> bcol_ptr(Gtot + 1, nullptr);  // edge g buffer lives on its consumer device
+  std::vector<int32_t*> flag_ptr(Gtot + 1, nullptr);
+  // column strips per device
+  for (int d = 0; d < ND; ++d) {
+    pd[d].g_first = ND > 1 ? d : 0;
+    pd[d].g_count = ND > 1 ? (d < Gtot ? 1 : 0) : Gtot;
+  }
+  // peer access between neighbours
+  if (ND > 1) {
+    for (int d = 0; d + 1 < ND; ++d) {
+      int ok = 0;
+      LK(cudaDeviceCanAccessPeer(&ok, devs[d].id, devs[d + 1].id));
+      if (!ok) {
+        *err = "peer access unavailable between devices " + std::to_string(devs[d].id) + " and " +
+               std::to_string(devs[d + 1].id);
+        return ANYSEQ_E_PEER;
+      }
+      cudaSetDevice(devs[d].id);
+      cudaError_t e = cudaDeviceEnablePeerAccess(devs[d + 1].id, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) LK(e);
+      cudaGetLastError();
+    }
+  }
+  // allocation + upload + pack
+  for (int d = 0; d < ND; ++d) {
+    PerDev& D = pd[d];
+    LK(cudaSetDevice(devs[d].id));
+    cudaStream_t st = devs[d].stream;
+    LK(cudaMalloc(&D.qa.p, n + 16));
+    LK(cudaMalloc(&D.sa.p, m + 16));
+    LK(cudaMalloc(&D.qc.p, n + 16));
+    LK(cudaMalloc(&D.sc.p, m + 16));
+    LK(cudaMalloc(&D.sum.p, sizeof(PlanSummary)));
+    LK(cudaMalloc(&D.flg.p, 16));
+    LK(cudaMemcpyAsync(D.qa.p, q, n, cudaMemcpyHostToDevice, st));
+    LK(cudaMemcpyAsync(D.sa.p, s, m, cudaMemcpyHostToDevice, st));
+    PlanSummary hs;
+    memset(&hs, 0, sizeof(hs));
+    hs.err_pos = ~0ull;
+    LK(cudaMemcpyAsync(D.sum.p, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+    LK(cudaStreamSynchronize(st));
+    uint64_t offs[2] = {0, 0};
+    Buf off;
+    LK(cudaMalloc(&off.p, 16));
+    offs[1] = n;
+    LK(cudaMemcpy(off.p, offs, 16, cudaMemcpyHostToDevice));
+    LK(launch_pack((const char*)D.qa.p, n, (uint8_t*)D.qc.p, 0, (const uint64_t*)off.p, 1,
+                   (uint32_t*)D.flg.p, (PlanSummary*)D.sum.p, st, devs[d].num_sms));
+    offs[1] = m;
+    Buf off2;
+    LK(cudaMalloc(&off2.p, 16));
+    LK(cudaMemcpy(off2.p, offs, 16, cudaMemcpyHostToDevice));
+    LK(launch_pack((const char*)D.sa.p, m, (uint8_t*)D.sc.p, 1ull << 62, (const uint64_t*)off2.p, 1,
+                   (uint32_t*)D.flg.p, (PlanSummary*)D.sum.p, st, devs[d].num_sms));
+    *launches += 2;
+    LK(cudaMemcpyAsync(&hs, D.sum.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    LK(cudaStreamSynchronize(st));
+    if (hs.err_pos != ~0ull) {
+      const bool in_s = hs.err_pos >= (1ull << 62);
+      *err = std::string("invalid symbol at ") + (in_s ? "s" : "q") + " offset " +
+             std::to_string(in_s ? hs.err_pos - (1ull << 62) : hs.err_pos);
+      return ANYSEQ_E_BADSEQ;
+    }
+    LK(cudaMalloc(&D.rowbuf.p, (m + 1) * sizeof(int2)));
+    LK(cudaMalloc(&D.prog.p, (size_t)Gtot * S * 4));
+    LK(cudaMalloc(&D.ticket.p, 4));
+    LK(cudaMalloc(&D.abort_.p, 4));
+    LK(cudaMalloc(&D.cbuf.p, (Gtot + 1) * 4));
+    LK(cudaMalloc(&D.bptr.p, (Gtot + 1) * sizeof(int2*)));
+    LK(cudaMalloc(&D.fptr.p, (Gtot + 1) * sizeof(int32_t*)));
+    LK(cudaMemsetAsync(D.prog.p, 0, (size_t)Gtot * S * 4, st));
+    LK(cudaMemsetAsync(D.ticket.p, 0, 4, st));
+    LK(cudaMemsetAsync(D.abort_.p, 0, 4, st));
+    LK(cudaMemcpyAsync(D.cbuf.p, cb.data(), (Gtot + 1) * 4, cudaMemcpyHostToDevice, st));
+    // column buffers consumed on this device: edges g_first .. g_first+g_count-1 (edge 0 = init)
+    if (D.g_count > 0) {
+      const size_t bytes = (size_t)D.g_count * (n + 1) * sizeof(int2);
+      LK(cudaMalloc(&D.bcol_own.p, bytes));
+      for (int k = 0; k < D.g_count; ++k)
+        bcol_ptr[D.g_first + k] = (int2*)D.bcol_own.p + (size_t)k * (n + 1);
+      LK(cudaMalloc(&D.flags.p, (size_t)D.g_count * S * 4));
+      LK(cudaMemsetAsync(D.flags.p, 0, (size_t)D.g_count * S * 4, st));
+      for (int k = 0; k < D.g_count; ++k) flag_ptr[D.g_first + k] = (int32_t*)D.flags.p + (size_t)k * S;
+    }
+    int nb = 0;
+    LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0));
+    D.grid = devs[d].num_sms * std::max(nb, 1);
+    if (opt.blocks > 0) D.grid = std::min(D.grid, opt.blocks);
+    LK(cudaMalloc(&D.parts.p, (size_t)D.grid * 4 * sizeof(LongPart)));
+  }
+  // In multi-GPU mode edge g (g >= 1) is produced on device g-1 and consumed on device g;
+  // flags of edge g live on the consumer as well (producer stores over NVLink).
+  for (int d = 0; d < ND; ++d) {
+    PerDev& D = pd[d];
+    LK(cudaSetDevice(devs[d].id));
+    LK(cudaMemcpyAsync(D.bptr.p, bcol_ptr.data(), (Gtot + 1) * sizeof(int2*), cudaMemcpyHostToDevice,
+                       devs[d].stream));
+    LK(cudaMemcpyAsync(D.fptr.p, flag_ptr.data(), (Gtot + 1) * sizeof(int32_t*), cudaMemcpyHostToDevice,
+                       devs[d].stream));
+    long_init_kernel<<<devs[d].num_sms * 4, 256, 0, devs[d].stream>>>(
+        P, (int)n, (int)m, (int2*)D.rowbuf.p, D.g_first == 0 && D.g_count > 0 ? bcol_ptr[0] : nullptr,
+        (int2* const*)D.bptr.p, (const int*)D.cbuf.p, Gtot, D.g_first, D.g_count);
+    LK(cudaGetLastError());
+    *launches += 1;
+    LK(cudaStreamSynchronize(devs[d].stream));
+  }
+  // launch (all devices concurrently; their kernels wait on each other only via flags)
+  for (int d = 0; d < ND; ++d) {
+    PerDev& D = pd[d];
+    if (D.g_count == 0) continue;
+    LK(cudaSetDevice(devs[d].id));
+    LongArgs a;
+    a.P = P;
+    a.qc = (const uint8_t*)D.qc.p;
+    a.sc = (const uint8_t*)D.sc.p;
+    a.n = (int)n;
+    a.m = (int)m;
+    a.Gtot = Gtot;
+    a.g_first = D.g_first;
+    a.g_count = D.g_count;
+    a.cb = (const int32_t*)D.cbuf.p;
+    a.S = S;
+    a.ticket = (int32_t*)D.ticket.p;
+    a.rowprog = (int32_t*)D.prog.p;
+    a.bflag = (int32_t* const*)D.fptr.p;  // edge g flags live on the consumer of edge g
+    a.bcol = (int2* const*)D.bptr.p;
+    a.rowbuf = (int2*)D.rowbuf.p;
+    a.parts = (LongPart*)D.parts.p;
+    a.abort_flag = (int32_t*)D.abort_.p;
+    a.chunk = chunk;
+    a.spin_limit = 1ll << 26;
+    LK(cudaEventCreate(&D.e0));
+    LK(cudaEventCreate(&D.e1));
+    LK(cudaEventRecord(D.e0, devs[d].stream));
+    fn<<<D.grid, 128, 0, devs[d].stream>>>(a);
+    LK(cudaGetLastError());
+    LK(cudaEventRecord(D.e1, devs[d].stream));
+    *launches += 1;
+  }
+  // gather
+  bool have_g = false;
+  LongPart best;
+  memset(&best, 0, sizeof(best));
+  int32_t lv = 0, li = 0, lj = 0, rv = 0, rj = 0, cv = 0, ci = 0, gv = 0;
+  int aborted = 0;
+  for (int d = 0; d < ND; ++d) {
+    PerDev& D = pd[d];
+    if (D.g_count == 0) continue;
+    LK(cudaSetDevice(devs[d].id));
+    LK(cudaStreamSynchronize(devs[d].stream));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, D.e0, D.e1);
+    out->kernel_ms = std::max(out->kernel_ms, (double)ms);
+    cudaEventDestroy(D.e0);
+    cudaEventDestroy(D.e1);
+    int ab = 0;
+    LK(cudaMemcpy(&ab, D.abort_.p, 4, cudaMemcpyDeviceToHost));
+    aborted |= ab;
+    std::vector<LongPart> parts((size_t)D.grid * 4);
+    LK(cudaMemcpy(parts.data(), D.parts.p, parts.size() * sizeof(LongPart), cudaMemcpyDeviceToHost));
+    for (const LongPart& p : parts) {
+      if (p.lv > lv || (p.lv == lv && (p.lj < lj || (p.lj == lj && p.li < li)))) { lv = p.lv; li = p.li; lj = p.lj; }
+      if (p.rv > rv || (p.rv == rv && p.rj < rj)) { rv = p.rv; rj = p.rj; }
+      if (p.cv > cv || (p.cv == cv && p.ci < ci)) { cv = p.cv; ci = p.ci; }
+      if (p.gset) { gv = p.gv; have_g = true; }
+    }
+  }
+  if (aborted) {
+    *err = "long kernel: a boundary wait exceeded its bound";
+    return ANYSEQ_E_TIMEOUT;
+  }
+  if (P.kind == KLOCAL) {
+    out->score = lv; out->end_i = li; out->end_j = lj;
+  } else if (P.kind == KSEMI) {
+    if (rv >= cv) { out->score = rv; out->end_i = (int64_t)n; out->end_j = rj; }
+    else { out->score = cv; out->end_i = ci; out->end_j = (int64_t)m; }
+  } else {
+    if (!have_g) {
+      *err = "long kernel: global end cell not produced";
+      return ANYSEQ_E_CUDA;
+    }
+    out->score = gv; out->end_i = (int64_t)n; out->end_j = (int64_t)m;
+  }
+  return 0;
+}
+
+}  // namespace anyseq

@@ -1,0 +1,35 @@
+// csrc/long.h -- long-pair (genome x genome) score-only driver (internal interface).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+#include "common.cuh"
+
+namespace anyseq {
+
+struct LongOptions {
+  int band_rows = 0;       // 0 = default (rows per warp task = 32 * R)
+  int blocks = 0;          // 0 = occupancy-derived persistent grid
+  int virtual_strips = 1;  // column strips on one device (tests the multi-GPU protocol)
+  int chunk_cols = 64;     // progress publication granularity
+};
+
+struct LongDevice {
+  int id;
+  cudaStream_t stream;
+  int num_sms;
+};
+
+struct LongResult {
+  int32_t score;
+  int64_t end_i, end_j;
+  double kernel_ms;
+};
+
+// Returns 0 or an anyseq_status code; err receives a message.
+int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, uint64_t n,
+             const char* s, uint64_t m, const LongOptions& opt, LongResult* out, std::string* err,
+             uint64_t* launches);
+
+}  // namespace anyseq

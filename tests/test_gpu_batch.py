@@ -1,0 +1,262 @@
+"""GPU parity of the batch path (score-only, end cells, traceback) against the CPU oracle.
+
+Every comparison is element by element and bit-exact (integers): score, end cell, begin
+cell and CIGAR.  Inputs are seeded synthetic DNA (synth/), with lengths spanning several
+strips of every kernel variant and ragged tails.  All calls go through the C-ABI.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ("global", "local", "semi")
+GAPS = (("linear", 0, 1), ("affine", 5, 1), ("affine", 2, 1), ("affine", 0, 2))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2002_04561_b200 as A
+    c = A.Context([0])
+    yield c
+    c.close()
+
+
+def _oracle(kind, gap, go, ge, q, qo, s, so, tb, ma=2, mi=-1):
+    from oracle import oracle as O
+    res, cig = O.batch(O.Scheme(kind, gap, ma, mi, go, ge), q, qo, s, so, traceback=tb)
+    return res, (O.batch_cigars(res, cig, qo, so) if tb else None)
+
+
+def _check_scores(ctx, sch, q, qo, s, so, res, ends=True):
+    sc, aln = ctx.align_batch(sch, q, qo, s, so, ends=True)
+    bad = np.flatnonzero(sc != res["score"].astype(np.int32))
+    assert len(bad) == 0, f"{sch}: {len(bad)} score mismatches, first pair {bad[:5]}"
+    if ends:
+        bi = np.flatnonzero((aln["q_end"] != res["q_end"]) | (aln["s_end"] != res["s_end"]))
+        assert len(bi) == 0, f"{sch}: end mismatches at {bi[:5]}"
+    # score-only path without ends
+    sc2 = ctx.align_batch(sch, q, qo, s, so)
+    assert np.array_equal(sc2, sc)
+
+
+def _check_tb(ctx, sch, q, qo, s, so, res, ocig):
+    import paper_2002_04561_b200 as A
+    aln, words = ctx.traceback(sch, q, qo, s, so)
+    assert np.array_equal(aln["score"], res["score"].astype(np.int32)), sch
+    for f in ("q_begin", "s_begin", "q_end", "s_end"):
+        bad = np.flatnonzero(aln[f] != res[f])
+        assert len(bad) == 0, f"{sch} {f} mismatch at {bad[:5]}"
+    got = A.cigars_of(aln, words)
+    bad = [k for k in range(len(got)) if got[k] != ocig[k]]
+    assert not bad, f"{sch}: cigar mismatch at pairs {bad[:5]}: {got[bad[0]]} vs {ocig[bad[0]]}"
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("gap", GAPS, ids=lambda g: f"{g[0]}{g[1]}_{g[2]}")
+def test_random_pairs_all_variants(ctx, kind, gap):
+    """Random pairs, lengths 0..330 (several strips of R=8/16/19 variants, ragged tails)."""
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    q, qo, s, so = random_pairs(300, 0, 330, seed=100 * KINDS.index(kind) + GAPS.index(gap))
+    g, go, ge = gap
+    res, ocig = _oracle(kind, g, go, ge, q, qo, s, so, tb=True)
+    sch = A.Scheme(kind, g, 2, -1, go, ge)
+    _check_scores(ctx, sch, q, qo, s, so, res)
+    _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+def test_forced_variants_score(ctx, variant):
+    """Every score variant (s16x2 R=8/16/19, s32 R=8/16) on the same inputs."""
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    q, qo, s, so = random_pairs(200, 1, 420, seed=50 + variant)
+    ctx.set_option("force_variant", variant)
+    try:
+        for kind in KINDS:
+            for g, go, ge in (("linear", 0, 1), ("affine", 5, 1)):
+                res, _ = _oracle(kind, g, go, ge, q, qo, s, so, tb=False)
+                _check_scores(ctx, A.Scheme(kind, g, 2, -1, go, ge), q, qo, s, so, res)
+    finally:
+        ctx.set_option("force_variant", -1)
+
+
+@pytest.mark.parametrize("variant", [5, 6])
+def test_forced_variants_traceback(ctx, variant):
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    q, qo, s, so = random_pairs(150, 0, 300, seed=70 + variant)
+    ctx.set_option("force_variant", variant)
+    try:
+        for kind in KINDS:
+            for g, go, ge in (("linear", 0, 1), ("affine", 5, 1)):
+                res, ocig = _oracle(kind, g, go, ge, q, qo, s, so, tb=True)
+                _check_tb(ctx, A.Scheme(kind, g, 2, -1, go, ge), q, qo, s, so, res, ocig)
+    finally:
+        ctx.set_option("force_variant", -1)
+
+
+def test_scoring_params_sweep(ctx):
+    """Random valid schemes (match 1..5, mismatch -5..0, Go 0..8, Ge 1..4)."""
+    import random
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    rng = random.Random(17)
+    for t in range(12):
+        kind = rng.choice(KINDS)
+        g = rng.choice(["linear", "affine"])
+        ma, mi, go, ge = rng.randint(1, 5), rng.randint(-5, 0), rng.randint(0, 8), rng.randint(1, 4)
+        q, qo, s, so = random_pairs(80, 0, 200, seed=1000 + t)
+        res, ocig = _oracle(kind, g, go, ge, q, qo, s, so, tb=True, ma=ma, mi=mi)
+        sch = A.Scheme(kind, g, ma, mi, go, ge)
+        _check_scores(ctx, sch, q, qo, s, so, res)
+        _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+
+
+def test_N_and_lowercase(ctx):
+    """N mismatches everything (reading R12) -> s32 path; lower case accepted."""
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    q, qo, s, so = random_pairs(120, 0, 180, seed=5, alphabet=b"ACGTNacgtn")
+    for kind in KINDS:
+        res, ocig = _oracle(kind, "affine", 3, 1, q, qo, s, so, tb=True)
+        sch = A.Scheme(kind, "affine", 2, -1, 3, 1)
+        _check_scores(ctx, sch, q, qo, s, so, res)
+        _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+
+
+def test_edge_shapes(ctx):
+    """n or m in {0, 1, 7, 8, 9, 31, 32, 33, 63, 64, 65, 151, 152, 153} against each other."""
+    import paper_2002_04561_b200 as A
+    from synth import csr, iid
+    L = [0, 1, 7, 8, 9, 31, 32, 33, 63, 64, 65, 151, 152, 153]
+    qs, ss = [], []
+    for i, a in enumerate(L):
+        for j, b in enumerate(L):
+            qs.append(iid(a, 3 * i + 1))
+            ss.append(iid(b, 7 * j + 2))
+    q, qo = csr(qs)
+    s, so = csr(ss)
+    for kind in KINDS:
+        for g, go, ge in (("linear", 0, 1), ("affine", 5, 1)):
+            res, ocig = _oracle(kind, g, go, ge, q, qo, s, so, tb=True)
+            sch = A.Scheme(kind, g, 2, -1, go, ge)
+            _check_scores(ctx, sch, q, qo, s, so, res)
+            _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+
+
+def test_golden_pins_on_gpu(ctx):
+    import os
+    import paper_2002_04561_b200 as A
+    from synth import csr
+    rows = []
+    with open(os.path.join(os.path.dirname(__file__), "golden", "pins.tsv")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            rows.append(line.rstrip("\n").split("\t"))
+    for r in rows:
+        qq, ss_, kind, gap, ma, mi, go, ge, score, qb, sb, qe, se, cig, _ = r
+        q, qo = csr([qq.encode()])
+        s, so = csr([ss_.encode()])
+        sch = A.Scheme(kind, gap, int(ma), int(mi), int(go), int(ge))
+        aln, words = ctx.traceback(sch, q, qo, s, so)
+        a = aln[0]
+        assert int(a["score"]) == int(score), r
+        assert (a["q_begin"], a["s_begin"], a["q_end"], a["s_end"]) == \
+            (int(qb), int(sb), int(qe), int(se)), r
+        got = "".join(f"{l}{o}" for l, o in A.decode_cigar(words[a["cigar_offset"]:
+                                                                 a["cigar_offset"] + a["cigar_len"]]))
+        assert (got or "*") == cig, r
+
+
+def test_c1_nw_traceback(ctx):
+    """C1: one 1000 x 1000 pair, global linear (2/-1/-1), score + traceback."""
+    import paper_2002_04561_b200 as A
+    from synth import c1_pair, csr
+    a, b = c1_pair(1)
+    q, qo = csr([a])
+    s, so = csr([b])
+    res, ocig = _oracle("global", "linear", 0, 1, q, qo, s, so, tb=True)
+    _check_tb(ctx, A.Scheme("global", "linear", 2, -1, 0, 1), q, qo, s, so, res, ocig)
+
+
+def test_c2_c3_shape_full_oracle(ctx):
+    """C2/C3 workload shape (150 bp reads vs windows), 20k pairs, full oracle."""
+    import paper_2002_04561_b200 as A
+    from synth import c2_reads, uniform_csr
+    qm, sm = c2_reads(20000, seed=2)
+    q, qo = uniform_csr(qm)
+    s, so = uniform_csr(sm)
+    res, _ = _oracle("semi", "affine", 5, 1, q, qo, s, so, tb=False)
+    _check_scores(ctx, A.Scheme("semi", "affine", 2, -1, 5, 1), q, qo, s, so, res)
+    res, ocig = _oracle("local", "affine", 5, 1, q, qo, s, so, tb=True)
+    _check_tb(ctx, A.Scheme("local", "affine", 2, -1, 5, 1), q, qo, s, so, res, ocig)
+
+
+def test_c2_full_size_sampled(ctx):
+    """C2 at BASELINE size (1M pairs, the launch configuration bench.py times); the oracle
+    checks a fixed sample of 3000 pairs one by one."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    from synth import c2_reads, uniform_csr
+    qm, sm = c2_reads(1_000_000, seed=2)
+    q, qo = uniform_csr(qm)
+    s, so = uniform_csr(sm)
+    sc = ctx.align_batch(A.Scheme("semi", "affine", 2, -1, 5, 1), q, qo, s, so)
+    idx = np.random.default_rng(0).choice(len(sc), 3000, replace=False)
+    sch = O.Scheme("semi", "affine", 2, -1, 5, 1)
+    for k in idx:
+        assert sc[k] == O.align(sch, qm[k].tobytes(), sm[k].tobytes(), traceback=False).score, k
+    # property at any size: semi-global >= 0 and <= 2 * 150
+    assert sc.min() >= 0 and sc.max() <= 300
+
+
+def test_c5_mixed_sample(ctx):
+    """C5 shape (mixed 100..1000 bp), all kinds x modes, 600 pairs."""
+    import paper_2002_04561_b200 as A
+    from synth import c5_mixed
+    q, qo, s, so = c5_mixed(600, seed=5)
+    for kind in KINDS:
+        res, ocig = _oracle(kind, "affine", 5, 1, q, qo, s, so, tb=True)
+        sch = A.Scheme(kind, "affine", 2, -1, 5, 1)
+        _check_scores(ctx, sch, q, qo, s, so, res)
+        _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+
+
+def test_s16_equals_s32_at_scale(ctx):
+    """GPU s16x2 == GPU s32 on the same 200k C2 pairs (invariant of SURVEY 8(c))."""
+    import paper_2002_04561_b200 as A
+    from synth import c2_reads, uniform_csr
+    qm, sm = c2_reads(200_000, seed=9)
+    q, qo = uniform_csr(qm)
+    s, so = uniform_csr(sm)
+    for kind in KINDS:
+        sch = A.Scheme(kind, "affine", 2, -1, 5, 1)
+        a16, e16 = ctx.align_batch(sch, q, qo, s, so, ends=True)
+        ctx.set_option("allow16", 0)
+        try:
+            a32, e32 = ctx.align_batch(sch, q, qo, s, so, ends=True)
+        finally:
+            ctx.set_option("allow16", 1)
+        assert np.array_equal(a16, a32)
+        assert np.array_equal(e16["q_end"], e32["q_end"]) and np.array_equal(e16["s_end"], e32["s_end"])
+
+
+def test_errors(ctx):
+    import paper_2002_04561_b200 as A
+    from synth import csr
+    q, qo = csr([b"ACGT", b"ACXT"])
+    s, so = csr([b"ACGT", b"ACGT"])
+    with pytest.raises(A.AnyseqError) as e:
+        ctx.align_batch(A.Scheme("global"), q, qo, s, so)
+    assert e.value.status_name == "E_BADSEQ"
+    assert "pair 1" in str(e.value) and "0x58" in str(e.value)
+    with pytest.raises(A.AnyseqError) as e:
+        ctx.align_batch(A.Scheme("global", "affine", 2, -1, -1, 1), q[:4], qo[:2], s[:4], so[:2])
+    assert e.value.status_name == "E_INVALID"
+    q, qo = csr([b"ACGTACGT", b"AAAA"])
+    s, so = csr([b"TTTT", b"CCCCCC"])
+    with pytest.raises(A.AnyseqError) as e:
+        ctx.traceback(A.Scheme("global"), q, qo, s, so, cigar_capacity=1)
+    assert e.value.status_name == "E_CAPACITY" and e.value.cigar_used > 1

@@ -1,0 +1,83 @@
+"""GPU parity of the long-pair kernel (anyseq_align_long) against the oracle's linear-space
+score variant, across virtual column strips (the multi-GPU boundary protocol on one
+device), band progress granularity and all kinds."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2002_04561_b200 as A
+    c = A.Context([0])
+    yield c
+    c.close()
+
+
+def _orc(kind, gap, go, q, s):
+    from oracle import oracle as O
+    return O.score_rolling(O.Scheme(kind, gap, 2, -1, go, 1), q, s)
+
+
+@pytest.mark.parametrize("kind", ["global", "local", "semi"])
+@pytest.mark.parametrize("gap,go", [("linear", 0), ("affine", 5)])
+@pytest.mark.parametrize("strips", [1, 3])
+def test_long_random_windows(ctx, kind, gap, go, strips):
+    import paper_2002_04561_b200 as A
+    from synth import iid, c4_genomes
+    for (n, m, seed) in ((1, 1, 1), (37, 1200, 2), (1500, 20, 3), (2600, 2300, 4)):
+        q, s = iid(n, seed), iid(m, seed + 100)
+        ctx.set_option("long_strips", strips)
+        ctx.set_option("long_chunk_cols", 64)
+        r = ctx.align_long(A.Scheme(kind, gap, 2, -1, go, 1), q, s)
+        o = _orc(kind, gap, go, q, s)
+        assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), (n, m)
+    ctx.set_option("long_strips", 1)
+
+
+def test_long_mutated_window(ctx):
+    """C4 variant (a) shape: a 40 kbp window of a mutated genome pair, SW affine 5/1."""
+    import paper_2002_04561_b200 as A
+    from synth import c4_genomes
+    g1, g2 = c4_genomes(40_000, "a", seed=4)
+    for strips, chunk in ((1, 64), (4, 32), (7, 256)):
+        ctx.set_option("long_strips", strips)
+        ctx.set_option("long_chunk_cols", chunk)
+        r = ctx.align_long(A.Scheme("local", "affine", 2, -1, 5, 1), g1, g2)
+        o = _orc("local", "affine", 5, g1, g2)
+        assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), strips
+    ctx.set_option("long_strips", 1)
+    ctx.set_option("long_chunk_cols", 64)
+
+
+def test_long_identical_closed_form(ctx):
+    """C4 variant (c): G2 = G1 -> local score 2n at (n, n) (closed form), 1 Mbp."""
+    import paper_2002_04561_b200 as A
+    from synth import c4_genomes
+    g1, g2 = c4_genomes(1_000_000, "c", seed=4)
+    for strips in (1, 2):
+        ctx.set_option("long_strips", strips)
+        r = ctx.align_long(A.Scheme("local", "affine", 2, -1, 5, 1), g1, g2)
+        assert (r["score"], r["q_end"], r["s_end"]) == (2_000_000, 1_000_000, 1_000_000)
+    ctx.set_option("long_strips", 1)
+
+
+def test_long_strip_invariance(ctx):
+    """Result unchanged for G = 1/2/4/8 virtual strips (SURVEY 8(c) invariants)."""
+    import paper_2002_04561_b200 as A
+    from synth import c4_genomes
+    g1, g2 = c4_genomes(200_000, "b", seed=8)
+    outs = []
+    for strips in (1, 2, 4, 8):
+        ctx.set_option("long_strips", strips)
+        outs.append(tuple(ctx.align_long(A.Scheme("local", "affine", 2, -1, 5, 1), g1, g2).values()))
+    ctx.set_option("long_strips", 1)
+    assert len(set(outs)) == 1, outs
+
+
+def test_long_bad_byte(ctx):
+    import paper_2002_04561_b200 as A
+    with pytest.raises(A.AnyseqError) as e:
+        ctx.align_long(A.Scheme("local"), b"ACGTQ", b"ACGT")
+    assert e.value.status_name == "E_BADSEQ"
