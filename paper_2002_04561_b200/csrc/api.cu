@@ -310,6 +310,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     fa.scores = d_scores;
     fa.end_i = D.end_i.as<int32_t>();
     fa.end_j = D.end_j.as<int32_t>();
+    fa.one = 1;
     const int HS = d.L * d.R;
     const int G = 32 / d.L;
     // strip row buffer only when some pair needs more than one strip

@@ -24,6 +24,7 @@ struct FillArgs {
   uint32_t* dirs;             // TB: direction nibbles
   int64_t dir_block_words;    // TB: words per slot block (fixed per launch)
   TbInfo* tb;                 // TB: per pair
+  int32_t one;                // = 1 at run time (keeps IMAD-based adds on the FMA pipe)
 };
 
 }  // namespace anyseq

@@ -16,8 +16,12 @@
 //  * sigma comes from one PRMT per register: per-row query profile bytes sigma(q_i, .)
 //    selected (with sign replication) by a per-column selector built from the subject
 //    symbol(s) -- one instruction for two cells in VS16.
-//  * Cells per register: PRMT, VIADDMNMX (E), VIADDMNMX (F), VIMNMX (E|F), VIADDMNMX (H,
-//    .RELU for local: nu = 0), VIADD (Hop = H - Go - Ge shared by E below and F right).
+//  * Cell ops per register: PRMT, VIADDMNMX (E), VIADDMNMX (F), VIMNMX (E|F), VIADDMNMX (H,
+//    .RELU for local: nu = 0) on the integer pipe, and Hop = H - Go - Ge (shared by E below
+//    and F right) as an IMAD on the FMA pipe: VS16 global/semi scores are stored with a
+//    +2^14 bias so that the packed subtraction can never borrow across the halves.
+//  * H lives in two register arrays used in ping-pong across steps (step k reads HA and
+//    writes HB, step k+1 the reverse), so the diagonal value H(i-1,j-1) never needs a copy.
 //  * Rows longer than one strip are handled strip after strip; the bottom row (H, E) of a
 //    strip is kept in a per-group global row buffer (the paper's tile border stripe,
 //    P:275, Fig. 2) and read back by lane 0 of the next strip.
@@ -30,26 +34,27 @@
 
 namespace anyseq {
 
-
-
-template <int L>
-__device__ __forceinline__ int group_max(int v) {
-#pragma unroll
-  for (int o = L / 2; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o, L));
-  return v;
-}
-
 // (value desc, j asc, i asc) merge used by the local end-cell rule (reading R10)
 __device__ __forceinline__ bool key_better(int v, int i, int j, int bv, int bi, int bj) {
   return v > bv || (v == bv && (j < bj || (j == bj && i < bi)));
 }
 
-template <class V, int KIND, int GAP, int L, int R, bool TB>
-__global__ void __launch_bounds__(128) fill_kernel(FillArgs a) {
+// x * one + k with `one` opaque to the compiler -> IMAD (FMA pipe), not IADD3 (ALU pipe)
+__device__ __forceinline__ uint32_t imad_add(uint32_t x, uint32_t one, uint32_t k) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(one), "r"(k));
+  return d;
+}
+
+template <class V, int KIND, int GAP, int L, int R, bool TB, bool POS>
+__global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(FillArgs a) {
   using T = typename V::T;
   constexpr int PP = V::P;
   constexpr int G = 32 / L;
   constexpr int HS = L * R;  // strip height
+  // biased VS16 representation (global/semi): stored = value + 2^14
+  constexpr bool BIAS = (PP == 2) && (KIND != KLOCAL);
+  constexpr int B0 = BIAS ? (1 << 14) : 0;
   const int lane = threadIdx.x & 31;
   const int g = lane / L, t = lane % L;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -59,10 +64,24 @@ __global__ void __launch_bounds__(128) fill_kernel(FillArgs a) {
   const int nsl = slot_hi - slot_lo;
   const int nws = (nsl + G - 1) / G;
   const DevParams P = a.P;
-  const bool pos = TB || a.pos;
-  const T NEG = V::neg();
+  constexpr bool pos = TB || POS;
+  const uint32_t one = (uint32_t)a.one;
+  const int cop = (GAP == GAFFINE) ? (P.go + P.ge) : P.ge;  // H -> Hop
+  const T NEG = (PP == 2) ? V::splat(NEG16 + B0) : V::splat(NEG32);
   const T NGE = V::splat(-P.ge);
-  const T NOC = V::splat(GAP == GAFFINE ? -(P.go + P.ge) : -P.ge);  // H -> Hop ("H - Go - Ge")
+  const T NOC = V::splat(-cop);
+  const uint32_t KOC = (uint32_t)(-(int)(cop * ((PP == 2) ? 65537 : 1)));
+  auto hop = [&](T h) -> T {  // Hop = H - Go - Ge (or H - g)
+    if (PP == 1 || BIAS) return (T)imad_add((uint32_t)h, one, KOC);
+    return V::add(h, NOC);
+  };
+  auto enc = [&](int v0, int v1) -> T { return V::make(v0 + B0, v1 + B0); };
+  // H(., m) of every lane at its last column (odd row stride R keeps banks distinct)
+  __shared__ uint32_t capbuf[KIND != KLOCAL ? PP : 1][128][KIND != KLOCAL ? R : 1];
+  // rarely touched per-lane state lives in shared memory, not in registers
+  struct LaneTrack { int nn[2], pad[2], cv[2], ci[2], gv[2]; };
+  __shared__ LaneTrack track[128];
+  auto dec = [&](T x, int X) -> int { return V::get(x, X) - B0; };
 
   for (int ws = warp; ws < nws; ws += nwarps) {
     const int sidx = ws * G + g;
@@ -93,6 +112,8 @@ __global__ void __launch_bounds__(128) fill_kernel(FillArgs a) {
       M = max(M, mm[X]);
       nmax = max(nmax, nn[X]);
     }
+    // a "uniform" slot: every present pair has M columns -> captures after the sweep
+    const bool uni = (PP == 1) || pr[PP - 1] < 0 || mm[0] == mm[PP - 1];
     const int NS = (M > 0) ? (nmax + HS - 1) / HS : 0;
     const int Mw = __reduce_max_sync(0xffffffffu, M);
     const int NSw = __reduce_max_sync(0xffffffffu, NS);
@@ -109,22 +130,26 @@ __global__ void __launch_bounds__(128) fill_kernel(FillArgs a) {
     }
 
     // ---- optimum trackers (readings R5, R10) ----
-    T best = V::splat(0);           // local running max / semi bottom-row max (j=0 -> H(n,0)=0)
+    T best = enc(0, 0);             // local running max / semi bottom-row max ((n,0) = 0)
     int bv[PP], bi[PP], bj[PP];      // local (POS) overall best per half
-    int cv[PP], ci[PP];              // semi column-m best per half (value, i); starts H(0,m)=0
     int rj[PP];                      // semi bottom-row best column
-    int gv[PP];                      // global H(n,m)
 #pragma unroll
     for (int X = 0; X < PP; ++X) {
-      bv[X] = 0; bi[X] = 0; bj[X] = 0;
-      cv[X] = 0; ci[X] = 0; rj[X] = 0; gv[X] = 0;
+      bv[X] = 0; bi[X] = 0; bj[X] = 0; rj[X] = 0;
+      // semi column-m best (value, i) starts at H(0,m) = 0; global H(n,m)
+      track[threadIdx.x].cv[X] = 0;
+      track[threadIdx.x].ci[X] = 0;
+      track[threadIdx.x].gv[X] = 0;
+      track[threadIdx.x].nn[X] = nn[X];
+      track[threadIdx.x].pad[X] = pad[X];
     }
 
     for (int st = 0; st < NSw; ++st) {
       const bool sact = st < NS;
+      const bool last_strip = (st == NS - 1);
       const int ip0 = st * HS + t * R;  // first physical row of this lane
       uint32_t p0[R], p1[R];
-      T Hh[R], Ho[R], Ff[R];
+      T HA[R], HB[R], Ff[R];
       uint32_t acc[TB ? R * PP : 1];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -147,9 +172,9 @@ __global__ void __launch_bounds__(128) fill_kernel(FillArgs a) {
           p0[r] = pf[0];
           p1[r] = pf[PP - 1];
         }
-        Hh[r] = V::make(iv[0], iv[PP - 1]);
-        Ho[r] = V::add(Hh[r], NOC);
-        Ff[r] = NEG;  // F(i,0) = -inf
+        HA[r] = enc(iv[0], iv[PP - 1]);
+        HB[r] = HA[r];
+        Ff[r] = NEG;
         if (TB) {
 #pragma unroll
           for (int X = 0; X < PP; ++X) acc[r * PP + X] = 0;
@@ -160,10 +185,16 @@ __global__ void __launch_bounds__(128) fill_kernel(FillArgs a) {
       {
         int dv = 0;
         if (KIND == KGLOBAL && ip0 >= 1) dv = -(P.go + ip0 * P.ge);
-        diag = V::splat(dv);
+        diag = enc(dv, dv);
       }
       T Hbot = NEG, Ebot = NEG;
       uint32_t selb = 0;
+      // lane 0: subject codes of the next column (prefetched one step ahead)
+      uint32_t nc0 = 0, nc1 = 0;
+      if (t == 0 && sact) {
+        if (mm[0] > 0) nc0 = a.scode[so[0]];
+        if (PP == 2 && mm[PP - 1] > 0) nc1 = a.scode[so[PP - 1]];
+      }
       // per-strip local trackers (merged by key at strip end)
       int sv[PP], si[PP], sj[PP];
 #pragma unroll
@@ -171,169 +202,174 @@ __global__ void __launch_bounds__(128) fill_kernel(FillArgs a) {
       T sbest = V::splat(0);
 
       const int K = Mw + L - 1;
-      for (int k = 0; k < K; ++k) {
+      // H(i, 0) of row ip (initial column, P:259 / P:262)
+      auto init_col = [&](int ip) -> T {
+        if (KIND == KGLOBAL) {
+          const int v = -(P.go + (ip + 1) * P.ge);
+          return enc(v, v);
+        }
+        return enc(0, 0);
+      };
+      // Every lane relaxes its rows in every step (no divergent "active" region: a lane
+      // outside its column range computes values nobody reads).  A lane loads its initial
+      // column when it reaches column 0 and hands over captures at its last column.
+      auto step = [&](const int k, T (&Hi)[R], T (&Hq)[R]) {
         T hin = V::shfl_up(Hbot, L);
         T ein = (GAP == GAFFINE) ? V::shfl_up(Ebot, L) : NEG;
         uint32_t sel = __shfl_up_sync(0xffffffffu, selb, 1, L);
         const int col = k - t;
         const bool act = sact && col >= 0 && col < M;
+        if (col == 0) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            Hi[r] = init_col(ip0 + r);
+            Ff[r] = NEG;  // F(i,0) = -inf
+          }
+          diag = (KIND == KGLOBAL && ip0 >= 1) ? init_col(ip0 - 1) : enc(0, 0);
+        }
         if (t == 0 && act) {
           if (st == 0) {
-            hin = V::splat((KIND == KGLOBAL) ? -(P.go + (col + 1) * P.ge) : 0);  // H(0,j)
-            ein = NEG;                                                             // E(0,j)
+            const int h0 = (KIND == KGLOBAL) ? -(P.go + (col + 1) * P.ge) : 0;  // H(0,j)
+            hin = enc(h0, h0);
+            ein = NEG;  // E(0,j) = -inf
           } else {
             const uint2 v = scr[col];
             hin = (T)v.x;
             ein = (T)v.y;
           }
-          uint32_t c0 = 0, c1 = 0;
-          if (col < mm[0]) c0 = a.scode[so[0] + col];
-          if (PP == 2 && col < mm[PP - 1]) c1 = a.scode[so[PP - 1] + col];
-          sel = V::selector(c0, c1);
+          sel = V::selector(nc0, nc1);
+          nc0 = (col + 1 < mm[0]) ? a.scode[so[0] + col + 1] : 0u;
+          if (PP == 2) nc1 = (col + 1 < mm[PP - 1]) ? a.scode[so[PP - 1] + col + 1] : 0u;
         }
-        if (act) {
-          T hup = V::add(hin, NOC);  // Hop of the row above
-          T e = ein;
-          T hd = diag;
-          if (!TB) {
+        T hup = hop(hin);  // Hop of the row above
+        T e = ein;
+        if (!TB) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-              const T sig = V::sigma(p0[r], p1[r], sel);
-              T tm;
-              if (GAP == GAFFINE) {
-                e = V::addmax(e, NGE, hup);           // Eq. (4)
-                Ff[r] = V::addmax(Ff[r], NGE, Ho[r]);  // Eq. (5)
-                tm = V::vmax(e, Ff[r]);
-              } else {
-                tm = V::vmax(hup, Ho[r]);  // Eqs. (2)-(3): H_up - g, H_left - g
-              }
-              const T h = (KIND == KLOCAL) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
-              hd = Hh[r];
-              Hh[r] = h;
-              Ho[r] = V::add(h, NOC);
-              hup = Ho[r];
+          for (int r = 0; r < R; ++r) {
+            const T hd = (r == 0) ? diag : Hi[r - 1];
+            const T sig = V::sigma(p0[r], p1[r], sel);
+            const T hleft = hop(Hi[r]);  // Hop(i, j-1), recomputed on the FMA pipe
+            T tm;
+            if (GAP == GAFFINE) {
+              e = V::addmax(e, NGE, hup);            // Eq. (4)
+              Ff[r] = V::addmax(Ff[r], NGE, hleft);  // Eq. (5)
+              tm = V::vmax(e, Ff[r]);
+            } else {
+              tm = V::vmax(hup, hleft);  // Eqs. (2)-(3): H_up - g, H_left - g
             }
+            const T h = (KIND == KLOCAL) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
+            Hq[r] = h;
+            hup = hop(h);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const T hd = (r == 0) ? diag : Hi[r - 1];
+            const T sig = V::sigma(p0[r], p1[r], sel);
+            uint32_t pe = 0, pf = 0, pef, pd;
+            T tm;
+            const T hleft = hop(Hi[r]);
+            if (GAP == GAFFINE) {
+              e = V::bmax(V::add(e, NGE), hup, pe);              // eext: extend >= open (R8)
+              Ff[r] = V::bmax(V::add(Ff[r], NGE), hleft, pf);    // fext
+              tm = V::bmax(e, Ff[r], pef);                       // E before F (R7)
+            } else {
+              tm = V::bmax(hup, hleft, pef);
+            }
+            T h = V::bmax(V::add(hd, sig), tm, pd);              // DIAG first (R7)
+            uint32_t stop = 0;
+            if (KIND == KLOCAL) {
+              // STOP where H <= 0 (nu wins ties, reading R9).  Not via bmax(0, h): ptxas
+              // 12.9 swaps the operands of a VIMNMX-with-predicates against a constant
+              // zero and the predicates then mean h >= 0.
+              h = V::vmax_relu(h, h);
+#pragma unroll
+              for (int X = 0; X < PP; ++X) stop |= (V::get(h, X) == 0 ? 1u : 0u) << X;
+            }
+#pragma unroll
+            for (int X = 0; X < PP; ++X) {
+              uint32_t src = ((pd >> X) & 1u) ? 0u : (((pef >> X) & 1u) ? 1u : 2u);
+              if ((stop >> X) & 1u) src = 3u;
+              const uint32_t nib = src | (((pe >> X) & 1u) << 2) | (((pf >> X) & 1u) << 3);
+              acc[r * PP + X] = (acc[r * PP + X] >> 4) | (nib << 28);
+            }
+            Hq[r] = h;
+            hup = hop(h);
+          }
+        }
+        diag = hin;
+        Hbot = Hq[R - 1];
+        Ebot = e;
+        selb = sel;
+        if (act && t == L - 1 && st + 1 < NS) scr[col] = make_uint2((uint32_t)Hq[R - 1], (uint32_t)e);
+
+        // ---- optimum bookkeeping ----
+        if (KIND == KLOCAL) {
+          T cm = Hq[0];
+#pragma unroll
+          for (int r = 1; r + 1 < R; r += 2) cm = V::vmax3(cm, Hq[r], Hq[r + 1]);
+          if ((R % 2) == 0) cm = V::vmax(cm, Hq[R - 1]);
+          uint32_t keep = 0;
+          if (act) {
+#pragma unroll
+            for (int X = 0; X < PP; ++X) keep |= (uni || col < mm[X] ? 1u : 0u) << X;
+          }
+          cm = V::select_mask(cm, keep, V::splat(0));
+          if (!pos) {
+            sbest = V::vmax(sbest, cm);
           } else {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              const T sig = V::sigma(p0[r], p1[r], sel);
-              uint32_t pe = 0, pf = 0, pef, pd;
-              T tm;
-              if (GAP == GAFFINE) {
-                e = V::bmax(V::add(e, NGE), hup, pe);              // eext: extend >= open (R8)
-                Ff[r] = V::bmax(V::add(Ff[r], NGE), Ho[r], pf);    // fext
-                tm = V::bmax(e, Ff[r], pef);                       // E before F (R7)
-              } else {
-                tm = V::bmax(hup, Ho[r], pef);
-              }
-              T h = V::bmax(V::add(hd, sig), tm, pd);              // DIAG first (R7)
-              uint32_t stop = 0;
-              if (KIND == KLOCAL) {
-                // STOP where H <= 0 (nu wins ties, reading R9).  Not via bmax(0, h): ptxas
-                // 12.9 swaps the operands of a VIMNMX-with-predicates against a constant
-                // zero and the predicates then mean h >= 0.
-                h = V::vmax_relu(h, h);
-#pragma unroll
-                for (int X = 0; X < PP; ++X) stop |= (V::get(h, X) == 0 ? 1u : 0u) << X;
-              }
+            uint32_t pb;
+            const T nb = V::bmax(sbest, cm, pb);  // bit: sbest >= cm
+            if ((~pb) & ((1u << PP) - 1u)) {
 #pragma unroll
               for (int X = 0; X < PP; ++X) {
-                uint32_t src = ((pd >> X) & 1u) ? 0u : (((pef >> X) & 1u) ? 1u : 2u);
-                if ((stop >> X) & 1u) src = 3u;
-                const uint32_t nib = src | (((pe >> X) & 1u) << 2) | (((pf >> X) & 1u) << 3);
-                acc[r * PP + X] = (acc[r * PP + X] >> 4) | (nib << 28);
-              }
-              hd = Hh[r];
-              Hh[r] = h;
-              Ho[r] = V::add(h, NOC);
-              hup = Ho[r];
-            }
-          }
-          diag = hin;
-          Hbot = Hh[R - 1];
-          Ebot = e;
-          selb = sel;
-          if (t == L - 1 && st + 1 < NS) scr[col] = make_uint2((uint32_t)Hh[R - 1], (uint32_t)e);
-
-          // ---- optimum bookkeeping ----
-          if (KIND == KLOCAL) {
-            T cm = Hh[0];
+                if (!((pb >> X) & 1u)) {
+                  const int v = V::get(cm, X);
+                  int rr = R - 1;
 #pragma unroll
-            for (int r = 1; r + 1 < R; r += 2) cm = V::vmax3(cm, Hh[r], Hh[r + 1]);
-            if ((R % 2) == 0) cm = V::vmax(cm, Hh[R - 1]);
-            uint32_t keep = 0;
-#pragma unroll
-            for (int X = 0; X < PP; ++X) keep |= (col < mm[X] ? 1u : 0u) << X;
-            cm = V::select_mask(cm, keep, V::splat(0));
-            if (!pos) {
-              sbest = V::vmax(sbest, cm);
-            } else {
-              uint32_t pb;
-              const T nb = V::bmax(sbest, cm, pb);  // bit: sbest >= cm
-              if ((~pb) & ((1u << PP) - 1u)) {
-#pragma unroll
-                for (int X = 0; X < PP; ++X) {
-                  if (!((pb >> X) & 1u)) {
-                    const int v = V::get(cm, X);
-                    int rr = R - 1;
-#pragma unroll
-                    for (int r = R - 1; r >= 0; --r)
-                      if (V::get(Hh[r], X) == v) rr = r;
-                    sv[X] = v;
-                    si[X] = ip0 + rr - pad[X] + 1;
-                    sj[X] = col + 1;
-                  }
+                  for (int r = R - 1; r >= 0; --r)
+                    if (V::get(Hq[r], X) == v) rr = r;
+                  sv[X] = v;
+                  si[X] = ip0 + rr - pad[X] + 1;
+                  sj[X] = col + 1;
                 }
               }
-              sbest = nb;
             }
-          } else if (KIND == KSEMI) {
-            // bottom row n, columns j = 1..m-1 (row candidates precede column m, R5)
+            sbest = nb;
+          }
+        } else if (KIND == KSEMI) {
+          // bottom row n (row candidates j = 1..m-1 precede column m, reading R5); only
+          // lane L-1 of the last strip holds row n, the others' values are ignored.
+          if (last_strip) {
             uint32_t keep = 0;
-            if (st == NS - 1) {
+            if (act) {
 #pragma unroll
-              for (int X = 0; X < PP; ++X) keep |= (col < mm[X] - 1 ? 1u : 0u) << X;
+              for (int X = 0; X < PP; ++X)
+                keep |= ((pos ? col < mm[X] - 1 : (uni || col < mm[X])) ? 1u : 0u) << X;
             }
-            const T cand = V::select_mask(Hh[R - 1], keep, NEG);
-            uint32_t pb;
-            const T nb = V::bmax(best, cand, pb);
-            if (pos) {
+            if (!pos) {
+              // without end cells j = m may join the row set: it is also a column candidate
+              best = V::vmax(best, V::select_mask(Hq[R - 1], keep, NEG));
+            } else {
+              uint32_t pb;
+              const T nb = V::bmax(best, V::select_mask(Hq[R - 1], keep, NEG), pb);
 #pragma unroll
               for (int X = 0; X < PP; ++X)
                 if (!((pb >> X) & 1u)) rj[X] = col + 1;
-            }
-            best = nb;
-            // column m: rows i = 1..n at the step where this lane reaches column m
-#pragma unroll
-            for (int X = 0; X < PP; ++X) {
-              if (col == mm[X] - 1) {
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                  const int i = ip0 + r - pad[X] + 1;
-                  const int v = V::get(Hh[r], X);
-                  if (i >= 1 && i <= nn[X] && v > cv[X]) { cv[X] = v; ci[X] = i; }
-                }
-              }
-            }
-          } else {  // global: H(n,m)
-#pragma unroll
-            for (int X = 0; X < PP; ++X) {
-              if (col == mm[X] - 1) {
-                const int ipn = nn[X] - 1;
-                if (ipn >= 0 && st == ipn / HS && t == (ipn % HS) / R) {
-                  const int rr = ipn % R;
-                  int v = 0;
-#pragma unroll
-                  for (int r = 0; r < R; ++r)
-                    if (r == rr) v = V::get(Hh[r], X);
-                  gv[X] = v;
-                }
-              }
+              best = nb;
             }
           }
-        } else if (TB) {
+        }
+        // a pair's last column m: park this lane's H(., m) in shared memory (semi: column
+        // candidates, global: H(n,m)); evaluated after the sweep, off the hot path
+        if (KIND != KLOCAL) {
 #pragma unroll
-          for (int r = 0; r < R * PP; ++r) acc[r] >>= 4;
+          for (int X = 0; X < PP; ++X) {
+            if (act && col == mm[X] - 1) {
+#pragma unroll
+              for (int r = 0; r < R; ++r) capbuf[X][threadIdx.x][r] = (uint32_t)Hq[r];
+            }
+          }
         }
         if (TB && valid && sact) {
           const int Kslot = M + L - 1;
@@ -347,8 +383,38 @@ __global__ void __launch_bounds__(128) fill_kernel(FillArgs a) {
             }
           }
         }
-      }  // steps
+      };
 
+      int k = 0;
+      for (; k + 1 < K; k += 2) {
+        step(k, HA, HB);
+        step(k + 1, HB, HA);
+      }
+      if (k < K) step(k, HA, HB);
+
+      __syncwarp();  // capbuf writes of this strip are visible (all lanes participate)
+      if (KIND != KLOCAL && sact) {
+        LaneTrack& tr = track[threadIdx.x];
+#pragma unroll 1
+        for (int X = 0; X < PP; ++X) {
+          const int nX = tr.nn[X], pX = tr.pad[X];
+          if (KIND == KSEMI) {  // column m candidates i = 1..n of this strip (reading R5)
+            int cvx = tr.cv[X], cix = tr.ci[X];
+#pragma unroll 1
+            for (int r = 0; r < R; ++r) {
+              const int i = ip0 + r - pX + 1;
+              const int v = dec((T)capbuf[X][threadIdx.x][r], X);
+              if (i >= 1 && i <= nX && v > cvx) { cvx = v; cix = i; }
+            }
+            tr.cv[X] = cvx;
+            tr.ci[X] = cix;
+          } else {
+            const int ipn = nX - 1;
+            if (ipn >= 0 && st == ipn / HS && t == (ipn % HS) / R)
+              tr.gv[X] = dec((T)capbuf[X][threadIdx.x][ipn % R], X);
+          }
+        }
+      }
       if (KIND == KLOCAL) {
         if (!pos) {
           best = V::vmax(best, sbest);
@@ -378,21 +444,21 @@ __global__ void __launch_bounds__(128) fill_kernel(FillArgs a) {
         }
         osc[X] = v; oi[X] = i; oj[X] = j;
       } else if (KIND == KSEMI) {
-        int v = cv[X], i = ci[X];
+        int v = track[threadIdx.x].cv[X], i = track[threadIdx.x].ci[X];
 #pragma unroll
         for (int o = L / 2; o > 0; o >>= 1) {
           const int v2 = __shfl_xor_sync(0xffffffffu, v, o, L);
           const int i2 = __shfl_xor_sync(0xffffffffu, i, o, L);
           if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
         }
-        const int rv = __shfl_sync(0xffffffffu, V::get(best, X), L - 1, L);
+        const int rv = __shfl_sync(0xffffffffu, dec(best, X), L - 1, L);
         const int rjj = __shfl_sync(0xffffffffu, rj[X], L - 1, L);
         if (rv >= v) { osc[X] = rv; oi[X] = nn[X]; oj[X] = rjj; }
         else { osc[X] = v; oi[X] = i; oj[X] = mm[X]; }
       } else {
         const int ipn = max(nn[X] - 1, 0);
         const int owner = (ipn % HS) / R;
-        osc[X] = __shfl_sync(0xffffffffu, gv[X], owner, L);
+        osc[X] = __shfl_sync(0xffffffffu, track[threadIdx.x].gv[X], owner, L);
         oi[X] = nn[X];
         oj[X] = mm[X];
       }

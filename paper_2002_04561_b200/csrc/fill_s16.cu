@@ -1,11 +1,11 @@
 // csrc/fill_s16.cu -- VS16 (two alignments per register) score-only instances.
 #include "fill_inst.cuh"
 namespace anyseq {
-FillFn fill_fn_s16(int v, int kind, int gap) {
+FillFn fill_fn_s16(int v, int kind, int gap, bool pos) {
   switch (v) {
-    case 0: return fill_fn<VS16, 8, 8, false>(kind, gap);
-    case 1: return fill_fn<VS16, 8, 16, false>(kind, gap);
-    case 2: return fill_fn<VS16, 8, 19, false>(kind, gap);
+    case 0: return fill_fn<VS16, 8, 8, false>(kind, gap, pos);
+    case 1: return fill_fn<VS16, 8, 16, false>(kind, gap, pos);
+    case 2: return fill_fn<VS16, 8, 19, false>(kind, gap, pos);
     default: return nullptr;
   }
 }

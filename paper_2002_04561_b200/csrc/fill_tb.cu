@@ -1,10 +1,10 @@
 // csrc/fill_tb.cu -- traceback (direction nibble) instances.
 #include "fill_inst.cuh"
 namespace anyseq {
-FillFn fill_fn_tb(int v, int kind, int gap) {
+FillFn fill_fn_tb(int v, int kind, int gap, bool pos) {
   switch (v) {
-    case 5: return fill_fn<VS32, 8, 8, true>(kind, gap);
-    case 6: return fill_fn<VS16, 8, 8, true>(kind, gap);
+    case 5: return fill_fn<VS32, 8, 8, true>(kind, gap, pos);
+    case 6: return fill_fn<VS16, 8, 8, true>(kind, gap, pos);
     default: return nullptr;
   }
 }

@@ -129,7 +129,10 @@ __global__ void classify_kernel(ClassifyArgs a) {
     const int64_t padded = n + 192;  // max strip padding of any variant
     const int64_t neg = 3 * (int64_t)a.cfg.bound_go + (padded + m + 2) * (int64_t)a.cfg.bound_ge + 256;
     const int64_t posb = (int64_t)max(a.cfg.bound_match, 0) * (padded < m ? padded : m);
-    const bool ok16 = a.cfg.allow16 && !hasN && neg <= 16000 && posb <= 16000;
+    // VS16 stores global/semi scores with a +2^14 bias; Hop = H - (Go+Ge) is a packed 32-bit
+    // IMAD that must not borrow across halves -> every biased value must stay >= Go+Ge.
+    const bool ok16 = a.cfg.allow16 && !hasN && neg + a.cfg.bound_go + a.cfg.bound_ge <= 16000 &&
+                      posb <= 16000;
     const bool ok32 = neg <= (1ll << 30) - (1ll << 24) && posb <= (1ll << 30) - (1ll << 24);
     if (!ok32) atomicExch(&a.sum->range_err, 1);
     int v = -1;
