@@ -47,7 +47,7 @@ __device__ __forceinline__ uint32_t imad_add(uint32_t x, uint32_t one, uint32_t 
 }
 
 template <class V, int KIND, int GAP, int L, int R, bool TB, bool POS>
-__global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(FillArgs a) {
+__global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(FillArgs a) {
   using T = typename V::T;
   constexpr int PP = V::P;
   constexpr int G = 32 / L;
@@ -65,6 +65,8 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(Fil
   const int nws = (nsl + G - 1) / G;
   const DevParams P = a.P;
   constexpr bool pos = TB || POS;
+  constexpr bool FAST = (GAP == GAFFINE) && !TB;  // reassociated affine recurrence
+  // VS16 local scores are unbiased; their Hop uses VIADD.16x2 (see hop) -- fine.
   const uint32_t one = (uint32_t)a.one;
   const int cop = (GAP == GAFFINE) ? (P.go + P.ge) : P.ge;  // H -> Hop
   const T NEG = (PP == 2) ? V::splat(NEG16 + B0) : V::splat(NEG32);
@@ -81,6 +83,11 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(Fil
   // rarely touched per-lane state lives in shared memory, not in registers
   struct LaneTrack { int nn[2], pad[2], cv[2], ci[2], gv[2]; };
   __shared__ LaneTrack track[128];
+  // per-group column selectors of the current slot (built once per slot, read by every lane
+  // at its own column: no selector shuffle, no per-step global loads)
+  constexpr int SELCAP = 512;
+  __shared__ uint16_t seltab[4 * G][SELCAP];
+  const int gb = (threadIdx.x >> 5) * G + g;
   auto dec = [&](T x, int X) -> int { return V::get(x, X) - B0; };
 
   for (int ws = warp; ws < nws; ws += nwarps) {
@@ -129,8 +136,19 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(Fil
       S8 = (M + L - 1 + 7) >> 3;
     }
 
+    const bool tab = Mw <= SELCAP;  // warp-uniform
+    if (tab) {
+      for (int c = t; c < M; c += L) {
+        const uint32_t c0 = (c < mm[0]) ? a.scode[so[0] + c] : 0u;
+        const uint32_t c1 = (PP == 2 && c < mm[PP - 1]) ? a.scode[so[PP - 1] + c] : 0u;
+        seltab[gb][c] = (uint16_t)V::selector(c0, c1);
+      }
+      __syncwarp();
+    }
+
     // ---- optimum trackers (readings R5, R10) ----
     T best = enc(0, 0);             // local running max / semi bottom-row max ((n,0) = 0)
+    T bfin = enc(0, 0);             // semi (plain score): bottom-row max at column m
     int bv[PP], bi[PP], bj[PP];      // local (POS) overall best per half
     int rj[PP];                      // semi bottom-row best column
 #pragma unroll
@@ -191,7 +209,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(Fil
       uint32_t selb = 0;
       // lane 0: subject codes of the next column (prefetched one step ahead)
       uint32_t nc0 = 0, nc1 = 0;
-      if (t == 0 && sact) {
+      if (t == 0 && sact && !tab) {
         if (mm[0] > 0) nc0 = a.scode[so[0]];
         if (PP == 2 && mm[PP - 1] > 0) nc1 = a.scode[so[PP - 1]];
       }
@@ -216,47 +234,69 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(Fil
       auto step = [&](const int k, T (&Hi)[R], T (&Hq)[R]) {
         T hin = V::shfl_up(Hbot, L);
         T ein = (GAP == GAFFINE) ? V::shfl_up(Ebot, L) : NEG;
-        uint32_t sel = __shfl_up_sync(0xffffffffu, selb, 1, L);
         const int col = k - t;
+        uint32_t sel;
+        if (tab) sel = seltab[gb][col & (SELCAP - 1)];
+        else sel = __shfl_up_sync(0xffffffffu, selb, 1, L);
         const bool act = sact && col >= 0 && col < M;
-        if (col == 0) {
+        if (col == 0 && sact) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             Hi[r] = init_col(ip0 + r);
             Ff[r] = NEG;  // F(i,0) = -inf
           }
           diag = (KIND == KGLOBAL && ip0 >= 1) ? init_col(ip0 - 1) : enc(0, 0);
+          if (KIND == KLOCAL && !pos) sbest = V::splat(0);
+          if (KIND == KSEMI) {
+            best = enc(0, 0);  // H(n,0) = 0 (first row candidate)
+#pragma unroll
+            for (int X = 0; X < PP; ++X) rj[X] = 0;
+          }
         }
         if (t == 0 && act) {
           if (st == 0) {
             const int h0 = (KIND == KGLOBAL) ? -(P.go + (col + 1) * P.ge) : 0;  // H(0,j)
             hin = enc(h0, h0);
-            ein = NEG;  // E(0,j) = -inf
+            ein = FAST ? hop(hin) : NEG;  // FAST: E(1,j) = H(0,j) - Go - Ge; else E(0,j) = -inf
           } else {
             const uint2 v = scr[col];
             hin = (T)v.x;
             ein = (T)v.y;
           }
-          sel = V::selector(nc0, nc1);
-          nc0 = (col + 1 < mm[0]) ? a.scode[so[0] + col + 1] : 0u;
-          if (PP == 2) nc1 = (col + 1 < mm[PP - 1]) ? a.scode[so[PP - 1] + col + 1] : 0u;
+          if (!tab) {
+            sel = V::selector(nc0, nc1);
+            nc0 = (col + 1 < mm[0]) ? a.scode[so[0] + col + 1] : 0u;
+            if (PP == 2) nc1 = (col + 1 < mm[PP - 1]) ? a.scode[so[PP - 1] + col + 1] : 0u;
+          }
         }
-        T hup = hop(hin);  // Hop of the row above
+        // FAST = affine score-only: the reassociated recurrence
+        //   F  = max(F - Ge, H_left - Go - Ge)          Eq. (5)
+        //   DF = max(H_diag + sigma, F)
+        //   H  = max(DF, E)        (.RELU: nu = 0)      Eq. (1)
+        //   E' = max(E - Ge, DF - Go - Ge)              Eq. (4) for the row below, exact since
+        //        H - Go - Ge = max(DF, E) - Go - Ge and E - Go - Ge <= E - Ge
+        // so the only dependency from row to row is one VIADDMNMX on E.  In this mode the
+        // value handed down the lanes / strips is E of the row BELOW the bottom row.
+        T hup = FAST ? NEG : hop(hin);  // Hop of the row above (other modes)
         T e = ein;
-        if (!TB) {
+        if (FAST) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const T hd = (r == 0) ? diag : Hi[r - 1];
+            const T sig = V::sigma(p0[r], p1[r], sel);
+            Ff[r] = V::addmax(Ff[r], NGE, hop(Hi[r]));
+            const T df = V::addmax(hd, sig, Ff[r]);
+            const T h = (KIND == KLOCAL) ? V::vmax_relu(df, e) : V::vmax(df, e);
+            e = V::addmax(e, NGE, hop(df));
+            Hq[r] = h;
+          }
+        } else if (!TB) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const T hd = (r == 0) ? diag : Hi[r - 1];
             const T sig = V::sigma(p0[r], p1[r], sel);
             const T hleft = hop(Hi[r]);  // Hop(i, j-1), recomputed on the FMA pipe
-            T tm;
-            if (GAP == GAFFINE) {
-              e = V::addmax(e, NGE, hup);            // Eq. (4)
-              Ff[r] = V::addmax(Ff[r], NGE, hleft);  // Eq. (5)
-              tm = V::vmax(e, Ff[r]);
-            } else {
-              tm = V::vmax(hup, hleft);  // Eqs. (2)-(3): H_up - g, H_left - g
-            }
+            const T tm = V::vmax(hup, hleft);  // Eqs. (2)-(3): H_up - g, H_left - g
             const T h = (KIND == KLOCAL) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
             Hq[r] = h;
             hup = hop(h);
@@ -303,21 +343,24 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(Fil
         selb = sel;
         if (act && t == L - 1 && st + 1 < NS) scr[col] = make_uint2((uint32_t)Hq[R - 1], (uint32_t)e);
 
-        // ---- optimum bookkeeping ----
+        // ---- optimum bookkeeping (P:259-264, P:421) ----
+        // Plain score mode tracks maxima in every lane and every step without masks: the
+        // trackers restart when a lane enters column 0 and are snapshotted when it leaves
+        // a pair's column m, so columns outside the pair never count.
         if (KIND == KLOCAL) {
           T cm = Hq[0];
 #pragma unroll
           for (int r = 1; r + 1 < R; r += 2) cm = V::vmax3(cm, Hq[r], Hq[r + 1]);
           if ((R % 2) == 0) cm = V::vmax(cm, Hq[R - 1]);
-          uint32_t keep = 0;
-          if (act) {
-#pragma unroll
-            for (int X = 0; X < PP; ++X) keep |= (uni || col < mm[X] ? 1u : 0u) << X;
-          }
-          cm = V::select_mask(cm, keep, V::splat(0));
           if (!pos) {
             sbest = V::vmax(sbest, cm);
           } else {
+            uint32_t keep = 0;
+            if (act) {
+#pragma unroll
+              for (int X = 0; X < PP; ++X) keep |= (uni || col < mm[X] ? 1u : 0u) << X;
+            }
+            cm = V::select_mask(cm, keep, V::splat(0));
             uint32_t pb;
             const T nb = V::bmax(sbest, cm, pb);  // bit: sbest >= cm
             if ((~pb) & ((1u << PP) - 1u)) {
@@ -340,35 +383,33 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(Fil
         } else if (KIND == KSEMI) {
           // bottom row n (row candidates j = 1..m-1 precede column m, reading R5); only
           // lane L-1 of the last strip holds row n, the others' values are ignored.
-          if (last_strip) {
+          if (!pos) {
+            best = V::vmax(best, Hq[R - 1]);  // j = m may join: it is also a column candidate
+          } else if (last_strip) {
             uint32_t keep = 0;
             if (act) {
 #pragma unroll
-              for (int X = 0; X < PP; ++X)
-                keep |= ((pos ? col < mm[X] - 1 : (uni || col < mm[X])) ? 1u : 0u) << X;
+              for (int X = 0; X < PP; ++X) keep |= (col < mm[X] - 1 ? 1u : 0u) << X;
             }
-            if (!pos) {
-              // without end cells j = m may join the row set: it is also a column candidate
-              best = V::vmax(best, V::select_mask(Hq[R - 1], keep, NEG));
-            } else {
-              uint32_t pb;
-              const T nb = V::bmax(best, V::select_mask(Hq[R - 1], keep, NEG), pb);
+            uint32_t pb;
+            const T nb = V::bmax(best, V::select_mask(Hq[R - 1], keep, NEG), pb);
 #pragma unroll
-              for (int X = 0; X < PP; ++X)
-                if (!((pb >> X) & 1u)) rj[X] = col + 1;
-              best = nb;
-            }
+            for (int X = 0; X < PP; ++X)
+              if (!((pb >> X) & 1u)) rj[X] = col + 1;
+            best = nb;
           }
         }
         // a pair's last column m: park this lane's H(., m) in shared memory (semi: column
         // candidates, global: H(n,m)); evaluated after the sweep, off the hot path
-        if (KIND != KLOCAL) {
 #pragma unroll
-          for (int X = 0; X < PP; ++X) {
-            if (act && col == mm[X] - 1) {
+        for (int X = 0; X < PP; ++X) {
+          if (act && col == mm[X] - 1) {
+            if (KIND != KLOCAL) {
 #pragma unroll
               for (int r = 0; r < R; ++r) capbuf[X][threadIdx.x][r] = (uint32_t)Hq[r];
             }
+            if (KIND == KLOCAL && !pos) best = V::select_mask(V::vmax(best, sbest), 1u << X, best);
+            if (KIND == KSEMI && !pos && last_strip) bfin = V::select_mask(best, 1u << X, bfin);
           }
         }
         if (TB && valid && sact) {
@@ -416,9 +457,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(Fil
         }
       }
       if (KIND == KLOCAL) {
-        if (!pos) {
-          best = V::vmax(best, sbest);
-        } else {
+        if (pos) {
 #pragma unroll
           for (int X = 0; X < PP; ++X)
             if (key_better(sv[X], si[X], sj[X], bv[X], bi[X], bj[X])) {
@@ -451,7 +490,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 3 : 4)) fill_kernel(Fil
           const int i2 = __shfl_xor_sync(0xffffffffu, i, o, L);
           if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
         }
-        const int rv = __shfl_sync(0xffffffffu, dec(best, X), L - 1, L);
+        const int rv = __shfl_sync(0xffffffffu, dec(pos ? best : bfin, X), L - 1, L);
         const int rjj = __shfl_sync(0xffffffffu, rj[X], L - 1, L);
         if (rv >= v) { osc[X] = rv; oi[X] = nn[X]; oj[X] = rjj; }
         else { osc[X] = v; oi[X] = i; oj[X] = mm[X]; }

@@ -36,48 +36,52 @@ __device__ int64_t find_pair(const uint64_t* off, uint64_t num_pairs, uint64_t p
   return lo;
 }
 
-__global__ void pack_kernel(const uint8_t* __restrict__ in, uint64_t len, uint8_t* __restrict__ out,
-                            uint64_t pos_base, const uint64_t* __restrict__ off, uint64_t num_pairs,
-                            uint32_t* flags, PlanSummary* sum) {
+__global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ in, uint64_t len,
+                                                   uint8_t* __restrict__ out, uint64_t pos_base,
+                                                   const uint64_t* __restrict__ off,
+                                                   uint64_t num_pairs, uint32_t* flags,
+                                                   PlanSummary* sum) {
+  __shared__ uint8_t lut[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = (uint8_t)code_of((uint32_t)i);
+  __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 16;
   for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; b < len; b += stride) {
     const bool vec = (b + 16 <= len) && ((((uintptr_t)(in + b)) & 15) == 0) &&
                      ((((uintptr_t)(out + b)) & 15) == 0);
-    uint8_t c[16];
+    uint32_t w[4] = {0, 0, 0, 0};
     int cnt = 16;
     if (vec) {
-      const uint4 v = *reinterpret_cast<const uint4*>(in + b);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int k = 0; k < 16; ++k) c[k] = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(in + b));  // streamed once
+      w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
     } else {
       cnt = (int)((len - b) < 16 ? (len - b) : 16);
-      for (int k = 0; k < cnt; ++k) c[k] = in[b + k];
+      for (int k = 0; k < cnt; ++k) w[k >> 2] |= (uint32_t)in[b + k] << (8 * (k & 3));
     }
-    uint8_t o[16];
-    bool hasN = false;
+    uint32_t o[4];
+    uint32_t bad = 0, nn = 0;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const uint32_t x = code_of(c[k]);
-      o[k] = (uint8_t)x;
-      if (k < cnt) {
-        if (x == 0xFFu) atomicMin(&sum->err_pos, (unsigned long long)(pos_base + b + k));
-        if (x == 4u) hasN = true;
+    for (int q = 0; q < 4; ++q) {
+      uint32_t r = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t x = lut[(w[q] >> (8 * k)) & 0xffu];
+        r |= x << (8 * k);
+        const bool in_range = (q * 4 + k) < cnt;
+        bad |= (in_range && x == 0xFFu) ? (1u << (q * 4 + k)) : 0u;
+        nn |= (in_range && x == 4u) ? 1u : 0u;
       }
+      o[q] = r;
     }
     if (vec) {
-      uint4 v;
-      v.x = o[0] | (o[1] << 8) | (o[2] << 16) | ((uint32_t)o[3] << 24);
-      v.y = o[4] | (o[5] << 8) | (o[6] << 16) | ((uint32_t)o[7] << 24);
-      v.z = o[8] | (o[9] << 8) | (o[10] << 16) | ((uint32_t)o[11] << 24);
-      v.w = o[12] | (o[13] << 8) | (o[14] << 16) | ((uint32_t)o[15] << 24);
-      *reinterpret_cast<uint4*>(out + b) = v;
+      *reinterpret_cast<uint4*>(out + b) = make_uint4(o[0], o[1], o[2], o[3]);
     } else {
-      for (int k = 0; k < cnt; ++k) out[b + k] = o[k];
+      for (int k = 0; k < cnt; ++k) out[b + k] = (uint8_t)(o[k >> 2] >> (8 * (k & 3)));
     }
-    if (hasN) {  // rare: mark every pair that owns an N in this chunk
+    if (bad) atomicMin(&sum->err_pos, (unsigned long long)(pos_base + b + __ffs(bad) - 1));
+    if (nn) {  // rare: mark every pair that owns an N in this chunk
       for (int k = 0; k < cnt; ++k)
-        if (o[k] == 4u) atomicOr(&flags[find_pair(off, num_pairs, b + k)], 1u);
+        if (((o[k >> 2] >> (8 * (k & 3))) & 0xffu) == 4u)
+          atomicOr(&flags[find_pair(off, num_pairs, b + k)], 1u);
     }
   }
 }
@@ -95,76 +99,109 @@ cudaError_t launch_pack(const char* d_ascii, uint64_t len, uint8_t* d_code, uint
 
 // --------------------------------------------------------------------------- classify
 __global__ void classify_kernel(ClassifyArgs a) {
+  // per-block plan summary (warp-aggregated, then one set of global atomics per block:
+  // the naive per-pair global atomics serialise on a handful of addresses)
+  __shared__ int s_cnt[NV], s_maxn[NV], s_maxm[NV];
+  __shared__ unsigned long long s_kmin[NV], s_kmax[NV];
+  if (threadIdx.x < NV) {
+    s_cnt[threadIdx.x] = 0;
+    s_maxn[threadIdx.x] = 0;
+    s_maxm[threadIdx.x] = 0;
+    s_kmin[threadIdx.x] = ~0ull;
+    s_kmax[threadIdx.x] = 0ull;
+  }
+  __syncthreads();
   const DevParams& P = a.P;
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.num_pairs;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    const int64_t n = (int64_t)(a.q_off[k + 1] - a.q_off[k]);
-    const int64_t m = (int64_t)(a.s_off[k + 1] - a.s_off[k]);
-    if (n == 0 || m == 0) {
-      // empty sequences (SURVEY 8(b) "Empty sequences"): global = one gap run, else 0
-      int32_t sc = 0, ei = 0, ej = 0;
-      if (P.kind == KGLOBAL) {
-        const int64_t len = n + m;
-        sc = len ? (int32_t)(-(P.go + len * P.ge)) : 0;
-        ei = (int32_t)n; ej = (int32_t)m;
-        if (a.ops && len) {
-          const uint64_t base = a.q_off[k] + a.s_off[k] + k;
-          a.ops[base] = ((uint32_t)len << 4) | (n ? 1u : 2u);
-          a.n_ops[k] = 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < a.num_pairs; base += stride) {
+    const uint64_t k = base + threadIdx.x;
+    int v = -1;
+    int64_t n = 0, m = 0;
+    unsigned long long key = 0;
+    if (k < a.num_pairs) {
+      n = (int64_t)(a.q_off[k + 1] - a.q_off[k]);
+      m = (int64_t)(a.s_off[k + 1] - a.s_off[k]);
+      if (n == 0 || m == 0) {
+        // empty sequences (SURVEY 8(b) "Empty sequences"): global = one gap run, else 0
+        int32_t sc = 0, ei = 0, ej = 0;
+        if (P.kind == KGLOBAL) {
+          const int64_t len = n + m;
+          sc = len ? (int32_t)(-(P.go + len * P.ge)) : 0;
+          ei = (int32_t)n; ej = (int32_t)m;
+          if (a.ops && len) {
+            const uint64_t obase = a.q_off[k] + a.s_off[k] + k;
+            a.ops[obase] = ((uint32_t)len << 4) | (n ? 1u : 2u);
+            a.n_ops[k] = 1;
+          } else if (a.ops) {
+            a.n_ops[k] = 0;
+          }
         } else if (a.ops) {
           a.n_ops[k] = 0;
         }
-      } else if (a.ops) {
-        a.n_ops[k] = 0;
-      }
-      a.scores[k] = sc;
-      if (a.end_i) { a.end_i[k] = ei; a.end_j[k] = ej; }
-      if (a.beg_i) { a.beg_i[k] = 0; a.beg_j[k] = 0; }
-      a.keys[k] = ~0ull;
-      a.vals[k] = (int32_t)k;
-      continue;
-    }
-    const bool hasN = a.flags[k] & 1u;
-    // range guards (reading R11): |all intermediate values| bounded by the all-gap path
-    const int64_t padded = n + 192;  // max strip padding of any variant
-    const int64_t neg = 3 * (int64_t)a.cfg.bound_go + (padded + m + 2) * (int64_t)a.cfg.bound_ge + 256;
-    const int64_t posb = (int64_t)max(a.cfg.bound_match, 0) * (padded < m ? padded : m);
-    // VS16 stores global/semi scores with a +2^14 bias; Hop = H - (Go+Ge) is a packed 32-bit
-    // IMAD that must not borrow across halves -> every biased value must stay >= Go+Ge.
-    const bool ok16 = a.cfg.allow16 && !hasN && neg + a.cfg.bound_go + a.cfg.bound_ge <= 16000 &&
-                      posb <= 16000;
-    const bool ok32 = neg <= (1ll << 30) - (1ll << 24) && posb <= (1ll << 30) - (1ll << 24);
-    if (!ok32) atomicExch(&a.sum->range_err, 1);
-    int v = -1;
-    if (a.cfg.force_variant >= 0) {
-      v = a.cfg.force_variant;
-      if (variant_desc(v).pairs == 2 && !ok16) v = a.cfg.tb ? 5 : 4;
-    } else {
-      int best_rows = 0x7fffffff, best_R = 0;
-      for (int c = 0; c < NV; ++c) {
-        const VariantDesc d = variant_desc(c);
-        if (d.tb != a.cfg.tb) continue;
-        if (d.pairs == 2 && !ok16) continue;
-        if (d.pairs == 1 && ok16) continue;
-        const int64_t hs = (int64_t)d.L * d.R;
-        const int64_t rows = (n + hs - 1) / hs * hs;
-        if (rows < best_rows || (rows == best_rows && d.R > best_R)) {
-          best_rows = (int)(rows < 0x7fffffff ? rows : 0x7fffffff);
-          best_R = d.R;
-          v = c;
+        a.scores[k] = sc;
+        if (a.end_i) { a.end_i[k] = ei; a.end_j[k] = ej; }
+        if (a.beg_i) { a.beg_i[k] = 0; a.beg_j[k] = 0; }
+        a.keys[k] = ~0ull;
+        a.vals[k] = (int32_t)k;
+      } else {
+        const bool hasN = a.flags[k] & 1u;
+        // range guards (reading R11): |all intermediate values| bounded by the all-gap path
+        const int64_t padded = n + 192;  // max strip padding of any variant
+        const int64_t neg = 3 * (int64_t)a.cfg.bound_go + (padded + m + 2) * (int64_t)a.cfg.bound_ge + 256;
+        const int64_t posb = (int64_t)max(a.cfg.bound_match, 0) * (padded < m ? padded : m);
+        // VS16 stores global/semi scores with a +2^14 bias; Hop = H - (Go+Ge) is a packed
+        // 32-bit IMAD that must not borrow across halves -> biased values stay >= Go+Ge.
+        const bool ok16 = a.cfg.allow16 && !hasN &&
+                          neg + a.cfg.bound_go + a.cfg.bound_ge <= 16000 && posb <= 16000;
+        const bool ok32 = neg <= (1ll << 30) - (1ll << 24) && posb <= (1ll << 30) - (1ll << 24);
+        if (!ok32) atomicExch(&a.sum->range_err, 1);
+        if (a.cfg.force_variant >= 0) {
+          v = a.cfg.force_variant;
+          if (variant_desc(v).pairs == 2 && !ok16) v = a.cfg.tb ? 5 : 4;
+        } else {
+          int best_rows = 0x7fffffff, best_R = 0;
+          for (int c = 0; c < NV; ++c) {
+            const VariantDesc d = variant_desc(c);
+            if (d.tb != a.cfg.tb) continue;
+            if (d.pairs == 2 && !ok16) continue;
+            if (d.pairs == 1 && ok16) continue;
+            const int64_t hs = (int64_t)d.L * d.R;
+            const int64_t rows = (n + hs - 1) / hs * hs;
+            if (rows < best_rows || (rows == best_rows && d.R > best_R)) {
+              best_rows = (int)(rows < 0x7fffffff ? rows : 0x7fffffff);
+              best_R = d.R;
+              v = c;
+            }
+          }
         }
+        key = ((unsigned long long)v << 58) |
+              ((unsigned long long)(m < (1 << 29) - 1 ? m : (1 << 29) - 1) << 29) |
+              (unsigned long long)(n < (1 << 29) - 1 ? n : (1 << 29) - 1);
+        a.keys[k] = key;
+        a.vals[k] = (int32_t)k;
       }
     }
-    const unsigned long long key = ((unsigned long long)v << 58) |
-                                   ((unsigned long long)(m < (1 << 29) - 1 ? m : (1 << 29) - 1) << 29) |
-                                   (unsigned long long)(n < (1 << 29) - 1 ? n : (1 << 29) - 1);
-    a.keys[k] = key;
-    a.vals[k] = (int32_t)k;
-    atomicAdd(&a.sum->count[v], 1);
-    atomicMax(&a.sum->maxn[v], (int32_t)n);
-    atomicMax(&a.sum->maxm[v], (int32_t)m);
-    atomicMin(&a.sum->kmin[v], key);
-    atomicMax(&a.sum->kmax[v], key);
+    const unsigned grp = __match_any_sync(0xffffffffu, v);
+    if (v >= 0) {
+      const int mxn = __reduce_max_sync(grp, (int)n);
+      const int mxm = __reduce_max_sync(grp, (int)m);
+      if ((threadIdx.x & 31) == __ffs(grp) - 1) {
+        atomicAdd(&s_cnt[v], __popc(grp));
+        atomicMax(&s_maxn[v], mxn);
+        atomicMax(&s_maxm[v], mxm);
+      }
+      atomicMin(&s_kmin[v], key);
+      atomicMax(&s_kmax[v], key);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < NV && s_cnt[threadIdx.x] > 0) {
+    const int v = threadIdx.x;
+    atomicAdd(&a.sum->count[v], s_cnt[v]);
+    atomicMax(&a.sum->maxn[v], s_maxn[v]);
+    atomicMax(&a.sum->maxm[v], s_maxm[v]);
+    atomicMin(&a.sum->kmin[v], s_kmin[v]);
+    atomicMax(&a.sum->kmax[v], s_kmax[v]);
   }
 }
 
