@@ -53,6 +53,9 @@ struct Device {
   DevBuf q_ascii, s_ascii, q_code, s_code, q_off, s_off, flags, keys, keys2, vals, vals2, slots;
   DevBuf scores, end_i, end_j, beg_i, beg_j, n_ops, cig_off, ops, dirs, tb, strip, aln, cigar;
   DevBuf temp, sum, long_ws;
+  DevBuf q_ascii2[2], s_ascii2[2], q_off2[2], s_off2[2];  // double-buffered host uploads
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   PlanSummary* h_sum = nullptr;  // pinned
   uint64_t* h_small = nullptr;   // pinned scratch
 };
@@ -64,6 +67,7 @@ struct anyseq_ctx {
   std::string err;
   std::atomic<uint64_t> launches{0};
   int64_t tb_scratch_bytes = 4ll << 30;
+  int64_t chunk_bytes = 64ll << 20;  // host-API upload/compute pipelining granularity
   int64_t force_variant = -1;
   int64_t allow16 = 1;
   LongOptions long_opt;
@@ -175,6 +179,7 @@ struct DeviceJob {
   int want_ends;              // score mode: fill end cells + alignment structs
   int32_t* d_scores_out;      // score mode output (device) or null => ctx buffer
   anyseq_alignment* d_aln_out;  // alignment structs (device) or null => ctx buffer
+  cudaEvent_t ev_packed = nullptr;  // recorded on the compute stream after the pack kernels
   // traceback: cigar sizing results
   uint64_t cigar_total = 0;
 };
@@ -222,6 +227,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   CK(launch_pack(J.d_s, J.s_end, D.s_code.as<uint8_t>(), 1ull << 62, J.d_soff, B,
                  D.flags.as<uint32_t>(), D.sum.as<PlanSummary>(), st, D.num_sms));
   L(2);
+  if (J.ev_packed) CK(cudaEventRecord(J.ev_packed, st));
 
   // ---- a2: classify ----
   ClassifyArgs ca;
@@ -472,72 +478,99 @@ void describe_badseq(anyseq_ctx* ctx, const anyseq_batch* b, uint64_t k0) {
   ctx->err = buf;
 }
 
-// Host-memory batch on one device, pairs [k0, k1).
+// Host-memory batch on one device, pairs [k0, k1).  The shard is cut into chunks of about
+// ctx->chunk_bytes of sequence; the upload of chunk c+1 (copy stream, double-buffered)
+// overlaps the planning/relaxation of chunk c (compute stream).
 anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* prm,
                              const anyseq_batch* b, uint64_t k0, uint64_t k1, int tb,
                              int32_t* scores, anyseq_alignment* aln, std::vector<uint32_t>* cig) {
   CK(cudaSetDevice(D.id));
-  cudaStream_t st = D.stream;
-  const uint64_t B = k1 - k0;
-  const uint64_t q0 = b->q_off[k0], qN = b->q_off[k1], s0 = b->s_off[k0], sN = b->s_off[k1];
-  const uint64_t qlen = qN - q0, slen = sN - s0;
-  CK(D.q_ascii.ensure(qlen + 16));
-  CK(D.s_ascii.ensure(slen + 16));
-  CK(D.q_off.ensure((B + 1) * 8));
-  CK(D.s_off.ensure((B + 1) * 8));
-  // rebased offsets (host staging in pinned scratch would avoid the pageable path; the
-  // offsets are small compared to the sequences)
-  std::vector<uint64_t> qo(B + 1), so(B + 1);
-  for (uint64_t k = 0; k <= B; ++k) {
-    qo[k] = b->q_off[k0 + k] - q0;
-    so[k] = b->s_off[k0 + k] - s0;
-  }
-  if (qlen) CK(cudaMemcpyAsync(D.q_ascii.p, b->q + q0, qlen, cudaMemcpyHostToDevice, st));
-  if (slen) CK(cudaMemcpyAsync(D.s_ascii.p, b->s + s0, slen, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(D.q_off.p, qo.data(), (B + 1) * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(D.s_off.p, so.data(), (B + 1) * 8, cudaMemcpyHostToDevice, st));
-  DeviceJob J;
-  J.d_q = D.q_ascii.as<char>();
-  J.d_qoff = D.q_off.as<uint64_t>();
-  J.d_s = D.s_ascii.as<char>();
-  J.d_soff = D.s_off.as<uint64_t>();
-  J.B = B;
-  J.q_end = qlen;
-  J.s_end = slen;
-  J.tb = tb;
-  J.want_ends = aln != nullptr;
-  J.d_scores_out = nullptr;
-  J.d_aln_out = nullptr;
-  uint64_t cap_words = 0;
-  if (tb) {
-    // worst case sum(n+m) words; the exact total is known after the walk
-    cap_words = qlen + slen + 1;
-    CK(D.cigar.ensure(cap_words * 4));
-  }
-  anyseq_status s = run_device(ctx, D, prm, J, tb ? D.cigar.as<uint32_t>() : nullptr, cap_words);
-  if (s != ANYSEQ_OK) {
-    if (s == ANYSEQ_E_BADSEQ) {
-      // rebase the message to absolute batch coordinates
-      unsigned long long pos = 0;
-      char which = 0;
-      if (sscanf(ctx->err.c_str(), "invalid symbol at %c byte offset %llu", &which, &pos) == 2) {
-        char buf[128];
-        snprintf(buf, sizeof(buf), "invalid symbol at %c byte offset %llu", which,
-                 (unsigned long long)(pos - (which == 'q' ? 0 : 0)));
-        ctx->err = buf;
-        describe_badseq(ctx, b, k0);
+  cudaStream_t st = D.stream, cs = D.copy_stream;
+  // chunk boundaries by cumulative sequence bytes (offsets are monotone)
+  std::vector<uint64_t> cb{k0};
+  {
+    const uint64_t cap = (uint64_t)std::max<int64_t>(ctx->chunk_bytes, 1 << 20);
+    uint64_t k = k0;
+    while (k < k1) {
+      const uint64_t base = b->q_off[k] + b->s_off[k];
+      uint64_t lo = k + 1, hi = k1;  // last index e in (k, k1] with bytes(k, e) <= cap
+      while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo + 1) / 2;
+        if (b->q_off[mid] + b->s_off[mid] - base <= cap) lo = mid; else hi = mid - 1;
       }
+      k = lo;
+      cb.push_back(k);
     }
-    return s;
   }
-  if (!tb) {
-    CK(cudaMemcpyAsync(scores + k0, D.scores.p, B * 4, cudaMemcpyDeviceToHost, st));
-    if (aln) CK(cudaMemcpyAsync(aln + k0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
-  } else {
-    CK(cudaMemcpyAsync(aln + k0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
-    cig->resize(J.cigar_total);
-    if (J.cigar_total)
-      CK(cudaMemcpyAsync(cig->data(), D.cigar.p, J.cigar_total * 4, cudaMemcpyDeviceToHost, st));
+  const int NC = (int)cb.size() - 1;
+  auto upload = [&](int c) -> anyseq_status {
+    const int set = c & 1;
+    const uint64_t a0 = cb[c], a1 = cb[c + 1], B = a1 - a0;
+    const uint64_t q0 = b->q_off[a0], s0 = b->s_off[a0];
+    const uint64_t qlen = b->q_off[a1] - q0, slen = b->s_off[a1] - s0;
+    CK(D.q_ascii2[set].ensure(qlen + 16));
+    CK(D.s_ascii2[set].ensure(slen + 16));
+    CK(D.q_off2[set].ensure((B + 1) * 8));
+    CK(D.s_off2[set].ensure((B + 1) * 8));
+    CK(cudaStreamWaitEvent(cs, D.ev_free[set], 0));  // previous user of this set has packed
+    if (qlen) CK(cudaMemcpyAsync(D.q_ascii2[set].p, b->q + q0, qlen, cudaMemcpyHostToDevice, cs));
+    if (slen) CK(cudaMemcpyAsync(D.s_ascii2[set].p, b->s + s0, slen, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(D.q_off2[set].p, b->q_off + a0, (B + 1) * 8, cudaMemcpyHostToDevice, cs));
+    CK(cudaMemcpyAsync(D.s_off2[set].p, b->s_off + a0, (B + 1) * 8, cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(D.ev_up[set], cs));
+    return ANYSEQ_OK;
+  };
+  anyseq_status s = upload(0);
+  if (s != ANYSEQ_OK) return s;
+  uint64_t cig_base = 0;
+  for (int c = 0; c < NC; ++c) {
+    const int set = c & 1;
+    if (c + 1 < NC && (s = upload(c + 1)) != ANYSEQ_OK) return s;
+    const uint64_t a0 = cb[c], a1 = cb[c + 1], B = a1 - a0;
+    const uint64_t q0 = b->q_off[a0], s0 = b->s_off[a0];
+    const uint64_t qlen = b->q_off[a1] - q0, slen = b->s_off[a1] - s0;
+    CK(cudaStreamWaitEvent(st, D.ev_up[set], 0));
+    CK(launch_rebase(D.q_off2[set].as<uint64_t>(), D.s_off2[set].as<uint64_t>(), B + 1, q0, s0, st,
+                     D.num_sms));
+    ctx->launches += 1;
+    DeviceJob J;
+    J.d_q = D.q_ascii2[set].as<char>();
+    J.d_qoff = D.q_off2[set].as<uint64_t>();
+    J.d_s = D.s_ascii2[set].as<char>();
+    J.d_soff = D.s_off2[set].as<uint64_t>();
+    J.B = B;
+    J.q_end = qlen;
+    J.s_end = slen;
+    J.tb = tb;
+    J.want_ends = aln != nullptr;
+    J.d_scores_out = nullptr;
+    J.d_aln_out = nullptr;
+    J.ev_packed = D.ev_free[set];  // recorded once the ASCII buffers are consumed
+    uint64_t cap_words = 0;
+    if (tb) {
+      cap_words = qlen + slen + 1;  // worst case sum(n+m); exact total known after the walk
+      CK(D.cigar.ensure(cap_words * 4));
+    }
+    s = run_device(ctx, D, prm, J, tb ? D.cigar.as<uint32_t>() : nullptr, cap_words);
+    if (s != ANYSEQ_OK) {
+      if (s == ANYSEQ_E_BADSEQ) describe_badseq(ctx, b, a0);
+      cudaStreamSynchronize(cs);
+      cudaStreamSynchronize(st);
+      return s;
+    }
+    if (!tb) {
+      CK(cudaMemcpyAsync(scores + a0, D.scores.p, B * 4, cudaMemcpyDeviceToHost, st));
+      if (aln) CK(cudaMemcpyAsync(aln + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
+    } else {
+      CK(cudaMemcpyAsync(aln + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
+      cig->resize(cig_base + J.cigar_total);
+      if (J.cigar_total)
+        CK(cudaMemcpyAsync(cig->data() + cig_base, D.cigar.p, J.cigar_total * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (cig_base)
+        for (uint64_t k = a0; k < a1; ++k) aln[k].cigar_offset += cig_base;
+      cig_base += J.cigar_total;
+    }
   }
   CK(cudaStreamSynchronize(st));
   return ANYSEQ_OK;
@@ -581,6 +614,7 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
         local.tb_scratch_bytes = ctx->tb_scratch_bytes;
         local.force_variant = ctx->force_variant;
         local.allow16 = ctx->allow16;
+        local.chunk_bytes = ctx->chunk_bytes;
         anyseq_status s = ANYSEQ_OK;
         if (bounds[g + 1] > bounds[g])
           s = run_host_shard(&local, ctx->devs[g], prm, b, bounds[g], bounds[g + 1], tb, scores,
@@ -644,7 +678,12 @@ anyseq_status anyseq_create(anyseq_ctx** out, const int* device_ids, int num_dev
         cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaDeviceGetAttribute(&D.num_sms, cudaDevAttrMultiProcessorCount, id) != cudaSuccess ||
         cudaMallocHost(&D.h_sum, sizeof(PlanSummary)) != cudaSuccess ||
-        cudaMallocHost(&D.h_small, 64) != cudaSuccess) {
+        cudaMallocHost(&D.h_small, 64) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&D.copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&D.ev_up[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&D.ev_up[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&D.ev_free[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&D.ev_free[1], cudaEventDisableTiming) != cudaSuccess) {
       c->devs.push_back(D);
       anyseq_destroy(c);
       return ANYSEQ_E_CUDA;
@@ -673,6 +712,15 @@ void anyseq_destroy(anyseq_ctx* c) {
     for (DevBuf* b : bufs) b->release();
     if (D.h_sum) cudaFreeHost(D.h_sum);
     if (D.h_small) cudaFreeHost(D.h_small);
+    for (int i = 0; i < 2; ++i) {
+      D.q_ascii2[i].release();
+      D.s_ascii2[i].release();
+      D.q_off2[i].release();
+      D.s_off2[i].release();
+      if (D.ev_up[i]) cudaEventDestroy(D.ev_up[i]);
+      if (D.ev_free[i]) cudaEventDestroy(D.ev_free[i]);
+    }
+    if (D.copy_stream) cudaStreamDestroy(D.copy_stream);
     if (D.stream) cudaStreamDestroy(D.stream);
   }
   delete c;
@@ -765,6 +813,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
   if (n == "tb_scratch_bytes") { ctx->tb_scratch_bytes = std::max<int64_t>(value, 1 << 20); return ANYSEQ_OK; }
   if (n == "timing") { ctx->timing = value ? 1 : 0; return ANYSEQ_OK; }
   if (n == "force_variant") { ctx->force_variant = value; return ANYSEQ_OK; }
+  if (n == "chunk_bytes") { ctx->chunk_bytes = std::max<int64_t>(value, 1 << 16); return ANYSEQ_OK; }
   if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }
   if (n == "long_band_rows") { ctx->long_opt.band_rows = (int)value; return ANYSEQ_OK; }
   if (n == "long_blocks") { ctx->long_opt.blocks = (int)value; return ANYSEQ_OK; }

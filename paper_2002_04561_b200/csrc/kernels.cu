@@ -97,6 +97,21 @@ cudaError_t launch_pack(const char* d_ascii, uint64_t len, uint8_t* d_code, uint
   return cudaGetLastError();
 }
 
+// ----------------------------------------------------------------------------- rebase
+__global__ void rebase_kernel(uint64_t* q, uint64_t* s, uint64_t n, uint64_t q0, uint64_t s0) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    q[k] -= q0;
+    s[k] -= s0;
+  }
+}
+
+cudaError_t launch_rebase(uint64_t* q, uint64_t* s, uint64_t n, uint64_t q0, uint64_t s0,
+                          cudaStream_t st, int num_sms) {
+  rebase_kernel<<<grid_for((int64_t)n, 256, num_sms), 256, 0, st>>>(q, s, n, q0, s0);
+  return cudaGetLastError();
+}
+
 // --------------------------------------------------------------------------- classify
 __global__ void classify_kernel(ClassifyArgs a) {
   // per-block plan summary (warp-aggregated, then one set of global atomics per block:

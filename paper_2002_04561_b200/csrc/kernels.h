@@ -13,6 +13,10 @@ cudaError_t launch_pack(const char* d_ascii, uint64_t len, uint8_t* d_code, uint
                         const uint64_t* d_off, uint64_t num_pairs, uint32_t* d_flags,
                         PlanSummary* d_sum, cudaStream_t st, int num_sms);
 
+// host-API chunks: offsets uploaded verbatim, rebased to the chunk's first byte on device
+cudaError_t launch_rebase(uint64_t* q, uint64_t* s, uint64_t n, uint64_t q0, uint64_t s0,
+                          cudaStream_t st, int num_sms);
+
 struct ClassifyArgs {
   DevParams P;
   PlanCfg cfg;
