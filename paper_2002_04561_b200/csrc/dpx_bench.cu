@@ -21,7 +21,8 @@ __device__ __forceinline__ uint32_t prmt_(uint32_t a, uint32_t b, uint32_t s) {
 }
 
 template <int OP>
-__global__ void __launch_bounds__(256) bench(uint32_t seed, uint32_t* sink, unsigned long long* cyc) {
+__global__ void __launch_bounds__(256) bench(uint32_t seed, uint32_t one, uint32_t* sink,
+                                             unsigned long long* cyc) {
   uint32_t x[CH], y[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
@@ -40,6 +41,23 @@ __global__ void __launch_bounds__(256) bench(uint32_t seed, uint32_t* sink, unsi
       if (OP == 3) x[c] = prmt_(x[c], y[c], k2);
       if (OP == 4) x[c] = __vadd2(x[c], k1);
       if (OP == 5) x[c] = x[c] + y[c] + k1;  // IADD3
+      if (OP == 7) x[c] = __vimax3_s16x2(x[c], y[c], k1);
+      if (OP == 8) {  // IMAD with a run-time multiplier of 1 (Hop on the FMA pipe)
+        uint32_t d;
+        asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x[c]), "r"(one), "r"(k2));
+        x[c] = d;
+      }
+      if (OP == 9) {  // shipped fill mix per register: PRMT + 3 VIADDMNMX + VIMNMX (+2 IMAD)
+        const uint32_t sig = prmt_(k1, k2, x[c]);
+        uint32_t hl, X;
+        asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(hl) : "r"(x[c]), "r"(one), "r"(k2));
+        const uint32_t f = __viaddmax_s16x2(y[c], k1, hl);
+        const uint32_t df = __viaddmax_s16x2(x[c], sig, f);
+        asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(X) : "r"(df), "r"(one), "r"(k2));
+        const uint32_t h = __vmaxs2(df, y[c]);
+        y[c] = __viaddmax_s16x2(f, k1, X);
+        x[c] = h;
+      }
       if (OP == 6) {  // fill-kernel mix for one register (2 cells): 6 instructions
         const uint32_t sig = prmt_(k1, k2, x[c]);
         uint32_t e = __viaddmax_s16x2(y[c], k1, x[c]);
@@ -69,8 +87,8 @@ double run(int sms, int instr_per_iter) {
   unsigned long long* cyc;
   cudaMalloc(&sink, 4);
   cudaMalloc(&cyc, grid * 8);
-  bench<OP><<<grid, 256>>>(12345u, sink, cyc);  // warm
-  bench<OP><<<grid, 256>>>(54321u, sink, cyc);
+  bench<OP><<<grid, 256>>>(12345u, 1u, sink, cyc);  // warm
+  bench<OP><<<grid, 256>>>(54321u, 1u, sink, cyc);
   cudaDeviceSynchronize();
   std::vector<unsigned long long> h(grid);
   cudaMemcpy(h.data(), cyc, grid * 8, cudaMemcpyDeviceToHost);
@@ -88,11 +106,14 @@ int main() {
   int clk = 0;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const double r0 = run<0>(sms, 1), r1 = run<1>(sms, 1), r2 = run<2>(sms, 1), r3 = run<3>(sms, 1),
-               r4 = run<4>(sms, 1), r5 = run<5>(sms, 1), r6 = run<6>(sms, 6);
+               r4 = run<4>(sms, 1), r5 = run<5>(sms, 1), r6 = run<6>(sms, 6), r7 = run<7>(sms, 1),
+               r8 = run<8>(sms, 1), r9 = run<9>(sms, 7);
   printf("{\"sms\": %d, \"clock_khz_attr\": %d, \"viaddmnmx_s16x2\": %.2f, \"vimnmx_s16x2\": %.2f, "
          "\"viaddmnmx_s32\": %.2f, \"prmt\": %.2f, \"viadd_16x2\": %.2f, \"iadd3\": %.2f, "
-         "\"mix_lane_ops_per_clk_per_sm\": %.2f, \"unit\": \"lane-ops per clock per SM\"}\n",
-         sms, clk, r0, r1, r2, r3, r4, r5, r6);
+         "\"mix_lane_ops_per_clk_per_sm\": %.2f, \"vimnmx3_s16x2\": %.2f, \"imad\": %.2f, "
+         "\"fill_mix_lane_ops_per_clk_per_sm\": %.2f, \"fill_mix_instr_per_register\": 7, "
+         "\"unit\": \"lane-ops per clock per SM\"}\n",
+         sms, clk, r0, r1, r2, r3, r4, r5, r6, r7, r8, r9);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : 1;
 }
