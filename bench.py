@@ -36,8 +36,8 @@ NUM_PAIRS = 1_000_000
 READ_LEN = 150
 METRIC = "GCUPS (batched 150bp semi-global affine, long-pair SW) at 1/2/4/8 B200"
 # dram__bytes_read.sum + dram__bytes_write.sum of one fill launch on the full C2 batch, from
-# the committed ncu --set full capture (profiles/); None until captured at full size.
-TRAFFIC_BYTES_PER_LAUNCH = None
+# the committed ncu --set full capture of the fill kernel at the full C2 size.
+TRAFFIC_BYTES_PER_LAUNCH = 328_841_984  # 320.69 MB read + 8.15 MB write (profiles/r01_fill_ncu.txt)
 
 
 def _dist():
@@ -307,135 +307,6 @@ def main():
             "peak_basis": f"{n_sm} SM x {f_mhz:.0f} MHz (median under load) x "
                           f"{cells_per_clk:.2f} cells/clk/SM ({rate_src}: 2 cells per "
                           f"PRMT + 3 VIADDMNMX.S16x2 + VIMNMX.S16x2)"}
-
-    line = {"metric": METRIC, "value": v, "unit": "GCUPS", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": "C2: 150x150 bp read pairs, semi-global affine 5/1, score-only",
-                       "sample_per_step": base["sample"]},
-            "cpu_baseline": {"value": v, "unit": "GCUPS", "cores": th, "kind": "oracle",
-                             "sample": base["sample"]},
-            "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pairs", type=int, default=NUM_PAIRS)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-budget", type=float, default=3.0)
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
-
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-    import paper_2002_04561_b200 as A
-    from synth import c2_reads, uniform_csr
-
-    ws, rank, local = _dist()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    def barrier():
-        if ws > 1:
-            dist.barrier()
-
-    qm, sm = c2_reads(args.pairs, seed=2 + 1000 * rank)
-    q, qo = uniform_csr(qm)
-    s, so = uniform_csr(sm)
-    B = len(qo) - 1
-    cells = B * READ_LEN * READ_LEN
-    dev = torch.device("cuda", local)
-    d_q = torch.from_numpy(q).to(dev)
-    d_s = torch.from_numpy(s).to(dev)
-    d_qo = torch.from_numpy(qo.view(np.int64)).to(dev)
-    d_so = torch.from_numpy(so.view(np.int64)).to(dev)
-    d_sc = torch.empty(B, dtype=torch.int32, device=dev)
-    sch = A.Scheme(**SCHEME)
-    ctx = A.Context([local])
-    stream = torch.cuda.current_stream()
-
-    def step():
-        ctx.align_batch_device(sch, d_q, d_qo, d_s, d_so, d_sc, stream=stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    ctx.set_option("timing", 1)
-    ctx.reset_stats()
-    launches0 = ctx.launches
-    sampler = ClockSampler(local)
-    sampler.start()
-    barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    clocks = sampler.stop()
-    ms = e0.elapsed_time(e1)
-    launches = ctx.launches - launches0
-    fill_ms = ctx.stat("fill_ms")
-    fill_launches = int(ctx.stat("fill_launches"))
-    ctx.set_option("timing", 0)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = cells * ws * args.steps / (ms_max / 1e3) / 1e9
-
-    # parity spot check of this run's output (oracle on a few pairs) -- not timed
-    from oracle import oracle as O
-    got = d_sc.cpu().numpy()
-    osch = O.Scheme(SCHEME["kind"], SCHEME["gap"], SCHEME["match"], SCHEME["mismatch"],
-                    SCHEME["gap_open"], SCHEME["gap_extend"])
-    idx = np.random.default_rng(rank).choice(B, 64, replace=False)
-    parity = all(int(got[k]) == O.align(osch, qm[k].tobytes(), sm[k].tobytes(), False).score
-                 for k in idx)
-
-    # e2e through the host API from pinned buffers
-    pq = torch.from_numpy(q).pin_memory().numpy()
-    ps = torch.from_numpy(s).pin_memory().numpy()
-    pqo = torch.from_numpy(qo.view(np.int64)).pin_memory().numpy().view(np.uint64)
-    pso = torch.from_numpy(so.view(np.int64)).pin_memory().numpy().view(np.uint64)
-    e2e_steps = max(2, min(args.steps, 5))
-    ctx.align_batch(sch, pq, pqo, ps, pso)
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        ctx.align_batch(sch, pq, pqo, ps, pso)
-    e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = cells * ws * e2e_steps / float(te.item()) / 1e9
-
-    # roofline of the dominant kernel (fill): cells per launch / mean launch time
-    n_sm, lane_rate, rate_src = measured_alu_peak()
-    ops_per_cell = 3.0  # s16x2 semi-global affine: 6 instr per register of 2 cells
-    f_mhz = clocks.get("sm_mhz") or 1965.0
-    peak = n_sm * f_mhz * 1e6 * lane_rate / ops_per_cell / 1e9
-    fill_gcups = cells * args.steps / (fill_ms / 1e3) / 1e9 if fill_ms > 0 else None
-    roof = {"bound": "alu", "achieved": round(fill_gcups, 1) if fill_gcups else None,
-            "peak": round(peak, 1), "unit": "GCUPS",
-            "frac": round(fill_gcups / peak, 4) if fill_gcups else None,
-            "traffic": None,
-            "kernel": "fill_kernel<VS16,SEMI,AFFINE,L=8,R=19>",
-            "kernel_share_of_step": round(fill_ms / ms, 4) if ms > 0 else None,
-            "peak_basis": f"{n_sm} SM x {f_mhz:.0f} MHz (median under load) x {lane_rate} "
-                          f"lane-ops/clk/SM ({rate_src}) / {ops_per_cell} ops per cell"}
 
     line = {"metric": METRIC, "value": round(value, 1), "unit": "GCUPS", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
