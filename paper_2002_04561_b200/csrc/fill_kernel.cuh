@@ -136,13 +136,17 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
       S8 = (M + L - 1 + 7) >> 3;
     }
 
-    const bool tab = Mw <= SELCAP;  // warp-uniform
-    if (tab) {
-      for (int c = t; c < M; c += L) {
-        const uint32_t c0 = (c < mm[0]) ? a.scode[so[0] + c] : 0u;
-        const uint32_t c1 = (PP == 2 && c < mm[PP - 1]) ? a.scode[so[PP - 1] + c] : 0u;
-        seltab[gb][c] = (uint16_t)V::selector(c0, c1);
+    // column selectors of this slot in a 512-entry shared ring: columns [0, 384) now, then
+    // 128 more every 128 steps (a lane at step k reads column k - t, t < L <= 8)
+    auto fill_sel = [&](int c0, int c1) {
+      for (int c = c0 + t; c < c1; c += L) {
+        const uint32_t x0 = (c < mm[0]) ? a.scode[so[0] + c] : 0u;
+        const uint32_t x1 = (PP == 2 && c < mm[PP - 1]) ? a.scode[so[PP - 1] + c] : 0u;
+        seltab[gb][c & (SELCAP - 1)] = (uint16_t)V::selector(x0, x1);
       }
+    };
+    if (Mw <= SELCAP) {  // the whole slot fits: built once for all strips
+      fill_sel(0, M);
       __syncwarp();
     }
 
@@ -164,6 +168,10 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
 
     for (int st = 0; st < NSw; ++st) {
       const bool sact = st < NS;
+      if (Mw > SELCAP) {  // ring restarts with every strip
+        fill_sel(0, min(M, 384));
+        __syncwarp();
+      }
       const bool last_strip = (st == NS - 1);
       const int ip0 = st * HS + t * R;  // first physical row of this lane
       uint32_t p0[R], p1[R];
@@ -206,13 +214,6 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         diag = enc(dv, dv);
       }
       T Hbot = NEG, Ebot = NEG;
-      uint32_t selb = 0;
-      // lane 0: subject codes of the next column (prefetched one step ahead)
-      uint32_t nc0 = 0, nc1 = 0;
-      if (t == 0 && sact && !tab) {
-        if (mm[0] > 0) nc0 = a.scode[so[0]];
-        if (PP == 2 && mm[PP - 1] > 0) nc1 = a.scode[so[PP - 1]];
-      }
       // per-strip local trackers (merged by key at strip end)
       int sv[PP], si[PP], sj[PP];
 #pragma unroll
@@ -235,9 +236,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         T hin = V::shfl_up(Hbot, L);
         T ein = (GAP == GAFFINE) ? V::shfl_up(Ebot, L) : NEG;
         const int col = k - t;
-        uint32_t sel;
-        if (tab) sel = seltab[gb][col & (SELCAP - 1)];
-        else sel = __shfl_up_sync(0xffffffffu, selb, 1, L);
+        const uint32_t sel = seltab[gb][col & (SELCAP - 1)];
         const bool act = sact && col >= 0 && col < M;
         if (col == 0 && sact) {
 #pragma unroll
@@ -253,21 +252,17 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
             for (int X = 0; X < PP; ++X) rj[X] = 0;
           }
         }
-        if (t == 0 && act) {
-          if (st == 0) {
-            const int h0 = (KIND == KGLOBAL) ? -(P.go + (col + 1) * P.ge) : 0;  // H(0,j)
-            hin = enc(h0, h0);
-            ein = FAST ? hop(hin) : NEG;  // FAST: E(1,j) = H(0,j) - Go - Ge; else E(0,j) = -inf
-          } else {
-            const uint2 v = scr[col];
-            hin = (T)v.x;
-            ein = (T)v.y;
+        if (st == 0) {  // the initial row (P:259 / P:262): no load, no branch
+          const int h0 = (KIND == KGLOBAL) ? -(P.go + (col + 1) * P.ge) : 0;  // H(0,j)
+          const T h0v = enc(h0, h0);
+          if (t == 0) {
+            hin = h0v;
+            ein = FAST ? hop(h0v) : NEG;  // FAST: E(1,j) = H(0,j) - Go - Ge; else E(0,j) = -inf
           }
-          if (!tab) {
-            sel = V::selector(nc0, nc1);
-            nc0 = (col + 1 < mm[0]) ? a.scode[so[0] + col + 1] : 0u;
-            if (PP == 2) nc1 = (col + 1 < mm[PP - 1]) ? a.scode[so[PP - 1] + col + 1] : 0u;
-          }
+        } else if (t == 0 && act) {
+          const uint2 v = scr[col];
+          hin = (T)v.x;
+          ein = (T)v.y;
         }
         // FAST = affine score-only: the reassociated recurrence
         //   F  = max(F - Ge, H_left - Go - Ge)          Eq. (5)
@@ -340,7 +335,6 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         diag = hin;
         Hbot = Hq[R - 1];
         Ebot = e;
-        selb = sel;
         if (act && t == L - 1 && st + 1 < NS) scr[col] = make_uint2((uint32_t)Hq[R - 1], (uint32_t)e);
 
         // ---- optimum bookkeeping ----
@@ -401,9 +395,10 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         }
         // a pair's last column m: park this lane's H(., m) in shared memory (semi: column
         // candidates, global: H(n,m)); evaluated after the sweep, off the hot path
+        if (act && (col == mm[0] - 1 || (PP == 2 && col == mm[PP - 1] - 1))) {
 #pragma unroll
         for (int X = 0; X < PP; ++X) {
-          if (act && col == mm[X] - 1) {
+          if (col == mm[X] - 1) {
             if (KIND != KLOCAL) {
 #pragma unroll
               for (int r = 0; r < R; ++r) capbuf[X][threadIdx.x][r] = (uint32_t)Hq[r];
@@ -411,6 +406,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
             if (KIND == KLOCAL && !pos) best = V::select_mask(V::vmax(best, sbest), 1u << X, best);
             if (KIND == KSEMI && !pos && last_strip) bfin = V::select_mask(best, 1u << X, bfin);
           }
+        }
         }
         if (TB && valid && sact) {
           const int Kslot = M + L - 1;
@@ -428,6 +424,10 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
 
       int k = 0;
       for (; k + 1 < K; k += 2) {
+        if (Mw > SELCAP && (k & 127) == 0 && k > 0) {  // warp-uniform ring refill
+          fill_sel(k + 256, min(M, k + 384));
+          __syncwarp();
+        }
         step(k, HA, HB);
         step(k + 1, HB, HA);
       }
