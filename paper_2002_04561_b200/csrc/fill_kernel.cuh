@@ -31,6 +31,7 @@
 #pragma once
 #include "common.cuh"
 #include "fill_args.h"
+#include <type_traits>
 
 namespace anyseq {
 
@@ -232,13 +233,16 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
       // Every lane relaxes its rows in every step (no divergent "active" region: a lane
       // outside its column range computes values nobody reads).  A lane loads its initial
       // column when it reaches column 0 and hands over captures at its last column.
-      auto step = [&](const int k, T (&Hi)[R], T (&Hq)[R]) {
+      // CHK = this step may contain a lane's column 0 (initial column) or a pair's column m
+      // (captures); the steady-state steps in between run without those checks.
+      auto step = [&](auto chk, const int k, T (&Hi)[R], T (&Hq)[R]) {
+        constexpr bool CHK = decltype(chk)::value;
         T hin = V::shfl_up(Hbot, L);
         T ein = (GAP == GAFFINE) ? V::shfl_up(Ebot, L) : NEG;
         const int col = k - t;
         const uint32_t sel = seltab[gb][col & (SELCAP - 1)];
         const bool act = sact && col >= 0 && col < M;
-        if (col == 0 && sact) {
+        if (CHK && col == 0 && sact) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             Hi[r] = init_col(ip0 + r);
@@ -395,7 +399,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         }
         // a pair's last column m: park this lane's H(., m) in shared memory (semi: column
         // candidates, global: H(n,m)); evaluated after the sweep, off the hot path
-        if (act && (col == mm[0] - 1 || (PP == 2 && col == mm[PP - 1] - 1))) {
+        if (CHK && act && (col == mm[0] - 1 || (PP == 2 && col == mm[PP - 1] - 1))) {
 #pragma unroll
         for (int X = 0; X < PP; ++X) {
           if (col == mm[X] - 1) {
@@ -422,16 +426,42 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         }
       };
 
+      // phases: [0, kA) checked (lanes enter column 0), [kA, kB) plain, [kB, K) checked
+      // (lanes leave a pair's last column); kA, kB even and warp-uniform.
+      const std::integral_constant<bool, true> CHK_ON{};
+      const std::integral_constant<bool, false> CHK_OFF{};
+      int mmin = 0x7fffffff;  // smallest pair width in the warp (captures start there)
+#pragma unroll
+      for (int X = 0; X < PP; ++X)
+        if (valid && pr[X] >= 0) mmin = min(mmin, mm[X]);
+      const int Mmin = __reduce_min_sync(0xffffffffu, mmin);
+      const int kA = min(K & ~1, (L + 1) & ~1);
+      const int kB = max(kA, min(K, Mmin - 1) & ~1);
       int k = 0;
-      for (; k + 1 < K; k += 2) {
+      for (; k < kA; k += 2) {
+        step(CHK_ON, k, HA, HB);
+        step(CHK_ON, k + 1, HB, HA);
+      }
+      while (k < kB) {
         if (Mw > SELCAP && (k & 127) == 0 && k > 0) {  // warp-uniform ring refill
           fill_sel(k + 256, min(M, k + 384));
           __syncwarp();
         }
-        step(k, HA, HB);
-        step(k + 1, HB, HA);
+        const int kend = min(kB, (k & ~127) + 128);
+        for (; k < kend; k += 2) {
+          step(CHK_OFF, k, HA, HB);
+          step(CHK_OFF, k + 1, HB, HA);
+        }
       }
-      if (k < K) step(k, HA, HB);
+      for (; k + 1 < K; k += 2) {
+        if (Mw > SELCAP && (k & 127) == 0 && k > 0) {
+          fill_sel(k + 256, min(M, k + 384));
+          __syncwarp();
+        }
+        step(CHK_ON, k, HA, HB);
+        step(CHK_ON, k + 1, HB, HA);
+      }
+      if (k < K) step(CHK_ON, k, HA, HB);
 
       __syncwarp();  // capbuf writes of this strip are visible (all lanes participate)
       if (KIND != KLOCAL && sact) {
