@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <type_traits>
 #include "../../include/anyseq.h"
 #include "kernels.h"
 #include "long.h"
@@ -51,6 +52,8 @@ struct LongArgs {
   LongPart* parts;
   int32_t* abort_flag;
   int32_t chunk;
+  int32_t one;
+  int32_t lag;
   long long spin_limit;
 };
 
@@ -75,22 +78,44 @@ __device__ __forceinline__ bool lkey_better(int v, int i, int j, int bv, int bi,
   return v > bv || (v == bv && (j < bj || (j == bj && i < bi)));
 }
 
-// lane 0 waits until *p >= need (acquire); returns false on timeout/abort (warp-uniform)
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_sys(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// lane 0 polls *p >= need with relaxed loads (no L1 invalidation per poll) and closes with
+// one acquire fence; returns false on timeout/abort (warp-uniform).
 template <bool SYS>
 __device__ __forceinline__ bool warp_wait(const int* p, int need, const LongArgs& a) {
   int ok = 1;
   if ((threadIdx.x & 31) == 0) {
-    long long spins = 0;
-    while ((SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p)) < need) {
-      if (++spins > a.spin_limit || *(volatile int*)a.abort_flag) {
-        atomicExch(a.abort_flag, 1);
-        ok = 0;
-        break;
+    if ((SYS ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) < need) {
+      long long spins = 0;
+      while ((SYS ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) < need) {
+        if ((++spins & 255) == 0 && (spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
+          atomicExch(a.abort_flag, 1);
+          ok = 0;
+          break;
+        }
+        __nanosleep(32);
       }
-      __nanosleep(64);
     }
+    if (SYS) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
+__device__ __forceinline__ int imad_add_s(int x, uint32_t one, int k) {
+  int d;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(one), "r"(k));
+  return d;
 }
 
 template <int KIND, int GAP, int R>
@@ -98,12 +123,20 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
   typedef VS32 V;
   constexpr int L = 32;
   constexpr int HS = L * R;
+  constexpr bool FAST = GAP == GAFFINE;  // reassociated affine recurrence (see fill_kernel.cuh)
+  constexpr int RING = 256;              // per-warp ring of lane-0 inputs and selectors
+  constexpr int PER = 64;                // refill period (steps)
+  __shared__ int2 ring_he[4][RING];
+  __shared__ uint16_t ring_sel[4][RING];
   const int t = threadIdx.x & 31;
+  const int wb = threadIdx.x >> 5;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const DevParams P = a.P;
   const int NEG = NEG32;
   const int NGE = -P.ge;
-  const int NOC = (GAP == GAFFINE) ? -(P.go + P.ge) : -P.ge;
+  const int cop = (GAP == GAFFINE) ? (P.go + P.ge) : P.ge;
+  const uint32_t one = (uint32_t)a.one;
+  auto hop = [&](int h) -> int { return imad_add_s(h, one, -cop); };  // FMA pipe
   const int n = a.n, m = a.m;
   // semi/global: where row n lives inside the last row strip
   const int tn = ((n - 1) % HS) / R, rn = (n - 1) % R;
@@ -127,13 +160,14 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
     const int ip0 = s * HS + t * R;
     const int2* bl = a.bcol[g];
     int2* br = (g + 1 < a.Gtot) ? a.bcol[g + 1] : nullptr;
+    const int* prog_up = (s > 0) ? &a.rowprog[g * a.S + s - 1] : nullptr;
 
     if (g > 0) {  // left boundary of this row strip (and the previous one: diag of row 0)
       if (!warp_wait<true>(&a.bflag[g][s], 1, a)) break;
       if (s > 0 && !warp_wait<true>(&a.bflag[g][s - 1], 1, a)) break;
     }
     uint32_t p0[R], p1[R];
-    int Hh[R], Ho[R], Ff[R];
+    int HA[R], HB[R], Ff[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int ip = ip0 + r;
@@ -141,129 +175,180 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
       const uint32_t c = real ? a.qc[ip] : 0u;
       p0[r] = real ? prof4(P, c) : 0u;
       p1[r] = real ? P.mism4 : 0u;
-      int2 b = make_int2(0, NEG);
-      if (real) b = bl[ip + 1];
-      Hh[r] = b.x;
-      Ff[r] = b.y;
-      Ho[r] = Hh[r] + NOC;
+      HA[r] = HB[r] = 0;
+      Ff[r] = NEG;
     }
-    int diag = (ip0 <= n) ? bl[ip0].x : 0;
-    int Hbot = NEG, Ebot = NEG;
-    uint32_t selb = 0;
+    // lane-0 inputs and selectors of columns [c0, c1) into the warp's ring (coalesced)
+    auto refill = [&](int c0, int c1) {
+      for (int c = c0 + t; c < c1; c += L) {
+        if (s > 0) ring_he[wb][c & (RING - 1)] = a.rowbuf[c_lo + c + 1];
+        ring_sel[wb][c & (RING - 1)] = (uint16_t)V::selector(a.sc[c_lo + c], 0);
+      }
+    };
+    // start only when the strip above is a.lag columns ahead: the steady-state distance
+    // between consecutive strips then stays above the 2*PER columns each refill needs
+    if (prog_up && !warp_wait<false>(prog_up, min(W, max(2 * PER, a.lag)), a)) break;
+    refill(0, min(W, 2 * PER));
+    __syncwarp();
+
+    int diag = 0, Hbot = NEG, Ebot = NEG;
     int sv = 0, si = 0, sj = 0;  // local per task
     bool aborted = false;
 
-    const int K = W + L - 1;
-    for (int k = 0; k < K; ++k) {
-      if (s > 0 && k < W && (k % a.chunk) == 0) {
-        if (!warp_wait<false>(&a.rowprog[g * a.S + s - 1], min(W, k + a.chunk), a)) {
-          aborted = true;
-          break;
-        }
-      }
+    auto step = [&](auto chk, const int k, int (&Hi)[R], int (&Hq)[R]) {
+      constexpr bool CHK = decltype(chk)::value;
       int hin = V::shfl_up(Hbot, L);
-      int ein = (GAP == GAFFINE) ? V::shfl_up(Ebot, L) : NEG;
-      uint32_t sel = __shfl_up_sync(0xffffffffu, selb, 1, L);
+      int ein = V::shfl_up(Ebot, L);
       const int lc = k - t;
-      const bool act = lc >= 0 && lc < W;
-      if (t == 0 && act) {
-        const int2 v = a.rowbuf[c_lo + lc + 1];
-        hin = v.x;
-        ein = v.y;
-        sel = V::selector(a.sc[c_lo + lc], 0);
-      }
-      if (act) {
-        int hup = hin + NOC;
-        int e = ein;
-        int hd = diag;
+      const uint32_t sel = ring_sel[wb][lc & (RING - 1)];
+      const bool act = !CHK || (lc >= 0 && lc < W);
+      if (CHK && lc == 0) {  // the left boundary column H(i, c_lo), F(i, c_lo)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int sig = V::sigma(p0[r], p1[r], sel);
-          int tm;
-          if (GAP == GAFFINE) {
-            e = V::addmax(e, NGE, hup);
-            Ff[r] = V::addmax(Ff[r], NGE, Ho[r]);
-            tm = max(e, Ff[r]);
-          } else {
-            tm = max(hup, Ho[r]);
-          }
-          const int h = (KIND == KLOCAL) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
-          hd = Hh[r];
-          Hh[r] = h;
-          Ho[r] = h + NOC;
-          hup = Ho[r];
+          const int ip = ip0 + r;
+          int2 b = make_int2(0, NEG);
+          if (ip < n) b = bl[ip + 1];
+          Hi[r] = b.x;
+          Ff[r] = b.y;
         }
-        diag = hin;
-        Hbot = Hh[R - 1];
-        Ebot = e;
-        selb = sel;
-        if (t == L - 1) {
-          a.rowbuf[c_lo + lc + 1] = make_int2(Hh[R - 1], e);
-          if ((lc % a.chunk) == a.chunk - 1 || lc == W - 1) st_release_gpu(&a.rowprog[g * a.S + s], lc + 1);
-        }
-        const int j = c_lo + lc + 1;  // real column
-        if (KIND == KLOCAL) {
-          int cm = 0;
-          if (!last_strip) {
-            cm = Hh[0];
-#pragma unroll
-            for (int r = 1; r + 1 < R; r += 2) cm = V::vmax3(cm, Hh[r], Hh[r + 1]);
-            if ((R % 2) == 0) cm = max(cm, Hh[R - 1]);
-          } else {
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-              if (ip0 + r < n) cm = max(cm, Hh[r]);
-          }
-          if (cm > sv) {
-            int rr = R - 1;
-#pragma unroll
-            for (int r = R - 1; r >= 0; --r)
-              if (Hh[r] == cm && ip0 + r < n) rr = r;
-            sv = cm;
-            si = ip0 + rr + 1;
-            sj = j;
-          }
-        } else if (KIND == KSEMI) {
-          if (last_strip && t == tn && j <= m - 1) {
-            int v = 0;
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-              if (r == rn) v = Hh[r];
-            if (v > part.rv || (v == part.rv && j < part.rj)) { part.rv = v; part.rj = j; }
-          }
-          if (last_col && lc == W - 1) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              const int i = ip0 + r + 1;
-              if (i <= n && (Hh[r] > part.cv || (Hh[r] == part.cv && i < part.ci))) {
-                part.cv = Hh[r];
-                part.ci = i;
-              }
-            }
-          }
+        diag = (ip0 <= n) ? bl[ip0].x : 0;
+      }
+      if (t == 0) {
+        if (s == 0) {
+          const int h0 = (KIND == KGLOBAL) ? -(P.go + (c_lo + lc + 1) * P.ge) : 0;  // H(0,j)
+          hin = h0;
+          ein = FAST ? hop(h0) : NEG;
         } else {
-          if (last_strip && last_col && lc == W - 1 && t == tn) {
-            int v = 0;
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-              if (r == rn) v = Hh[r];
-            part.gv = v;
-            part.gset = 1;
-          }
-        }
-        if (br && lc == W - 1) {
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (ip0 + r < n) br[ip0 + r + 1] = make_int2(Hh[r], Ff[r]);
+          const int2 v = ring_he[wb][lc & (RING - 1)];
+          hin = v.x;
+          ein = v.y;
         }
       }
+      int e = ein;
+      if (FAST) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int hd = (r == 0) ? diag : Hi[r - 1];
+          const int sig = V::sigma(p0[r], p1[r], sel);
+          Ff[r] = V::addmax(Ff[r], NGE, hop(Hi[r]));
+          const int df = V::addmax(hd, sig, Ff[r]);
+          Hq[r] = (KIND == KLOCAL) ? V::vmax_relu(df, e) : max(df, e);
+          e = V::addmax(e, NGE, hop(df));
+        }
+      } else {
+        int hup = hop(hin);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int hd = (r == 0) ? diag : Hi[r - 1];
+          const int sig = V::sigma(p0[r], p1[r], sel);
+          const int tm = max(hup, hop(Hi[r]));
+          Hq[r] = (KIND == KLOCAL) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
+          hup = hop(Hq[r]);
+        }
+        e = NEG;
+      }
+      diag = hin;
+      Hbot = Hq[R - 1];
+      Ebot = e;
+      if (t == L - 1 && act) {
+        a.rowbuf[c_lo + lc + 1] = make_int2(Hq[R - 1], e);  // in place: strip s+1 reads it
+        if ((lc & (a.chunk - 1)) == a.chunk - 1 || lc == W - 1) st_release_gpu(&a.rowprog[g * a.S + s], lc + 1);
+      }
+      const int j = c_lo + lc + 1;  // real column
+      if (KIND == KLOCAL) {
+        int cm = 0;
+        if (!last_strip) {
+          cm = Hq[0];
+#pragma unroll
+          for (int r = 1; r + 1 < R; r += 2) cm = V::vmax3(cm, Hq[r], Hq[r + 1]);
+          if ((R % 2) == 0) cm = max(cm, Hq[R - 1]);
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (ip0 + r < n) cm = max(cm, Hq[r]);
+        }
+        if (CHK && !act) cm = 0;
+        if (cm > sv) {
+          int rr = R - 1;
+#pragma unroll
+          for (int r = R - 1; r >= 0; --r)
+            if (Hq[r] == cm && ip0 + r < n) rr = r;
+          sv = cm;
+          si = ip0 + rr + 1;
+          sj = j;
+        }
+      } else if (KIND == KSEMI) {
+        if (last_strip && t == tn && act && j <= m - 1) {
+          int v = 0;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (r == rn) v = Hq[r];
+          if (v > part.rv || (v == part.rv && j < part.rj)) { part.rv = v; part.rj = j; }
+        }
+      }
+      if (CHK && lc == W - 1) {  // a lane's last column of this task
+        if (KIND == KSEMI && last_col) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int i = ip0 + r + 1;
+            if (i <= n && (Hq[r] > part.cv || (Hq[r] == part.cv && i < part.ci))) {
+              part.cv = Hq[r];
+              part.ci = i;
+            }
+          }
+        }
+        if (KIND == KGLOBAL && last_strip && last_col && t == tn) {
+          int v = 0;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (r == rn) v = Hq[r];
+          part.gv = v;
+          part.gset = 1;
+        }
+        if (br) {
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (ip0 + r < n) br[ip0 + r + 1] = make_int2(Hq[r], Ff[r]);
+        }
+      }
+    };
+
+    const std::integral_constant<bool, true> ON{};
+    const std::integral_constant<bool, false> OFF{};
+    const int K = W + L - 1;
+    const int kA = min(K & ~1, L);               // every lane has reached column 0
+    const int kB = max(kA, (W - 1) & ~1);        // no lane has reached column W-1 yet
+    int k = 0;
+    auto maybe_refill = [&](int kk) -> bool {  // warp-uniform, every PER steps
+      if ((kk % PER) == 0 && kk > 0 && kk + PER < W) {
+        if (prog_up && !warp_wait<false>(prog_up, min(W, kk + 2 * PER), a)) return false;
+        refill(kk + PER, min(W, kk + 2 * PER));
+        __syncwarp();
+      }
+      return true;
+    };
+    for (; k < kA; k += 2) {
+      if (!maybe_refill(k)) { aborted = true; break; }
+      step(ON, k, HA, HB);
+      step(ON, k + 1, HB, HA);
     }
+    for (; !aborted && k < kB; k += 2) {
+      if (!maybe_refill(k)) { aborted = true; break; }
+      step(OFF, k, HA, HB);
+      step(OFF, k + 1, HB, HA);
+    }
+    for (; !aborted && k + 1 < K; k += 2) {
+      if (!maybe_refill(k)) { aborted = true; break; }
+      step(ON, k, HA, HB);
+      step(ON, k + 1, HB, HA);
+    }
+    if (!aborted && k < K) step(ON, k, HA, HB);
     if (aborted) break;
     if (KIND == KLOCAL && lkey_better(sv, si, sj, part.lv, part.li, part.lj)) {
       part.lv = sv; part.li = si; part.lj = sj;
     }
+    __syncwarp();
     if (br) {
-      __syncwarp();
       if (t == 0) {
         __threadfence_system();
         st_release_sys(&a.bflag[g + 1][s], 1);
@@ -360,7 +445,8 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   const int S = (int)((n + HS - 1) / HS);
   std::vector<int32_t> cb(Gtot + 1);
   for (int g = 0; g <= Gtot; ++g) cb[g] = (int32_t)((m * (uint64_t)g) / Gtot);
-  const int chunk = std::max(8, opt.chunk_cols);
+  int chunk = 8;  // power of two (the kernel masks with chunk - 1)
+  while (chunk < opt.chunk_cols && chunk < (1 << 20)) chunk <<= 1;
   LongFn fn = long_fn<R>(P.kind, P.gap);
 
   struct PerDev {
@@ -499,7 +585,9 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     a.parts = (LongPart*)D.parts.p;
     a.abort_flag = (int32_t*)D.abort_.p;
     a.chunk = chunk;
-    a.spin_limit = 1ll << 26;
+    a.one = 1;
+    a.lag = opt.start_lag > 0 ? opt.start_lag : 256;
+    a.spin_limit = 1ll << 28;
     LK(cudaEventCreate(&D.e0));
     LK(cudaEventCreate(&D.e1));
     LK(cudaEventRecord(D.e0, devs[d].stream));

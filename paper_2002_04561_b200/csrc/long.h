@@ -13,6 +13,7 @@ struct LongOptions {
   int blocks = 0;          // 0 = occupancy-derived persistent grid
   int virtual_strips = 1;  // column strips on one device (tests the multi-GPU protocol)
   int chunk_cols = 64;     // progress publication granularity
+  int start_lag = 0;       // columns the strip above must be ahead before a strip starts
 };
 
 struct LongDevice {

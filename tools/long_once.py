@@ -1,0 +1,6 @@
+import sys; sys.path.insert(0, '.')
+import paper_2002_04561_b200 as A, synth
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 500_000
+g1, g2 = synth.c4_genomes(n, "a", seed=4)
+ctx = A.Context([0])
+print(ctx.align_long(A.Scheme("local", "affine", 2, -1, 5, 1), g1, g2))
