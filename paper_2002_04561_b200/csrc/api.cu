@@ -317,6 +317,8 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     fa.end_i = D.end_i.as<int32_t>();
     fa.end_j = D.end_j.as<int32_t>();
     fa.one = 1;
+    fa.nge_s16 = (uint32_t)(-P.ge & 0xffff) * 0x10001u;
+    fa.koc_s16 = (uint32_t)(-(int)((P.go + P.ge) * 65537));
     const int HS = d.L * d.R;
     const int G = 32 / d.L;
     // strip row buffer only when some pair needs more than one strip

@@ -25,6 +25,8 @@ struct FillArgs {
   int64_t dir_block_words;    // TB: words per slot block (fixed per launch)
   TbInfo* tb;                 // TB: per pair
   int32_t one;                // = 1 at run time (keeps IMAD-based adds on the FMA pipe)
+  uint32_t nge_s16;           // packed (-Ge, -Ge): read from the constant bank in the hot loop
+  uint32_t koc_s16;           // -(Go+Ge)*65537 (biased VS16 Hop addend)
 };
 
 }  // namespace anyseq

@@ -7,6 +7,7 @@ namespace anyseq {
 FillFn fill_fn_s16(int v, int kind, int gap, bool pos);
 FillFn fill_fn_s32(int v, int kind, int gap, bool pos);
 FillFn fill_fn_tb(int v, int kind, int gap, bool pos);
+FillFn fill_fn_s16_spec(int v, int kind, bool pos);
 
 static FillFn pick(int v, int kind, int gap, bool pos) {
   if (v <= 2) return fill_fn_s16(v, kind, gap, pos);
@@ -17,10 +18,12 @@ static FillFn pick(int v, int kind, int gap, bool pos) {
 cudaError_t launch_fill(int variant, int kind, int gap, const FillArgs& a, cudaStream_t st,
                         int num_sms, int* grid_out) {
   static std::mutex mu;
-  static int occ[NV][3][2][2][16];  // per device up to 16
+  static int occ[NV][3][2][2][2][16];  // per device up to 16
   static bool init = false;
   const int pos = a.pos ? 1 : 0;
-  FillFn fn = pick(variant, kind, gap, pos != 0);
+  // compile-time-specialised instance for the common scheme (affine, G_o = 5, G_e = 1)
+  const int spec = (variant <= 2 && gap == GAFFINE && a.P.go == 5 && a.P.ge == 1) ? 1 : 0;
+  FillFn fn = spec ? fill_fn_s16_spec(variant, kind, pos != 0) : pick(variant, kind, gap, pos != 0);
   if (!fn) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -28,12 +31,12 @@ cudaError_t launch_fill(int variant, int kind, int gap, const FillArgs& a, cudaS
   {
     std::lock_guard<std::mutex> lk(mu);
     if (!init) { memset(occ, 0, sizeof(occ)); init = true; }
-    nb = occ[variant][kind][gap][pos][dev & 15];
+    nb = occ[variant][kind][gap][pos][spec][dev & 15];
     if (nb == 0) {
       cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0);
       if (e != cudaSuccess) return e;
       if (nb < 1) nb = 1;
-      occ[variant][kind][gap][pos][dev & 15] = nb;
+      occ[variant][kind][gap][pos][spec][dev & 15] = nb;
     }
   }
   const int grid = num_sms * nb;

@@ -6,6 +6,14 @@ namespace anyseq {
 
 typedef void (*FillFn)(FillArgs);
 
+// affine scoring with compile-time G_e = 1, G_o = 5 (the C2-C5 scheme, reading R18/R19)
+template <class V, int L, int R, bool POS>
+FillFn fill_fn_spec(int kind) {
+  if (kind == KGLOBAL) return fill_kernel<V, KGLOBAL, GAFFINE, L, R, false, POS, 1, 5>;
+  if (kind == KLOCAL) return fill_kernel<V, KLOCAL, GAFFINE, L, R, false, POS, 1, 5>;
+  return fill_kernel<V, KSEMI, GAFFINE, L, R, false, POS, 1, 5>;
+}
+
 template <class V, int L, int R, bool TB, bool POS>
 FillFn fill_fn_p(int kind, int gap) {
   if (kind == KGLOBAL) return gap == GAFFINE ? fill_kernel<V, KGLOBAL, GAFFINE, L, R, TB, POS>

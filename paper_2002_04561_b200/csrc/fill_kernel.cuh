@@ -47,7 +47,10 @@ __device__ __forceinline__ uint32_t imad_add(uint32_t x, uint32_t one, uint32_t 
   return d;
 }
 
-template <class V, int KIND, int GAP, int L, int R, bool TB, bool POS>
+// CGE/CGO > 0: the gap extend / open values are compile-time constants (the paper's partial
+// evaluation of the scoring scheme): the packed constants then become
+// instruction immediates and the 3-source DPX/IMAD ops read one register less.
+template <class V, int KIND, int GAP, int L, int R, bool TB, bool POS, int CGE = 0, int CGO = 0>
 __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(FillArgs a) {
   using T = typename V::T;
   constexpr int PP = V::P;
@@ -69,11 +72,15 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
   constexpr bool FAST = (GAP == GAFFINE) && !TB;  // reassociated affine recurrence
   // VS16 local scores are unbiased; their Hop uses VIADD.16x2 (see hop) -- fine.
   const uint32_t one = (uint32_t)a.one;
-  const int cop = (GAP == GAFFINE) ? (P.go + P.ge) : P.ge;  // H -> Hop
+  constexpr bool SPEC = CGE > 0;
+  const int cop = SPEC ? ((GAP == GAFFINE) ? CGO + CGE : CGE)
+                       : ((GAP == GAFFINE) ? (P.go + P.ge) : P.ge);  // H -> Hop
   const T NEG = (PP == 2) ? V::splat(NEG16 + B0) : V::splat(NEG32);
-  const T NGE = V::splat(-P.ge);
+  // packed constants straight from the kernel-parameter bank (no register-file bank reads)
+  const T NGE = SPEC ? V::splat(-CGE) : ((PP == 2) ? (T)a.nge_s16 : V::splat(-P.ge));
   const T NOC = V::splat(-cop);
-  const uint32_t KOC = (uint32_t)(-(int)(cop * ((PP == 2) ? 65537 : 1)));
+  const uint32_t KOC = (!SPEC && PP == 2 && GAP == GAFFINE) ? a.koc_s16
+                                                            : (uint32_t)(-(int)(cop * ((PP == 2) ? 65537 : 1)));
   auto hop = [&](T h) -> T {  // Hop = H - Go - Ge (or H - g)
     if (PP == 1 || BIAS) return (T)imad_add((uint32_t)h, one, KOC);
     return V::add(h, NOC);
