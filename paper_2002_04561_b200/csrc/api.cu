@@ -326,12 +326,12 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     if (S.maxn[v] > HS) {
       fa.strip_stride = S.maxm[v] + 1;
       const int64_t groups = (int64_t)grid_est * 4 * G;
-      CK(D.strip.ensure((size_t)groups * fa.strip_stride * sizeof(uint2)));
-      fa.strip_scratch = D.strip.as<uint2>();
+      CK(D.strip.ensure((size_t)groups * fa.strip_stride * sizeof(uint4)));
+      fa.strip_scratch = D.strip.as<uint4>();
     } else {
       fa.strip_stride = 0;
       CK(D.strip.ensure(256));
-      fa.strip_scratch = D.strip.as<uint2>();
+      fa.strip_scratch = D.strip.as<uint4>();
     }
     if (!d.tb) {
       fa.slot_lo = sbase[v];
@@ -350,8 +350,8 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
       L(1);
     } else {
       const int64_t ns = (S.maxn[v] + HS - 1) / HS;
-      const int64_t s8 = (S.maxm[v] + d.L - 1 + 7) / 8;
-      const int64_t block_words = ns * s8 * d.R * d.L * d.pairs;
+      const int64_t s4 = (S.maxm[v] + d.L - 1 + 3) / 4;  // 4 steps per direction word
+      const int64_t block_words = ns * s4 * d.R * d.L;    // both halves share a word
       const int64_t cap_words = std::max<int64_t>(ctx->tb_scratch_bytes / 4, block_words);
       int64_t chunk = std::max<int64_t>(1, cap_words / block_words);
       chunk = std::min<int64_t>(chunk, nslot[v]);

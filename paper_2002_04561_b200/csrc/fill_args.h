@@ -19,7 +19,7 @@ struct FillArgs {
   int32_t* scores;            // [num_pairs]
   int32_t* end_i;             // [num_pairs] (pos)
   int32_t* end_j;
-  uint2* strip_scratch;       // per resident lane group: strip_stride entries (H, E)
+  uint4* strip_scratch;       // per resident lane group: strip_stride entries (H, E, bits)
   int64_t strip_stride;
   uint32_t* dirs;             // TB: direction nibbles
   int64_t dir_block_words;    // TB: words per slot block (fixed per launch)

@@ -70,6 +70,12 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
   const DevParams P = a.P;
   constexpr bool pos = TB || POS;
   constexpr bool FAST = (GAP == GAFFINE) && !TB;  // reassociated affine recurrence
+  constexpr uint32_t LOWBITS = (PP == 2) ? 0x00010001u : 1u;
+  // 0 iff x == y, per half (bit 0 of each half)
+  auto mneq = [&](T x, T y) -> uint32_t {
+    if (PP == 2) return __vminu2((uint32_t)x ^ (uint32_t)y, 0x00010001u);
+    return min((uint32_t)x ^ (uint32_t)y, 1u);
+  };
   // VS16 local scores are unbiased; their Hop uses VIADD.16x2 (see hop) -- fine.
   const uint32_t one = (uint32_t)a.one;
   constexpr bool SPEC = CGE > 0;
@@ -136,12 +142,12 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
     int pad[PP];
 #pragma unroll
     for (int X = 0; X < PP; ++X) pad[X] = (KIND == KGLOBAL) ? 0 : npad - nn[X];
-    uint2* scr = a.strip_scratch + (int64_t)(warp * G + g) * a.strip_stride;
+    uint4* scr = a.strip_scratch + (int64_t)(warp * G + g) * a.strip_stride;
     int64_t dbase = 0;
-    int S8 = 0;
+    int S4 = 0;
     if (TB && valid) {
       dbase = (int64_t)sidx * a.dir_block_words;
-      S8 = (M + L - 1 + 7) >> 3;
+      S4 = (M + L - 1 + 3) >> 2;
     }
 
     // column selectors of this slot in a 512-entry shared ring: columns [0, 384) now, then
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
       const int ip0 = st * HS + t * R;  // first physical row of this lane
       uint32_t p0[R], p1[R];
       T HA[R], HB[R], Ff[R];
-      uint32_t acc[TB ? R * PP : 1];
+      uint32_t acc[TB ? R : 1];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int ip = ip0 + r;
@@ -209,10 +215,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         HA[r] = enc(iv[0], iv[PP - 1]);
         HB[r] = HA[r];
         Ff[r] = NEG;
-        if (TB) {
-#pragma unroll
-          for (int X = 0; X < PP; ++X) acc[r * PP + X] = 0;
-        }
+        if (TB) acc[r] = 0;
       }
       // H of the row above this lane's first row at column 0
       T diag;
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         diag = enc(dv, dv);
       }
       T Hbot = NEG, Ebot = NEG;
+      uint32_t MEbot = 0;
       // per-strip local trackers (merged by key at strip end)
       int sv[PP], si[PP], sj[PP];
 #pragma unroll
@@ -245,7 +249,8 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
       auto step = [&](auto chk, const int k, T (&Hi)[R], T (&Hq)[R]) {
         constexpr bool CHK = decltype(chk)::value;
         T hin = V::shfl_up(Hbot, L);
-        T ein = (GAP == GAFFINE) ? V::shfl_up(Ebot, L) : NEG;
+        T ein = (GAP == GAFFINE || TB) ? V::shfl_up(Ebot, L) : NEG;
+        uint32_t mein = TB ? __shfl_up_sync(0xffffffffu, MEbot, 1, L) : 0u;
         const int col = k - t;
         const uint32_t sel = seltab[gb][col & (SELCAP - 1)];
         const bool act = sact && col >= 0 && col < M;
@@ -268,12 +273,15 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
           const T h0v = enc(h0, h0);
           if (t == 0) {
             hin = h0v;
-            ein = FAST ? hop(h0v) : NEG;  // FAST: E(1,j) = H(0,j) - Go - Ge; else E(0,j) = -inf
+            // E-below convention (FAST, TB): E(1,j) = H(0,j) - Go - Ge, opened; else E(0,j)
+            ein = (FAST || TB) ? hop(h0v) : NEG;
+            mein = LOWBITS;
           }
         } else if (t == 0 && act) {
-          const uint2 v = scr[col];
+          const uint4 v = scr[col];
           hin = (T)v.x;
           ein = (T)v.y;
+          mein = v.z;
         }
         // FAST = affine score-only: the reassociated recurrence
         //   F  = max(F - Ge, H_left - Go - Ge)          Eq. (5)
@@ -285,6 +293,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         // value handed down the lanes / strips is E of the row BELOW the bottom row.
         T hup = FAST ? NEG : hop(hin);  // Hop of the row above (other modes)
         T e = ein;
+        uint32_t me = mein;
         if (FAST) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -308,45 +317,52 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
             hup = hop(h);
           }
         } else {
+          // Traceback fill: direction bits in packed form, no predicates.  For a pair of
+          // values x, y (both halves at once) m(x, y) = min_u16(x ^ y, 1) is 0 iff x == y,
+          // so each of the four decisions of the relax listing costs two
+          // instructions for both alignments:
+          //   b0 = m(H, D)      1 = not DIAG             (DIAG first, R7)
+          //   b1 = m(tm, E)     1 = F beats E            (E before F, R7)
+          //   b2 = m(E, Ex)     1 = E opened (not extended, R8)
+          //   b3 = m(F, Fx)     1 = F opened
+          // local: STOP (H <= 0, R9) is stored as b0 = 0, b1 = 1.
+          // nibble = b0 | b1<<1 | b2<<2 | b3<<3 (built with IMAD shift-adds on the FMA pipe);
+          // acc = acc*16 + nibble holds 4 steps per half: half A in bits 0-15, half B 16-31.
+          // Like FAST, the value handed down is E of the row below, with its extend bit.
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const T hd = (r == 0) ? diag : Hi[r - 1];
             const T sig = V::sigma(p0[r], p1[r], sel);
-            uint32_t pe = 0, pf = 0, pef, pd;
-            T tm;
-            const T hleft = hop(Hi[r]);
-            if (GAP == GAFFINE) {
-              e = V::bmax(V::add(e, NGE), hup, pe);              // eext: extend >= open (R8)
-              Ff[r] = V::bmax(V::add(Ff[r], NGE), hleft, pf);    // fext
-              tm = V::bmax(e, Ff[r], pef);                       // E before F (R7)
-            } else {
-              tm = V::bmax(hup, hleft, pef);
-            }
-            T h = V::bmax(V::add(hd, sig), tm, pd);              // DIAG first (R7)
-            uint32_t stop = 0;
+            const T d = V::add(hd, sig);
+            const T fx = V::add(Ff[r], NGE);
+            const T f = V::vmax(fx, hop(Hi[r]));
+            Ff[r] = f;
+            const T tm = V::vmax(e, f);
+            T h = (KIND == KLOCAL) ? V::vmax_relu(d, tm) : V::vmax(d, tm);
+            uint32_t b0 = mneq(h, d);
+            uint32_t b1 = mneq(tm, e);
             if (KIND == KLOCAL) {
-              // STOP where H <= 0 (nu wins ties, reading R9).  Not via bmax(0, h): ptxas
-              // 12.9 swaps the operands of a VIMNMX-with-predicates against a constant
-              // zero and the predicates then mean h >= 0.
-              h = V::vmax_relu(h, h);
-#pragma unroll
-              for (int X = 0; X < PP; ++X) stop |= (V::get(h, X) == 0 ? 1u : 0u) << X;
+              const uint32_t mz = mneq(h, V::splat(0));  // 0 iff STOP
+              b1 = (b0 & b1) | (mz ^ LOWBITS);
+              b0 = b0 & mz;
+            } else {
+              b1 = b0 & b1;  // canonical DIAG = (0, 0)
             }
-#pragma unroll
-            for (int X = 0; X < PP; ++X) {
-              uint32_t src = ((pd >> X) & 1u) ? 0u : (((pef >> X) & 1u) ? 1u : 2u);
-              if ((stop >> X) & 1u) src = 3u;
-              const uint32_t nib = src | (((pe >> X) & 1u) << 2) | (((pf >> X) & 1u) << 3);
-              acc[r * PP + X] = (acc[r * PP + X] >> 4) | (nib << 28);
-            }
+            const uint32_t w = imad_add(imad_add(imad_add(mneq(f, fx), 2u, me), 2u, b1), 2u, b0);
+            acc[r] = imad_add(acc[r], 16u, w);
             Hq[r] = h;
-            hup = hop(h);
+            // E of the row below (reassociated, exact; see FAST above) and its extend bit
+            const T ex = V::add(e, NGE);
+            e = V::vmax(ex, hop(V::vmax(d, f)));
+            me = mneq(e, ex);
           }
         }
         diag = hin;
         Hbot = Hq[R - 1];
         Ebot = e;
-        if (act && t == L - 1 && st + 1 < NS) scr[col] = make_uint2((uint32_t)Hq[R - 1], (uint32_t)e);
+        if (TB) MEbot = me;
+        if (act && t == L - 1 && st + 1 < NS)
+          scr[col] = make_uint4((uint32_t)Hq[R - 1], (uint32_t)e, TB ? me : 0u, 0u);
 
         // ---- optimum bookkeeping ----
         // Plain score mode tracks maxima in every lane and every step without masks: the
@@ -419,16 +435,17 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
           }
         }
         }
-        if (TB && valid && sact) {
+        if (TB) {
           const int Kslot = M + L - 1;
-          if (k < Kslot && ((k & 7) == 7 || k == Kslot - 1)) {
-            const int sh = 4 * (7 - (k & 7));
-            uint32_t* wp = a.dirs + dbase + ((((int64_t)st * S8 + (k >> 3)) * R) * L + t) * PP;
+          if (valid && sact && k < Kslot && ((k & 3) == 3 || k == Kslot - 1)) {
+            const int sh = 4 * (3 - (k & 3));  // a partial last word keeps the 4-step layout
+            uint32_t* wp = a.dirs + dbase + (((int64_t)st * S4 + (k >> 2)) * R) * L + t;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
+            for (int r = 0; r < R; ++r) wp[(int64_t)r * L] = acc[r] << sh;
+          }
+          if ((k & 3) == 3) {
 #pragma unroll
-              for (int X = 0; X < PP; ++X) wp[((int64_t)r * L) * PP + X] = acc[r * PP + X] >> sh;
-            }
+            for (int r = 0; r < R; ++r) acc[r] = 0;
           }
         }
       };

@@ -294,6 +294,8 @@ cudaError_t exclusive_scan_i32_to_u64(void* d_temp, size_t& temp_bytes, const in
 }
 
 // ------------------------------------------------------------------------------- walk
+// direction nibble of cell (i, j): bit0 = not DIAG, bit1 = F beats E (b0 = 0 & b1 = 1:
+// STOP), bit2 = E opened here, bit3 = F opened here (fill_kernel.cuh, traceback branch)
 __device__ __forceinline__ uint32_t fetch_nib(const uint32_t* __restrict__ dirs, const TbInfo& ti,
                                               int i, int j) {
   const int L = ti.L, R = ti.R, HS = L * R;
@@ -301,9 +303,9 @@ __device__ __forceinline__ uint32_t fetch_nib(const uint32_t* __restrict__ dirs,
   const int st = ip / HS, lr = ip - st * HS;
   const int tt = lr / R, r = lr - tt * R;
   const int k = (j - 1) + tt;
-  const int S8 = (ti.slot_M + L - 1 + 7) >> 3;
-  const int64_t w = ti.dir_base + ((((int64_t)st * S8 + (k >> 3)) * R + r) * L + tt) * ti.P + ti.half;
-  return (__ldg(dirs + w) >> (4 * (k & 7))) & 15u;
+  const int S4 = (ti.slot_M + L - 1 + 3) >> 2;
+  const int64_t w = ti.dir_base + ((((int64_t)st * S4 + (k >> 2)) * R + r) * L + tt);
+  return (__ldg(dirs + w) >> (4 * (3 - (k & 3)) + 16 * ti.half)) & 15u;
 }
 
 struct RunWriter {
@@ -346,17 +348,18 @@ __global__ void walk_kernel(WalkArgs a) {
           }
           break;
         }
-        const uint32_t src = fetch_nib(a.dirs, ti, i, j) & 3u;
-        if (src == 3u) break;             // STOP (local, H <= 0, reading R9)
-        if (src == 0u) { rw.push(0u, 1); --i; --j; }
-        else state = (src == 1u) ? 1 : 2;
+        const uint32_t nib = fetch_nib(a.dirs, ti, i, j);
+        if ((nib & 3u) == 2u) break;      // STOP (local, H <= 0, reading R9)
+        if (!(nib & 1u)) { rw.push(0u, 1); --i; --j; }   // DIAG
+        else state = (nib & 2u) ? 2 : 1;                  // F : E
+
       } else if (state == 1) {
-        const uint32_t ext = (fetch_nib(a.dirs, ti, i, j) >> 2) & 1u;
+        const uint32_t ext = ((fetch_nib(a.dirs, ti, i, j) >> 2) & 1u) ^ 1u;
         rw.push(1u, 1);
         --i;
         if (!ext || linear || i == 0) state = 0;
       } else {
-        const uint32_t ext = (fetch_nib(a.dirs, ti, i, j) >> 3) & 1u;
+        const uint32_t ext = ((fetch_nib(a.dirs, ti, i, j) >> 3) & 1u) ^ 1u;
         rw.push(2u, 1);
         --j;
         if (!ext || linear || j == 0) state = 0;

@@ -14,7 +14,7 @@ struct VariantDesc {
   int tb;     // 1 = writes direction nibbles
 };
 
-constexpr int NV = 7;
+constexpr int NV = 8;
 // Score-only variants: s16x2 with R in {8,16,19} (19*8 = 152 rows fits 150 bp reads with
 // one strip), s32 with R in {8,16}; traceback variants: s32 / s16x2 with R = 8.
 __host__ __device__ inline VariantDesc variant_desc(int v) {
@@ -26,6 +26,7 @@ __host__ __device__ inline VariantDesc variant_desc(int v) {
     case 4: return {1, 8, 16, 0};
     case 5: return {1, 8, 8, 1};
     case 6: return {2, 8, 8, 1};
+    case 7: return {2, 8, 19, 1};
     default: return {0, 0, 0, 0};
   }
 }
