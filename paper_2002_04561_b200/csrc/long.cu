@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
   constexpr int HS = L * R;
   constexpr bool FAST = GAP == GAFFINE;  // reassociated affine recurrence (see fill_kernel.cuh)
   constexpr int RING = 256;              // per-warp ring of lane-0 inputs and selectors
-  constexpr int PER = 64;                // refill period (steps)
+  constexpr int PER = 32;                // refill period (steps)
   __shared__ int2 ring_he[4][RING];
   __shared__ uint16_t ring_sel[4][RING];
   const int t = threadIdx.x & 31;
@@ -586,7 +586,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     a.abort_flag = (int32_t*)D.abort_.p;
     a.chunk = chunk;
     a.one = 1;
-    a.lag = opt.start_lag > 0 ? opt.start_lag : 256;
+    a.lag = opt.start_lag > 0 ? opt.start_lag : 96;
     a.spin_limit = 1ll << 28;
     LK(cudaEventCreate(&D.e0));
     LK(cudaEventCreate(&D.e1));
