@@ -127,8 +127,9 @@ def measured_alu_peak():
     per-instruction lane rates MEASURED on a B200 by the DPX microbenchmark
     (paper_2002_04561_b200/csrc/dpx_bench.cu -> profiles/dpx_rates.json): per register
     the fill issues 1 PRMT + 3 VIADDMNMX.S16x2 + 1 VIMNMX.S16x2 on the ALU pipe (and 2
-    IMAD on the FMA pipe, which is not binding).  Falls back to 64 lane-ops/clk/SM for
-    every ALU op when the file is absent."""
+    IMAD on the FMA pipe, which is not binding).  All five run at ~64 lane-ops/clk/SM
+    (16 lanes/clk per SM sub-partition), i.e. 25.6 cells/clk/SM.  Falls back to 64
+    lane-ops/clk/SM for every ALU op when the file is absent."""
     import torch
     props = torch.cuda.get_device_properties(0)
     path = os.path.join(ROOT, "profiles", "dpx_rates.json")

@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
   // per-group column selectors of the current slot (built once per slot, read by every lane
   // at its own column: no selector shuffle, no per-step global loads)
   constexpr int SELCAP = 512;
-  __shared__ uint16_t seltab[4 * G][SELCAP];
+  constexpr int SELMIR = 128;  // mirror of the first 128 slots after the end
+  __shared__ uint16_t seltab[4 * G][SELCAP + SELMIR];
   const int gb = (threadIdx.x >> 5) * G + g;
   auto dec = [&](T x, int X) -> int { return V::get(x, X) - B0; };
 
@@ -156,7 +157,9 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
       for (int c = c0 + t; c < c1; c += L) {
         const uint32_t x0 = (c < mm[0]) ? a.scode[so[0] + c] : 0u;
         const uint32_t x1 = (PP == 2 && c < mm[PP - 1]) ? a.scode[so[PP - 1] + c] : 0u;
-        seltab[gb][c & (SELCAP - 1)] = (uint16_t)V::selector(x0, x1);
+        const uint16_t sv = (uint16_t)V::selector(x0, x1);
+        seltab[gb][c & (SELCAP - 1)] = sv;
+        if ((c & (SELCAP - 1)) < SELMIR) seltab[gb][SELCAP + (c & (SELCAP - 1))] = sv;
       }
     };
     if (Mw <= SELCAP) {  // the whole slot fits: built once for all strips
@@ -246,14 +249,26 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
       // column when it reaches column 0 and hands over captures at its last column.
       // CHK = this step may contain a lane's column 0 (initial column) or a pair's column m
       // (captures); the steady-state steps in between run without those checks.
+      const uint32_t selbase = (uint32_t)__cvta_generic_to_shared(&seltab[gb][0]);
+      uint32_t selo = 0;
+      auto rebase = [&](int kk) { selo = selbase + (uint32_t)(((kk - t) & (SELCAP - 1)) * 2); };
       auto step = [&](auto chk, const int k, T (&Hi)[R], T (&Hq)[R]) {
         constexpr bool CHK = decltype(chk)::value;
         T hin = V::shfl_up(Hbot, L);
         T ein = (GAP == GAFFINE || TB) ? V::shfl_up(Ebot, L) : NEG;
         uint32_t mein = TB ? __shfl_up_sync(0xffffffffu, MEbot, 1, L) : 0u;
         const int col = k - t;
-        const uint32_t sel = seltab[gb][col & (SELCAP - 1)];
-        const bool act = sact && col >= 0 && col < M;
+        // selector of this lane's column: a shared-memory pointer that advances by one slot
+        // per step (IMAD, FMA pipe) and is re-based every 128 steps (the mirror covers the
+        // wrap in between), so the hot loop spends no ALU instruction on addressing
+        uint32_t sel;
+        {
+          unsigned short v16;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v16) : "r"(selo));
+          sel = v16;
+        }
+        selo = imad_add(selo, one, 2u);
+        const bool act = CHK ? (sact && col >= 0 && col < M) : sact;
         if (CHK && col == 0 && sact) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -361,7 +376,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         Hbot = Hq[R - 1];
         Ebot = e;
         if (TB) MEbot = me;
-        if (act && t == L - 1 && st + 1 < NS)
+        if (NSw > 1 && act && t == L - 1 && st + 1 < NS)
           scr[col] = make_uint4((uint32_t)Hq[R - 1], (uint32_t)e, TB ? me : 0u, 0u);
 
         // ---- optimum bookkeeping ----
@@ -462,15 +477,23 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
       const int kA = min(K & ~1, (L + 1) & ~1);
       const int kB = max(kA, min(K, Mmin - 1) & ~1);
       int k = 0;
+      rebase(0);
       for (; k < kA; k += 2) {
         step(CHK_ON, k, HA, HB);
         step(CHK_ON, k + 1, HB, HA);
       }
-      while (k < kB) {
-        if (Mw > SELCAP && (k & 127) == 0 && k > 0) {  // warp-uniform ring refill
-          fill_sel(k + 256, min(M, k + 384));
-          __syncwarp();
+      // every 128 steps (warp-uniform): selector ring refill (long rows) and pointer rebase
+      auto block_start = [&](int kk) {
+        if ((kk & 127) == 0) {
+          if (Mw > SELCAP && kk > 0) {
+            fill_sel(kk + 256, min(M, kk + 384));
+            __syncwarp();
+          }
+          rebase(kk);
         }
+      };
+      while (k < kB) {
+        block_start(k);
         const int kend = min(kB, (k & ~127) + 128);
         for (; k < kend; k += 2) {
           step(CHK_OFF, k, HA, HB);
@@ -478,14 +501,14 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         }
       }
       for (; k + 1 < K; k += 2) {
-        if (Mw > SELCAP && (k & 127) == 0 && k > 0) {
-          fill_sel(k + 256, min(M, k + 384));
-          __syncwarp();
-        }
+        block_start(k);
         step(CHK_ON, k, HA, HB);
         step(CHK_ON, k + 1, HB, HA);
       }
-      if (k < K) step(CHK_ON, k, HA, HB);
+      if (k < K) {
+        block_start(k);
+        step(CHK_ON, k, HA, HB);
+      }
 
       __syncwarp();  // capbuf writes of this strip are visible (all lanes participate)
       if (KIND != KLOCAL && sact) {
