@@ -260,3 +260,64 @@ def test_errors(ctx):
     with pytest.raises(A.AnyseqError) as e:
         ctx.traceback(A.Scheme("global"), q, qo, s, so, cigar_capacity=1)
     assert e.value.status_name == "E_CAPACITY" and e.value.cigar_used > 1
+
+
+def test_device_api_matches_oracle(ctx):
+    """anyseq_align_batch_device on torch device tensors, on the caller's stream."""
+    import torch
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    q, qo, s, so = random_pairs(400, 0, 300, seed=77)
+    dev = torch.device("cuda", 0)
+    d_q = torch.from_numpy(q).to(dev)
+    d_s = torch.from_numpy(s).to(dev)
+    d_qo = torch.from_numpy(qo.view(np.int64)).to(dev)
+    d_so = torch.from_numpy(so.view(np.int64)).to(dev)
+    B = len(qo) - 1
+    for kind in KINDS:
+        sch = A.Scheme(kind, "affine", 2, -1, 5, 1)
+        res, _ = _oracle(kind, "affine", 5, 1, q, qo, s, so, tb=False)
+        d_sc = torch.empty(B, dtype=torch.int32, device=dev)
+        d_ends = torch.empty(B * A.ALIGNMENT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            ctx.align_batch_device(sch, d_q, d_qo, d_s, d_so, d_sc, d_ends, stream=stream)
+        stream.synchronize()
+        assert np.array_equal(d_sc.cpu().numpy(), res["score"].astype(np.int32))
+        ends = d_ends.cpu().numpy().view(A.ALIGNMENT_DTYPE)
+        assert np.array_equal(ends["q_end"], res["q_end"]) and np.array_equal(ends["s_end"], res["s_end"])
+
+
+def test_host_chunking_and_tb_scratch_chunks(ctx):
+    """Tiny upload chunks (host pipeline) and tiny traceback scratch (several fill/walk
+    chunks per variant) give the same results."""
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    q, qo, s, so = random_pairs(700, 0, 260, seed=78)
+    res, ocig = _oracle("local", "affine", 5, 1, q, qo, s, so, tb=True)
+    sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+    ctx.set_option("chunk_bytes", 1 << 16)
+    ctx.set_option("tb_scratch_bytes", 1 << 20)
+    try:
+        _check_scores(ctx, sch, q, qo, s, so, res)
+        _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+    finally:
+        ctx.set_option("chunk_bytes", 64 << 20)
+        ctx.set_option("tb_scratch_bytes", 4 << 30)
+
+
+def test_multi_device_context():
+    """A context over all visible GPUs shards the batch by cells; identical results."""
+    import torch
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    q, qo, s, so = random_pairs(500, 0, 300, seed=79)
+    with A.Context(list(range(n))) as c:
+        for kind in KINDS:
+            sch = A.Scheme(kind, "affine", 2, -1, 5, 1)
+            res, ocig = _oracle(kind, "affine", 5, 1, q, qo, s, so, tb=True)
+            _check_scores(c, sch, q, qo, s, so, res)
+            _check_tb(c, sch, q, qo, s, so, res, ocig)

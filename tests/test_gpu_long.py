@@ -81,3 +81,36 @@ def test_long_bad_byte(ctx):
     with pytest.raises(A.AnyseqError) as e:
         ctx.align_long(A.Scheme("local"), b"ACGTQ", b"ACGT")
     assert e.value.status_name == "E_BADSEQ"
+
+
+def test_long_multi_device():
+    """Column strips across real GPUs (peer stores of the boundary column)."""
+    import torch
+    import paper_2002_04561_b200 as A
+    from synth import c4_genomes
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    g1, g2 = c4_genomes(60_000, "a", seed=4)
+    o = _orc("local", "affine", 5, g1, g2)
+    with A.Context(list(range(n))) as c:
+        r = c.align_long(A.Scheme("local", "affine", 2, -1, 5, 1), g1, g2)
+    assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end)
+
+
+def test_long_kinds_and_gaps_small_strips(ctx):
+    """All kinds x gaps with short strips and tiny progress chunks."""
+    import paper_2002_04561_b200 as A
+    from synth import iid
+    q, s = iid(3000, 91), iid(2800, 92)
+    ctx.set_option("long_chunk_cols", 8)
+    ctx.set_option("long_strips", 5)
+    try:
+        for kind in ("global", "local", "semi"):
+            for gap, go in (("linear", 0), ("affine", 3)):
+                r = ctx.align_long(A.Scheme(kind, gap, 2, -1, go, 1), q, s)
+                o = _orc(kind, gap, go, q, s)
+                assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), (kind, gap)
+    finally:
+        ctx.set_option("long_chunk_cols", 64)
+        ctx.set_option("long_strips", 1)
