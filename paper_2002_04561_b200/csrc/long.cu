@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <cstdio>
 #include <type_traits>
 #include "../../include/anyseq.h"
 #include "kernels.h"
@@ -54,6 +55,7 @@ struct LongArgs {
   int32_t chunk;
   int32_t one;
   int32_t lag;
+  unsigned long long* prof;  // optional: [0] cycles waiting, [1] cycles in tasks, [2] tasks
   long long spin_limit;
 };
 
@@ -95,19 +97,21 @@ template <bool SYS>
 __device__ __forceinline__ bool warp_wait(const int* p, int need, const LongArgs& a) {
   int ok = 1;
   if ((threadIdx.x & 31) == 0) {
-    if ((SYS ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) < need) {
-      long long spins = 0;
-      while ((SYS ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) < need) {
-        if ((++spins & 255) == 0 && (spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
-          atomicExch(a.abort_flag, 1);
-          ok = 0;
-          break;
-        }
-        __nanosleep(32);
+    const long long t0 = a.prof ? clock64() : 0;
+    long long spins = 0;
+    // relaxed polls, then one acquire load once the value is there (no full fence)
+    while (true) {
+      if ((SYS ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) >= need &&
+          (SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= need)
+        break;
+      if ((++spins & 255) == 0 && (spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
+        atomicExch(a.abort_flag, 1);
+        ok = 0;
+        break;
       }
+      __nanosleep(32);
     }
-    if (SYS) asm volatile("fence.acq_rel.sys;" ::: "memory");
-    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (a.prof) atomicAdd(&a.prof[0], (unsigned long long)(clock64() - t0));
   }
   return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
@@ -153,6 +157,7 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
     task = __shfl_sync(0xffffffffu, task, 0);
     if (task >= a.S * a.g_count) break;
     if (*(volatile int*)a.abort_flag) break;
+    const long long task_t0 = (a.prof && t == 0) ? clock64() : 0;
     const int s = task / a.g_count;
     const int g = a.g_first + task % a.g_count;
     const int c_lo = a.cb[g], c_hi = a.cb[g + 1], W = c_hi - c_lo;
@@ -347,6 +352,10 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
     if (KIND == KLOCAL && lkey_better(sv, si, sj, part.lv, part.li, part.lj)) {
       part.lv = sv; part.li = si; part.lj = sj;
     }
+    if (a.prof && t == 0) {
+      atomicAdd(&a.prof[1], (unsigned long long)(clock64() - task_t0));
+      atomicAdd(&a.prof[2], 1ull);
+    }
     __syncwarp();
     if (br) {
       if (t == 0) {
@@ -446,11 +455,11 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   std::vector<int32_t> cb(Gtot + 1);
   for (int g = 0; g <= Gtot; ++g) cb[g] = (int32_t)((m * (uint64_t)g) / Gtot);
   int chunk = 8;  // power of two (the kernel masks with chunk - 1)
-  while (chunk < opt.chunk_cols && chunk < (1 << 20)) chunk <<= 1;
+  while (chunk < opt.chunk_cols && chunk < (1 << 20)) chunk <<= 1;  // publication period
   LongFn fn = long_fn<R>(P.kind, P.gap);
 
   struct PerDev {
-    Buf qa, sa, qc, sc, rowbuf, bcol_own, prog, flags, ticket, abort_, parts, cbuf, bptr, fptr, sum, flg;
+    Buf qa, sa, qc, sc, rowbuf, bcol_own, prog, flags, ticket, abort_, parts, cbuf, bptr, fptr, sum, flg, profbuf;
     int g_first = 0, g_count = 0, grid = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
   };
@@ -586,7 +595,13 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     a.abort_flag = (int32_t*)D.abort_.p;
     a.chunk = chunk;
     a.one = 1;
-    a.lag = opt.start_lag > 0 ? opt.start_lag : 96;
+    a.lag = opt.start_lag > 0 ? opt.start_lag : chunk + 2 * 32 + 64;
+    a.prof = nullptr;
+    if (opt.profile) {
+      LK(cudaMalloc(&D.profbuf.p, 64));
+      LK(cudaMemset(D.profbuf.p, 0, 64));
+      a.prof = (unsigned long long*)D.profbuf.p;
+    }
     a.spin_limit = 1ll << 28;
     LK(cudaEventCreate(&D.e0));
     LK(cudaEventCreate(&D.e1));
@@ -614,6 +629,12 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     cudaEventDestroy(D.e1);
     int ab = 0;
     LK(cudaMemcpy(&ab, D.abort_.p, 4, cudaMemcpyDeviceToHost));
+    if (opt.profile && D.profbuf.p) {
+      unsigned long long pr[3];
+      LK(cudaMemcpy(pr, D.profbuf.p, 24, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[anyseq long] device %d: wait cycles %llu, task cycles %llu, tasks %llu, wait share %.3f, grid %d\n",
+              devs[d].id, pr[0], pr[1], pr[2], pr[1] ? (double)pr[0] / pr[1] : 0.0, D.grid);
+    }
     aborted |= ab;
     std::vector<LongPart> parts((size_t)D.grid * 4);
     LK(cudaMemcpy(parts.data(), D.parts.p, parts.size() * sizeof(LongPart), cudaMemcpyDeviceToHost));
