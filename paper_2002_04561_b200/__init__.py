@@ -170,11 +170,18 @@ class Context:
         b = _Batch(_ptr(q), q_off.ctypes.data, _ptr(s), s_off.ctypes.data, len(q_off) - 1)
         return b, (q, s, q_off, s_off)
 
-    def align_batch(self, scheme: Scheme, q, q_off, s, s_off, ends: bool = False):
-        """Score-only batch (host buffers).  Returns scores, or (scores, alignments) if ends."""
+    def align_batch(self, scheme: Scheme, q, q_off, s, s_off, ends: bool = False, out=None):
+        """Score-only batch (host buffers).  Returns scores, or (scores, alignments) if ends.
+        `out`: optional preallocated int32 array of B scores (pinned memory avoids staging)."""
         b, keep = self._batch(q, q_off, s, s_off)
         B = int(b.num_pairs)
-        scores = np.zeros(B, dtype=np.int32)
+        if out is not None:
+            if not (isinstance(out, np.ndarray) and out.dtype == np.int32 and out.shape == (B,)
+                    and out.flags.c_contiguous):
+                raise ValueError("out must be a contiguous int32 array of num_pairs scores")
+            scores = out
+        else:
+            scores = np.empty(B, dtype=np.int32)
         aln = np.zeros(B, dtype=ALIGNMENT_DTYPE) if ends else None
         p = scheme.c()
         self._check(_lib.anyseq_align_batch(self._h, ctypes.byref(p), ctypes.byref(b),

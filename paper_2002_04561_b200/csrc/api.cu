@@ -46,6 +46,35 @@ struct DevBuf {
   }
 };
 
+// Growable pinned host buffer (staging for device->host results into pageable memory).
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMallocHost(&p, std::max<size_t>(bytes, 4096));
+    if (e == cudaSuccess) cap = std::max<size_t>(bytes, 4096);
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+bool host_pinned(const void* ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 struct Device {
   int id = 0;
   int num_sms = 148;
@@ -56,7 +85,8 @@ struct Device {
   DevBuf q_ascii2[2], s_ascii2[2], q_off2[2], s_off2[2];  // double-buffered host uploads
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
-  PlanSummary* h_sum = nullptr;  // pinned
+  PlanSummary* h_sum = nullptr;  // pinned, mapped (written by the publish kernel)
+  HostBuf h_stage;               // pinned staging of score-mode results
   uint64_t* h_small = nullptr;   // pinned scratch
 };
 
@@ -76,6 +106,31 @@ struct anyseq_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> fill_ev, walk_ev, pool;
   double fill_ms = 0, walk_ms = 0;
   uint64_t fill_launches = 0;
+  // timing >= 2: labelled events on the device streams, printed by the host API (debug)
+  std::vector<std::pair<std::string, cudaEvent_t>> trace;
+  void mark(cudaStream_t x, const std::string& label) {
+    if (timing < 2) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, x);
+    std::lock_guard<std::mutex> lk(ev_mu);
+    trace.emplace_back(label, e);
+  }
+  void dump_trace() {
+    if (trace.empty()) return;
+    std::vector<std::pair<float, std::string>> rows;
+    for (auto& t : trace) {
+      float ms = 0;
+      cudaEventSynchronize(t.second);
+      cudaEventElapsedTime(&ms, trace[0].second, t.second);
+      rows.emplace_back(ms, t.first);
+    }
+    std::stable_sort(rows.begin(), rows.end(),
+                     [](const auto& x, const auto& y) { return x.first < y.first; });
+    for (auto& r : rows) fprintf(stderr, "[trace] %8.3f ms  %s\n", r.first, r.second.c_str());
+    for (auto& t : trace) cudaEventDestroy(t.second);
+    trace.clear();
+  }
 };
 
 namespace {
@@ -158,14 +213,6 @@ DevParams dev_params(const anyseq_params* p) {
   return d;
 }
 
-void init_summary(PlanSummary* s) {
-  memset(s, 0, sizeof(*s));
-  s->err_pos = ~0ull;
-  for (int v = 0; v < NV; ++v) {
-    s->kmin[v] = ~0ull;
-    s->kmax[v] = 0;
-  }
-}
 
 // Device-side batch job: offsets and sequences are already in device memory.
 struct DeviceJob {
@@ -177,9 +224,11 @@ struct DeviceJob {
   uint64_t q_end, s_end;      // q_off[B], s_off[B] (absolute ends; codes are indexed absolutely)
   int tb;                     // traceback mode
   int want_ends;              // score mode: fill end cells + alignment structs
+  uint64_t* rebase_qoff = nullptr;  // host-API chunk: offsets to rebase by (q0, s0) first
+  uint64_t* rebase_soff = nullptr;
+  uint64_t rebase_q0 = 0, rebase_s0 = 0;
   int32_t* d_scores_out;      // score mode output (device) or null => ctx buffer
   anyseq_alignment* d_aln_out;  // alignment structs (device) or null => ctx buffer
-  cudaEvent_t ev_packed = nullptr;  // recorded on the compute stream after the pack kernels
   // traceback: cigar sizing results
   uint64_t cigar_total = 0;
 };
@@ -217,17 +266,16 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   }
 
   // ---- a1: pack + validate ----
-  init_summary(D.h_sum);
-  CK(cudaMemcpyAsync(D.sum.p, D.h_sum, sizeof(PlanSummary), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(D.flags.p, 0, B * 4 + 4, st));
+  CK(launch_prep(D.flags.as<uint32_t>(), B + 1, D.sum.as<PlanSummary>(), J.rebase_qoff,
+                 J.rebase_soff, J.rebase_q0, J.rebase_s0, st, D.num_sms));
+  L(1);
   // byte codes are indexed by absolute CSR position; pack the whole [0, end) range the
   // caller's offsets cover (bytes before off[0] are never read by a pair)
-  CK(launch_pack(J.d_q, J.q_end, D.q_code.as<uint8_t>(), 0, J.d_qoff, B, D.flags.as<uint32_t>(),
+  CK(launch_pack(J.d_q, J.q_end, D.q_code.as<uint8_t>(), J.d_qoff, J.d_s, J.s_end,
+                 D.s_code.as<uint8_t>(), J.d_soff, B, D.flags.as<uint32_t>(),
                  D.sum.as<PlanSummary>(), st, D.num_sms));
-  CK(launch_pack(J.d_s, J.s_end, D.s_code.as<uint8_t>(), 1ull << 62, J.d_soff, B,
-                 D.flags.as<uint32_t>(), D.sum.as<PlanSummary>(), st, D.num_sms));
-  L(2);
-  if (J.ev_packed) CK(cudaEventRecord(J.ev_packed, st));
+  L(1);
+  ctx->mark(st, "packed");
 
   // ---- a2: classify ----
   ClassifyArgs ca;
@@ -244,6 +292,8 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   ca.num_pairs = B;
   ca.flags = D.flags.as<uint32_t>();
   ca.sum = D.sum.as<PlanSummary>();
+  ca.host_sum = D.h_sum;
+  ca.slots = D.slots.as<Slot>();
   ca.keys = D.keys.as<unsigned long long>();
   ca.vals = D.vals.as<int32_t>();
   ca.scores = d_scores;
@@ -257,9 +307,10 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   }
   CK(launch_classify(ca, st, D.num_sms));
   L(1);
-  CK(cudaMemcpyAsync(D.h_sum, D.sum.p, sizeof(PlanSummary), cudaMemcpyDeviceToHost, st));
+  ctx->mark(st, "classified");
   CK(cudaStreamSynchronize(st));
   const PlanSummary S = *D.h_sum;
+  ctx->mark(st, "host-planned");
   if (S.err_pos != ~0ull) {
     const bool in_s = S.err_pos >= (1ull << 62);
     return fail(ctx, ANYSEQ_E_BADSEQ, "invalid symbol at %s byte offset %llu", in_s ? "s" : "q",
@@ -294,7 +345,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     L(4);
     order = D.vals2.as<int32_t>();
   }
-  if (nontriv > 0) {
+  if (nontriv > 0 && !uniform) {  // uniform: classify's speculative slots are the slots
     CK(launch_slots(order, nontriv, voff, S.count, sbase, D.slots.as<Slot>(), st, D.num_sms));
     L(1);
   }
@@ -339,7 +390,9 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
       int grid = 0;
       std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
       if (ctx->timing) { ev = take_events(ctx); CK(cudaEventRecord(ev.first, st)); }
+      ctx->mark(st, "fill-begin");
       CK(launch_fill(v, prm->kind, prm->gap, fa, st, D.num_sms, &grid));
+      ctx->mark(st, "fill-end");
       if (ctx->timing) {
         CK(cudaEventRecord(ev.second, st));
         std::lock_guard<std::mutex> lk(ctx->ev_mu);
@@ -450,15 +503,24 @@ anyseq_status check_batch_host(anyseq_ctx* ctx, const anyseq_batch* b) {
   if (b->num_pairs == 0) return ANYSEQ_OK;
   if (!b->q_off || !b->s_off) return fail(ctx, ANYSEQ_E_INVALID, "offsets are NULL");
   if (b->num_pairs >= (1ull << 31)) return fail(ctx, ANYSEQ_E_INVALID, "too many pairs");
-  for (uint64_t k = 0; k < b->num_pairs; ++k) {
+  if (b->q_off[b->num_pairs] < b->q_off[0] || b->s_off[b->num_pairs] < b->s_off[0])
+    return fail(ctx, ANYSEQ_E_INVALID, "offsets decrease");
+  if ((b->q_off[b->num_pairs] > b->q_off[0] && !b->q) ||
+      (b->s_off[b->num_pairs] > b->s_off[0] && !b->s))
+    return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
+  return ANYSEQ_OK;
+}
+
+// Per-pair offset checks of pairs [k0, k1), run by the host API on each chunk before its
+// upload (off the critical path: the host thread checks chunk c+1 while chunk c computes).
+anyseq_status check_pairs_host(anyseq_ctx* ctx, const anyseq_batch* b, uint64_t k0, uint64_t k1) {
+  for (uint64_t k = k0; k < k1; ++k) {
     if (b->q_off[k + 1] < b->q_off[k] || b->s_off[k + 1] < b->s_off[k])
       return fail(ctx, ANYSEQ_E_INVALID, "pair %llu: offsets decrease", (unsigned long long)k);
     if (b->q_off[k + 1] - b->q_off[k] >= (1ull << 31) || b->s_off[k + 1] - b->s_off[k] >= (1ull << 31))
       return fail(ctx, ANYSEQ_E_INVALID, "pair %llu: sequence longer than 2^31-1",
                   (unsigned long long)k);
   }
-  if ((b->q_off[b->num_pairs] > 0 && !b->q) || (b->s_off[b->num_pairs] > 0 && !b->s))
-    return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
   return ANYSEQ_OK;
 }
 
@@ -491,9 +553,14 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
   // chunk boundaries by cumulative sequence bytes (offsets are monotone)
   std::vector<uint64_t> cb{k0};
   {
-    const uint64_t cap = (uint64_t)std::max<int64_t>(ctx->chunk_bytes, 1 << 20);
+    // ramp-up: the first upload is not overlapped with anything, so the first chunks are
+    // small (1/8, 1/4, 1/2 of chunk_bytes) and the compute stream starts early
+    const uint64_t full = (uint64_t)std::max<int64_t>(ctx->chunk_bytes, 1 << 20);
     uint64_t k = k0;
+    int c = 0;
     while (k < k1) {
+      const uint64_t cap = std::max<uint64_t>(1 << 20, c < 3 ? full >> (3 - c) : full);
+      ++c;
       const uint64_t base = b->q_off[k] + b->s_off[k];
       uint64_t lo = k + 1, hi = k1;  // last index e in (k, k1] with bytes(k, e) <= cap
       while (lo < hi) {
@@ -505,16 +572,37 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     }
   }
   const int NC = (int)cb.size() - 1;
+  // Score-mode results go to the caller's buffers directly when those are pinned; a D2H copy
+  // into pageable memory would block the host until the chunk finished and stall the upload
+  // pipeline, so pageable outputs are staged in pinned memory and copied out one chunk late.
+  const bool stage_s = !tb && !host_pinned(scores);
+  const bool stage_a = !tb && aln && !host_pinned(aln);
+  const uint64_t nloc = k1 - k0;
+  const size_t st_a_off = stage_s ? ((nloc * 4 + 63) & ~63ull) : 0;
+  if (stage_s || stage_a)
+    CK(D.h_stage.ensure(st_a_off + (stage_a ? nloc * sizeof(anyseq_alignment) : 0)));
+  int32_t* h_sc = stage_s ? (int32_t*)D.h_stage.p - k0 : scores;
+  anyseq_alignment* h_al =
+      stage_a ? (anyseq_alignment*)((char*)D.h_stage.p + st_a_off) - k0 : aln;
+  auto copy_out = [&](int c) {  // chunk c's results are complete on the host side
+    const uint64_t a0 = cb[c], B = cb[c + 1] - a0;
+    if (stage_s) memcpy(scores + a0, h_sc + a0, B * 4);
+    if (stage_a) memcpy(aln + a0, h_al + a0, B * sizeof(anyseq_alignment));
+  };
   auto upload = [&](int c) -> anyseq_status {
     const int set = c & 1;
     const uint64_t a0 = cb[c], a1 = cb[c + 1], B = a1 - a0;
+    const anyseq_status chk = check_pairs_host(ctx, b, a0, a1);
+    if (chk != ANYSEQ_OK) return chk;
     const uint64_t q0 = b->q_off[a0], s0 = b->s_off[a0];
     const uint64_t qlen = b->q_off[a1] - q0, slen = b->s_off[a1] - s0;
     CK(D.q_ascii2[set].ensure(qlen + 16));
     CK(D.s_ascii2[set].ensure(slen + 16));
     CK(D.q_off2[set].ensure((B + 1) * 8));
     CK(D.s_off2[set].ensure((B + 1) * 8));
-    CK(cudaStreamWaitEvent(cs, D.ev_free[set], 0));  // previous user of this set has packed
+    // the previous user of this set (chunk c-2) is finished: its offsets are read up to the
+    // last kernel of the chunk, not just by the pack kernels
+    CK(cudaStreamWaitEvent(cs, D.ev_free[set], 0));
     if (qlen) CK(cudaMemcpyAsync(D.q_ascii2[set].p, b->q + q0, qlen, cudaMemcpyHostToDevice, cs));
     if (slen) CK(cudaMemcpyAsync(D.s_ascii2[set].p, b->s + s0, slen, cudaMemcpyHostToDevice, cs));
     CK(cudaMemcpyAsync(D.q_off2[set].p, b->q_off + a0, (B + 1) * 8, cudaMemcpyHostToDevice, cs));
@@ -522,24 +610,41 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     CK(cudaEventRecord(D.ev_up[set], cs));
     return ANYSEQ_OK;
   };
+  auto mark = [&](cudaStream_t x, const char* what, int c) {
+    if (ctx->timing >= 2) ctx->mark(x, std::string(what) + " " + std::to_string(c));
+  };
+  mark(cs, "up-begin", 0);
   anyseq_status s = upload(0);
   if (s != ANYSEQ_OK) return s;
+  mark(cs, "up-end", 0);
   uint64_t cig_base = 0;
   for (int c = 0; c < NC; ++c) {
     const int set = c & 1;
-    if (c + 1 < NC && (s = upload(c + 1)) != ANYSEQ_OK) return s;
+    if (c + 1 < NC) {
+      mark(cs, "up-begin", c + 1);
+      if ((s = upload(c + 1)) != ANYSEQ_OK) {
+        cudaStreamSynchronize(cs);  // chunk c may be in flight: leave the device idle
+        cudaStreamSynchronize(st);
+        return s;
+      }
+      mark(cs, "up-end", c + 1);
+    }
+    mark(st, "compute-begin", c);
     const uint64_t a0 = cb[c], a1 = cb[c + 1], B = a1 - a0;
     const uint64_t q0 = b->q_off[a0], s0 = b->s_off[a0];
     const uint64_t qlen = b->q_off[a1] - q0, slen = b->s_off[a1] - s0;
     CK(cudaStreamWaitEvent(st, D.ev_up[set], 0));
-    CK(launch_rebase(D.q_off2[set].as<uint64_t>(), D.s_off2[set].as<uint64_t>(), B + 1, q0, s0, st,
-                     D.num_sms));
-    ctx->launches += 1;
+    mark(st, "compute-wait", c);
+
     DeviceJob J;
     J.d_q = D.q_ascii2[set].as<char>();
     J.d_qoff = D.q_off2[set].as<uint64_t>();
     J.d_s = D.s_ascii2[set].as<char>();
     J.d_soff = D.s_off2[set].as<uint64_t>();
+    J.rebase_qoff = D.q_off2[set].as<uint64_t>();
+    J.rebase_soff = D.s_off2[set].as<uint64_t>();
+    J.rebase_q0 = q0;
+    J.rebase_s0 = s0;
     J.B = B;
     J.q_end = qlen;
     J.s_end = slen;
@@ -547,13 +652,13 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     J.want_ends = aln != nullptr;
     J.d_scores_out = nullptr;
     J.d_aln_out = nullptr;
-    J.ev_packed = D.ev_free[set];  // recorded once the ASCII buffers are consumed
     uint64_t cap_words = 0;
     if (tb) {
       cap_words = qlen + slen + 1;  // worst case sum(n+m); exact total known after the walk
       CK(D.cigar.ensure(cap_words * 4));
     }
     s = run_device(ctx, D, prm, J, tb ? D.cigar.as<uint32_t>() : nullptr, cap_words);
+    if (s == ANYSEQ_OK && c > 0 && !tb) copy_out(c - 1);  // run_device synchronised past it
     if (s != ANYSEQ_OK) {
       if (s == ANYSEQ_E_BADSEQ) describe_badseq(ctx, b, a0);
       cudaStreamSynchronize(cs);
@@ -561,8 +666,9 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
       return s;
     }
     if (!tb) {
-      CK(cudaMemcpyAsync(scores + a0, D.scores.p, B * 4, cudaMemcpyDeviceToHost, st));
-      if (aln) CK(cudaMemcpyAsync(aln + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_sc + a0, D.scores.p, B * 4, cudaMemcpyDeviceToHost, st));
+      mark(st, "scores-d2h-issued", c);
+      if (aln) CK(cudaMemcpyAsync(h_al + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
     } else {
       CK(cudaMemcpyAsync(aln + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
       cig->resize(cig_base + J.cigar_total);
@@ -573,8 +679,14 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
         for (uint64_t k = a0; k < a1; ++k) aln[k].cigar_offset += cig_base;
       cig_base += J.cigar_total;
     }
+    CK(cudaEventRecord(D.ev_free[set], st));  // every kernel reading this set is enqueued
   }
   CK(cudaStreamSynchronize(st));
+  if (!tb && NC > 0) copy_out(NC - 1);
+  if (ctx->timing >= 2) {
+    CK(cudaStreamSynchronize(cs));
+    ctx->dump_trace();
+  }
   return ANYSEQ_OK;
 }
 
@@ -679,7 +791,7 @@ anyseq_status anyseq_create(anyseq_ctx** out, const int* device_ids, int num_dev
     if (cudaSetDevice(id) != cudaSuccess ||
         cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaDeviceGetAttribute(&D.num_sms, cudaDevAttrMultiProcessorCount, id) != cudaSuccess ||
-        cudaMallocHost(&D.h_sum, sizeof(PlanSummary)) != cudaSuccess ||
+        cudaHostAlloc((void**)&D.h_sum, sizeof(PlanSummary), cudaHostAllocMapped) != cudaSuccess ||
         cudaMallocHost(&D.h_small, 64) != cudaSuccess ||
         cudaStreamCreateWithFlags(&D.copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&D.ev_up[0], cudaEventDisableTiming) != cudaSuccess ||
@@ -712,6 +824,7 @@ void anyseq_destroy(anyseq_ctx* c) {
                       &D.cig_off, &D.ops,     &D.dirs,   &D.tb,     &D.strip, &D.aln,
                       &D.cigar,   &D.temp,    &D.sum,    &D.long_ws};
     for (DevBuf* b : bufs) b->release();
+    D.h_stage.release();
     if (D.h_sum) cudaFreeHost(D.h_sum);
     if (D.h_small) cudaFreeHost(D.h_small);
     for (int i = 0; i < 2; ++i) {
@@ -813,7 +926,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
   if (!ctx || !name) return ANYSEQ_E_INVALID;
   std::string n(name);
   if (n == "tb_scratch_bytes") { ctx->tb_scratch_bytes = std::max<int64_t>(value, 1 << 20); return ANYSEQ_OK; }
-  if (n == "timing") { ctx->timing = value ? 1 : 0; return ANYSEQ_OK; }
+  if (n == "timing") { ctx->timing = (int)value; return ANYSEQ_OK; }
   if (n == "force_variant") { ctx->force_variant = value; return ANYSEQ_OK; }
   if (n == "chunk_bytes") { ctx->chunk_bytes = std::max<int64_t>(value, 1 << 16); return ANYSEQ_OK; }
   if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }

@@ -36,16 +36,28 @@ __device__ int64_t find_pair(const uint64_t* off, uint64_t num_pairs, uint64_t p
   return lo;
 }
 
-__global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ in, uint64_t len,
-                                                   uint8_t* __restrict__ out, uint64_t pos_base,
-                                                   const uint64_t* __restrict__ off,
-                                                   uint64_t num_pairs, uint32_t* flags,
-                                                   PlanSummary* sum) {
+struct PackSeg {
+  const uint8_t* in;
+  uint64_t len;
+  uint8_t* out;
+  uint64_t pos_base;
+  const uint64_t* off;
+};
+
+// One launch packs both sequence sets: units [0, u0) are q's 16-byte units, [u0, u0+u1) s's.
+__global__ void __launch_bounds__(256) pack_kernel(PackSeg q, PackSeg s, uint64_t num_pairs,
+                                                   uint32_t* flags, PlanSummary* sum) {
   __shared__ uint8_t lut[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = (uint8_t)code_of((uint32_t)i);
   __syncthreads();
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 16;
-  for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; b < len; b += stride) {
+  const uint64_t u0 = (q.len + 15) / 16, units = u0 + (s.len + 15) / 16;
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const bool isq = u < u0;
+    const PackSeg& g = isq ? q : s;
+    const uint64_t b = (isq ? u : u - u0) * 16, len = g.len;
+    const uint8_t* in = g.in;
+    uint8_t* out = g.out;
     const bool vec = (b + 16 <= len) && ((((uintptr_t)(in + b)) & 15) == 0) &&
                      ((((uintptr_t)(out + b)) & 15) == 0);
     uint32_t w[4] = {0, 0, 0, 0};
@@ -60,55 +72,75 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* __restrict__ i
     uint32_t o[4];
     uint32_t bad = 0, nn = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int t = 0; t < 4; ++t) {
       uint32_t r = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint32_t x = lut[(w[q] >> (8 * k)) & 0xffu];
+        const uint32_t x = lut[(w[t] >> (8 * k)) & 0xffu];
         r |= x << (8 * k);
-        const bool in_range = (q * 4 + k) < cnt;
-        bad |= (in_range && x == 0xFFu) ? (1u << (q * 4 + k)) : 0u;
+        const bool in_range = (t * 4 + k) < cnt;
+        bad |= (in_range && x == 0xFFu) ? (1u << (t * 4 + k)) : 0u;
         nn |= (in_range && x == 4u) ? 1u : 0u;
       }
-      o[q] = r;
+      o[t] = r;
     }
     if (vec) {
       *reinterpret_cast<uint4*>(out + b) = make_uint4(o[0], o[1], o[2], o[3]);
     } else {
       for (int k = 0; k < cnt; ++k) out[b + k] = (uint8_t)(o[k >> 2] >> (8 * (k & 3)));
     }
-    if (bad) atomicMin(&sum->err_pos, (unsigned long long)(pos_base + b + __ffs(bad) - 1));
-    if (nn) {  // rare: mark every pair that owns an N in this chunk
+    if (bad) atomicMin(&sum->err_pos, (unsigned long long)(g.pos_base + b + __ffs(bad) - 1));
+    if (nn) {  // rare: mark every pair that owns an N in this unit
       for (int k = 0; k < cnt; ++k)
         if (((o[k >> 2] >> (8 * (k & 3))) & 0xffu) == 4u)
-          atomicOr(&flags[find_pair(off, num_pairs, b + k)], 1u);
+          atomicOr(&flags[find_pair(g.off, num_pairs, b + k)], 1u);
     }
   }
 }
 
-cudaError_t launch_pack(const char* d_ascii, uint64_t len, uint8_t* d_code, uint64_t pos_base,
-                        const uint64_t* d_off, uint64_t num_pairs, uint32_t* d_flags,
-                        PlanSummary* d_sum, cudaStream_t st, int num_sms) {
-  if (len == 0) return cudaSuccess;
-  const int threads = 256;
-  const int grid = grid_for((int64_t)((len + 15) / 16), threads, num_sms, 16);
-  pack_kernel<<<grid, threads, 0, st>>>((const uint8_t*)d_ascii, len, d_code, pos_base, d_off,
-                                        num_pairs, d_flags, d_sum);
+cudaError_t launch_pack(const char* d_q, uint64_t q_len, uint8_t* d_qcode, const uint64_t* d_qoff,
+                        const char* d_s, uint64_t s_len, uint8_t* d_scode, const uint64_t* d_soff,
+                        uint64_t num_pairs, uint32_t* d_flags, PlanSummary* d_sum,
+                        cudaStream_t st, int num_sms) {
+  const uint64_t units = (q_len + 15) / 16 + (s_len + 15) / 16;
+  if (units == 0) return cudaSuccess;
+  PackSeg q{(const uint8_t*)d_q, q_len, d_qcode, 0, d_qoff};
+  PackSeg s{(const uint8_t*)d_s, s_len, d_scode, 1ull << 62, d_soff};
+  pack_kernel<<<grid_for((int64_t)units, 256, num_sms, 16), 256, 0, st>>>(q, s, num_pairs, d_flags,
+                                                                           d_sum);
   return cudaGetLastError();
 }
 
-// ----------------------------------------------------------------------------- rebase
-__global__ void rebase_kernel(uint64_t* q, uint64_t* s, uint64_t n, uint64_t q0, uint64_t s0) {
+// ------------------------------------------------------------------------ prep / publish
+__global__ void prep_kernel(uint32_t* flags, uint64_t n, PlanSummary* sum, uint64_t* qoff,
+                            uint64_t* soff, uint64_t q0, uint64_t s0) {
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (uint64_t)gridDim.x * blockDim.x) {
-    q[k] -= q0;
-    s[k] -= s0;
+    flags[k] = 0;
+    if (qoff) {  // host-API chunk: offsets were uploaded verbatim
+      qoff[k] -= q0;
+      soff[k] -= s0;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < NV) {
+    const int v = threadIdx.x;
+    sum->count[v] = 0;
+    sum->maxn[v] = 0;
+    sum->maxm[v] = 0;
+    sum->kmin[v] = ~0ull;
+    sum->kmax[v] = 0ull;
+    if (v == 0) {
+      sum->err_pos = ~0ull;
+      sum->range_err = 0;
+      sum->blocks_done = 0;
+    }
   }
 }
 
-cudaError_t launch_rebase(uint64_t* q, uint64_t* s, uint64_t n, uint64_t q0, uint64_t s0,
-                          cudaStream_t st, int num_sms) {
-  rebase_kernel<<<grid_for((int64_t)n, 256, num_sms), 256, 0, st>>>(q, s, n, q0, s0);
+cudaError_t launch_prep(uint32_t* flags, uint64_t n, PlanSummary* sum, uint64_t* qoff,
+                        uint64_t* soff, uint64_t q0, uint64_t s0, cudaStream_t st, int num_sms) {
+  prep_kernel<<<grid_for((int64_t)n, 256, num_sms), 256, 0, st>>>(flags, n, sum, qoff, soff, q0,
+                                                                  s0);
   return cudaGetLastError();
 }
 
@@ -189,6 +221,21 @@ __global__ void classify_kernel(ClassifyArgs a) {
             }
           }
         }
+        // speculative slots for the uniform case (every pair in one variant, identity
+        // order); the host re-forms slots from the sorted order otherwise
+        if (variant_desc(v).pairs == 2) {
+          if (!(k & 1)) {
+            Slot sl;
+            sl.pair[0] = (int32_t)k;
+            sl.pair[1] = k + 1 < a.num_pairs ? (int32_t)(k + 1) : -1;
+            a.slots[k >> 1] = sl;
+          }
+        } else {
+          Slot sl;
+          sl.pair[0] = (int32_t)k;
+          sl.pair[1] = -1;
+          a.slots[k] = sl;
+        }
         key = ((unsigned long long)v << 58) |
               ((unsigned long long)(m < (1 << 29) - 1 ? m : (1 << 29) - 1) << 29) |
               (unsigned long long)(n < (1 << 29) - 1 ? n : (1 << 29) - 1);
@@ -218,10 +265,23 @@ __global__ void classify_kernel(ClassifyArgs a) {
     atomicMin(&a.sum->kmin[v], s_kmin[v]);
     atomicMax(&a.sum->kmax[v], s_kmax[v]);
   }
+  // the last block to finish publishes the summary into host-mapped memory (no copy-engine
+  // transfer: the host API's uploads keep the copy engine and the PCIe link busy)
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.sum->blocks_done, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    static_assert(sizeof(PlanSummary) % 8 == 0, "summary is copied in 8-byte words");
+    const volatile uint64_t* src = reinterpret_cast<const volatile uint64_t*>(a.sum);
+    volatile uint64_t* dst = reinterpret_cast<volatile uint64_t*>(a.host_sum);
+    for (int i = threadIdx.x; i < (int)(sizeof(PlanSummary) / 8); i += blockDim.x) dst[i] = src[i];
+  }
 }
 
 cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t st, int num_sms) {
-  if (a.num_pairs == 0) return cudaSuccess;
   const int threads = 256;
   classify_kernel<<<grid_for((int64_t)a.num_pairs, threads, num_sms), threads, 0, st>>>(a);
   return cudaGetLastError();

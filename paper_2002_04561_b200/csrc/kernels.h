@@ -8,14 +8,17 @@
 
 namespace anyseq {
 
-// a1: ASCII -> byte codes (A,C,G,T -> 0..3, N -> 4), validation, per-pair N flags.
-cudaError_t launch_pack(const char* d_ascii, uint64_t len, uint8_t* d_code, uint64_t pos_base,
-                        const uint64_t* d_off, uint64_t num_pairs, uint32_t* d_flags,
-                        PlanSummary* d_sum, cudaStream_t st, int num_sms);
+// a1: ASCII -> byte codes (A,C,G,T -> 0..3, N -> 4), validation, per-pair N flags; q and s
+// in one launch.
+cudaError_t launch_pack(const char* d_q, uint64_t q_len, uint8_t* d_qcode, const uint64_t* d_qoff,
+                        const char* d_s, uint64_t s_len, uint8_t* d_scode, const uint64_t* d_soff,
+                        uint64_t num_pairs, uint32_t* d_flags, PlanSummary* d_sum,
+                        cudaStream_t st, int num_sms);
 
-// host-API chunks: offsets uploaded verbatim, rebased to the chunk's first byte on device
-cudaError_t launch_rebase(uint64_t* q, uint64_t* s, uint64_t n, uint64_t q0, uint64_t s0,
-                          cudaStream_t st, int num_sms);
+// per-call plan state: clear the per-pair flags, initialise the device summary and (host-API
+// chunks, qoff != null) rebase the verbatim-uploaded offsets to the chunk's first byte
+cudaError_t launch_prep(uint32_t* flags, uint64_t n, PlanSummary* sum, uint64_t* qoff,
+                        uint64_t* soff, uint64_t q0, uint64_t s0, cudaStream_t st, int num_sms);
 
 struct ClassifyArgs {
   DevParams P;
@@ -25,6 +28,8 @@ struct ClassifyArgs {
   uint64_t num_pairs;
   const uint32_t* flags;
   PlanSummary* sum;
+  PlanSummary* host_sum;     // host-mapped copy written by the last block
+  Slot* slots;               // speculative uniform-case slots
   unsigned long long* keys;  // [num_pairs]
   int32_t* vals;             // [num_pairs]
   int32_t* scores;           // trivial pairs are finished here

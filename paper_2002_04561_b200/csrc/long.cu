@@ -505,20 +505,14 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     hs.err_pos = ~0ull;
     LK(cudaMemcpyAsync(D.sum.p, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
     LK(cudaStreamSynchronize(st));
-    uint64_t offs[2] = {0, 0};
+    uint64_t offs[4] = {0, n, 0, m};
     Buf off;
-    LK(cudaMalloc(&off.p, 16));
-    offs[1] = n;
-    LK(cudaMemcpy(off.p, offs, 16, cudaMemcpyHostToDevice));
-    LK(launch_pack((const char*)D.qa.p, n, (uint8_t*)D.qc.p, 0, (const uint64_t*)off.p, 1,
+    LK(cudaMalloc(&off.p, 32));
+    LK(cudaMemcpy(off.p, offs, 32, cudaMemcpyHostToDevice));
+    LK(launch_pack((const char*)D.qa.p, n, (uint8_t*)D.qc.p, (const uint64_t*)off.p,
+                   (const char*)D.sa.p, m, (uint8_t*)D.sc.p, (const uint64_t*)off.p + 2, 1,
                    (uint32_t*)D.flg.p, (PlanSummary*)D.sum.p, st, devs[d].num_sms));
-    offs[1] = m;
-    Buf off2;
-    LK(cudaMalloc(&off2.p, 16));
-    LK(cudaMemcpy(off2.p, offs, 16, cudaMemcpyHostToDevice));
-    LK(launch_pack((const char*)D.sa.p, m, (uint8_t*)D.sc.p, 1ull << 62, (const uint64_t*)off2.p, 1,
-                   (uint32_t*)D.flg.p, (PlanSummary*)D.sum.p, st, devs[d].num_sms));
-    *launches += 2;
+    *launches += 1;
     LK(cudaMemcpyAsync(&hs, D.sum.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     LK(cudaStreamSynchronize(st));
     if (hs.err_pos != ~0ull) {

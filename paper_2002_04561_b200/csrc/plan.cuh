@@ -38,7 +38,7 @@ struct PlanSummary {
   int32_t maxn[NV], maxm[NV];
   unsigned long long kmin[NV], kmax[NV];
   int32_t range_err;           // a pair exceeds the 32-bit score range
-  int32_t pad_;
+  int32_t blocks_done;         // classify's last-block detection
 };
 
 // Planner inputs decided on the host.
