@@ -188,15 +188,31 @@ class Context:
                                             _ptr(scores), _ptr(aln) if ends else None))
         return (scores, aln) if ends else scores
 
-    def traceback(self, scheme: Scheme, q, q_off, s, s_off, cigar_capacity: int | None = None):
-        """Full alignments.  Returns (alignments structured array, cigar uint32 words)."""
+    def traceback(self, scheme: Scheme, q, q_off, s, s_off, cigar_capacity: int | None = None,
+                  out_aln=None, out_cigar=None):
+        """Full alignments.  Returns (alignments structured array, cigar uint32 words).
+        `out_aln` / `out_cigar`: optional preallocated outputs (ALIGNMENT_DTYPE[B] and uint32
+        words; pinned memory avoids staging); out_cigar's length is the capacity."""
         b, keep = self._batch(q, q_off, s, s_off)
         B = int(b.num_pairs)
         q_off, s_off = keep[2], keep[3]
-        cap = int(q_off[-1] - q_off[0] + s_off[-1] - s_off[0]) if cigar_capacity is None \
-            else cigar_capacity
-        aln = np.zeros(B, dtype=ALIGNMENT_DTYPE)
-        cig = np.zeros(max(cap, 1), dtype=np.uint32)
+        if out_aln is not None:
+            if not (isinstance(out_aln, np.ndarray) and out_aln.dtype == ALIGNMENT_DTYPE
+                    and out_aln.shape == (B,) and out_aln.flags.c_contiguous):
+                raise ValueError("out_aln must be a contiguous ALIGNMENT_DTYPE array of B entries")
+            aln = out_aln
+        else:
+            aln = np.empty(B, dtype=ALIGNMENT_DTYPE)
+        if out_cigar is not None:
+            if not (isinstance(out_cigar, np.ndarray) and out_cigar.dtype == np.uint32
+                    and out_cigar.ndim == 1 and out_cigar.flags.c_contiguous):
+                raise ValueError("out_cigar must be a contiguous uint32 array")
+            cig = out_cigar
+            cap = len(cig) if cigar_capacity is None else min(cigar_capacity, len(cig))
+        else:
+            cap = int(q_off[-1] - q_off[0] + s_off[-1] - s_off[0]) if cigar_capacity is None \
+                else cigar_capacity
+            cig = np.empty(max(cap, 1), dtype=np.uint32)
         used = ctypes.c_uint64(0)
         p = scheme.c()
         st = _lib.anyseq_traceback(self._h, ctypes.byref(p), ctypes.byref(b), _ptr(aln),

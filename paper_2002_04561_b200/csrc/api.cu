@@ -227,6 +227,7 @@ struct DeviceJob {
   uint64_t* rebase_qoff = nullptr;  // host-API chunk: offsets to rebase by (q0, s0) first
   uint64_t* rebase_soff = nullptr;
   uint64_t rebase_q0 = 0, rebase_s0 = 0;
+  uint64_t cig_base = 0;            // traceback: added to every cigar_offset of this job
   int32_t* d_scores_out;      // score mode output (device) or null => ctx buffer
   anyseq_alignment* d_aln_out;  // alignment structs (device) or null => ctx buffer
   // traceback: cigar sizing results
@@ -474,9 +475,11 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     CK(exclusive_scan_i32_to_u64(D.temp.p, tbytes, D.n_ops.as<int32_t>(), D.cig_off.as<uint64_t>(),
                                  (int64_t)B + 1, st));
     L(1);
+    ctx->mark(st, "walked+scanned");
     CK(cudaMemcpyAsync(D.h_small, D.cig_off.as<uint64_t>() + B, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     J.cigar_total = D.h_small[0];
+    ctx->mark(st, "host-has-total");
     fz.beg_i = D.beg_i.as<int32_t>();
     fz.beg_j = D.beg_j.as<int32_t>();
     fz.n_ops = D.n_ops.as<int32_t>();
@@ -484,6 +487,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     fz.ops = D.ops.as<uint32_t>();
     fz.cigar = d_cigar_out_or_null;
     fz.cigar_cap = cigar_cap;
+    fz.cig_base = J.cig_base;
   }
   if (J.tb || J.want_ends) {
     anyseq_alignment* out = J.d_aln_out;
@@ -494,6 +498,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     fz.out_aln = out;
     CK(launch_finalize(fz, st, D.num_sms));
     L(1);
+    ctx->mark(st, "finalized");
   }
   return ANYSEQ_OK;
 }
@@ -545,9 +550,13 @@ void describe_badseq(anyseq_ctx* ctx, const anyseq_batch* b, uint64_t k0) {
 // Host-memory batch on one device, pairs [k0, k1).  The shard is cut into chunks of about
 // ctx->chunk_bytes of sequence; the upload of chunk c+1 (copy stream, double-buffered)
 // overlaps the planning/relaxation of chunk c (compute stream).
+// Traceback cigar words go straight into the caller's buffer when cig_direct is set (one
+// device: offsets are final), else into *cig (multi-device: rebased after all shards finish).
+// *cig_words receives the shard's total cigar words either way.
 anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* prm,
                              const anyseq_batch* b, uint64_t k0, uint64_t k1, int tb,
-                             int32_t* scores, anyseq_alignment* aln, std::vector<uint32_t>* cig) {
+                             int32_t* scores, anyseq_alignment* aln, uint32_t* cig_direct,
+                             uint64_t cig_cap, std::vector<uint32_t>* cig, uint64_t* cig_words) {
   CK(cudaSetDevice(D.id));
   cudaStream_t st = D.stream, cs = D.copy_stream;
   // chunk boundaries by cumulative sequence bytes (offsets are monotone)
@@ -555,11 +564,11 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
   {
     // ramp-up: the first upload is not overlapped with anything, so the first chunks are
     // small (1/8, 1/4, 1/2 of chunk_bytes) and the compute stream starts early
-    const uint64_t full = (uint64_t)std::max<int64_t>(ctx->chunk_bytes, 1 << 20);
+    const uint64_t full = (uint64_t)std::max<int64_t>(ctx->chunk_bytes, 1 << 12);
     uint64_t k = k0;
     int c = 0;
     while (k < k1) {
-      const uint64_t cap = std::max<uint64_t>(1 << 20, c < 3 ? full >> (3 - c) : full);
+      const uint64_t cap = std::max<uint64_t>(1 << 12, c < 3 ? full >> (3 - c) : full);
       ++c;
       const uint64_t base = b->q_off[k] + b->s_off[k];
       uint64_t lo = k + 1, hi = k1;  // last index e in (k, k1] with bytes(k, e) <= cap
@@ -576,7 +585,7 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
   // into pageable memory would block the host until the chunk finished and stall the upload
   // pipeline, so pageable outputs are staged in pinned memory and copied out one chunk late.
   const bool stage_s = !tb && !host_pinned(scores);
-  const bool stage_a = !tb && aln && !host_pinned(aln);
+  const bool stage_a = aln && !host_pinned(aln);
   const uint64_t nloc = k1 - k0;
   const size_t st_a_off = stage_s ? ((nloc * 4 + 63) & ~63ull) : 0;
   if (stage_s || stage_a)
@@ -645,6 +654,7 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     J.rebase_soff = D.s_off2[set].as<uint64_t>();
     J.rebase_q0 = q0;
     J.rebase_s0 = s0;
+    J.cig_base = cig_base;
     J.B = B;
     J.q_end = qlen;
     J.s_end = slen;
@@ -658,7 +668,7 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
       CK(D.cigar.ensure(cap_words * 4));
     }
     s = run_device(ctx, D, prm, J, tb ? D.cigar.as<uint32_t>() : nullptr, cap_words);
-    if (s == ANYSEQ_OK && c > 0 && !tb) copy_out(c - 1);  // run_device synchronised past it
+    if (s == ANYSEQ_OK && c > 0) copy_out(c - 1);  // run_device synchronised past it
     if (s != ANYSEQ_OK) {
       if (s == ANYSEQ_E_BADSEQ) describe_badseq(ctx, b, a0);
       cudaStreamSynchronize(cs);
@@ -670,19 +680,27 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
       mark(st, "scores-d2h-issued", c);
       if (aln) CK(cudaMemcpyAsync(h_al + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
     } else {
-      CK(cudaMemcpyAsync(aln + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
-      cig->resize(cig_base + J.cigar_total);
-      if (J.cigar_total)
-        CK(cudaMemcpyAsync(cig->data() + cig_base, D.cigar.p, J.cigar_total * 4, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (cig_base)
-        for (uint64_t k = a0; k < a1; ++k) aln[k].cigar_offset += cig_base;
+      // cigar offsets already include cig_base (finalize adds J.cig_base on the device)
+      CK(cudaMemcpyAsync(h_al + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
+      if (J.cigar_total && cig_direct) {
+        if (cig_base + J.cigar_total <= cig_cap)
+          CK(cudaMemcpyAsync(cig_direct + cig_base, D.cigar.p, J.cigar_total * 4,
+                             cudaMemcpyDeviceToHost, st));
+      } else if (J.cigar_total) {
+        // the vector may reallocate: its previous contents must have landed
+        CK(cudaStreamSynchronize(st));
+        cig->resize(cig_base + J.cigar_total);
+        CK(cudaMemcpyAsync(cig->data() + cig_base, D.cigar.p, J.cigar_total * 4,
+                           cudaMemcpyDeviceToHost, st));
+      }
+      mark(st, "tb-d2h-issued", c);
       cig_base += J.cigar_total;
     }
     CK(cudaEventRecord(D.ev_free[set], st));  // every kernel reading this set is enqueued
   }
   CK(cudaStreamSynchronize(st));
-  if (!tb && NC > 0) copy_out(NC - 1);
+  if (NC > 0) copy_out(NC - 1);
+  if (cig_words) *cig_words = cig_base;
   if (ctx->timing >= 2) {
     CK(cudaStreamSynchronize(cs));
     ctx->dump_trace();
@@ -716,8 +734,10 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
   std::vector<anyseq_status> st(G, ANYSEQ_OK);
   std::vector<std::string> errs(G);
   std::vector<std::vector<uint32_t>> cigs(G);
+  std::vector<uint64_t> words(G, 0);
   if (G == 1) {
-    st[0] = run_host_shard(ctx, ctx->devs[0], prm, b, 0, b->num_pairs, tb, scores, aln, &cigs[0]);
+    st[0] = run_host_shard(ctx, ctx->devs[0], prm, b, 0, b->num_pairs, tb, scores, aln,
+                           tb ? cigar : nullptr, cap, &cigs[0], &words[0]);
   } else {
     std::vector<anyseq_ctx*> sub(G);
     std::vector<std::thread> th;
@@ -732,7 +752,7 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
         anyseq_status s = ANYSEQ_OK;
         if (bounds[g + 1] > bounds[g])
           s = run_host_shard(&local, ctx->devs[g], prm, b, bounds[g], bounds[g + 1], tb, scores,
-                             aln, &cigs[g]);
+                             aln, nullptr, 0, &cigs[g], &words[g]);
         std::lock_guard<std::mutex> lk(mu);
         st[g] = s;
         errs[g] = local.err;
@@ -749,16 +769,18 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
   if (st[0] != ANYSEQ_OK) return st[0];
   if (tb) {
     uint64_t total = 0;
-    for (int g = 0; g < G; ++g) total += cigs[g].size();
+    for (int g = 0; g < G; ++g) total += words[g];
     if (used) *used = total;
     if (total > cap) return fail(ctx, ANYSEQ_E_CAPACITY, "cigar needs %llu words, capacity %llu",
                                  (unsigned long long)total, (unsigned long long)cap);
-    uint64_t base = 0;
-    for (int g = 0; g < G; ++g) {
-      if (!cigs[g].empty()) memcpy(cigar + base, cigs[g].data(), cigs[g].size() * 4);
-      if (base)
-        for (uint64_t k = bounds[g]; k < bounds[g + 1]; ++k) aln[k].cigar_offset += base;
-      base += cigs[g].size();
+    if (G > 1) {
+      uint64_t base = 0;
+      for (int g = 0; g < G; ++g) {
+        if (!cigs[g].empty()) memcpy(cigar + base, cigs[g].data(), cigs[g].size() * 4);
+        if (base)
+          for (uint64_t k = bounds[g]; k < bounds[g + 1]; ++k) aln[k].cigar_offset += base;
+        base += cigs[g].size();
+      }
     }
   }
   return ANYSEQ_OK;

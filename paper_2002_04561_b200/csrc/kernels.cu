@@ -456,7 +456,7 @@ __global__ void finalize_kernel(FinalizeArgs a) {
     if (a.n_ops) {
       const int nops = a.n_ops[k];
       const uint64_t off = a.cig_off[k];
-      o.cigar_offset = off;
+      o.cigar_offset = a.cig_base + off;
       o.cigar_len = (uint32_t)nops;
       if (a.cigar && off + nops <= a.cigar_cap) {
         const uint32_t* src = a.ops + a.q_off[k] + a.s_off[k] + k;

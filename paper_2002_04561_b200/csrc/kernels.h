@@ -93,6 +93,7 @@ struct FinalizeArgs {
   void* out_aln;          // anyseq_alignment[num_pairs]
   uint32_t* cigar;        // compacted cigar (may be null)
   uint64_t cigar_cap;
+  uint64_t cig_base;      // added to every output cigar_offset
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t st, int num_sms);
 

@@ -306,6 +306,37 @@ def test_host_chunking_and_tb_scratch_chunks(ctx):
         ctx.set_option("tb_scratch_bytes", 4 << 30)
 
 
+def test_host_pipeline_many_chunks_pinned_outputs(ctx):
+    """Many upload chunks (4 KB), pinned and pageable outputs, cigar written straight into a
+    caller buffer across chunks, and the capacity error when that buffer is one word short."""
+    import torch
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    q, qo, s, so = random_pairs(900, 0, 200, seed=81)
+    res, ocig = _oracle("semi", "affine", 5, 1, q, qo, s, so, tb=True)
+    sch = A.Scheme("semi", "affine", 2, -1, 5, 1)
+    pin = lambda a: torch.from_numpy(a.view(np.uint8)).pin_memory().numpy().view(a.dtype)
+    B = len(qo) - 1
+    ctx.set_option("chunk_bytes", 1 << 12)
+    try:
+        _check_scores(ctx, sch, q, qo, s, so, res)
+        _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+        out = pin(np.full(B, -7, np.int32))
+        ctx.align_batch(sch, pin(q), pin(qo), pin(s), pin(so), out=out)
+        assert np.array_equal(out, res["score"].astype(np.int32))
+        aln, cig = ctx.traceback(sch, q, qo, s, so)
+        paln = pin(np.zeros(B, A.ALIGNMENT_DTYPE))
+        pcig = pin(np.zeros(len(cig) + 5, np.uint32))
+        aln2, cig2 = ctx.traceback(sch, pin(q), pin(qo), pin(s), pin(so), out_aln=paln,
+                                   out_cigar=pcig)
+        assert np.array_equal(aln2, aln) and np.array_equal(cig2, cig)
+        with pytest.raises(A.AnyseqError) as e:
+            ctx.traceback(sch, q, qo, s, so, out_cigar=np.zeros(len(cig) - 1, np.uint32))
+        assert e.value.status_name == "E_CAPACITY" and e.value.cigar_used == len(cig)
+    finally:
+        ctx.set_option("chunk_bytes", 64 << 20)
+
+
 def test_multi_device_context():
     """A context over all visible GPUs shards the batch by cells; identical results."""
     import torch
