@@ -50,8 +50,11 @@ __device__ __forceinline__ uint32_t imad_add(uint32_t x, uint32_t one, uint32_t 
 // CGE/CGO > 0: the gap extend / open values are compile-time constants (the paper's partial
 // evaluation of the scoring scheme): the packed constants then become
 // instruction immediates and the 3-source DPX/IMAD ops read one register less.
+#ifndef FILL_MINB_SCORE
+#define FILL_MINB_SCORE 4  // resident 128-thread blocks per SM the score kernels are built for
+#endif
 template <class V, int KIND, int GAP, int L, int R, bool TB, bool POS, int CGE = 0, int CGO = 0>
-__global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(FillArgs a) {
+__global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(FillArgs a) {
   using T = typename V::T;
   constexpr int PP = V::P;
   constexpr int G = 32 / L;
@@ -183,7 +186,10 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
       track[threadIdx.x].pad[X] = pad[X];
     }
 
-    for (int st = 0; st < NSw; ++st) {
+    // one strip of the sweep; MULTI = the warp has more than one strip (strip scratch rows
+    // are read and written): single-strip warps (short reads) compile without any of it
+    auto strip = [&](auto multi, const int st) {
+      constexpr bool MULTI = decltype(multi)::value;
       const bool sact = st < NS;
       if (Mw > SELCAP) {  // ring restarts with every strip
         fill_sel(0, min(M, 384));
@@ -250,8 +256,16 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
       // CHK = this step may contain a lane's column 0 (initial column) or a pair's column m
       // (captures); the steady-state steps in between run without those checks.
       const uint32_t selbase = (uint32_t)__cvta_generic_to_shared(&seltab[gb][0]);
-      uint32_t selo = 0;
-      auto rebase = [&](int kk) { selo = selbase + (uint32_t)(((kk - t) & (SELCAP - 1)) * 2); };
+      uint32_t selo = 0, selv = 0;  // selv = selector of the next step (loaded one step ahead)
+      auto lds16 = [&](uint32_t addr) -> uint32_t {
+        unsigned short v16;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v16) : "r"(addr));
+        return v16;
+      };
+      auto rebase = [&](int kk) {
+        selo = selbase + (uint32_t)(((kk - t) & (SELCAP - 1)) * 2);
+        selv = lds16(selo);
+      };
       auto step = [&](auto chk, const int k, T (&Hi)[R], T (&Hq)[R]) {
         constexpr bool CHK = decltype(chk)::value;
         T hin = V::shfl_up(Hbot, L);
@@ -261,13 +275,9 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         // selector of this lane's column: a shared-memory pointer that advances by one slot
         // per step (IMAD, FMA pipe) and is re-based every 128 steps (the mirror covers the
         // wrap in between), so the hot loop spends no ALU instruction on addressing
-        uint32_t sel;
-        {
-          unsigned short v16;
-          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v16) : "r"(selo));
-          sel = v16;
-        }
+        const uint32_t sel = selv;
         selo = imad_add(selo, one, 2u);
+        selv = lds16(selo);  // prefetch: the load latency overlaps this step's rows
         const bool act = CHK ? (sact && col >= 0 && col < M) : sact;
         if (CHK && col == 0 && sact) {
 #pragma unroll
@@ -283,7 +293,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
             for (int X = 0; X < PP; ++X) rj[X] = 0;
           }
         }
-        if (st == 0) {  // the initial row (P:259 / P:262): no load, no branch
+        if (!MULTI || st == 0) {  // the initial row (P:259 / P:262): no load, no branch
           const int h0 = (KIND == KGLOBAL) ? -(P.go + (col + 1) * P.ge) : 0;  // H(0,j)
           const T h0v = enc(h0, h0);
           if (t == 0) {
@@ -376,7 +386,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         Hbot = Hq[R - 1];
         Ebot = e;
         if (TB) MEbot = me;
-        if (NSw > 1 && act && t == L - 1 && st + 1 < NS)
+        if (MULTI && act && t == L - 1 && st + 1 < NS)
           scr[col] = make_uint4((uint32_t)Hq[R - 1], (uint32_t)e, TB ? me : 0u, 0u);
 
         // ---- optimum bookkeeping ----
@@ -543,7 +553,12 @@ __global__ void __launch_bounds__(128, TB ? 2 : (R > 8 ? 4 : 4)) fill_kernel(Fil
         }
       }
       __syncwarp();
-    }  // strips
+    };  // strip
+    if (NSw == 1) {
+      strip(std::false_type{}, 0);
+    } else {
+      for (int st = 0; st < NSw; ++st) strip(std::true_type{}, st);
+    }
 
     // ---- reduce across the lane group and write results (P:424-436 steps 8, 10) ----
     int osc[PP], oi[PP], oj[PP];
