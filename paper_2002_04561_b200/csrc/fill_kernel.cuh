@@ -157,12 +157,24 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
     // column selectors of this slot in a 512-entry shared ring: columns [0, 384) now, then
     // 128 more every 128 steps (a lane at step k reads column k - t, t < L <= 8)
     auto fill_sel = [&](int c0, int c1) {
-      for (int c = c0 + t; c < c1; c += L) {
-        const uint32_t x0 = (c < mm[0]) ? a.scode[so[0] + c] : 0u;
-        const uint32_t x1 = (PP == 2 && c < mm[PP - 1]) ? a.scode[so[PP - 1] + c] : 0u;
-        const uint16_t sv = (uint16_t)V::selector(x0, x1);
-        seltab[gb][c & (SELCAP - 1)] = sv;
-        if ((c & (SELCAP - 1)) < SELMIR) seltab[gb][SELCAP + (c & (SELCAP - 1))] = sv;
+      constexpr int U = 4;  // loads in flight per lane before the first use
+      for (int cb = c0 + t; cb < c1; cb += L * U) {
+        uint32_t x0[U], x1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = cb + u * L;
+          x0[u] = (c < c1 && c < mm[0]) ? a.scode[so[0] + c] : 0u;
+          x1[u] = (PP == 2 && c < c1 && c < mm[PP - 1]) ? a.scode[so[PP - 1] + c] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = cb + u * L;
+          if (c < c1) {
+            const uint16_t sv = (uint16_t)V::selector(x0[u], x1[u]);
+            seltab[gb][c & (SELCAP - 1)] = sv;
+            if ((c & (SELCAP - 1)) < SELMIR) seltab[gb][SELCAP + (c & (SELCAP - 1))] = sv;
+          }
+        }
       }
     };
     if (Mw <= SELCAP) {  // the whole slot fits: built once for all strips
@@ -526,7 +538,14 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
 #pragma unroll 1
         for (int X = 0; X < PP; ++X) {
           const int nX = tr.nn[X], pX = tr.pad[X];
-          if (KIND == KSEMI) {  // column m candidates i = 1..n of this strip (reading R5)
+          if (KIND == KSEMI && !pos) {
+            // score only: the column-m maximum without its row (pad rows hold H = 0, which
+            // is the H(0,m) candidate anyway)
+            T cmx = (T)capbuf[X][threadIdx.x][0];
+#pragma unroll
+            for (int r = 1; r < R; ++r) cmx = V::vmax(cmx, (T)capbuf[X][threadIdx.x][r]);
+            tr.cv[X] = max(tr.cv[X], dec(cmx, X));
+          } else if (KIND == KSEMI) {  // column m candidates i = 1..n of this strip (R5)
             int cvx = tr.cv[X], cix = tr.ci[X];
 #pragma unroll 1
             for (int r = 0; r < R; ++r) {
