@@ -1,4 +1,5 @@
 // csrc/fill_dispatch.cu -- variant -> kernel instance, persistent grid sizing.
+#include <cstdlib>
 #include <mutex>
 #include "kernels.h"
 #include "fill_inst.cuh"
@@ -39,6 +40,12 @@ cudaError_t launch_fill(int variant, int kind, int gap, const FillArgs& a, cudaS
       occ[variant][kind][gap][pos][spec][dev & 15] = nb;
     }
   }
+  // debug/tuning: ANYSEQ_FILL_BPS caps the resident blocks per SM of the persistent grid
+  static const int bps_cap = [] {
+    const char* e = getenv("ANYSEQ_FILL_BPS");
+    return e ? atoi(e) : 0;
+  }();
+  if (bps_cap > 0 && nb > bps_cap) nb = bps_cap;
   const int grid = num_sms * nb;
   if (grid_out) *grid_out = grid;
   fn<<<grid, 128, 0, st>>>(a);
