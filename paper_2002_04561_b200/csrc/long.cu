@@ -55,6 +55,7 @@ struct LongArgs {
   int32_t chunk;
   int32_t one;
   int32_t lag;
+  int32_t keyed;  // local: 32 * (max score) fits in 31 bits -> packed (value, row) tracking
   unsigned long long* prof;  // optional: [0] cycles waiting, [1] cycles in tasks, [2] tasks
   long long spin_limit;
 };
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
   const int NGE = -P.ge;
   const int cop = (GAP == GAFFINE) ? (P.go + P.ge) : P.ge;
   const uint32_t one = (uint32_t)a.one;
+  const uint32_t k32 = one << 5;  // 32, opaque to the compiler: key = H * 32 + row stays an IMAD
   auto hop = [&](int h) -> int { return imad_add_s(h, one, -cop); };  // FMA pipe
   const int n = a.n, m = a.m;
   // semi/global: where row n lives inside the last row strip
@@ -198,157 +200,189 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
 
     int diag = 0, Hbot = NEG, Ebot = NEG;
     int sv = 0, si = 0, sj = 0;  // local per task
-    bool aborted = false;
+    int skey = 0;                // keyed local tracking: best (H << 5 | 31 - r) of this lane
 
-    auto step = [&](auto chk, const int k, int (&Hi)[R], int (&Hq)[R]) {
-      constexpr bool CHK = decltype(chk)::value;
-      int hin = V::shfl_up(Hbot, L);
-      int ein = V::shfl_up(Ebot, L);
-      const int lc = k - t;
-      const uint32_t sel = ring_sel[wb][lc & (RING - 1)];
-      const bool act = !CHK || (lc >= 0 && lc < W);
-      if (CHK && lc == 0) {  // the left boundary column H(i, c_lo), F(i, c_lo)
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int ip = ip0 + r;
-          int2 b = make_int2(0, NEG);
-          if (ip < n) b = bl[ip + 1];
-          Hi[r] = b.x;
-          Ff[r] = b.y;
-        }
-        diag = (ip0 <= n) ? bl[ip0].x : 0;
-      }
-      if (t == 0) {
-        if (s == 0) {
-          const int h0 = (KIND == KGLOBAL) ? -(P.go + (c_lo + lc + 1) * P.ge) : 0;  // H(0,j)
-          hin = h0;
-          ein = FAST ? hop(h0) : NEG;
-        } else {
-          const int2 v = ring_he[wb][lc & (RING - 1)];
-          hin = v.x;
-          ein = v.y;
-        }
-      }
-      int e = ein;
-      if (FAST) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int hd = (r == 0) ? diag : Hi[r - 1];
-          const int sig = V::sigma(p0[r], p1[r], sel);
-          Ff[r] = V::addmax(Ff[r], NGE, hop(Hi[r]));
-          const int df = V::addmax(hd, sig, Ff[r]);
-          Hq[r] = (KIND == KLOCAL) ? V::vmax_relu(df, e) : max(df, e);
-          e = V::addmax(e, NGE, hop(df));
-        }
-      } else {
-        int hup = hop(hin);
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int hd = (r == 0) ? diag : Hi[r - 1];
-          const int sig = V::sigma(p0[r], p1[r], sel);
-          const int tm = max(hup, hop(Hi[r]));
-          Hq[r] = (KIND == KLOCAL) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
-          hup = hop(Hq[r]);
-        }
-        e = NEG;
-      }
-      diag = hin;
-      Hbot = Hq[R - 1];
-      Ebot = e;
-      if (t == L - 1 && act) {
-        a.rowbuf[c_lo + lc + 1] = make_int2(Hq[R - 1], e);  // in place: strip s+1 reads it
-        if ((lc & (a.chunk - 1)) == a.chunk - 1 || lc == W - 1) st_release_gpu(&a.rowprog[g * a.S + s], lc + 1);
-      }
-      const int j = c_lo + lc + 1;  // real column
-      if (KIND == KLOCAL) {
-        int cm = 0;
-        if (!last_strip) {
-          cm = Hq[0];
-#pragma unroll
-          for (int r = 1; r + 1 < R; r += 2) cm = V::vmax3(cm, Hq[r], Hq[r + 1]);
-          if ((R % 2) == 0) cm = max(cm, Hq[R - 1]);
-        } else {
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (ip0 + r < n) cm = max(cm, Hq[r]);
-        }
-        if (CHK && !act) cm = 0;
-        if (cm > sv) {
-          int rr = R - 1;
-#pragma unroll
-          for (int r = R - 1; r >= 0; --r)
-            if (Hq[r] == cm && ip0 + r < n) rr = r;
-          sv = cm;
-          si = ip0 + rr + 1;
-          sj = j;
-        }
-      } else if (KIND == KSEMI) {
-        if (last_strip && t == tn && act && j <= m - 1) {
-          int v = 0;
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (r == rn) v = Hq[r];
-          if (v > part.rv || (v == part.rv && j < part.rj)) { part.rv = v; part.rj = j; }
-        }
-      }
-      if (CHK && lc == W - 1) {  // a lane's last column of this task
-        if (KIND == KSEMI && last_col) {
+    // FIRST: the task's row strip is the matrix's first (lane 0 reads H(0, j) directly);
+    // KEYED: local maximum tracked as one packed key per lane (value, first row) -- no
+    // per-step row search (host sets a.keyed when 32 * max score fits in 31 bits).
+    auto sweep = [&](auto first_c, auto keyed_c) -> bool {
+      constexpr bool FIRST = decltype(first_c)::value;
+      constexpr bool KEYED = decltype(keyed_c)::value;
+      auto step = [&](auto chk, const int k, int (&Hi)[R], int (&Hq)[R]) {
+        constexpr bool CHK = decltype(chk)::value;
+        int hin = V::shfl_up(Hbot, L);
+        int ein = V::shfl_up(Ebot, L);
+        const int lc = k - t;
+        const uint32_t sel = ring_sel[wb][lc & (RING - 1)];
+        const bool act = !CHK || (lc >= 0 && lc < W);
+        if (CHK && lc == 0) {  // the left boundary column H(i, c_lo), F(i, c_lo)
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            const int i = ip0 + r + 1;
-            if (i <= n && (Hq[r] > part.cv || (Hq[r] == part.cv && i < part.ci))) {
-              part.cv = Hq[r];
-              part.ci = i;
-            }
+            const int ip = ip0 + r;
+            int2 b = make_int2(0, NEG);
+            if (ip < n) b = bl[ip + 1];
+            Hi[r] = b.x;
+            Ff[r] = b.y;
+          }
+          diag = (ip0 <= n) ? bl[ip0].x : 0;
+        }
+        if (t == 0) {
+          if (FIRST) {
+            const int h0 = (KIND == KGLOBAL) ? -(P.go + (c_lo + lc + 1) * P.ge) : 0;  // H(0,j)
+            hin = h0;
+            ein = FAST ? hop(h0) : NEG;
+          } else {
+            const int2 v = ring_he[wb][lc & (RING - 1)];
+            hin = v.x;
+            ein = v.y;
           }
         }
-        if (KIND == KGLOBAL && last_strip && last_col && t == tn) {
-          int v = 0;
+        int e = ein;
+        if (FAST) {
 #pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (r == rn) v = Hq[r];
-          part.gv = v;
-          part.gset = 1;
-        }
-        if (br) {
+          for (int r = 0; r < R; ++r) {
+            const int hd = (r == 0) ? diag : Hi[r - 1];
+            const int sig = V::sigma(p0[r], p1[r], sel);
+            Ff[r] = V::addmax(Ff[r], NGE, hop(Hi[r]));
+            const int df = V::addmax(hd, sig, Ff[r]);
+            Hq[r] = (KIND == KLOCAL) ? V::vmax_relu(df, e) : max(df, e);
+            e = V::addmax(e, NGE, hop(df));
+          }
+        } else {
+          int hup = hop(hin);
 #pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (ip0 + r < n) br[ip0 + r + 1] = make_int2(Hq[r], Ff[r]);
+          for (int r = 0; r < R; ++r) {
+            const int hd = (r == 0) ? diag : Hi[r - 1];
+            const int sig = V::sigma(p0[r], p1[r], sel);
+            const int tm = max(hup, hop(Hi[r]));
+            Hq[r] = (KIND == KLOCAL) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
+            hup = hop(Hq[r]);
+          }
+          e = NEG;
         }
-      }
-    };
+        diag = hin;
+        Hbot = Hq[R - 1];
+        Ebot = e;
+        if (t == L - 1 && act) {
+          a.rowbuf[c_lo + lc + 1] = make_int2(Hq[R - 1], e);  // in place: strip s+1 reads it
+          if ((lc & (a.chunk - 1)) == a.chunk - 1 || lc == W - 1) st_release_gpu(&a.rowprog[g * a.S + s], lc + 1);
+        }
+        const int j = c_lo + lc + 1;  // real column
+        if (KIND == KLOCAL && KEYED) {
+          // rows below n (last strip) never win: their values come from real cells of an
+          // earlier column (sigma = 0 diagonal) or are strictly smaller (gaps), and the
+          // (value, j, i) order prefers the earlier column / smaller row (reading R10)
+          int key = imad_add_s(Hq[0], k32, 31);
+#pragma unroll
+          for (int r = 1; r + 1 < R; r += 2)
+            key = V::vmax3(key, imad_add_s(Hq[r], k32, 31 - r), imad_add_s(Hq[r + 1], k32, 30 - r));
+          if ((R % 2) == 0) key = max(key, imad_add_s(Hq[R - 1], k32, 32 - R));
+          if (CHK && !act) key = 0;
+          // a strictly larger value (the key's row part only orders rows of one column)
+          if (key > (skey | 31)) { skey = key; sj = j; }
+        } else if (KIND == KLOCAL) {
+          int cm = 0;
+          if (!last_strip) {
+            cm = Hq[0];
+#pragma unroll
+            for (int r = 1; r + 1 < R; r += 2) cm = V::vmax3(cm, Hq[r], Hq[r + 1]);
+            if ((R % 2) == 0) cm = max(cm, Hq[R - 1]);
+          } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (ip0 + r < n) cm = max(cm, Hq[r]);
+          }
+          if (CHK && !act) cm = 0;
+          if (cm > sv) {
+            int rr = R - 1;
+#pragma unroll
+            for (int r = R - 1; r >= 0; --r)
+              if (Hq[r] == cm && ip0 + r < n) rr = r;
+            sv = cm;
+            si = ip0 + rr + 1;
+            sj = j;
+          }
+        } else if (KIND == KSEMI) {
+          if (last_strip && t == tn && act && j <= m - 1) {
+            int v = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (r == rn) v = Hq[r];
+            if (v > part.rv || (v == part.rv && j < part.rj)) { part.rv = v; part.rj = j; }
+          }
+        }
+        if (CHK && lc == W - 1) {  // a lane's last column of this task
+          if (KIND == KSEMI && last_col) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int i = ip0 + r + 1;
+              if (i <= n && (Hq[r] > part.cv || (Hq[r] == part.cv && i < part.ci))) {
+                part.cv = Hq[r];
+                part.ci = i;
+              }
+            }
+          }
+          if (KIND == KGLOBAL && last_strip && last_col && t == tn) {
+            int v = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (r == rn) v = Hq[r];
+            part.gv = v;
+            part.gset = 1;
+          }
+          if (br) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              if (ip0 + r < n) br[ip0 + r + 1] = make_int2(Hq[r], Ff[r]);
+          }
+        }
+      };
 
-    const std::integral_constant<bool, true> ON{};
-    const std::integral_constant<bool, false> OFF{};
-    const int K = W + L - 1;
-    const int kA = min(K & ~1, L);               // every lane has reached column 0
-    const int kB = max(kA, (W - 1) & ~1);        // no lane has reached column W-1 yet
-    int k = 0;
-    auto maybe_refill = [&](int kk) -> bool {  // warp-uniform, every PER steps
-      if ((kk % PER) == 0 && kk > 0 && kk + PER < W) {
-        if (prog_up && !warp_wait<false>(prog_up, min(W, kk + 2 * PER), a)) return false;
-        refill(kk + PER, min(W, kk + 2 * PER));
-        __syncwarp();
+      const std::integral_constant<bool, true> ON{};
+      const std::integral_constant<bool, false> OFF{};
+      const int K = W + L - 1;
+      const int kA = min(K & ~1, L);               // every lane has reached column 0
+      const int kB = max(kA, (W - 1) & ~1);        // no lane has reached column W-1 yet
+      int k = 0;
+      auto maybe_refill = [&](int kk) -> bool {  // warp-uniform, every PER steps
+        if ((kk % PER) == 0 && kk > 0 && kk + PER < W) {
+          if (prog_up && !warp_wait<false>(prog_up, min(W, kk + 2 * PER), a)) return false;
+          refill(kk + PER, min(W, kk + 2 * PER));
+          __syncwarp();
+        }
+        return true;
+      };
+      for (; k < kA; k += 2) {
+        if (!maybe_refill(k)) return false;
+        step(ON, k, HA, HB);
+        step(ON, k + 1, HB, HA);
+      }
+      for (; k < kB; k += 2) {
+        if (!maybe_refill(k)) return false;
+        step(OFF, k, HA, HB);
+        step(OFF, k + 1, HB, HA);
+      }
+      for (; k + 1 < K; k += 2) {
+        if (!maybe_refill(k)) return false;
+        step(ON, k, HA, HB);
+        step(ON, k + 1, HB, HA);
+      }
+      if (k < K) step(ON, k, HA, HB);
+      if (KIND == KLOCAL && KEYED && skey > 0) {
+        sv = skey >> 5;
+        si = ip0 + (31 - (skey & 31)) + 1;
       }
       return true;
     };
-    for (; k < kA; k += 2) {
-      if (!maybe_refill(k)) { aborted = true; break; }
-      step(ON, k, HA, HB);
-      step(ON, k + 1, HB, HA);
+    bool done;
+    if (s == 0) {
+      done = (KIND == KLOCAL && a.keyed) ? sweep(std::true_type{}, std::true_type{})
+                                          : sweep(std::true_type{}, std::false_type{});
+    } else {
+      done = (KIND == KLOCAL && a.keyed) ? sweep(std::false_type{}, std::true_type{})
+                                          : sweep(std::false_type{}, std::false_type{});
     }
-    for (; !aborted && k < kB; k += 2) {
-      if (!maybe_refill(k)) { aborted = true; break; }
-      step(OFF, k, HA, HB);
-      step(OFF, k + 1, HB, HA);
-    }
-    for (; !aborted && k + 1 < K; k += 2) {
-      if (!maybe_refill(k)) { aborted = true; break; }
-      step(ON, k, HA, HB);
-      step(ON, k + 1, HB, HA);
-    }
-    if (!aborted && k < K) step(ON, k, HA, HB);
-    if (aborted) break;
+    if (!done) break;
     if (KIND == KLOCAL && lkey_better(sv, si, sj, part.lv, part.li, part.lj)) {
       part.lv = sv; part.li = si; part.lj = sj;
     }
@@ -590,6 +624,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     a.chunk = chunk;
     a.one = 1;
     a.lag = opt.start_lag > 0 ? opt.start_lag : chunk + 2 * 32 + 64;
+    a.keyed = (long double)std::max(P.match, 0) * std::min(n, m) < (long double)(1 << 25) ? 1 : 0;
     a.prof = nullptr;
     if (opt.profile) {
       LK(cudaMalloc(&D.profbuf.p, 64));
