@@ -208,12 +208,19 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
     auto sweep = [&](auto first_c, auto keyed_c) -> bool {
       constexpr bool FIRST = decltype(first_c)::value;
       constexpr bool KEYED = decltype(keyed_c)::value;
+      uint32_t sel_nx = 0;
+      int2 he_nx = make_int2(0, 0);
       auto step = [&](auto chk, const int k, int (&Hi)[R], int (&Hq)[R]) {
         constexpr bool CHK = decltype(chk)::value;
         int hin = V::shfl_up(Hbot, L);
         int ein = V::shfl_up(Ebot, L);
         const int lc = k - t;
-        const uint32_t sel = ring_sel[wb][lc & (RING - 1)];
+        // this step's selector / lane-0 input were loaded one step ahead (the ring holds
+        // columns up to the next refill point, see maybe_refill)
+        const uint32_t sel = sel_nx;
+        const int2 he = he_nx;
+        sel_nx = ring_sel[wb][(lc + 1) & (RING - 1)];
+        if (!FIRST) he_nx = ring_he[wb][(lc + 1) & (RING - 1)];
         const bool act = !CHK || (lc >= 0 && lc < W);
         if (CHK && lc == 0) {  // the left boundary column H(i, c_lo), F(i, c_lo)
 #pragma unroll
@@ -232,9 +239,8 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
             hin = h0;
             ein = FAST ? hop(h0) : NEG;
           } else {
-            const int2 v = ring_he[wb][lc & (RING - 1)];
-            hin = v.x;
-            ein = v.y;
+            hin = he.x;
+            ein = he.y;
           }
         }
         int e = ein;
@@ -263,9 +269,12 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
         diag = hin;
         Hbot = Hq[R - 1];
         Ebot = e;
-        if (t == L - 1 && act) {
-          a.rowbuf[c_lo + lc + 1] = make_int2(Hq[R - 1], e);  // in place: strip s+1 reads it
-          if ((lc & (a.chunk - 1)) == a.chunk - 1 || lc == W - 1) st_release_gpu(&a.rowprog[g * a.S + s], lc + 1);
+        if (t == L - 1 && act) a.rowbuf[c_lo + lc + 1] = make_int2(Hq[R - 1], e);  // strip s+1
+        {  // progress publication: warp-uniform test on lane L-1's column, lane L-1 releases
+          const int lcl = k - (L - 1);
+          if (lcl >= 0 && lcl < W && ((lcl & (a.chunk - 1)) == a.chunk - 1 || lcl == W - 1) &&
+              t == L - 1)
+            st_release_gpu(&a.rowprog[g * a.S + s], lcl + 1);
         }
         const int j = c_lo + lc + 1;  // real column
         if (KIND == KLOCAL && KEYED) {
@@ -341,6 +350,8 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
       const std::integral_constant<bool, true> ON{};
       const std::integral_constant<bool, false> OFF{};
       const int K = W + L - 1;
+      sel_nx = ring_sel[wb][(0 - t) & (RING - 1)];
+      if (!FIRST) he_nx = ring_he[wb][(0 - t) & (RING - 1)];
       const int kA = min(K & ~1, L);               // every lane has reached column 0
       const int kB = max(kA, (W - 1) & ~1);        // no lane has reached column W-1 yet
       int k = 0;
