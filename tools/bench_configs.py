@@ -1,6 +1,7 @@
 """Measure the secondary configs (C1, C3, C4, C5) on one GPU: device time of the library's
 kernels per call (CUDA events inside the library, option "timing") and host wall time of
-the synchronous host-API call, plus an oracle parity sample.  Prints one JSON per config.
+the synchronous host-API call from page-locked buffers (as bench.py e2e), plus an oracle
+parity sample.  Prints one JSON per config.
 Not the driver's bench line (bench.py is); numbers go to BASELINE.md."""
 import argparse
 import json
@@ -14,6 +15,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2002_04561_b200 as A  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 import synth  # noqa: E402
+
+
+def pin(a):
+    """Copy into page-locked host memory (the host API's fast path, as in bench.py's e2e)."""
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).pin_memory().numpy().view(a.dtype)
 
 
 def timed(ctx, fn, reps=3):
@@ -38,6 +45,7 @@ def main():
     args = ap.parse_args()
     ctx = A.Context([0])
     res = []
+    printed = 0
     for c in args.configs.split(","):
         if c == "c1":
             a, b = synth.c1_pair(1)
@@ -53,8 +61,12 @@ def main():
         elif c == "c3":
             qm, sm = synth.c2_reads(1_000_000, seed=2)
             q, qo = synth.uniform_csr(qm); s, so = synth.uniform_csr(sm)
+            q, qo, s, so = pin(q), pin(qo), pin(s), pin(so)
+            paln = pin(np.zeros(len(qo) - 1, A.ALIGNMENT_DTYPE))
+            pcig = pin(np.zeros(32 * (len(qo) - 1), np.uint32))
             sch = A.Scheme("local", "affine", 2, -1, 5, 1)
-            (aln, cig), wall, fill, walk = timed(ctx, lambda: ctx.traceback(sch, q, qo, s, so), 2)
+            (aln, cig), wall, fill, walk = timed(
+                ctx, lambda: ctx.traceback(sch, q, qo, s, so, out_aln=paln, out_cigar=pcig), 2)
             idx = np.random.default_rng(0).choice(len(qm), 300, replace=False)
             osch = O.Scheme("local", "affine", 2, -1, 5, 1)
             cigs = A.cigars_of(aln[idx], cig)
@@ -68,11 +80,18 @@ def main():
                         "gcups_fill_walk": cells / ((fill + walk) / 1e3) / 1e9, "parity_300": ok})
         elif c == "c5":
             q, qo, s, so = synth.c5_mixed(args.c5pairs, seed=5)
+            q, qo, s, so = pin(q), pin(qo), pin(s), pin(so)
+            B = len(qo) - 1
+            psc = pin(np.zeros(B, np.int32))
+            paln = pin(np.zeros(B, A.ALIGNMENT_DTYPE))
+            pcig = pin(np.zeros(int(qo[-1] + so[-1]) + B, np.uint32))
             cells = float(np.sum(np.diff(qo).astype(np.float64) * np.diff(so).astype(np.float64)))
             for kind in ("global", "semi", "local"):
                 sch = A.Scheme(kind, "affine", 2, -1, 5, 1)
-                sc, wall, fill, _ = timed(ctx, lambda: ctx.align_batch(sch, q, qo, s, so))
-                (aln, cig), wall2, fill2, walk2 = timed(ctx, lambda: ctx.traceback(sch, q, qo, s, so), 1)
+                sc, wall, fill, _ = timed(ctx, lambda: ctx.align_batch(sch, q, qo, s, so, out=psc))
+                sc = sc.copy()
+                (aln, cig), wall2, fill2, walk2 = timed(
+                    ctx, lambda: ctx.traceback(sch, q, qo, s, so, out_aln=paln, out_cigar=pcig), 1)
                 idx = np.random.default_rng(1).choice(len(qo) - 1, 100, replace=False)
                 osch = O.Scheme(kind, "affine", 2, -1, 5, 1)
                 ok = all(int(sc[k]) == O.align(osch, q[qo[k]:qo[k + 1]].tobytes(),
@@ -96,7 +115,9 @@ def main():
                 res.append({"config": f"C4 {args.c4n}bp x {len(g2)}bp SW affine variant {variant}",
                             "cells": cells, "wall_ms": wall * 1e3,
                             "gcups_wall": cells / wall / 1e9, "result": r, "closed_form_ok": ok})
-        print(json.dumps(res[-1]), flush=True)
+        while printed < len(res):
+            print(json.dumps(res[printed]), flush=True)
+            printed += 1
 
 
 if __name__ == "__main__":

@@ -1,12 +1,12 @@
-# round measurement: microbench, bench (plain), launch list, full ncu capture of the fill kernel
+# round measurement, call 1: microbench, bench (default command, plain), secondary configs,
+# then the launch list of the same bench command under ncu (one ncu tool per call)
 set -x
 ./paper_2002_04561_b200/lib/dpx_bench > gpurun_out/dpx.json 2> gpurun_out/dpx.err
-cp gpurun_out/dpx.json profiles/dpx_rates.json
-CMD="python bench.py --steps 5 --warmup 3"
+./tools/pipebench > gpurun_out/pipebench.txt 2>&1
+CMD="python bench.py"
 $CMD > gpurun_out/bench_full.log 2>&1
 tail -1 gpurun_out/bench_full.log
-CMD2="python bench.py --steps 2 --warmup 1 --no-cpu-baseline"
-$CMD2 > gpurun_out/plain2.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD2 > gpurun_out/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 1 -c 1 -o gpurun_out/fill_full $CMD2 > gpurun_out/ncu_full.log 2>&1
-tail -2 gpurun_out/ncu_full.log
+python tools/bench_configs.py > gpurun_out/configs.log 2>&1
+tail -8 gpurun_out/configs.log
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+tail -1 gpurun_out/ncu_launch.log | cut -c1-200
