@@ -81,12 +81,17 @@ struct Device {
   cudaStream_t stream = nullptr;
   DevBuf q_ascii, s_ascii, q_code, s_code, q_off, s_off, flags, keys, keys2, vals, vals2, slots;
   DevBuf scores, end_i, end_j, beg_i, beg_j, n_ops, cig_off, ops, dirs, tb, strip, aln, cigar;
-  DevBuf temp, sum, long_ws;
+  DevBuf temp, sum, long_ws, tickets;
   DevBuf q_ascii2[2], s_ascii2[2], q_off2[2], s_off2[2];  // double-buffered host uploads
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   PlanSummary* h_sum = nullptr;  // pinned, mapped (written by the publish kernel)
   HostBuf h_stage;               // pinned staging of score-mode results
+  // score-mode variant launches of one plan run concurrently (each with its own strip
+  // scratch): small per-variant launches of mixed-length batches then share the GPU
+  DevBuf strip_v[NV];
+  cudaStream_t vstream[NV] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[NV] = {};
   uint64_t* h_small = nullptr;   // pinned scratch
 };
 
@@ -267,8 +272,17 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   }
 
   // ---- a1: pack + validate ----
+  CK(D.tickets.ensure(kNumTickets * 4));
   CK(launch_prep(D.flags.as<uint32_t>(), B + 1, D.sum.as<PlanSummary>(), J.rebase_qoff,
-                 J.rebase_soff, J.rebase_q0, J.rebase_s0, st, D.num_sms));
+                 J.rebase_soff, J.rebase_q0, J.rebase_s0, D.tickets.as<int32_t>(), st,
+                 D.num_sms));
+  static const int dbg_asc = getenv("ANYSEQ_ASCENDING") ? 1 : 0;    // debug/tuning
+  static const int dbg_static = getenv("ANYSEQ_STATIC_SLOTS") ? 1 : 0;
+  int ticket_next = 0;
+  auto take_ticket = [&]() -> int32_t* {
+    return (!dbg_static && ticket_next < kNumTickets) ? D.tickets.as<int32_t>() + ticket_next++
+                                                      : nullptr;
+  };
   L(1);
   // byte codes are indexed by absolute CSR position; pack the whole [0, end) range the
   // caller's offsets cover (bytes before off[0] are never read by a pair)
@@ -288,6 +302,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   ca.cfg.bound_go = P.go;
   ca.cfg.bound_ge = P.ge;
   ca.cfg.bound_match = std::max(P.match, P.mismatch);
+  ca.cfg.ascending = dbg_asc;
   ca.q_off = J.d_qoff;
   ca.s_off = J.d_soff;
   ca.num_pairs = B;
@@ -352,9 +367,21 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   }
 
   // ---- a3/a4: fill (+ a5 walk) per variant ----
+  // score mode with several variants: fork the variant launches onto their own streams
+  int nvar = 0;
+  for (int v = 0; v < NV; ++v) nvar += S.count[v] ? 1 : 0;
+  const bool fork = !J.tb && nvar > 1;
+  std::pair<cudaEvent_t, cudaEvent_t> fev{nullptr, nullptr};
+  if (fork) {
+    if (ctx->timing) { fev = take_events(ctx); CK(cudaEventRecord(fev.first, st)); }
+    CK(cudaEventRecord(D.ev_fork, st));
+  }
   for (int v = 0; v < NV; ++v) {
     if (!S.count[v]) continue;
     const VariantDesc d = variant_desc(v);
+    cudaStream_t vst = fork ? D.vstream[v] : st;
+    DevBuf& strip = fork ? D.strip_v[v] : D.strip;
+    if (fork) CK(cudaStreamWaitEvent(vst, D.ev_fork, 0));
     FillArgs fa;
     memset(&fa, 0, sizeof(fa));
     fa.P = P;
@@ -378,27 +405,34 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     if (S.maxn[v] > HS) {
       fa.strip_stride = S.maxm[v] + 1;
       const int64_t groups = (int64_t)grid_est * 4 * G;
-      CK(D.strip.ensure((size_t)groups * fa.strip_stride * sizeof(uint4)));
-      fa.strip_scratch = D.strip.as<uint4>();
+      CK(strip.ensure((size_t)groups * fa.strip_stride * sizeof(uint4)));
+      fa.strip_scratch = strip.as<uint4>();
     } else {
       fa.strip_stride = 0;
-      CK(D.strip.ensure(256));
-      fa.strip_scratch = D.strip.as<uint4>();
+      CK(strip.ensure(256));
+      fa.strip_scratch = strip.as<uint4>();
     }
     if (!d.tb) {
       fa.slot_lo = sbase[v];
       fa.slot_hi = sbase[v] + nslot[v];
       int grid = 0;
       std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-      if (ctx->timing) { ev = take_events(ctx); CK(cudaEventRecord(ev.first, st)); }
-      ctx->mark(st, "fill-begin");
-      CK(launch_fill(v, prm->kind, prm->gap, fa, st, D.num_sms, &grid));
-      ctx->mark(st, "fill-end");
+      if (ctx->timing && !fork) { ev = take_events(ctx); CK(cudaEventRecord(ev.first, st)); }
+      ctx->mark(vst, "fill-begin");
+      fa.ticket = take_ticket();
+      CK(launch_fill(v, prm->kind, prm->gap, fa, vst, D.num_sms, &grid));
+      ctx->mark(vst, "fill-end");
       if (ctx->timing) {
-        CK(cudaEventRecord(ev.second, st));
         std::lock_guard<std::mutex> lk(ctx->ev_mu);
-        ctx->fill_ev.push_back(ev);
+        if (!fork) {
+          CK(cudaEventRecord(ev.second, st));
+          ctx->fill_ev.push_back(ev);
+        }
         ctx->fill_launches++;
+      }
+      if (fork) {
+        CK(cudaEventRecord(D.ev_join[v], vst));
+        CK(cudaStreamWaitEvent(st, D.ev_join[v], 0));
       }
       if (grid > grid_est) return fail(ctx, ANYSEQ_E_CUDA, "occupancy above scratch estimate");
       L(1);
@@ -420,6 +454,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
         int grid = 0;
         std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
         if (ctx->timing) { ev = take_events(ctx); CK(cudaEventRecord(ev.first, st)); }
+        fa.ticket = take_ticket();
         CK(launch_fill(v, prm->kind, prm->gap, fa, st, D.num_sms, &grid));
         if (ctx->timing) {
           CK(cudaEventRecord(ev.second, st));
@@ -454,6 +489,12 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
         L(2);
       }
     }
+  }
+
+  if (fork && ctx->timing) {  // one fill interval: fork to join
+    CK(cudaEventRecord(fev.second, st));
+    std::lock_guard<std::mutex> lk(ctx->ev_mu);
+    ctx->fill_ev.push_back(fev);
   }
 
   // ---- output assembly ----
@@ -819,12 +860,21 @@ anyseq_status anyseq_create(anyseq_ctx** out, const int* device_ids, int num_dev
         cudaEventCreateWithFlags(&D.ev_up[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&D.ev_up[1], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&D.ev_free[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&D.ev_free[1], cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&D.ev_free[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&D.ev_fork, cudaEventDisableTiming) != cudaSuccess) {
       c->devs.push_back(D);
       anyseq_destroy(c);
       return ANYSEQ_E_CUDA;
     }
+    bool vok = true;
+    for (int v = 0; v < NV && vok; ++v)
+      vok = cudaStreamCreateWithFlags(&D.vstream[v], cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&D.ev_join[v], cudaEventDisableTiming) == cudaSuccess;
     c->devs.push_back(D);
+    if (!vok) {
+      anyseq_destroy(c);
+      return ANYSEQ_E_CUDA;
+    }
   }
   cudaSetDevice(c->devs[0].id);
   *out = c;
@@ -844,7 +894,7 @@ void anyseq_destroy(anyseq_ctx* c) {
                       &D.flags,   &D.keys,    &D.keys2,  &D.vals,   &D.vals2, &D.slots,
                       &D.scores,  &D.end_i,   &D.end_j,  &D.beg_i,  &D.beg_j, &D.n_ops,
                       &D.cig_off, &D.ops,     &D.dirs,   &D.tb,     &D.strip, &D.aln,
-                      &D.cigar,   &D.temp,    &D.sum,    &D.long_ws};
+                      &D.cigar,   &D.temp,    &D.sum,    &D.long_ws, &D.tickets};
     for (DevBuf* b : bufs) b->release();
     D.h_stage.release();
     if (D.h_sum) cudaFreeHost(D.h_sum);
@@ -857,6 +907,12 @@ void anyseq_destroy(anyseq_ctx* c) {
       if (D.ev_up[i]) cudaEventDestroy(D.ev_up[i]);
       if (D.ev_free[i]) cudaEventDestroy(D.ev_free[i]);
     }
+    for (int v = 0; v < NV; ++v) {
+      D.strip_v[v].release();
+      if (D.vstream[v]) cudaStreamDestroy(D.vstream[v]);
+      if (D.ev_join[v]) cudaEventDestroy(D.ev_join[v]);
+    }
+    if (D.ev_fork) cudaEventDestroy(D.ev_fork);
     if (D.copy_stream) cudaStreamDestroy(D.copy_stream);
     if (D.stream) cudaStreamDestroy(D.stream);
   }

@@ -15,6 +15,7 @@ struct FillArgs {
   const Slot* slots;          // this variant's slot array
   const int32_t* nslots_dev;  // if non-null: slot range is [0, *nslots_dev)
   int32_t slot_lo, slot_hi;   // otherwise [slot_lo, slot_hi)
+  int32_t* ticket;            // if non-null (zeroed): warp-slots handed out dynamically
   int32_t pos;                // also produce end cells
   int32_t* scores;            // [num_pairs]
   int32_t* end_i;             // [num_pairs] (pos)

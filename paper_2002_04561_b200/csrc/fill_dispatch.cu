@@ -48,7 +48,13 @@ cudaError_t launch_fill(int variant, int kind, int gap, const FillArgs& a, cudaS
   if (bps_cap > 0 && nb > bps_cap) nb = bps_cap;
   const int grid = num_sms * nb;
   if (grid_out) *grid_out = grid;
-  fn<<<grid, 128, 0, st>>>(a);
+  // dynamic slot hand-out pays off only with several warp-slots per warp: with fewer, the
+  // static order (warp-slot w -> warp w, i.e. spread over the blocks and so over the SMs)
+  // keeps the few busy warps on separate sub-partitions
+  FillArgs b = a;
+  const int64_t nws = ((int64_t)a.slot_hi - a.slot_lo + 3) / 4;  // L = 8: 4 slots per warp
+  if (b.ticket && (a.nslots_dev || nws < 2ll * grid * 4)) b.ticket = nullptr;
+  fn<<<grid, 128, 0, st>>>(b);
   return cudaGetLastError();
 }
 }  // namespace anyseq

@@ -108,7 +108,15 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
   const int gb = (threadIdx.x >> 5) * G + g;
   auto dec = [&](T x, int X) -> int { return V::get(x, X) - B0; };
 
-  for (int ws = warp; ws < nws; ws += nwarps) {
+  // warp-slots in plan order (largest first): handed out by ticket when the launch has a
+  // zeroed counter (balances mixed lengths), else statically round-robin
+  auto next_ws = [&](int stat) -> int {
+    if (!a.ticket) return stat;
+    int v = 0;
+    if (lane == 0) v = atomicAdd(a.ticket, 1);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  for (int ws = next_ws(warp); ws < nws; ws = next_ws(ws + nwarps)) {
     const int sidx = ws * G + g;
     const bool valid = (g < G) && (sidx < nsl);
     int pr[PP], nn[PP], mm[PP];
@@ -278,7 +286,14 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
         selo = selbase + (uint32_t)(((kk - t) & (SELCAP - 1)) * 2);
         selv = lds16(selo);
       };
-      auto step = [&](auto chk, const int k, T (&Hi)[R], T (&Hq)[R]) {
+      // strips after the first: lane 0's input row (H, E of the strip above) is prefetched
+      // two steps ahead from the strip scratch (L2) in two registers used alternately
+      uint4 pfA = make_uint4(0, 0, 0, 0), pfB = pfA;
+      if (MULTI && st > 0 && t == 0 && sact) {
+        pfA = scr[0];
+        if (M > 1) pfB = scr[1];
+      }
+      auto step = [&](auto chk, const int k, T (&Hi)[R], T (&Hq)[R], uint4& pf) {
         constexpr bool CHK = decltype(chk)::value;
         T hin = V::shfl_up(Hbot, L);
         T ein = (GAP == GAFFINE || TB) ? V::shfl_up(Ebot, L) : NEG;
@@ -315,11 +330,12 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
             mein = LOWBITS;
           }
         } else if (t == 0 && act) {
-          const uint4 v = scr[col];
+          const uint4 v = pf;
           hin = (T)v.x;
           ein = (T)v.y;
           mein = v.z;
         }
+        if (MULTI && st > 0 && t == 0 && sact && col + 2 < M) pf = scr[col + 2];
         // FAST = affine score-only: the reassociated recurrence
         //   F  = max(F - Ge, H_left - Go - Ge)          Eq. (5)
         //   DF = max(H_diag + sigma, F)
@@ -501,8 +517,8 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
       int k = 0;
       rebase(0);
       for (; k < kA; k += 2) {
-        step(CHK_ON, k, HA, HB);
-        step(CHK_ON, k + 1, HB, HA);
+        step(CHK_ON, k, HA, HB, pfA);
+        step(CHK_ON, k + 1, HB, HA, pfB);
       }
       // every 128 steps (warp-uniform): selector ring refill (long rows) and pointer rebase
       auto block_start = [&](int kk) {
@@ -518,18 +534,18 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
         block_start(k);
         const int kend = min(kB, (k & ~127) + 128);
         for (; k < kend; k += 2) {
-          step(CHK_OFF, k, HA, HB);
-          step(CHK_OFF, k + 1, HB, HA);
+          step(CHK_OFF, k, HA, HB, pfA);
+          step(CHK_OFF, k + 1, HB, HA, pfB);
         }
       }
       for (; k + 1 < K; k += 2) {
         block_start(k);
-        step(CHK_ON, k, HA, HB);
-        step(CHK_ON, k + 1, HB, HA);
+        step(CHK_ON, k, HA, HB, pfA);
+        step(CHK_ON, k + 1, HB, HA, pfB);
       }
       if (k < K) {
         block_start(k);
-        step(CHK_ON, k, HA, HB);
+        step(CHK_ON, k, HA, HB, pfA);
       }
 
       __syncwarp();  // capbuf writes of this strip are visible (all lanes participate)

@@ -113,7 +113,8 @@ cudaError_t launch_pack(const char* d_q, uint64_t q_len, uint8_t* d_qcode, const
 
 // ------------------------------------------------------------------------ prep / publish
 __global__ void prep_kernel(uint32_t* flags, uint64_t n, PlanSummary* sum, uint64_t* qoff,
-                            uint64_t* soff, uint64_t q0, uint64_t s0) {
+                            uint64_t* soff, uint64_t q0, uint64_t s0, int32_t* tickets) {
+  if (blockIdx.x == 0 && threadIdx.x < kNumTickets) tickets[threadIdx.x] = 0;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (uint64_t)gridDim.x * blockDim.x) {
     flags[k] = 0;
@@ -138,9 +139,10 @@ __global__ void prep_kernel(uint32_t* flags, uint64_t n, PlanSummary* sum, uint6
 }
 
 cudaError_t launch_prep(uint32_t* flags, uint64_t n, PlanSummary* sum, uint64_t* qoff,
-                        uint64_t* soff, uint64_t q0, uint64_t s0, cudaStream_t st, int num_sms) {
+                        uint64_t* soff, uint64_t q0, uint64_t s0, int32_t* tickets,
+                        cudaStream_t st, int num_sms) {
   prep_kernel<<<grid_for((int64_t)n, 256, num_sms), 256, 0, st>>>(flags, n, sum, qoff, soff, q0,
-                                                                  s0);
+                                                                  s0, tickets);
   return cudaGetLastError();
 }
 
@@ -236,9 +238,13 @@ __global__ void classify_kernel(ClassifyArgs a) {
           sl.pair[1] = -1;
           a.slots[k] = sl;
         }
+        // plan order: by variant, then largest (m, n) first (the fill hands out slots in
+        // this order, so the tail of a launch is made of the smallest slots)
+        constexpr int64_t KM = (1 << 29) - 1;
+        const int64_t mk = m < KM ? m : KM, nk = n < KM ? n : KM;
         key = ((unsigned long long)v << 58) |
-              ((unsigned long long)(m < (1 << 29) - 1 ? m : (1 << 29) - 1) << 29) |
-              (unsigned long long)(n < (1 << 29) - 1 ? n : (1 << 29) - 1);
+              ((unsigned long long)(a.cfg.ascending ? mk : KM - mk) << 29) |
+              (unsigned long long)(a.cfg.ascending ? nk : KM - nk);
         a.keys[k] = key;
         a.vals[k] = (int32_t)k;
       }

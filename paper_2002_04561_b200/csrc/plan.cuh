@@ -47,6 +47,7 @@ struct PlanCfg {
   int32_t allow16;     // s16x2 permitted (debug/tests can force s32)
   int32_t force_variant;  // -1 = auto
   int32_t bound_go, bound_ge, bound_match;  // for the range guards
+  int32_t ascending;   // plan order smallest-first (debug; default largest-first)
 };
 
 }  // namespace anyseq
