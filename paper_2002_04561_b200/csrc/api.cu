@@ -101,7 +101,7 @@ struct anyseq_ctx {
   std::vector<Device> devs;
   std::string err;
   std::atomic<uint64_t> launches{0};
-  int64_t tb_scratch_bytes = 4ll << 30;
+  int64_t tb_scratch_bytes = 16ll << 30;  // traceback H store per fill/walk chunk
   int64_t chunk_bytes = 64ll << 20;  // host-API upload/compute pipelining granularity
   int64_t force_variant = -1;
   int64_t allow16 = 1;
@@ -438,8 +438,8 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
       L(1);
     } else {
       const int64_t ns = (S.maxn[v] + HS - 1) / HS;
-      const int64_t s4 = (S.maxm[v] + d.L - 1 + 3) / 4;  // 4 steps per direction word
-      const int64_t block_words = ns * s4 * d.R * d.L;    // both halves share a word
+      const int64_t dk = S.maxm[v] + d.L - 1 + d.R - 1;  // diagonals (step - row) per strip
+      const int64_t block_words = ns * dk * d.R * d.L;    // one H word per (diag, row, lane)
       const int64_t cap_words = std::max<int64_t>(ctx->tb_scratch_bytes / 4, block_words);
       int64_t chunk = std::max<int64_t>(1, cap_words / block_words);
       chunk = std::min<int64_t>(chunk, nslot[v]);
@@ -466,6 +466,9 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
         WalkArgs wa;
         wa.kind = prm->kind;
         wa.gap = prm->gap;
+        wa.P = P;
+        wa.qcode = D.q_code.as<uint8_t>();
+        wa.scode = D.s_code.as<uint8_t>();
         wa.slots = D.slots.as<Slot>();
         wa.slot_lo = fa.slot_lo;
         wa.slot_hi = fa.slot_hi;

@@ -3,8 +3,8 @@
 // What it computes: Eq. (1) H = max{H_diag + sigma, E, F, nu},
 // linear gaps Eqs. (2)-(3), affine gaps Eqs. (4)-(5), the per-kind
 // initialisation and optimum, max-tracking only where needed, and
-// optionally the predecessor information of the relax listing as a packed
-// direction nibble per cell for the traceback walk.
+// optionally (traceback) every cell's H for the walk that re-derives the predecessor
+// decisions of the relax listing from it.
 //
 // How (B200 design):
 //  * A lane group of L lanes (L | 32) relaxes one "slot" = one alignment (VS32) or two
@@ -54,7 +54,7 @@ __device__ __forceinline__ uint32_t imad_add(uint32_t x, uint32_t one, uint32_t 
 #define FILL_MINB_SCORE 4  // resident 128-thread blocks per SM the score kernels are built for
 #endif
 template <class V, int KIND, int GAP, int L, int R, bool TB, bool POS, int CGE = 0, int CGO = 0>
-__global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(FillArgs a) {
+__global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) {
   using T = typename V::T;
   constexpr int PP = V::P;
   constexpr int G = 32 / L;
@@ -72,13 +72,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
   const int nws = (nsl + G - 1) / G;
   const DevParams P = a.P;
   constexpr bool pos = TB || POS;
-  constexpr bool FAST = (GAP == GAFFINE) && !TB;  // reassociated affine recurrence
-  constexpr uint32_t LOWBITS = (PP == 2) ? 0x00010001u : 1u;
-  // 0 iff x == y, per half (bit 0 of each half)
-  auto mneq = [&](T x, T y) -> uint32_t {
-    if (PP == 2) return __vminu2((uint32_t)x ^ (uint32_t)y, 0x00010001u);
-    return min((uint32_t)x ^ (uint32_t)y, 1u);
-  };
+  constexpr bool FAST = (GAP == GAFFINE);  // reassociated affine recurrence (score and TB)
   // VS16 local scores are unbiased; their Hop uses VIADD.16x2 (see hop) -- fine.
   const uint32_t one = (uint32_t)a.one;
   constexpr bool SPEC = CGE > 0;
@@ -156,11 +150,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
     for (int X = 0; X < PP; ++X) pad[X] = (KIND == KGLOBAL) ? 0 : npad - nn[X];
     uint4* scr = a.strip_scratch + (int64_t)(warp * G + g) * a.strip_stride;
     int64_t dbase = 0;
-    int S4 = 0;
-    if (TB && valid) {
-      dbase = (int64_t)sidx * a.dir_block_words;
-      S4 = (M + L - 1 + 3) >> 2;
-    }
+    if (TB && valid) dbase = (int64_t)sidx * a.dir_block_words;
 
     // column selectors of this slot in a 512-entry shared ring: columns [0, 384) now, then
     // 128 more every 128 steps (a lane at step k reads column k - t, t < L <= 8)
@@ -219,7 +209,6 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
       const int ip0 = st * HS + t * R;  // first physical row of this lane
       uint32_t p0[R], p1[R];
       T HA[R], HB[R], Ff[R];
-      uint32_t acc[TB ? R : 1];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int ip = ip0 + r;
@@ -244,7 +233,6 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
         HA[r] = enc(iv[0], iv[PP - 1]);
         HB[r] = HA[r];
         Ff[r] = NEG;
-        if (TB) acc[r] = 0;
       }
       // H of the row above this lane's first row at column 0
       T diag;
@@ -254,7 +242,6 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
         diag = enc(dv, dv);
       }
       T Hbot = NEG, Ebot = NEG;
-      uint32_t MEbot = 0;
       // per-strip local trackers (merged by key at strip end)
       int sv[PP], si[PP], sj[PP];
 #pragma unroll
@@ -296,8 +283,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
       auto step = [&](auto chk, const int k, T (&Hi)[R], T (&Hq)[R], uint4& pf) {
         constexpr bool CHK = decltype(chk)::value;
         T hin = V::shfl_up(Hbot, L);
-        T ein = (GAP == GAFFINE || TB) ? V::shfl_up(Ebot, L) : NEG;
-        uint32_t mein = TB ? __shfl_up_sync(0xffffffffu, MEbot, 1, L) : 0u;
+        T ein = (GAP == GAFFINE) ? V::shfl_up(Ebot, L) : NEG;
         const int col = k - t;
         // selector of this lane's column: a shared-memory pointer that advances by one slot
         // per step (IMAD, FMA pipe) and is re-based every 128 steps (the mirror covers the
@@ -325,15 +311,13 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
           const T h0v = enc(h0, h0);
           if (t == 0) {
             hin = h0v;
-            // E-below convention (FAST, TB): E(1,j) = H(0,j) - Go - Ge, opened; else E(0,j)
-            ein = (FAST || TB) ? hop(h0v) : NEG;
-            mein = LOWBITS;
+            // E-below convention (FAST): E(1,j) = H(0,j) - Go - Ge; else E(0,j)
+            ein = FAST ? hop(h0v) : NEG;
           }
         } else if (t == 0 && act) {
           const uint4 v = pf;
           hin = (T)v.x;
           ein = (T)v.y;
-          mein = v.z;
         }
         if (MULTI && st > 0 && t == 0 && sact && col + 2 < M) pf = scr[col + 2];
         // FAST = affine score-only: the reassociated recurrence
@@ -346,7 +330,6 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
         // value handed down the lanes / strips is E of the row BELOW the bottom row.
         T hup = FAST ? NEG : hop(hin);  // Hop of the row above (other modes)
         T e = ein;
-        uint32_t me = mein;
         if (FAST) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -358,7 +341,7 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
             e = V::addmax(e, NGE, hop(df));
             Hq[r] = h;
           }
-        } else if (!TB) {
+        } else {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const T hd = (r == 0) ? diag : Hi[r - 1];
@@ -369,53 +352,25 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
             Hq[r] = h;
             hup = hop(h);
           }
-        } else {
-          // Traceback fill: direction bits in packed form, no predicates.  For a pair of
-          // values x, y (both halves at once) m(x, y) = min_u16(x ^ y, 1) is 0 iff x == y,
-          // so each of the four decisions of the relax listing costs two
-          // instructions for both alignments:
-          //   b0 = m(H, D)      1 = not DIAG             (DIAG first, R7)
-          //   b1 = m(tm, E)     1 = F beats E            (E before F, R7)
-          //   b2 = m(E, Ex)     1 = E opened (not extended, R8)
-          //   b3 = m(F, Fx)     1 = F opened
-          // local: STOP (H <= 0, R9) is stored as b0 = 0, b1 = 1.
-          // nibble = b0 | b1<<1 | b2<<2 | b3<<3 (built with IMAD shift-adds on the FMA pipe);
-          // acc = acc*16 + nibble holds 4 steps per half: half A in bits 0-15, half B 16-31.
-          // Like FAST, the value handed down is E of the row below, with its extend bit.
+        }
+        // Traceback mode: the score recurrence above plus every cell's H, stored packed
+        // (both alignments of an s16x2 register in one word, 2 B per cell) step-major and
+        // lane-contiguous per slot; the walk re-derives each decision of the relax listing
+        // (R7-R9) from H alone (walk_kernel).  Storing H instead of direction
+        // bits keeps the fill at the score-only instruction count.
+        if (TB && valid && sact && k < M + L - 1) {
+          // word ((st * DK + k - r + R - 1) * R + r) * L + t: diagonal-major per lane (the
+          // walk's diagonal runs are sequential), lanes of a group contiguous (32 B/row)
+          uint32_t* wp = a.dirs + dbase +
+                         (((int64_t)st * (M + L - 1 + R - 1) + k + R - 1) * R) * L + t;
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const T hd = (r == 0) ? diag : Hi[r - 1];
-            const T sig = V::sigma(p0[r], p1[r], sel);
-            const T d = V::add(hd, sig);
-            const T fx = V::add(Ff[r], NGE);
-            const T f = V::vmax(fx, hop(Hi[r]));
-            Ff[r] = f;
-            const T tm = V::vmax(e, f);
-            T h = (KIND == KLOCAL) ? V::vmax_relu(d, tm) : V::vmax(d, tm);
-            uint32_t b0 = mneq(h, d);
-            uint32_t b1 = mneq(tm, e);
-            if (KIND == KLOCAL) {
-              const uint32_t mz = mneq(h, V::splat(0));  // 0 iff STOP
-              b1 = (b0 & b1) | (mz ^ LOWBITS);
-              b0 = b0 & mz;
-            } else {
-              b1 = b0 & b1;  // canonical DIAG = (0, 0)
-            }
-            const uint32_t w = imad_add(imad_add(imad_add(mneq(f, fx), 2u, me), 2u, b1), 2u, b0);
-            acc[r] = imad_add(acc[r], 16u, w);
-            Hq[r] = h;
-            // E of the row below (reassociated, exact; see FAST above) and its extend bit
-            const T ex = V::add(e, NGE);
-            e = V::vmax(ex, hop(V::vmax(d, f)));
-            me = mneq(e, ex);
-          }
+          for (int r = 0; r < R; ++r) wp[-(int64_t)r * (R - 1) * L] = (uint32_t)Hq[r];
         }
         diag = hin;
         Hbot = Hq[R - 1];
         Ebot = e;
-        if (TB) MEbot = me;
         if (MULTI && act && t == L - 1 && st + 1 < NS)
-          scr[col] = make_uint4((uint32_t)Hq[R - 1], (uint32_t)e, TB ? me : 0u, 0u);
+          scr[col] = make_uint4((uint32_t)Hq[R - 1], (uint32_t)e, 0u, 0u);
 
         // ---- optimum bookkeeping ----
         // Plain score mode tracks maxima in every lane and every step without masks: the
@@ -487,19 +442,6 @@ __global__ void __launch_bounds__(128, TB ? 2 : FILL_MINB_SCORE) fill_kernel(Fil
             if (KIND == KSEMI && !pos && last_strip) bfin = V::select_mask(best, 1u << X, bfin);
           }
         }
-        }
-        if (TB) {
-          const int Kslot = M + L - 1;
-          if (valid && sact && k < Kslot && ((k & 3) == 3 || k == Kslot - 1)) {
-            const int sh = 4 * (3 - (k & 3));  // a partial last word keeps the 4-step layout
-            uint32_t* wp = a.dirs + dbase + (((int64_t)st * S4 + (k >> 2)) * R) * L + t;
-#pragma unroll
-            for (int r = 0; r < R; ++r) wp[(int64_t)r * L] = acc[r] << sh;
-          }
-          if ((k & 3) == 3) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = 0;
-          }
         }
       };
 

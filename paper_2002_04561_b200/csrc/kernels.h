@@ -67,6 +67,9 @@ cudaError_t launch_fill(int variant, int kind, int gap, const FillArgs& a, cudaS
 // a5: traceback walk of one chunk of slots of a variant
 struct WalkArgs {
   int32_t kind, gap;
+  DevParams P;
+  const uint8_t* qcode;  // byte codes at the CSR positions (sigma of the DIAG test)
+  const uint8_t* scode;
   const Slot* slots;
   int32_t slot_lo, slot_hi;
   int32_t pairs_per_slot;

@@ -303,7 +303,7 @@ def test_host_chunking_and_tb_scratch_chunks(ctx):
         _check_tb(ctx, sch, q, qo, s, so, res, ocig)
     finally:
         ctx.set_option("chunk_bytes", 64 << 20)
-        ctx.set_option("tb_scratch_bytes", 4 << 30)
+        ctx.set_option("tb_scratch_bytes", 16 << 30)
 
 
 def test_host_pipeline_many_chunks_pinned_outputs(ctx):
