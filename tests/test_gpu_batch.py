@@ -212,6 +212,43 @@ def test_c2_full_size_sampled(ctx):
     assert sc.min() >= 0 and sc.max() <= 300
 
 
+def test_c3_full_size_sampled(ctx):
+    """C3 at BASELINE size (1M pairs, local affine, traceback + CIGAR; several H-store
+    chunks): the oracle checks score, begin, end and CIGAR of a fixed sample of 1000 pairs,
+    and every CIGAR is checked against its pair's coordinates (property at any size)."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    from synth import c2_reads, uniform_csr
+    qm, sm = c2_reads(1_000_000, seed=2)
+    q, qo = uniform_csr(qm)
+    s, so = uniform_csr(sm)
+    ctx.set_option("tb_scratch_bytes", 4 << 30)  # > 1 fill/walk chunk
+    try:
+        aln, words = ctx.traceback(A.Scheme("local", "affine", 2, -1, 5, 1), q, qo, s, so)
+    finally:
+        ctx.set_option("tb_scratch_bytes", 16 << 30)
+    sch = O.Scheme("local", "affine", 2, -1, 5, 1)
+    idx = np.random.default_rng(1).choice(len(aln), 1000, replace=False)
+    cigs = A.cigars_of(aln[idx], words)
+    for n, k in enumerate(idx):
+        o = O.align(sch, qm[k].tobytes(), sm[k].tobytes())
+        got = (int(aln["score"][k]), int(aln["q_begin"][k]), int(aln["s_begin"][k]),
+               int(aln["q_end"][k]), int(aln["s_end"][k]))
+        assert got == (o.score, o.q_begin, o.s_begin, o.q_end, o.s_end), k
+        assert cigs[n] == o.cigar, k
+    # every CIGAR spans exactly its alignment: M+I rows, M+D columns
+    ops = words & 15
+    lens = (words >> 4).astype(np.int64)
+    off = aln["cigar_offset"].astype(np.int64)
+    cnt = aln["cigar_len"].astype(np.int64)
+    seg = np.repeat(np.arange(len(aln)), cnt)
+    rows = np.bincount(seg, weights=lens * (ops != 2), minlength=len(aln))
+    cols = np.bincount(seg, weights=lens * (ops != 1), minlength=len(aln))
+    assert np.all(off[1:] == off[:-1] + cnt[:-1])
+    assert np.array_equal(rows.astype(np.int64), aln["q_end"] - aln["q_begin"])
+    assert np.array_equal(cols.astype(np.int64), aln["s_end"] - aln["s_begin"])
+
+
 def test_c5_mixed_sample(ctx):
     """C5 shape (mixed 100..1000 bp), all kinds x modes, 600 pairs."""
     import paper_2002_04561_b200 as A
