@@ -49,7 +49,7 @@ struct LongArgs {
   int32_t* rowprog;   // [Gtot * S]
   int32_t* const* bflag;  // [Gtot+1] per-edge flag arrays of S ints (on the consumer)
   int2* const* bcol;  // [Gtot+1] column buffers: (H(i, cb[g]), F(i, cb[g])), i = 0..n
-  int2* rowbuf;       // [m+1]: (H, E) of the last completed row at column j
+  int4* rowbuf;       // [m+1]: (H, tag, E, tag) of the last completed row at column j
   LongPart* parts;
   int32_t* abort_flag;
   int32_t chunk;
@@ -75,6 +75,23 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
 }
 __device__ __forceinline__ void st_release_sys(int* p, int v) {
   asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Row hand-off words: (value, tag) pairs in one 8-byte access each, so a reader that sees
+// the tag of the strip it waits for also sees the value (single-copy atomicity of aligned
+// 8-byte accesses) -- no fences, no progress counters (the LL idea of NCCL's protocols).
+__device__ __forceinline__ void st_row(int4* p, int h, int e, int tag) {
+  asm volatile("st.relaxed.gpu.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(h), "r"(tag),
+               "r"(e), "r"(tag)
+               : "memory");
+}
+__device__ __forceinline__ int4 ld_row(const int4* p) {
+  int4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
 }
 
 __device__ __forceinline__ bool lkey_better(int v, int i, int j, int bv, int bi, int bj) {
@@ -167,7 +184,6 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
     const int ip0 = s * HS + t * R;
     const int2* bl = a.bcol[g];
     int2* br = (g + 1 < a.Gtot) ? a.bcol[g + 1] : nullptr;
-    const int* prog_up = (s > 0) ? &a.rowprog[g * a.S + s - 1] : nullptr;
 
     if (g > 0) {  // left boundary of this row strip (and the previous one: diag of row 0)
       if (!warp_wait<true>(&a.bflag[g][s], 1, a)) break;
@@ -185,17 +201,32 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
       HA[r] = HB[r] = 0;
       Ff[r] = NEG;
     }
-    // lane-0 inputs and selectors of columns [c0, c1) into the warp's ring (coalesced)
-    auto refill = [&](int c0, int c1) {
-      for (int c = c0 + t; c < c1; c += L) {
-        if (s > 0) ring_he[wb][c & (RING - 1)] = a.rowbuf[c_lo + c + 1];
-        ring_sel[wb][c & (RING - 1)] = (uint16_t)V::selector(a.sc[c_lo + c], 0);
+    // lane-0 inputs and selectors of columns [c0, c1) (c1 - c0 <= 32: one per lane) into
+    // the warp's ring; the row entries are polled until they carry this strip's tag s
+    // (written by strip s-1), bounded like every wait (-> abort, ANYSEQ_E_TIMEOUT)
+    auto refill = [&](int c0, int c1) -> bool {
+      const int c = c0 + t;
+      const bool mine = c < c1;
+      if (mine) ring_sel[wb][c & (RING - 1)] = (uint16_t)V::selector(a.sc[c_lo + c], 0);
+      if (s == 0) return true;
+      const int4* src = a.rowbuf + c_lo + c + 1;
+      int4 v = mine ? ld_row(src) : make_int4(0, s, 0, s);
+      long long spins = 0;
+      while (!__all_sync(0xffffffffu, v.y == s && v.w == s)) {
+        const long long t0 = (a.prof && t == 0) ? clock64() : 0;
+        __nanosleep(64);
+        if (v.y != s || v.w != s) v = ld_row(src);
+        if ((++spins & 255) == 0 &&
+            __any_sync(0xffffffffu, spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
+          if (t == 0) atomicExch(a.abort_flag, 1);
+          return false;
+        }
+        if (a.prof && t == 0) atomicAdd(&a.prof[0], (unsigned long long)(clock64() - t0));
       }
+      if (mine) ring_he[wb][c & (RING - 1)] = make_int2(v.x, v.z);
+      return true;
     };
-    // start only when the strip above is a.lag columns ahead: the steady-state distance
-    // between consecutive strips then stays above the 2*PER columns each refill needs
-    if (prog_up && !warp_wait<false>(prog_up, min(W, max(2 * PER, a.lag)), a)) break;
-    refill(0, min(W, 2 * PER));
+    if (!refill(0, min(W, PER)) || !refill(PER, min(W, 2 * PER))) break;
     __syncwarp();
 
     int diag = 0, Hbot = NEG, Ebot = NEG;
@@ -269,13 +300,7 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
         diag = hin;
         Hbot = Hq[R - 1];
         Ebot = e;
-        if (t == L - 1 && act) a.rowbuf[c_lo + lc + 1] = make_int2(Hq[R - 1], e);  // strip s+1
-        {  // progress publication: warp-uniform test on lane L-1's column, lane L-1 releases
-          const int lcl = k - (L - 1);
-          if (lcl >= 0 && lcl < W && ((lcl & (a.chunk - 1)) == a.chunk - 1 || lcl == W - 1) &&
-              t == L - 1)
-            st_release_gpu(&a.rowprog[g * a.S + s], lcl + 1);
-        }
+        if (t == L - 1 && act) st_row(a.rowbuf + c_lo + lc + 1, Hq[R - 1], e, s + 1);  // strip s+1
         const int j = c_lo + lc + 1;  // real column
         if (KIND == KLOCAL && KEYED) {
           // rows below n (last strip) never win: their values come from real cells of an
@@ -357,8 +382,7 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
       int k = 0;
       auto maybe_refill = [&](int kk) -> bool {  // warp-uniform, every PER steps
         if ((kk % PER) == 0 && kk > 0 && kk + PER < W) {
-          if (prog_up && !warp_wait<false>(prog_up, min(W, kk + 2 * PER), a)) return false;
-          refill(kk + PER, min(W, kk + 2 * PER));
+          if (!refill(kk + PER, min(W, kk + 2 * PER))) return false;
           __syncwarp();
         }
         return true;
@@ -429,14 +453,14 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
   if (t == 0) a.parts[wg] = part;
 }
 
-__global__ void long_init_kernel(DevParams P, int n, int m, int2* rowbuf, int2* bcol0,
+__global__ void long_init_kernel(DevParams P, int n, int m, int4* rowbuf, int2* bcol0,
                                  int2* const* bcol, const int* cb, int Gtot, int g_first,
                                  int g_count) {
   const int NEG = NEG32;
   const bool glob = P.kind == KGLOBAL;
   for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= (int64_t)max(n, m);
        x += (int64_t)gridDim.x * blockDim.x) {
-    if (x <= m) rowbuf[x] = make_int2(glob && x > 0 ? -(P.go + (int)x * P.ge) : 0, NEG);  // H(0,j), E(0,j)
+    if (x <= m) rowbuf[x] = make_int4(0, 0, NEG, 0);  // tag 0: no strip has written yet
     if (bcol0 && x <= n) bcol0[x] = make_int2(glob && x > 0 ? -(P.go + (int)x * P.ge) : 0, NEG);  // H(i,0), F(i,0)
     if (x == 0) {
       for (int g = g_first; g < g_first + g_count; ++g) {
@@ -566,7 +590,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
              std::to_string(in_s ? hs.err_pos - (1ull << 62) : hs.err_pos);
       return ANYSEQ_E_BADSEQ;
     }
-    LK(cudaMalloc(&D.rowbuf.p, (m + 1) * sizeof(int2)));
+    LK(cudaMalloc(&D.rowbuf.p, (m + 1) * sizeof(int4)));
     LK(cudaMalloc(&D.prog.p, (size_t)Gtot * S * 4));
     LK(cudaMalloc(&D.ticket.p, 4));
     LK(cudaMalloc(&D.abort_.p, 4));
@@ -603,7 +627,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     LK(cudaMemcpyAsync(D.fptr.p, flag_ptr.data(), (Gtot + 1) * sizeof(int32_t*), cudaMemcpyHostToDevice,
                        devs[d].stream));
     long_init_kernel<<<devs[d].num_sms * 4, 256, 0, devs[d].stream>>>(
-        P, (int)n, (int)m, (int2*)D.rowbuf.p, D.g_first == 0 && D.g_count > 0 ? bcol_ptr[0] : nullptr,
+        P, (int)n, (int)m, (int4*)D.rowbuf.p, D.g_first == 0 && D.g_count > 0 ? bcol_ptr[0] : nullptr,
         (int2* const*)D.bptr.p, (const int*)D.cbuf.p, Gtot, D.g_first, D.g_count);
     LK(cudaGetLastError());
     *launches += 1;
@@ -629,7 +653,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     a.rowprog = (int32_t*)D.prog.p;
     a.bflag = (int32_t* const*)D.fptr.p;  // edge g flags live on the consumer of edge g
     a.bcol = (int2* const*)D.bptr.p;
-    a.rowbuf = (int2*)D.rowbuf.p;
+    a.rowbuf = (int4*)D.rowbuf.p;
     a.parts = (LongPart*)D.parts.p;
     a.abort_flag = (int32_t*)D.abort_.p;
     a.chunk = chunk;
