@@ -177,8 +177,10 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
     if (task >= a.S * a.g_count) break;
     if (*(volatile int*)a.abort_flag) break;
     const long long task_t0 = (a.prof && t == 0) ? clock64() : 0;
-    const int s = task / a.g_count;
-    const int g = a.g_first + task % a.g_count;
+    // column-strip major: task (s, g) waits on (s-1, g) (row hand-off) and (s, g-1) (left
+    // edge, finished a whole pass earlier) -- both lower tickets held by resident warps
+    const int s = task % a.S;
+    const int g = a.g_first + task / a.S;
     const int c_lo = a.cb[g], c_hi = a.cb[g + 1], W = c_hi - c_lo;
     const bool last_strip = (s == a.S - 1), last_col = (c_hi == m);
     const int ip0 = s * HS + t * R;
@@ -516,16 +518,33 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     }
   }
   const int ND = (int)devs.size();
-  int Gtot = ND > 1 ? ND : std::max(1, opt.virtual_strips);
-  Gtot = (int)std::min<uint64_t>(Gtot, m);
   constexpr int R = 16;
   const int HS = 32 * R;
   const int S = (int)((n + HS - 1) / HS);
+  LongFn fn = long_fn<R>(P.kind, P.gap);
+  int Gtot = ND > 1 ? ND : std::max(1, opt.virtual_strips);
+  if (ND == 1 && opt.virtual_strips <= 0) {
+    // Auto: every task spans its column strip, so the last round of S*G tasks over W
+    // resident warps idles the rest; G column passes (tickets column-strip major, so a
+    // task's left edge was finished a pass earlier) shrink that round's share.
+    int nb = 0;
+    cudaSetDevice(devs[0].id);
+    LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0));
+    int grid = devs[0].num_sms * std::max(nb, 1);
+    if (opt.blocks > 0) grid = std::min(grid, opt.blocks);
+    const double W = 4.0 * grid;
+    double best = -1;
+    for (int G = 1; G <= 8; ++G) {
+      const double rounds = S * (double)G / W;
+      const double score = rounds / std::ceil(rounds) - 0.005 * (G - 1);
+      if (score > best + 1e-9) { best = score; Gtot = G; }
+    }
+  }
+  Gtot = (int)std::min<uint64_t>(Gtot, m);
   std::vector<int32_t> cb(Gtot + 1);
   for (int g = 0; g <= Gtot; ++g) cb[g] = (int32_t)((m * (uint64_t)g) / Gtot);
   int chunk = 8;  // power of two (the kernel masks with chunk - 1)
   while (chunk < opt.chunk_cols && chunk < (1 << 20)) chunk <<= 1;  // publication period
-  LongFn fn = long_fn<R>(P.kind, P.gap);
 
   struct PerDev {
     Buf qa, sa, qc, sc, rowbuf, bcol_own, prog, flags, ticket, abort_, parts, cbuf, bptr, fptr, sum, flg, profbuf;

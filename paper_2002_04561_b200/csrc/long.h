@@ -11,7 +11,8 @@ namespace anyseq {
 struct LongOptions {
   int band_rows = 0;       // 0 = default (rows per warp task = 32 * R)
   int blocks = 0;          // 0 = occupancy-derived persistent grid
-  int virtual_strips = 1;  // column strips on one device (tests the multi-GPU protocol)
+  int virtual_strips = 0;  // column strips on one device (0 = auto from the round count;
+                           // > 0 also tests the multi-GPU protocol)
   int chunk_cols = 256;    // progress publication period (a release = full memory barrier)
   int start_lag = 0;       // columns the strip above must be ahead before a strip starts
   int profile = 0;         // print wait/task cycle counters to stderr
