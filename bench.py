@@ -148,6 +148,16 @@ def measured_alu_peak():
     return props.multi_processor_count, cells, src
 
 
+def arm_config(pairs_per_gpu: int, ws: int) -> dict:
+    """The workload description both arms print (the reference arm times bounded samples of
+    exactly this workload; its cpu_baseline.sample says how many pairs per step)."""
+    return {"workload": "C2: 1M Illumina-like 150x150 bp pairs per GPU, semi-global, "
+                        "affine open 5 / extend 1, match 2 / mismatch -1, score-only",
+            "pairs_per_gpu": pairs_per_gpu, "cells_per_gpu": pairs_per_gpu * READ_LEN * READ_LEN,
+            "l2": "inputs 300 MB > 126 MB L2 (no flush needed)",
+            "parallelism": f"dp{ws} (pairs sharded, no collective)"}
+
+
 def run_reference(args):
     """Reference arm of this tier: the CPU oracle (as it stands), timed on the host cores.
     Each step aligns a bounded sample of the C2 workload (calibrated once to about
@@ -184,8 +194,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": round(k * READ_LEN * READ_LEN / v / 1e6, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C2: 150x150 bp read pairs, semi-global affine 5/1, score-only",
-                       "sample_per_step": sample},
+            "config": arm_config(args.pairs, ws),
             "cpu_baseline": {"value": v, "unit": "GCUPS", "cores": th, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -314,11 +323,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "s16x2",
             "data": "synthetic",
-            "config": {"workload": "C2: 1M Illumina-like 150x150 bp pairs per GPU, semi-global, "
-                                   "affine open 5 / extend 1, match 2 / mismatch -1, score-only",
-                       "pairs_per_gpu": B, "cells_per_gpu": cells,
-                       "l2": "inputs 300 MB > 126 MB L2 (no flush needed)",
-                       "parallelism": f"dp{ws} (pairs sharded, no collective)"},
+            "config": arm_config(B, ws),
             "e2e": {"value": round(e2e_value, 1), "unit": "GCUPS",
                     "h2d_bytes_per_step": int(q.nbytes + s.nbytes + qo.nbytes + so.nbytes),
                     "d2h_bytes_per_step": int(B * 4)},
