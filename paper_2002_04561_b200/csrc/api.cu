@@ -232,6 +232,7 @@ struct DeviceJob {
   uint64_t* rebase_qoff = nullptr;  // host-API chunk: offsets to rebase by (q0, s0) first
   uint64_t* rebase_soff = nullptr;
   uint64_t rebase_q0 = 0, rebase_s0 = 0;
+  int64_t gen_q = -1, gen_s = -1;   // >= 0: offsets are k * gen (not uploaded), see prep
   uint64_t cig_base = 0;            // traceback: added to every cigar_offset of this job
   int32_t* d_scores_out;      // score mode output (device) or null => ctx buffer
   anyseq_alignment* d_aln_out;  // alignment structs (device) or null => ctx buffer
@@ -274,8 +275,8 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   // ---- a1: pack + validate ----
   CK(D.tickets.ensure(kNumTickets * 4));
   CK(launch_prep(D.flags.as<uint32_t>(), B + 1, D.sum.as<PlanSummary>(), J.rebase_qoff,
-                 J.rebase_soff, J.rebase_q0, J.rebase_s0, D.tickets.as<int32_t>(), st,
-                 D.num_sms));
+                 J.rebase_soff, J.rebase_q0, J.rebase_s0, J.gen_q, J.gen_s,
+                 D.tickets.as<int32_t>(), st, D.num_sms));
   static const int dbg_asc = getenv("ANYSEQ_ASCENDING") ? 1 : 0;    // debug/tuning
   static const int dbg_static = getenv("ANYSEQ_STATIC_SLOTS") ? 1 : 0;
   int ticket_next = 0;
@@ -562,14 +563,22 @@ anyseq_status check_batch_host(anyseq_ctx* ctx, const anyseq_batch* b) {
 
 // Per-pair offset checks of pairs [k0, k1), run by the host API on each chunk before its
 // upload (off the critical path: the host thread checks chunk c+1 while chunk c computes).
-anyseq_status check_pairs_host(anyseq_ctx* ctx, const anyseq_batch* b, uint64_t k0, uint64_t k1) {
+// *uq / *us: the common q / s length when every pair of the range has the same lengths
+// (then the chunk's offsets are generated on the device instead of uploaded), else -1.
+anyseq_status check_pairs_host(anyseq_ctx* ctx, const anyseq_batch* b, uint64_t k0, uint64_t k1,
+                               int64_t* uq, int64_t* us) {
+  const uint64_t lq = b->q_off[k0 + 1] - b->q_off[k0], ls = b->s_off[k0 + 1] - b->s_off[k0];
+  bool uni = true;
   for (uint64_t k = k0; k < k1; ++k) {
+    uni = uni && b->q_off[k + 1] - b->q_off[k] == lq && b->s_off[k + 1] - b->s_off[k] == ls;
     if (b->q_off[k + 1] < b->q_off[k] || b->s_off[k + 1] < b->s_off[k])
       return fail(ctx, ANYSEQ_E_INVALID, "pair %llu: offsets decrease", (unsigned long long)k);
     if (b->q_off[k + 1] - b->q_off[k] >= (1ull << 31) || b->s_off[k + 1] - b->s_off[k] >= (1ull << 31))
       return fail(ctx, ANYSEQ_E_INVALID, "pair %llu: sequence longer than 2^31-1",
                   (unsigned long long)k);
   }
+  *uq = uni ? (int64_t)lq : -1;
+  *us = uni ? (int64_t)ls : -1;
   return ANYSEQ_OK;
 }
 
@@ -607,14 +616,19 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
   std::vector<uint64_t> cb{k0};
   {
     // ramp-up: the first upload is not overlapped with anything, so the first chunks are
-    // small (1/8, 1/4, 1/2 of chunk_bytes) and the compute stream starts early
+    // small (1/8, 1/4, 1/2 of chunk_bytes) and the compute stream starts early; ramp-down:
+    // the last chunk's compute is not overlapped either, so the tail halves likewise
     const uint64_t full = (uint64_t)std::max<int64_t>(ctx->chunk_bytes, 1 << 12);
+    const uint64_t end_bytes = b->q_off[k1] + b->s_off[k1];
     uint64_t k = k0;
     int c = 0;
     while (k < k1) {
-      const uint64_t cap = std::max<uint64_t>(1 << 12, c < 3 ? full >> (3 - c) : full);
-      ++c;
       const uint64_t base = b->q_off[k] + b->s_off[k];
+      const uint64_t left = end_bytes - base;
+      uint64_t cap = c < 3 ? full >> (3 - c) : full;
+      if (c >= 3 && left < 2 * full) cap = std::max<uint64_t>(full >> 3, left / 2);
+      cap = std::max<uint64_t>(1 << 12, cap);
+      ++c;
       uint64_t lo = k + 1, hi = k1;  // last index e in (k, k1] with bytes(k, e) <= cap
       while (lo < hi) {
         const uint64_t mid = lo + (hi - lo + 1) / 2;
@@ -642,10 +656,11 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     if (stage_s) memcpy(scores + a0, h_sc + a0, B * 4);
     if (stage_a) memcpy(aln + a0, h_al + a0, B * sizeof(anyseq_alignment));
   };
+  int64_t gen_q[2] = {-1, -1}, gen_s[2] = {-1, -1};  // per buffer set (see check_pairs_host)
   auto upload = [&](int c) -> anyseq_status {
     const int set = c & 1;
     const uint64_t a0 = cb[c], a1 = cb[c + 1], B = a1 - a0;
-    const anyseq_status chk = check_pairs_host(ctx, b, a0, a1);
+    const anyseq_status chk = check_pairs_host(ctx, b, a0, a1, &gen_q[set], &gen_s[set]);
     if (chk != ANYSEQ_OK) return chk;
     const uint64_t q0 = b->q_off[a0], s0 = b->s_off[a0];
     const uint64_t qlen = b->q_off[a1] - q0, slen = b->s_off[a1] - s0;
@@ -658,8 +673,10 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     CK(cudaStreamWaitEvent(cs, D.ev_free[set], 0));
     if (qlen) CK(cudaMemcpyAsync(D.q_ascii2[set].p, b->q + q0, qlen, cudaMemcpyHostToDevice, cs));
     if (slen) CK(cudaMemcpyAsync(D.s_ascii2[set].p, b->s + s0, slen, cudaMemcpyHostToDevice, cs));
-    CK(cudaMemcpyAsync(D.q_off2[set].p, b->q_off + a0, (B + 1) * 8, cudaMemcpyHostToDevice, cs));
-    CK(cudaMemcpyAsync(D.s_off2[set].p, b->s_off + a0, (B + 1) * 8, cudaMemcpyHostToDevice, cs));
+    if (gen_q[set] < 0) {  // uniform chunks: offsets generated on the device (prep kernel)
+      CK(cudaMemcpyAsync(D.q_off2[set].p, b->q_off + a0, (B + 1) * 8, cudaMemcpyHostToDevice, cs));
+      CK(cudaMemcpyAsync(D.s_off2[set].p, b->s_off + a0, (B + 1) * 8, cudaMemcpyHostToDevice, cs));
+    }
     CK(cudaEventRecord(D.ev_up[set], cs));
     return ANYSEQ_OK;
   };
@@ -698,6 +715,8 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     J.rebase_soff = D.s_off2[set].as<uint64_t>();
     J.rebase_q0 = q0;
     J.rebase_s0 = s0;
+    J.gen_q = gen_q[set];
+    J.gen_s = gen_s[set];
     J.cig_base = cig_base;
     J.B = B;
     J.q_end = qlen;

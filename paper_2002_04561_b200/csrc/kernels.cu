@@ -114,12 +114,16 @@ cudaError_t launch_pack(const char* d_q, uint64_t q_len, uint8_t* d_qcode, const
 
 // ------------------------------------------------------------------------ prep / publish
 __global__ void prep_kernel(uint32_t* flags, uint64_t n, PlanSummary* sum, uint64_t* qoff,
-                            uint64_t* soff, uint64_t q0, uint64_t s0, int32_t* tickets) {
+                            uint64_t* soff, uint64_t q0, uint64_t s0, int64_t gq, int64_t gs,
+                            int32_t* tickets) {
   if (blockIdx.x == 0 && threadIdx.x < kNumTickets) tickets[threadIdx.x] = 0;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (uint64_t)gridDim.x * blockDim.x) {
     flags[k] = 0;
-    if (qoff) {  // host-API chunk: offsets were uploaded verbatim
+    if (qoff && gq >= 0) {  // host-API uniform chunk: offsets were not uploaded
+      qoff[k] = k * (uint64_t)gq;
+      soff[k] = k * (uint64_t)gs;
+    } else if (qoff) {  // host-API chunk: offsets were uploaded verbatim
       qoff[k] -= q0;
       soff[k] -= s0;
     }
@@ -140,10 +144,10 @@ __global__ void prep_kernel(uint32_t* flags, uint64_t n, PlanSummary* sum, uint6
 }
 
 cudaError_t launch_prep(uint32_t* flags, uint64_t n, PlanSummary* sum, uint64_t* qoff,
-                        uint64_t* soff, uint64_t q0, uint64_t s0, int32_t* tickets,
-                        cudaStream_t st, int num_sms) {
+                        uint64_t* soff, uint64_t q0, uint64_t s0, int64_t gq, int64_t gs,
+                        int32_t* tickets, cudaStream_t st, int num_sms) {
   prep_kernel<<<grid_for((int64_t)n, 256, num_sms), 256, 0, st>>>(flags, n, sum, qoff, soff, q0,
-                                                                  s0, tickets);
+                                                                  s0, gq, gs, tickets);
   return cudaGetLastError();
 }
 

@@ -21,8 +21,8 @@ cudaError_t launch_pack(const char* d_q, uint64_t q_len, uint8_t* d_qcode, const
 // than this fall back to static slot assignment)
 constexpr int kNumTickets = 64;
 cudaError_t launch_prep(uint32_t* flags, uint64_t n, PlanSummary* sum, uint64_t* qoff,
-                        uint64_t* soff, uint64_t q0, uint64_t s0, int32_t* tickets,
-                        cudaStream_t st, int num_sms);
+                        uint64_t* soff, uint64_t q0, uint64_t s0, int64_t gq, int64_t gs,
+                        int32_t* tickets, cudaStream_t st, int num_sms);
 
 struct ClassifyArgs {
   DevParams P;
