@@ -20,7 +20,8 @@ LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libanyseq.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cu", "kernels.cu", "fill_dispatch.cu", "fill_s16.cu", "fill_s32.cu", "fill_tb.cu",
+SOURCES = ["api.cu", "kernels.cu", "fill_dispatch.cu", "fill_s16.cu", "fill_s16_spec.cu", "fill_s32.cu",
+           "fill_tb.cu",
            "long.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr",

@@ -9,6 +9,8 @@ FillFn fill_fn_s16(int v, int kind, int gap, bool pos);
 FillFn fill_fn_s32(int v, int kind, int gap, bool pos);
 FillFn fill_fn_tb(int v, int kind, int gap, bool pos);
 FillFn fill_fn_s16_spec(int v, int kind, bool pos);
+FillFn fill_fn_s16_spec_a21(int v, int kind, bool pos);
+FillFn fill_fn_s16_spec_l1(int v, int kind, bool pos);
 
 static FillFn pick(int v, int kind, int gap, bool pos) {
   if (v <= 2) return fill_fn_s16(v, kind, gap, pos);
@@ -19,12 +21,21 @@ static FillFn pick(int v, int kind, int gap, bool pos) {
 cudaError_t launch_fill(int variant, int kind, int gap, const FillArgs& a, cudaStream_t st,
                         int num_sms, int* grid_out) {
   static std::mutex mu;
-  static int occ[NV][3][2][2][2][16];  // per device up to 16
+  static int occ[NV][3][2][2][4][16];  // per device up to 16
   static bool init = false;
   const int pos = a.pos ? 1 : 0;
-  // compile-time-specialised instance for the common scheme (affine, G_o = 5, G_e = 1)
-  const int spec = (variant <= 2 && gap == GAFFINE && a.P.go == 5 && a.P.ge == 1) ? 1 : 0;
-  FillFn fn = spec ? fill_fn_s16_spec(variant, kind, pos != 0) : pick(variant, kind, gap, pos != 0);
+  // compile-time-specialised instances: affine (5, 1) (C2-C5), the paper's affine (2, 1) and
+  // linear g = 1 (Fig. 5); everything else takes its constants from the parameter bank
+  int spec = 0;
+  if (variant <= 2 && a.P.ge == 1) {
+    if (gap == GAFFINE && a.P.go == 5) spec = 1;
+    else if (gap == GAFFINE && a.P.go == 2) spec = 2;
+    else if (gap == GLINEAR) spec = 3;
+  }
+  FillFn fn = spec == 1 ? fill_fn_s16_spec(variant, kind, pos != 0)
+            : spec == 2 ? fill_fn_s16_spec_a21(variant, kind, pos != 0)
+            : spec == 3 ? fill_fn_s16_spec_l1(variant, kind, pos != 0)
+                        : pick(variant, kind, gap, pos != 0);
   if (!fn) return cudaErrorInvalidValue;
   int dev = 0;
   cudaGetDevice(&dev);

@@ -6,12 +6,13 @@ namespace anyseq {
 
 typedef void (*FillFn)(FillArgs);
 
-// affine scoring with compile-time G_e = 1, G_o = 5 (the C2-C5 scheme, reading R18/R19)
-template <class V, int L, int R, bool POS>
+// compile-time scoring constants (the paper's partial evaluation of the scheme):
+// GAP = affine with (G_o, G_e) = (CGO, CGE), or linear with g = CGE (CGO unused)
+template <class V, int L, int R, bool POS, int GAP, int CGE, int CGO>
 FillFn fill_fn_spec(int kind) {
-  if (kind == KGLOBAL) return fill_kernel<V, KGLOBAL, GAFFINE, L, R, false, POS, 1, 5>;
-  if (kind == KLOCAL) return fill_kernel<V, KLOCAL, GAFFINE, L, R, false, POS, 1, 5>;
-  return fill_kernel<V, KSEMI, GAFFINE, L, R, false, POS, 1, 5>;
+  if (kind == KGLOBAL) return fill_kernel<V, KGLOBAL, GAP, L, R, false, POS, CGE, CGO>;
+  if (kind == KLOCAL) return fill_kernel<V, KLOCAL, GAP, L, R, false, POS, CGE, CGO>;
+  return fill_kernel<V, KSEMI, GAP, L, R, false, POS, CGE, CGO>;
 }
 
 template <class V, int L, int R, bool TB, bool POS>
