@@ -22,7 +22,7 @@ def _orc(kind, gap, go, q, s):
 
 @pytest.mark.parametrize("kind", ["global", "local", "semi"])
 @pytest.mark.parametrize("gap,go", [("linear", 0), ("affine", 5)])
-@pytest.mark.parametrize("strips", [1, 3])
+@pytest.mark.parametrize("strips", [0, 1, 3])
 def test_long_random_windows(ctx, kind, gap, go, strips):
     import paper_2002_04561_b200 as A
     from synth import iid, c4_genomes
@@ -33,7 +33,7 @@ def test_long_random_windows(ctx, kind, gap, go, strips):
         r = ctx.align_long(A.Scheme(kind, gap, 2, -1, go, 1), q, s)
         o = _orc(kind, gap, go, q, s)
         assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), (n, m)
-    ctx.set_option("long_strips", 1)
+    ctx.set_option("long_strips", 0)
 
 
 def test_long_mutated_window(ctx):
@@ -47,7 +47,7 @@ def test_long_mutated_window(ctx):
         r = ctx.align_long(A.Scheme("local", "affine", 2, -1, 5, 1), g1, g2)
         o = _orc("local", "affine", 5, g1, g2)
         assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), strips
-    ctx.set_option("long_strips", 1)
+    ctx.set_option("long_strips", 0)
     ctx.set_option("long_chunk_cols", 64)
 
 
@@ -60,19 +60,19 @@ def test_long_identical_closed_form(ctx):
         ctx.set_option("long_strips", strips)
         r = ctx.align_long(A.Scheme("local", "affine", 2, -1, 5, 1), g1, g2)
         assert (r["score"], r["q_end"], r["s_end"]) == (2_000_000, 1_000_000, 1_000_000)
-    ctx.set_option("long_strips", 1)
+    ctx.set_option("long_strips", 0)
 
 
 def test_long_strip_invariance(ctx):
-    """Result unchanged for G = 1/2/4/8 virtual strips (SURVEY 8(c) invariants)."""
+    """Result unchanged for G = auto/1/2/4/8 virtual strips (SURVEY 8(c) invariants)."""
     import paper_2002_04561_b200 as A
     from synth import c4_genomes
     g1, g2 = c4_genomes(200_000, "b", seed=8)
     outs = []
-    for strips in (1, 2, 4, 8):
+    for strips in (0, 1, 2, 4, 8):
         ctx.set_option("long_strips", strips)
         outs.append(tuple(ctx.align_long(A.Scheme("local", "affine", 2, -1, 5, 1), g1, g2).values()))
-    ctx.set_option("long_strips", 1)
+    ctx.set_option("long_strips", 0)
     assert len(set(outs)) == 1, outs
 
 
@@ -113,4 +113,4 @@ def test_long_kinds_and_gaps_small_strips(ctx):
                 assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), (kind, gap)
     finally:
         ctx.set_option("long_chunk_cols", 64)
-        ctx.set_option("long_strips", 1)
+        ctx.set_option("long_strips", 0)
