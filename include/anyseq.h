@@ -124,7 +124,9 @@ anyseq_status anyseq_traceback(anyseq_ctx* ctx, const anyseq_params* params,
                                uint32_t* cigar, uint64_t cigar_capacity, uint64_t* cigar_used);
 
 /* Long-pair score-only alignment (tiled wavefront) of host
-   sequences q[0..n) and s[0..m).  out receives score and end cell (cigar_len = 0). */
+   sequences q[0..n) and s[0..m).  out receives score and end cell (cigar_len = 0).
+   32-bit arithmetic; ANYSEQ_E_UNSUPPORTED if the score range could exceed it (R11);
+   ANYSEQ_E_TIMEOUT if a bounded inter-warp wait expires (device state stays valid). */
 anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, const char* q,
                                 uint64_t n, const char* s, uint64_t m, anyseq_alignment* out);
 
@@ -135,14 +137,25 @@ anyseq_status anyseq_sync(anyseq_ctx* ctx);
 uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx);
 
 /* Instrumentation: with option "timing" = 1 the context brackets every fill (relaxation)
-   kernel launch with CUDA events on its stream.  anyseq_get_stat reads
-   "fill_ms" (summed device time of fill kernels), "fill_launches", "walk_ms";
-   anyseq_reset_stats clears them.  Returns ANYSEQ_E_INVALID for unknown names. */
+   launch with CUDA events (score mode with several concurrent variant launches: one
+   interval from the first start to the last end).  anyseq_get_stat reads "fill_ms"
+   (summed device time of fill intervals), "fill_launches", "walk_ms"; anyseq_reset_stats
+   clears them.  "timing" = 2 also prints a per-chunk event timeline of the host API to
+   stderr (debug).  Returns ANYSEQ_E_INVALID for unknown names. */
 anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value);
 anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
 
-/* Tunables (benchmarking): name = "long_band_rows", "long_blocks", ...; returns
-   ANYSEQ_E_INVALID for unknown names. */
+/* Tunables; returns ANYSEQ_E_INVALID for unknown names.
+     "chunk_bytes"       host API: bytes of sequence per upload chunk (default 64 MiB;
+                         the first and last chunks are smaller)
+     "tb_scratch_bytes"  traceback: device bytes of the per-cell H store per fill/walk
+                         chunk (default 16 GiB; 2 B per cell for s16x2 slots)
+     "allow16"           0 forces 32-bit arithmetic (debug); "force_variant" (debug)
+     "long_strips"       long pairs on one device: column passes (0 = automatic from the
+                         round count; > 0 also exercises the multi-GPU boundary protocol)
+     "long_blocks"       long pairs: cap on the persistent grid (0 = occupancy)
+     "long_profile"      long pairs: print wait / task cycle counters to stderr
+     "timing"            see above */
 anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value);
 
 const char* anyseq_status_str(anyseq_status st);
