@@ -18,8 +18,10 @@ from functools import lru_cache
 OPS = "MID"
 
 
-def sigma(match: int, mismatch: int, a: str, b: str) -> int:
+def sigma(match: int, mismatch: int, a: str, b: str, matrix=None) -> int:
     a, b = a.upper(), b.upper()
+    if matrix is not None:  # matrix scoring over A,C,G,T,N
+        return int(matrix["ACGTN".index(a)]["ACGTN".index(b)])
     return match if (a == b and a in "ACGT") else mismatch
 
 
@@ -32,7 +34,8 @@ def rescore(scheme, q_sub: str, s_sub: str, ops: str) -> int:
     prev = None
     for op in ops:
         if op == "M":
-            sc += sigma(scheme.match, scheme.mismatch, q_sub[i], s_sub[j])
+            sc += sigma(scheme.match, scheme.mismatch, q_sub[i], s_sub[j],
+                        getattr(scheme, "matrix", None))
             i += 1
             j += 1
         elif op == "I":          # q_i against a gap (vertical, consumes q only)
@@ -122,7 +125,8 @@ def brute(scheme, q: str, s: str):
             last = ops[-1] if ops else None
             if i < n and j < m:
                 stack.append((i + 1, j + 1, ops + "M",
-                              sc + sigma(scheme.match, scheme.mismatch, q[i], s[j])))
+                              sc + sigma(scheme.match, scheme.mismatch, q[i], s[j],
+                                    getattr(scheme, "matrix", None))))
             if i < n:
                 stack.append((i + 1, j, ops + "I", sc - ge - (go if last != "I" else 0)))
             if j < m:

@@ -49,6 +49,8 @@ typedef struct {
   int32_t mismatch;  /* sigma(a,b), a != b, and anything involving N */
   int32_t gap_open;  /* G_o (ignored for linear) */
   int32_t gap_extend;/* G_e (linear: g) */
+  int32_t has_subst; /* 1: sigma from subst (P:416-419 matrix scoring), else match/mismatch */
+  int32_t subst[25]; /* sigma(a, b) = subst[5*a + b], codes A,C,G,T,N = 0..4 */
 } oracle_params;
 
 typedef struct {
@@ -69,8 +71,10 @@ static int oracle_code(char c) {
   }
 }
 
-/* simple_subst_scoring(match, mismatch); N mismatches everything (L12) */
+/* simple_subst_scoring(match, mismatch); N mismatches everything (L12);
+   or a full substitution matrix over {A,C,G,T,N} (matrix scoring) */
 static int64_t oracle_sigma(const oracle_params* p, int a, int b) {
+  if (p->has_subst) return p->subst[5 * a + b];
   if (a == b && a < 4) return p->match;
   return p->mismatch;
 }

@@ -137,6 +137,44 @@ def test_random_with_N_vs_brute():
         _check_vs_brute(sch, q, s)
 
 
+def _rand_matrix(rng):
+    """A random 5x5 substitution matrix over A,C,G,T,N (matrix scoring)."""
+    return tuple(tuple(rng.randint(-6, 6) for _ in range(5)) for _ in range(5))
+
+
+def test_matrix_scoring_vs_brute():
+    """Matrix scoring: the oracle against exhaustive enumeration (brute.sigma reads the
+    matrix itself) on tiny pairs with N, all kinds x gap models."""
+    rng = random.Random(13)
+    for t in range(300):
+        m = _rand_matrix(rng)
+        sch = O.Scheme(rng.choice(["global", "local", "semi"]), rng.choice(["linear", "affine"]),
+                       0, 0, rng.randint(0, 6), rng.randint(1, 3), matrix=m)
+        lim = 5 if sch.kind == "local" else 6
+        q = "".join(rng.choice("ACGTN") for _ in range(rng.randint(0, lim)))
+        s = "".join(rng.choice("ACGTN") for _ in range(rng.randint(0, lim)))
+        _check_vs_brute(sch, q, s)
+
+
+def test_matrix_closed_forms():
+    """A matrix with +1 on the diagonal and 0 elsewhere (N included) and zero gap cost is
+    the LCS over the 5-letter alphabet; a matrix that spells the simple scheme gives the
+    simple scheme's alignments."""
+    rng = random.Random(17)
+    ident = tuple(tuple(1 if a == b else 0 for b in range(5)) for a in range(5))
+    simple = tuple(tuple(2 if (a == b and a < 4) else -1 for b in range(5)) for a in range(5))
+    for _ in range(40):
+        q = "".join(rng.choice("ACGTN") for _ in range(rng.randint(0, 50)))
+        s = "".join(rng.choice("ACGTN") for _ in range(rng.randint(0, 50)))
+        assert O.align(O.Scheme("global", "linear", 0, 0, 0, 0, matrix=ident), q, s).score == \
+            _lcs(q, s)
+        for kind in ("global", "local", "semi"):
+            a = O.align(O.Scheme(kind, "affine", 2, -1, 3, 1), q, s)
+            b = O.align(O.Scheme(kind, "affine", 0, 0, 3, 1, matrix=simple), q, s)
+            assert (a.score, a.q_begin, a.s_begin, a.q_end, a.s_end, a.cigar) == \
+                (b.score, b.q_begin, b.s_begin, b.q_end, b.s_end, b.cigar)
+
+
 # ---------------- closed forms ----------------
 
 def _lcs(a, b):
