@@ -67,6 +67,10 @@ typedef struct {
   int32_t mismatch;   /* sigma(a,b), a != b, and every pair involving N; [-128, 127] */
   int32_t gap_open;   /* G_o >= 0 (ignored for LINEAR); <= 32767 */
   int32_t gap_extend; /* G_e >= 0 (LINEAR: g); <= 32767 */
+  /* Matrix scoring: if has_subst != 0, sigma(a, b) = subst[5*a + b] for codes
+     A,C,G,T,N = 0..4 (each in [-128, 127]) and match / mismatch are ignored. */
+  int32_t has_subst;
+  int32_t subst[25];
 } anyseq_params;
 
 /* CSR batch: pair k is q[q_off[k] .. q_off[k+1]) vs s[s_off[k] .. s_off[k+1]).

@@ -38,7 +38,8 @@ OPS = "MID"
 class _Params(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("gap", ctypes.c_int32), ("match", ctypes.c_int32),
                 ("mismatch", ctypes.c_int32), ("gap_open", ctypes.c_int32),
-                ("gap_extend", ctypes.c_int32)]
+                ("gap_extend", ctypes.c_int32), ("has_subst", ctypes.c_int32),
+                ("subst", ctypes.c_int32 * 25)]
 
 
 class _Batch(ctypes.Structure):
@@ -98,10 +99,17 @@ class Scheme:
     mismatch: int = -1
     gap_open: int = 0
     gap_extend: int = 1
+    matrix: tuple = None  # optional 5x5 sigma over codes A,C,G,T,N (matrix scoring)
 
     def c(self) -> _Params:
-        return _Params(KINDS[self.kind], GAPS[self.gap], self.match, self.mismatch,
-                       self.gap_open, self.gap_extend)
+        p = _Params(KINDS[self.kind], GAPS[self.gap], self.match, self.mismatch,
+                    self.gap_open, self.gap_extend)
+        if self.matrix is not None:
+            p.has_subst = 1
+            for a in range(5):
+                for b in range(5):
+                    p.subst[5 * a + b] = int(self.matrix[a][b])
+        return p
 
 
 def version() -> str:

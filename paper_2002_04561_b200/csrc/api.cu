@@ -198,6 +198,10 @@ anyseq_status validate_params(anyseq_ctx* ctx, const anyseq_params* p) {
   if (p->gap < 0 || p->gap > 1) return fail(ctx, ANYSEQ_E_INVALID, "gap %d invalid", p->gap);
   if (p->match < -128 || p->match > 127 || p->mismatch < -128 || p->mismatch > 127)
     return fail(ctx, ANYSEQ_E_INVALID, "match/mismatch must be in [-128,127]");
+  if (p->has_subst)
+    for (int k = 0; k < 25; ++k)
+      if (p->subst[k] < -128 || p->subst[k] > 127)
+        return fail(ctx, ANYSEQ_E_INVALID, "subst[%d] must be in [-128,127]", k);
   if (p->gap_extend < 0 || p->gap_extend > 32767)
     return fail(ctx, ANYSEQ_E_INVALID, "gap_extend must be in [0,32767]");
   if (p->gap == ANYSEQ_GAP_AFFINE && (p->gap_open < 0 || p->gap_open > 32767))
@@ -213,8 +217,18 @@ DevParams dev_params(const anyseq_params* p) {
   d.mismatch = p->mismatch;
   d.go = p->gap == ANYSEQ_GAP_AFFINE ? p->gap_open : 0;
   d.ge = p->gap_extend;
-  d.mism4 = ((uint32_t)(p->mismatch & 0xff)) * 0x01010101u;
-  d.xm = ((uint32_t)(p->match ^ p->mismatch)) & 0xffu;
+  // sigma tables: simple_subst_scoring(match, mismatch) with N mismatching everything
+  // (reading R12) or the caller's 5x5 matrix
+  d.smax = -1 << 30;
+  for (int a = 0; a < 5; ++a) {
+    d.prof[a] = 0;
+    for (int b = 0; b < 5; ++b) {
+      const int v = p->has_subst ? p->subst[5 * a + b] : ((a == b && a < 4) ? p->match : p->mismatch);
+      d.smax = std::max(d.smax, v);
+      if (b < 4) d.prof[a] |= ((uint32_t)(v & 0xff)) << (8 * b);
+      else d.pn[a] = ((uint32_t)(v & 0xff)) * 0x01010101u;
+    }
+  }
   return d;
 }
 
@@ -302,7 +316,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   ca.cfg.force_variant = (int32_t)ctx->force_variant;
   ca.cfg.bound_go = P.go;
   ca.cfg.bound_ge = P.ge;
-  ca.cfg.bound_match = std::max(P.match, P.mismatch);
+  ca.cfg.bound_match = P.smax;
   ca.cfg.ascending = dbg_asc;
   ca.q_off = J.d_qoff;
   ca.s_off = J.d_soff;

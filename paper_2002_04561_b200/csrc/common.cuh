@@ -25,10 +25,11 @@ constexpr uint8_t CODE_BAD = 0xFF;
 struct DevParams {
   int32_t kind, gap;
   int32_t match, mismatch;
-  int32_t go;      // effective gap open (0 for linear)
-  int32_t ge;      // gap extend (linear: g)
-  uint32_t mism4;  // mismatch byte replicated
-  uint32_t xm;     // (match ^ mismatch) & 0xff
+  int32_t go;       // effective gap open (0 for linear)
+  int32_t ge;       // gap extend (linear: g)
+  int32_t smax;     // max sigma (range guards, walk bounds)
+  uint32_t prof[5]; // query profile of code c: bytes sigma(c, A..T) (simple or matrix scoring)
+  uint32_t pn[5];   // byte 0: sigma(c, N) (the s32 profile's fifth byte)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -42,8 +43,18 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 
 // profile word of a query symbol c: byte k = sigma(c, k) for subject codes k = 0..3
 // (simple_subst_scoring).  N (code 4) mismatches everything (reading R12).
+// (P should refer to the kernel parameter itself: the index then becomes one constant-bank
+// load with a register offset instead of a local-memory copy of DevParams)
 __device__ __forceinline__ uint32_t prof4(const DevParams& P, uint32_t c) {
-  return c < 4 ? (P.mism4 ^ (P.xm << (8 * c))) : P.mism4;
+  return P.prof[c < 4 ? c : 4];
+}
+__device__ __forceinline__ uint32_t pn_of(const DevParams& P, uint32_t c) {
+  return P.pn[c < 4 ? c : 4];
+}
+// sigma(a, b) for codes 0..4 (traceback walk)
+__device__ __forceinline__ int sigma_of(const DevParams& P, uint32_t a, uint32_t b) {
+  const uint32_t aa = a < 4 ? a : 4;
+  return b < 4 ? (int)(int8_t)(prof4(P, aa) >> (8 * b)) : (int)(int8_t)pn_of(P, aa);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) 
   const int slot_hi = a.nslots_dev ? *a.nslots_dev : a.slot_hi;
   const int nsl = slot_hi - slot_lo;
   const int nws = (nsl + G - 1) / G;
-  const DevParams P = a.P;
+  const DevParams& P = a.P;
   constexpr bool pos = TB || POS;
   constexpr bool FAST = (GAP == GAFFINE);  // reassociated affine recurrence (score and TB)
   // VS16 local scores are unbiased; their Hop uses VIADD.16x2 (see hop) -- fine.
@@ -215,17 +215,19 @@ __global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) 
         int iv[PP];
         uint32_t pf[PP];
         bool rl[PP];
+        uint32_t c0 = 0;
 #pragma unroll
         for (int X = 0; X < PP; ++X) {
           const int i = (KIND == KGLOBAL) ? ip + 1 : ip - pad[X] + 1;  // real row, 1-based
           rl[X] = sact && i >= 1 && i <= nn[X];
           const uint32_t c = rl[X] ? a.qcode[qo[X] + i - 1] : 0u;
+          if (X == 0) c0 = c;
           pf[X] = rl[X] ? prof4(P, c) : 0u;  // pad rows: sigma = 0
           iv[X] = (KIND == KGLOBAL && i >= 1) ? -(P.go + i * P.ge) : 0;  // H(i,0)
         }
         if (PP == 1) {
           p0[r] = pf[0];
-          p1[r] = rl[0] ? P.mism4 : 0u;  // byte 4 = sigma(q_i, N) = mismatch
+          p1[r] = rl[0] ? pn_of(P, c0) : 0u;  // byte 4 = sigma(q_i, N)
         } else {
           p0[r] = pf[0];
           p1[r] = pf[PP - 1];

@@ -453,8 +453,7 @@ __global__ void walk_kernel(WalkArgs a) {
         for (int l = 0; l < DW; ++l) {
           if (l < lim) {
             hv[l] = hval(a, ti, i - 1 - l, j - 1 - l);
-            const uint32_t cq = qc[i - l], cs = sc[j - l];
-            sg[l] = (cq == cs && cq < 4u) ? a.P.match : a.P.mismatch;
+            sg[l] = sigma_of(a.P, qc[i - l], sc[j - l]);
           }
         }
         int taken = 0;
@@ -473,8 +472,7 @@ __global__ void walk_kernel(WalkArgs a) {
         }
       }
       const int hd = hval(a, ti, i - 1, j - 1);
-      const uint32_t ci = qc[i], cj = sc[j];
-      const int sig = (ci == cj && ci < 4u) ? a.P.match : a.P.mismatch;
+      const int sig = sigma_of(a.P, qc[i], sc[j]);
       if (h == hd + sig) {  // DIAG
         rw.push(0u, 1);
         --i; --j;
@@ -495,7 +493,7 @@ __global__ void walk_kernel(WalkArgs a) {
       int kb = 0, hb = 0;
       {
         constexpr int SB = 8;
-        const int mt = max(max(a.P.match, a.P.mismatch), 0);
+        const int mt = max(a.P.smax, 0);
         for (int k0 = 1; k0 <= i; k0 += SB) {
           if (mt * min(i - k0, j) - go - k0 * ge < h) break;
           int hv[SB];
@@ -515,7 +513,7 @@ __global__ void walk_kernel(WalkArgs a) {
       }
       {  // LEFT: F(i,j) = h, the largest such k along the row
         constexpr int SB = 8;
-        const int mt = max(max(a.P.match, a.P.mismatch), 0);
+        const int mt = max(a.P.smax, 0);
         for (int k0 = 1; k0 <= j; k0 += SB) {
           if (mt * min(i, j - k0) - go - k0 * ge < h) break;
           int hv[SB];

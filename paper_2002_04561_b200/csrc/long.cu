@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
   const int t = threadIdx.x & 31;
   const int wb = threadIdx.x >> 5;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const DevParams P = a.P;
+  const DevParams P = a.P;  // copy: hot-loop constants in registers
   const int NEG = NEG32;
   const int NGE = -P.ge;
   const int cop = (GAP == GAFFINE) ? (P.go + P.ge) : P.ge;
@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
       const int ip = ip0 + r;
       const bool real = ip < n;
       const uint32_t c = real ? a.qc[ip] : 0u;
-      p0[r] = real ? prof4(P, c) : 0u;
-      p1[r] = real ? P.mism4 : 0u;
+      p0[r] = real ? prof4(a.P, c) : 0u;  // indexed from the parameter bank, not the copy
+      p1[r] = real ? pn_of(a.P, c) : 0u;  // byte 4 of the profile: sigma(q_i, N)
       HA[r] = HB[r] = 0;
       Ff[r] = NEG;
     }
@@ -511,7 +511,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   }
   {  // 32-bit range guard (reading R11)
     const long double neg = 3.0L * P.go + ((long double)n + m + 2) * P.ge + 256;
-    const long double pos = (long double)std::max(P.match, 0) * std::min(n, m);
+    const long double pos = (long double)std::max(P.smax, 0) * std::min(n, m);
     if (neg > (1u << 30) - (1u << 24) || pos > (1u << 30) - (1u << 24)) {
       *err = "score range exceeds 32-bit arithmetic";
       return ANYSEQ_E_UNSUPPORTED;
@@ -678,7 +678,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     a.chunk = chunk;
     a.one = 1;
     a.lag = opt.start_lag > 0 ? opt.start_lag : chunk + 2 * 32 + 64;
-    a.keyed = (long double)std::max(P.match, 0) * std::min(n, m) < (long double)(1 << 25) ? 1 : 0;
+    a.keyed = (long double)std::max(P.smax, 0) * std::min(n, m) < (long double)(1 << 25) ? 1 : 0;
     a.prof = nullptr;
     if (opt.profile) {
       LK(cudaMalloc(&D.profbuf.p, 64));

@@ -249,6 +249,36 @@ def test_c3_full_size_sampled(ctx):
     assert np.array_equal(cols.astype(np.int64), aln["s_end"] - aln["s_begin"])
 
 
+def _matrix(seed):
+    rng = np.random.default_rng(seed)
+    m = rng.integers(-5, 6, size=(5, 5))
+    m[np.arange(4), np.arange(4)] = rng.integers(1, 6, size=4)  # matches score positive
+    return tuple(tuple(int(x) for x in row) for row in m)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("gap", [("linear", 0, 1), ("affine", 4, 1)], ids=lambda g: g[0])
+def test_matrix_scoring(ctx, kind, gap):
+    """Matrix scoring: random 5x5 sigma, pairs with and without N (s16x2 and
+    s32 paths), score + ends and traceback against the oracle."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    from synth import random_pairs
+    g, go, ge = gap
+    m = _matrix(200 + KINDS.index(kind))
+    for with_n in (False, True):
+        q, qo, s, so = random_pairs(250, 0, 240, seed=300 + with_n)
+        if with_n:  # sprinkle N so those pairs take the s32 path
+            rng = np.random.default_rng(5)
+            q = q.copy()
+            q[rng.choice(len(q), size=len(q) // 40, replace=False)] = ord("N")
+        res, cig = O.batch(O.Scheme(kind, g, 0, 0, go, ge, matrix=m), q, qo, s, so, traceback=True)
+        ocig = O.batch_cigars(res, cig, qo, so)
+        sch = A.Scheme(kind, g, 0, 0, go, ge, matrix=m)
+        _check_scores(ctx, sch, q, qo, s, so, res)
+        _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+
+
 def test_c5_mixed_sample(ctx):
     """C5 shape (mixed 100..1000 bp), all kinds x modes, 600 pairs."""
     import paper_2002_04561_b200 as A

@@ -114,3 +114,21 @@ def test_long_kinds_and_gaps_small_strips(ctx):
     finally:
         ctx.set_option("long_chunk_cols", 64)
         ctx.set_option("long_strips", 0)
+
+
+def test_long_matrix_scoring(ctx):
+    """Matrix scoring on the long kernel: windows with N against the oracle."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    from synth import iid
+    m = ((3, -2, -1, -2, -1), (-2, 4, -2, -1, -1), (-1, -2, 3, -2, -1), (-2, -1, -2, 4, -1),
+         (-1, -1, -1, -1, 1))
+    q, s = bytearray(iid(2100, 61)), bytearray(iid(1900, 62))
+    for k in range(0, len(q), 97):
+        q[k] = ord("N")
+    q, s = bytes(q), bytes(s)
+    for kind in ("global", "local", "semi"):
+        for gap, go in (("linear", 0), ("affine", 3)):
+            r = ctx.align_long(A.Scheme(kind, gap, 0, 0, go, 1, matrix=m), q, s)
+            o = O.score_rolling(O.Scheme(kind, gap, 0, 0, go, 1, matrix=m), q, s)
+            assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), (kind, gap)
