@@ -37,7 +37,7 @@ READ_LEN = 150
 METRIC = "GCUPS (batched 150bp semi-global affine, long-pair SW) at 1/2/4/8 B200"
 # dram__bytes_read.sum + dram__bytes_write.sum of one fill launch on the full C2 batch, from
 # the committed ncu --set full capture of the fill kernel at the full C2 size.
-TRAFFIC_BYTES_PER_LAUNCH = 328_192_768  # 320.36 MB read + 7.83 MB write (profiles/r01_fill_ncu.txt)
+TRAFFIC_BYTES_PER_LAUNCH = 328_585_984  # 320.27 MB read + 8.32 MB write (profiles/r01_fill_ncu.txt)
 
 
 def _dist():
