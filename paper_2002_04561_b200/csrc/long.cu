@@ -518,10 +518,12 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     }
   }
   const int ND = (int)devs.size();
-  constexpr int R = 16;
+  // rows per lane: 16 (168 registers, 3 blocks/SM; default) or 12 (128 registers, 4
+  // blocks/SM; option long_band_rows = 384) -- measured equal within noise on C4
+  const int R = opt.band_rows == 384 ? 12 : 16;
   const int HS = 32 * R;
   const int S = (int)((n + HS - 1) / HS);
-  LongFn fn = long_fn<R>(P.kind, P.gap);
+  LongFn fn = R == 16 ? long_fn<16>(P.kind, P.gap) : long_fn<12>(P.kind, P.gap);
   int Gtot = ND > 1 ? ND : std::max(1, opt.virtual_strips);
   if (ND == 1 && opt.virtual_strips <= 0) {
     // Auto: every task spans its column strip, so the last round of S*G tasks over W
