@@ -89,7 +89,7 @@ struct Device {
   HostBuf h_stage;               // pinned staging of score-mode results
   // score-mode variant launches of one plan run concurrently (each with its own strip
   // scratch): small per-variant launches of mixed-length batches then share the GPU
-  DevBuf strip_v[NV];
+  DevBuf strip_v[NV], dirs_v[NV];
   cudaStream_t vstream[NV] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[NV] = {};
   uint64_t* h_small = nullptr;   // pinned scratch
@@ -385,10 +385,12 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   // score mode with several variants: fork the variant launches onto their own streams
   int nvar = 0;
   for (int v = 0; v < NV; ++v) nvar += S.count[v] ? 1 : 0;
+  // score mode only: the traceback fill is bound by its H-store writes, and splitting the
+  // store between concurrent variants measured slower (C5 traceback 0.9x)
   const bool fork = !J.tb && nvar > 1;
   std::pair<cudaEvent_t, cudaEvent_t> fev{nullptr, nullptr};
   if (fork) {
-    if (ctx->timing) { fev = take_events(ctx); CK(cudaEventRecord(fev.first, st)); }
+    if (ctx->timing && !J.tb) { fev = take_events(ctx); CK(cudaEventRecord(fev.first, st)); }
     CK(cudaEventRecord(D.ev_fork, st));
   }
   for (int v = 0; v < NV; ++v) {
@@ -445,21 +447,19 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
         }
         ctx->fill_launches++;
       }
-      if (fork) {
-        CK(cudaEventRecord(D.ev_join[v], vst));
-        CK(cudaStreamWaitEvent(st, D.ev_join[v], 0));
-      }
       if (grid > grid_est) return fail(ctx, ANYSEQ_E_CUDA, "occupancy above scratch estimate");
       L(1);
     } else {
       const int64_t ns = (S.maxn[v] + HS - 1) / HS;
       const int64_t dk = S.maxm[v] + d.L - 1 + d.R - 1;  // diagonals (step - row) per strip
       const int64_t block_words = ns * dk * d.R * d.L;    // one H word per (diag, row, lane)
-      const int64_t cap_words = std::max<int64_t>(ctx->tb_scratch_bytes / 4, block_words);
+      DevBuf& dirs = fork ? D.dirs_v[v] : D.dirs;
+      const int64_t cap_words =
+          std::max<int64_t>(ctx->tb_scratch_bytes / 4 / (fork ? nvar : 1), block_words);
       int64_t chunk = std::max<int64_t>(1, cap_words / block_words);
       chunk = std::min<int64_t>(chunk, nslot[v]);
-      CK(D.dirs.ensure((size_t)(chunk * block_words) * 4));
-      fa.dirs = D.dirs.as<uint32_t>();
+      CK(dirs.ensure((size_t)(chunk * block_words) * 4));
+      fa.dirs = dirs.as<uint32_t>();
       fa.dir_block_words = block_words;
       fa.tb = D.tb.as<TbInfo>();
       for (int64_t lo = 0; lo < nslot[v]; lo += chunk) {
@@ -468,11 +468,11 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
         fa.slot_hi = (int32_t)(sbase[v] + hi);
         int grid = 0;
         std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
-        if (ctx->timing) { ev = take_events(ctx); CK(cudaEventRecord(ev.first, st)); }
+        if (ctx->timing) { ev = take_events(ctx); CK(cudaEventRecord(ev.first, vst)); }
         fa.ticket = take_ticket();
-        CK(launch_fill(v, prm->kind, prm->gap, fa, st, D.num_sms, &grid));
+        CK(launch_fill(v, prm->kind, prm->gap, fa, vst, D.num_sms, &grid));
         if (ctx->timing) {
-          CK(cudaEventRecord(ev.second, st));
+          CK(cudaEventRecord(ev.second, vst));
           std::lock_guard<std::mutex> lk(ctx->ev_mu);
           ctx->fill_ev.push_back(ev);
           ctx->fill_launches++;
@@ -489,7 +489,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
         wa.slot_hi = fa.slot_hi;
         wa.pairs_per_slot = d.pairs;
         wa.tb = D.tb.as<TbInfo>();
-        wa.dirs = D.dirs.as<uint32_t>();
+        wa.dirs = dirs.as<uint32_t>();
         wa.q_off = J.d_qoff;
         wa.s_off = J.d_soff;
         wa.ops = D.ops.as<uint32_t>();
@@ -497,19 +497,23 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
         wa.beg_i = D.beg_i.as<int32_t>();
         wa.beg_j = D.beg_j.as<int32_t>();
         std::pair<cudaEvent_t, cudaEvent_t> ew{nullptr, nullptr};
-        if (ctx->timing) { ew = take_events(ctx); CK(cudaEventRecord(ew.first, st)); }
-        CK(launch_walk(wa, st, D.num_sms));
+        if (ctx->timing) { ew = take_events(ctx); CK(cudaEventRecord(ew.first, vst)); }
+        CK(launch_walk(wa, vst, D.num_sms));
         if (ctx->timing) {
-          CK(cudaEventRecord(ew.second, st));
+          CK(cudaEventRecord(ew.second, vst));
           std::lock_guard<std::mutex> lk(ctx->ev_mu);
           ctx->walk_ev.push_back(ew);
         }
         L(2);
       }
     }
+    if (fork) {  // join this variant's stream back into the compute stream
+      CK(cudaEventRecord(D.ev_join[v], vst));
+      CK(cudaStreamWaitEvent(st, D.ev_join[v], 0));
+    }
   }
 
-  if (fork && ctx->timing) {  // one fill interval: fork to join
+  if (fork && ctx->timing && !J.tb) {  // one fill interval: fork to join (traceback: per launch)
     CK(cudaEventRecord(fev.second, st));
     std::lock_guard<std::mutex> lk(ctx->ev_mu);
     ctx->fill_ev.push_back(fev);
@@ -945,6 +949,7 @@ void anyseq_destroy(anyseq_ctx* c) {
     }
     for (int v = 0; v < NV; ++v) {
       D.strip_v[v].release();
+      D.dirs_v[v].release();
       if (D.vstream[v]) cudaStreamDestroy(D.vstream[v]);
       if (D.ev_join[v]) cudaEventDestroy(D.ev_join[v]);
     }
