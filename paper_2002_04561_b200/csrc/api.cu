@@ -385,9 +385,9 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   // score mode with several variants: fork the variant launches onto their own streams
   int nvar = 0;
   for (int v = 0; v < NV; ++v) nvar += S.count[v] ? 1 : 0;
-  // score mode only: the traceback fill is bound by its H-store writes, and splitting the
-  // store between concurrent variants measured slower (C5 traceback 0.9x)
-  const bool fork = !J.tb && nvar > 1;
+  // (traceback too: each concurrent variant gets its own full H store -- at most the three
+  // traceback variants, 3 x tb_scratch_bytes of device memory)
+  const bool fork = nvar > 1;
   std::pair<cudaEvent_t, cudaEvent_t> fev{nullptr, nullptr};
   if (fork) {
     if (ctx->timing && !J.tb) { fev = take_events(ctx); CK(cudaEventRecord(fev.first, st)); }
@@ -454,8 +454,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
       const int64_t dk = S.maxm[v] + d.L - 1 + d.R - 1;  // diagonals (step - row) per strip
       const int64_t block_words = ns * dk * d.R * d.L;    // one H word per (diag, row, lane)
       DevBuf& dirs = fork ? D.dirs_v[v] : D.dirs;
-      const int64_t cap_words =
-          std::max<int64_t>(ctx->tb_scratch_bytes / 4 / (fork ? nvar : 1), block_words);
+      const int64_t cap_words = std::max<int64_t>(ctx->tb_scratch_bytes / 4, block_words);
       int64_t chunk = std::max<int64_t>(1, cap_words / block_words);
       chunk = std::min<int64_t>(chunk, nslot[v]);
       CK(dirs.ensure((size_t)(chunk * block_words) * 4));
