@@ -62,7 +62,7 @@ struct RunWriter {
 
 // Walk one pair from its end cell; runs in walk order (reversed) at ops_out, the number of
 // runs and the begin cell to the pointers.  qc / sc: 1-based code pointers of the pair.
-__device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t* __restrict__ dirs,
+static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t* __restrict__ dirs,
                                        const TbInfo& ti, const uint8_t* qc, const uint8_t* sc,
                                        uint32_t* ops_out, int32_t* n_ops, int32_t* beg_i,
                                        int32_t* beg_j) {
