@@ -87,11 +87,28 @@ static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t
       constexpr int DW = 8;
       const int lim = min(DW, min(i, j));
       int hv[DW], sg[DW];
+      // the 8 query / subject codes of the run: two aligned 8-byte loads each (the code
+      // buffers carry 16 bytes of slack), instead of 16 scattered byte loads
+      uint64_t vq = 0, vs = 0;
+      const bool vec = i > DW && j > DW;
+      if (vec) {
+        auto load8 = [](const uint8_t* p) -> uint64_t {  // bytes p[0..7], p unaligned
+          const uintptr_t a = (uintptr_t)p & ~(uintptr_t)7;
+          const uint64_t lo = __ldg((const unsigned long long*)a);
+          const uint64_t hi = __ldg((const unsigned long long*)(a + 8));
+          const int sh = (int)((uintptr_t)p - a) * 8;
+          return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+        };
+        vq = load8(qc + i - (DW - 1));  // byte 7 - l = code of row i - l
+        vs = load8(sc + j - (DW - 1));
+      }
 #pragma unroll
       for (int l = 0; l < DW; ++l) {
         if (l < lim) {
           hv[l] = hval(P, dirs, ti, i - 1 - l, j - 1 - l);
-          sg[l] = sigma_of(P, qc[i - l], sc[j - l]);
+          const uint32_t cq = vec ? (uint32_t)(vq >> (8 * (DW - 1 - l))) & 0xffu : qc[i - l];
+          const uint32_t cs = vec ? (uint32_t)(vs >> (8 * (DW - 1 - l))) & 0xffu : sc[j - l];
+          sg[l] = sigma_of(P, cq, cs);
         }
       }
       int taken = 0;
