@@ -106,6 +106,8 @@ struct anyseq_ctx {
   int64_t force_variant = -1;
   int64_t allow16 = 1;
   LongOptions long_opt;
+  int long_narrow = 0;   // the last anyseq_align_long ran the 16-bit differential kernel
+  double long_ms = 0;    // ... and its kernel time (max over devices)
   int timing = 0;
   std::mutex ev_mu;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> fill_ev, walk_ev, pool;
@@ -1053,6 +1055,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
   if (n == "long_strips") { ctx->long_opt.virtual_strips = (int)value; return ANYSEQ_OK; }
   if (n == "long_profile") { ctx->long_opt.profile = (int)value; return ANYSEQ_OK; }
   if (n == "long_start_lag") { ctx->long_opt.start_lag = (int)value; return ANYSEQ_OK; }
+  if (n == "long_narrow") { ctx->long_opt.narrow = (int)value; return ANYSEQ_OK; }
   if (n == "long_chunk_cols") { ctx->long_opt.chunk_cols = (int)value; return ANYSEQ_OK; }
   return fail(ctx, ANYSEQ_E_INVALID, "unknown option %s", name);
 }
@@ -1080,6 +1083,8 @@ anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, co
   const int rc = run_long(ld, dev_params(params), q, n, s, m, ctx->long_opt, &r, &err, &launches);
   ctx->launches += launches;
   if (rc != 0) return fail(ctx, (anyseq_status)rc, "%s", err.c_str());
+  ctx->long_narrow = r.narrow ? 1 : 0;
+  ctx->long_ms = r.kernel_ms;
   memset(out, 0, sizeof(*out));
   out->score = r.score;
   out->q_end = out->q_begin = r.end_i;
@@ -1096,6 +1101,8 @@ anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) 
   std::string n(name);
   if (n == "fill_ms") { *value = ctx->fill_ms; return ANYSEQ_OK; }
   if (n == "walk_ms") { *value = ctx->walk_ms; return ANYSEQ_OK; }
+  if (n == "long_narrow") { *value = ctx->long_narrow; return ANYSEQ_OK; }
+  if (n == "long_kernel_ms") { *value = ctx->long_ms; return ANYSEQ_OK; }
   if (n == "fill_launches") { *value = (double)ctx->fill_launches; return ANYSEQ_OK; }
   return fail(ctx, ANYSEQ_E_INVALID, "unknown stat %s", name);
 }

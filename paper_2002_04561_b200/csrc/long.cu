@@ -56,6 +56,10 @@ struct LongArgs {
   int32_t one;
   int32_t lag;
   int32_t keyed;  // local: 32 * (max score) fits in 31 bits -> packed (value, row) tracking
+  int32_t hopc;    // long16: packed -(G_o+G_e) for both halves, low-half borrow compensated
+  int32_t neg16;   // long16: relative "-inf" (below every real relative value)
+  int32_t margin;  // long16: the warp maximum is re-based to -margin
+  int32_t bspan;   // long16: bound on |H(x) - H(y)| over one task window (Lipschitz, d * dist)
   unsigned long long* prof;  // optional: [0] cycles waiting, [1] cycles in tasks, [2] tasks
   long long spin_limit;
 };
@@ -455,6 +459,9 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
   if (t == 0) a.parts[wg] = part;
 }
 
+#include "long16.cuh"
+
+
 __global__ void long_init_kernel(DevParams P, int n, int m, int4* rowbuf, int2* bcol0,
                                  int2* const* bcol, const int* cb, int Gtot, int g_first,
                                  int g_count) {
@@ -502,6 +509,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
              const char* s, uint64_t m, const LongOptions& opt, LongResult* out, std::string* err,
              uint64_t* launches) {
   out->kernel_ms = 0;
+  out->narrow = false;
   if (n == 0 || m == 0) {  // empty sequences: one gap run (global) or the empty alignment
     const int64_t len = (int64_t)(n + m);
     out->score = (P.kind == KGLOBAL && len) ? (int32_t)(-(P.go + len * P.ge)) : 0;
@@ -521,9 +529,30 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   // rows per lane: 16 (168 registers, 3 blocks/SM; default) or 12 (128 registers, 4
   // blocks/SM; option long_band_rows = 384) -- measured equal within noise on C4
   const int R = opt.band_rows == 384 ? 12 : 16;
-  const int HS = 32 * R;
-  const int S = (int)((n + HS - 1) / HS);
+  int HS = 32 * R;
   LongFn fn = R == 16 ? long_fn<16>(P.kind, P.gap) : long_fn<12>(P.kind, P.gap);
+  // 16-bit differential kernel (long16.cuh): local affine, subject without
+  // N (the s16x2 selector has no fifth byte), and the relative frame of DESIGN.md §5.4b:
+  // every value of a task window within bspan = (rows + 66) * d of one reference cell
+  // (d = G_o + G_e + max sigma bounds |H(x) - H(y)| per unit of Manhattan distance),
+  // 2 bspan + margin (drift over 96 steps between re-basings) + slack inside the s16 range
+  // above the relative -inf.
+  const int NR16 = opt.band_rows == 1024 ? 16 : 8;
+  const int64_t d16 = (int64_t)P.go + P.ge + std::max(P.smax, 0);
+  const int64_t bspan16 = (int64_t)(64 * NR16 + 66) * d16;
+  const int64_t margin16 = 100 * d16 + 16;
+  const int NEG16C = -24576;
+  bool narrow = opt.narrow != 0 && P.kind == KLOCAL && P.gap == GAFFINE &&
+                2 * bspan16 + margin16 + 96 * d16 + P.go + P.ge + 256 < -NEG16C &&
+                (int64_t)P.go + 2 * P.ge < 4096;
+  if (narrow)
+    for (uint64_t x = 0; x < m && narrow; ++x) narrow = (s[x] | 0x20) != 'n';
+  if (narrow) {
+    HS = 64 * NR16;
+    fn = NR16 == 16 ? long16_kernel<16> : long16_kernel<8>;
+  }
+  out->narrow = narrow;
+  const int S = (int)((n + HS - 1) / HS);
   int Gtot = ND > 1 ? ND : std::max(1, opt.virtual_strips);
   if (ND == 1 && opt.virtual_strips <= 0) {
     // Auto: every task spans its column strip, so the last round of S*G tasks over W
@@ -681,6 +710,13 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     a.one = 1;
     a.lag = opt.start_lag > 0 ? opt.start_lag : chunk + 2 * 32 + 64;
     a.keyed = (long double)std::max(P.smax, 0) * std::min(n, m) < (long double)(1 << 25) ? 1 : 0;
+    {
+      const int c = P.go + P.ge;  // low half always borrows (values < 0): pre-add 1 to the high half
+      a.hopc = c == 0 ? 0 : (int32_t)((((uint32_t)(-c - 1) & 0xffffu) << 16) | (uint32_t)((65536 - c) & 0xffff));
+    }
+    a.neg16 = NEG16C;
+    a.margin = (int32_t)margin16;
+    a.bspan = (int32_t)bspan16;
     a.prof = nullptr;
     if (opt.profile) {
       LK(cudaMalloc(&D.profbuf.p, 64));

@@ -16,6 +16,7 @@ struct LongOptions {
   int chunk_cols = 256;    // progress publication period (a release = full memory barrier)
   int start_lag = 0;       // columns the strip above must be ahead before a strip starts
   int profile = 0;         // print wait/task cycle counters to stderr
+  int narrow = 1;          // 1: 16-bit differential kernel where eligible (local affine)
 };
 
 struct LongDevice {
@@ -28,6 +29,7 @@ struct LongResult {
   int32_t score;
   int64_t end_i, end_j;
   double kernel_ms;
+  bool narrow;             // the 16-bit differential kernel ran
 };
 
 // Returns 0 or an anyseq_status code; err receives a message.

@@ -1,0 +1,299 @@
+// csrc/long16.cuh -- long-pair local affine score-only kernel in 16-bit differential
+// arithmetic (included by long.cu after the s32 kernel's helpers).
+//
+// Paper: 16-bit scores where the value range allows (SIMD lanes of half
+// width double the cells per instruction).  Long pairs exceed 16 bits absolutely, so the
+// kernel keeps every value relative to a per-warp base: the DP only compares sums of
+// neighbouring cells, and neighbouring H values differ by at most d = G_o + G_e + max(σ,0)
+// (DESIGN.md §5.4b), so the 576 (or 1088) cells a warp holds at one step fit in s16.
+//
+// Same task shell as long_kernel (tickets, tagged row hand-off, boundary columns, flags,
+// bounded waits).  What changes is the warp's inner layout: lane t owns 2·NR rows of the
+// task; rows [0, NR) live in the low halves of its NR registers, rows [NR, 2NR) in the high
+// halves, and the high half runs ONE COLUMN BEHIND the low half (at step k the low half
+// relaxes column k − 2t, the high half column k − 2t − 1).  That makes the two halves 64
+// "virtual lanes" of one anti-diagonal wavefront: the high half's upper neighbour is its own
+// low half of the previous step, the low half's is lane t−1's high half (one shuffle), so
+// every s16x2 instruction relaxes two independent cells.
+//
+// Values are kept strictly negative (rel = abs − base ∈ [−24576, −1]): then H − (G_o+G_e)
+// can be formed on the FMA pipe as one 32-bit IMAD on the packed register (the low half
+// always borrows, the constant pre-compensates the high half), leaving the ALU pipe per two
+// cells: PRMT (σ of both halves), 3 VIADDMNMX.S16x2, VIMNMX3.S16x2 (local floor).
+// The base is re-chosen every 32 steps once all virtual lanes are active (warp max of H →
+// −margin); the local optimum is tracked per half as a packed running maximum (one
+// VIMNMX3 per two registers) and resolved to (value, i, j) in a rare branch.
+#pragma once
+
+__device__ __forceinline__ uint32_t h16_set(uint32_t x, int h, int v) {
+  return h ? ((x & 0xffffu) | ((uint32_t)v << 16)) : ((x & 0xffff0000u) | ((uint32_t)v & 0xffffu));
+}
+__device__ __forceinline__ int h16_get(uint32_t x, int h) {
+  return (int)(int16_t)(uint16_t)(h ? (x >> 16) : (x & 0xffffu));
+}
+__device__ __forceinline__ uint32_t h16_pack(int lo, int hi) {
+  return ((uint32_t)lo & 0xffffu) | ((uint32_t)hi << 16);
+}
+
+template <int NR>
+__global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
+  constexpr int HS = 64 * NR;  // rows per task: 32 lanes x 2 halves x NR
+  constexpr int RING = 256;
+  constexpr int PER = 32;
+  __shared__ int2 ring_he[4][RING];
+  __shared__ uint16_t ring_sel[4][RING];  // subject code c of a column as c * 0x11
+  const int t = threadIdx.x & 31;
+  const int wb = threadIdx.x >> 5;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const DevParams P = a.P;
+  const int cop = P.go + P.ge;
+  const uint32_t NGE2 = VS16::splat(-P.ge);
+  const uint32_t one = (uint32_t)a.one;
+  const int hopc = a.hopc;  // packed (-cop, -cop) with the low half's borrow pre-compensated
+  auto hop = [&](uint32_t h) -> uint32_t { return (uint32_t)imad_add_s((int)h, one, hopc); };
+  const int NEGc = a.neg16;
+  const int n = a.n;
+  // subject codes of columns past a task's end are read (and ignored) by the warp's last
+  // steps: keep every ring entry a valid code so the active half's selector stays intact
+  for (int x = t; x < RING; x += 32) {
+    ring_sel[wb][x] = 0;
+    ring_he[wb][x] = make_int2(0, 0);
+  }
+  __syncwarp();
+
+  LongPart part;
+  part.lv = 0; part.li = 0; part.lj = 0;
+  part.rv = 0; part.rj = 0; part.cv = 0; part.ci = 0; part.gv = 0; part.gset = 0; part.pad_ = 0;
+
+  for (;;) {
+    int task = 0;
+    if (t == 0) task = atomicAdd(a.ticket, 1);
+    task = __shfl_sync(0xffffffffu, task, 0);
+    if (task >= a.S * a.g_count) break;
+    if (*(volatile int*)a.abort_flag) break;
+    const int s = task % a.S;
+    const int g = a.g_first + task / a.S;
+    const int c_lo = a.cb[g], c_hi = a.cb[g + 1], W = c_hi - c_lo;
+    const int ip0 = s * HS + t * 2 * NR;
+    const int2* bl = a.bcol[g];
+    int2* br = (g + 1 < a.Gtot) ? a.bcol[g + 1] : nullptr;
+
+    if (g > 0) {
+      if (!warp_wait<true>(&a.bflag[g][s], 1, a)) break;
+      if (s > 0 && !warp_wait<true>(&a.bflag[g][s - 1], 1, a)) break;
+    }
+    uint32_t p0[NR], p1[NR], HA[NR], HB[NR], Ff[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int iA = ip0 + r, iB = ip0 + NR + r;
+      p0[r] = iA < n ? prof4(a.P, a.qc[iA]) : 0u;  // sigma rows of the low half
+      p1[r] = iB < n ? prof4(a.P, a.qc[iB]) : 0u;  // ... and of the high half
+      HA[r] = HB[r] = VS16::splat(NEGc);
+      Ff[r] = VS16::splat(NEGc);
+    }
+    auto refill = [&](int c0, int c1) -> bool {
+      const int c = c0 + t;
+      const bool mine = c < c1;
+      if (mine) ring_sel[wb][c & (RING - 1)] = (uint16_t)(a.sc[c_lo + c] * 0x11u);
+      if (s == 0) return true;
+      const int4* src = a.rowbuf + c_lo + c + 1;
+      int4 v = mine ? ld_row(src) : make_int4(0, s, 0, s);
+      long long spins = 0;
+      while (!__all_sync(0xffffffffu, v.y == s && v.w == s)) {
+        __nanosleep(64);
+        if (v.y != s || v.w != s) v = ld_row(src);
+        if ((++spins & 255) == 0 &&
+            __any_sync(0xffffffffu, spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
+          if (t == 0) atomicExch(a.abort_flag, 1);
+          return false;
+        }
+      }
+      if (mine) ring_he[wb][c & (RING - 1)] = make_int2(v.x, v.z);
+      return true;
+    };
+    if (!refill(0, min(W, PER)) || !refill(PER, min(W, 2 * PER))) break;
+    __syncwarp();
+
+    // frame: every value of the task lies within a.bspan of H(ip0, c_lo + 1) (the row
+    // above, first column), so base = that + bspan puts them all in [-2 bspan, -margin]
+    int base = (s > 0 ? ring_he[wb][0].x : 0) + a.bspan;
+    auto cv = [&](int x) -> int { return max(x - base, NEGc); };  // absolute -> relative
+    int bv0 = 0, bi0 = 0, bj0 = 0, bv1 = 0, bi1 = 0, bj1 = 0;   // per-half best (absolute)
+    uint32_t Z, best;  // the local floor (absolute 0) and the running maxima, relative
+    auto frame_consts = [&]() {
+      Z = VS16::splat(max(-base, NEGc));
+      best = h16_pack(min(max(bv0 - base, -32768), 32767), min(max(bv1 - base, -32768), 32767));
+    };
+    frame_consts();
+    uint32_t diag = VS16::splat(NEGc), Hbot = VS16::splat(NEGc), Ebot = VS16::splat(NEGc);
+
+    auto sweep = [&](auto first_c) -> bool {
+      constexpr bool FIRST = decltype(first_c)::value;
+      uint32_t cur_nx = ring_sel[wb][(0 - 2 * t) & (RING - 1)];
+      uint32_t prev = 0;
+      int2 he_nx = ring_he[wb][0];
+      auto step = [&](auto chk, const int k, uint32_t (&Hi)[NR], uint32_t (&Hq)[NR]) {
+        constexpr bool CHK = decltype(chk)::value;
+        const uint32_t hs = __shfl_up_sync(0xffffffffu, Hbot, 1);
+        const uint32_t es = __shfl_up_sync(0xffffffffu, Ebot, 1);
+        // low half <- lane t-1's high half (row above, same column); high half <- own low
+        // half of the previous step (row above, one column behind)
+        uint32_t hin = __byte_perm(hs, Hbot, 0x5432);
+        uint32_t ein = __byte_perm(es, Ebot, 0x5432);
+        const int lc = k - 2 * t;  // low half's column (task-relative); high half: lc - 1
+        const uint32_t cur = cur_nx;
+        cur_nx = ring_sel[wb][(lc + 1) & (RING - 1)];
+        const uint32_t sel = cur | (prev << 8) | 0xC480u;  // VS16::selector(c(lc), c(lc-1))
+        prev = cur;
+        const int2 he = he_nx;
+        if (!FIRST) he_nx = ring_he[wb][(k + 1) & (RING - 1)];  // lane 0's next column
+        const bool act0 = !CHK || (lc >= 0 && lc < W);
+        const bool act1 = !CHK || (lc >= 1 && lc <= W);
+        if (CHK && (lc == 0 || lc == 1)) {  // half h reaches the left boundary column
+          const int h = lc;
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const int ip = ip0 + h * NR + r;
+            int2 b = make_int2(0, NEG32);
+            if (ip < n) b = bl[ip + 1];
+            Hi[r] = h16_set(Hi[r], h, cv(b.x));
+            Ff[r] = h16_set(Ff[r], h, cv(b.y));
+          }
+          const int id = ip0 + h * NR;
+          diag = h16_set(diag, h, cv(id <= n ? bl[id].x : 0));
+        }
+        if (t == 0) {  // row above the task: H(ip0, j), E(ip0 + 1, j)
+          const int hx = FIRST ? 0 : he.x;
+          const int ex = FIRST ? -cop : he.y;
+          hin = h16_set(hin, 0, cv(hx));
+          ein = h16_set(ein, 0, cv(ex));
+        }
+        uint32_t e = ein;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const uint32_t hd = (r == 0) ? diag : Hi[r - 1];
+          const uint32_t sig = prmt(p0[r], p1[r], sel);
+          Ff[r] = __viaddmax_s16x2(Ff[r], NGE2, hop(Hi[r]));
+          const uint32_t df = __viaddmax_s16x2(hd, sig, Ff[r]);
+          Hq[r] = __vimax3_s16x2(df, e, Z);
+          e = __viaddmax_s16x2(e, NGE2, hop(df));
+        }
+        diag = hin;
+        Hbot = Hq[NR - 1];
+        Ebot = e;
+        if (t == 31 && act1)  // the task's last row (high half), column lc - 1 -> strip s+1
+          st_row(a.rowbuf + c_lo + lc, h16_get(Hq[NR - 1], 1) + base, h16_get(e, 1) + base, s + 1);
+        // local optimum: packed running maximum per half; strictly larger values only
+        uint32_t cm;
+        if (CHK) {
+          uint32_t mx = Hq[0];
+#pragma unroll
+          for (int r = 1; r + 1 < NR; r += 2) mx = __vimax3_s16x2(mx, Hq[r], Hq[r + 1]);
+          if ((NR % 2) == 0) mx = __vmaxs2(mx, Hq[NR - 1]);
+          mx = VS16::select_mask(mx, (act0 ? 1u : 0u) | (act1 ? 2u : 0u), VS16::splat(-32768));
+          cm = __vmaxs2(mx, best);
+        } else {
+          cm = __vimax3_s16x2(best, Hq[0], Hq[1]);
+#pragma unroll
+          for (int r = 2; r + 1 < NR; r += 2) cm = __vimax3_s16x2(cm, Hq[r], Hq[r + 1]);
+          if ((NR % 2) == 1) cm = __vmaxs2(cm, Hq[NR - 1]);
+        }
+        if (cm != best) {  // rare: resolve (value, first row, column) of the improved half(s)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int v = h16_get(cm, h);
+            if (v != h16_get(best, h)) {
+              int rr = NR - 1;
+#pragma unroll
+              for (int r = NR - 1; r >= 0; --r)
+                if (h16_get(Hq[r], h) == v) rr = r;
+              if (h == 0) { bv0 = v + base; bi0 = ip0 + rr + 1; bj0 = c_lo + lc + 1; }
+              else { bv1 = v + base; bi1 = ip0 + NR + rr + 1; bj1 = c_lo + lc; }
+            }
+          }
+          best = cm;
+        }
+        if (CHK && br && (lc == W - 1 || lc == W)) {  // half h's last column: right edge
+          const int h = lc - (W - 1);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const int ip = ip0 + h * NR + r;
+            if (ip < n) br[ip + 1] = make_int2(h16_get(Hq[r], h) + base, h16_get(Ff[r], h) + base);
+          }
+        }
+      };
+      // re-choose the base: warp max of H over the (all active) halves -> -margin
+      auto reframe = [&]() {
+        uint32_t mx = HA[0];
+#pragma unroll
+        for (int r = 1; r + 1 < NR; r += 2) mx = __vimax3_s16x2(mx, HA[r], HA[r + 1]);
+        if ((NR % 2) == 0) mx = __vmaxs2(mx, HA[NR - 1]);
+        const int ml = max(h16_get(mx, 0), h16_get(mx, 1));
+        const int M = __reduce_max_sync(0xffffffffu, ml);
+        const int dl = M + a.margin;
+        const uint32_t sub = VS16::splat(-dl);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          HA[r] = __vadd2(HA[r], sub);
+          Ff[r] = __vadd2(Ff[r], sub);
+        }
+        Hbot = __vadd2(Hbot, sub);
+        Ebot = __vadd2(Ebot, sub);
+        diag = __vadd2(diag, sub);
+        base += dl;
+        frame_consts();
+      };
+
+      const std::integral_constant<bool, true> ON{};
+      const std::integral_constant<bool, false> OFF{};
+      const int K = W + 63;
+      const int kA = min(K & ~1, 64);          // every virtual lane has reached column 0
+      const int kB = max(kA, (W - 1) & ~1);    // no virtual lane has reached column W-1
+      int k = 0;
+      auto maybe_refill = [&](int kk) -> bool {
+        if ((kk % PER) == 0 && kk > 0 && kk + PER < W) {
+          if (!refill(kk + PER, min(W, kk + 2 * PER))) return false;
+          __syncwarp();
+        }
+        return true;
+      };
+      for (; k < kA; k += 2) {
+        if (!maybe_refill(k)) return false;
+        step(ON, k, HA, HB);
+        step(ON, k + 1, HB, HA);
+      }
+      for (; k < kB; k += 2) {
+        if (!maybe_refill(k)) return false;
+        if ((k % PER) == 0) reframe();
+        step(OFF, k, HA, HB);
+        step(OFF, k + 1, HB, HA);
+      }
+      for (; k + 1 < K; k += 2) {
+        if (!maybe_refill(k)) return false;
+        step(ON, k, HA, HB);
+        step(ON, k + 1, HB, HA);
+      }
+      if (k < K) step(ON, k, HA, HB);
+      return true;
+    };
+    const bool done = (s == 0) ? sweep(std::true_type{}) : sweep(std::false_type{});
+    if (!done) break;
+    if (lkey_better(bv0, bi0, bj0, part.lv, part.li, part.lj)) { part.lv = bv0; part.li = bi0; part.lj = bj0; }
+    if (lkey_better(bv1, bi1, bj1, part.lv, part.li, part.lj)) { part.lv = bv1; part.li = bi1; part.lj = bj1; }
+    __syncwarp();
+    if (br) {
+      if (t == 0) {
+        __threadfence_system();
+        st_release_sys(&a.bflag[g + 1][s], 1);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int lv = __shfl_xor_sync(0xffffffffu, part.lv, o);
+    const int li = __shfl_xor_sync(0xffffffffu, part.li, o);
+    const int lj = __shfl_xor_sync(0xffffffffu, part.lj, o);
+    if (lkey_better(lv, li, lj, part.lv, part.li, part.lj)) { part.lv = lv; part.li = li; part.lj = lj; }
+  }
+  if (t == 0) a.parts[wg] = part;
+}
