@@ -1055,6 +1055,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
   if (n == "long_strips") { ctx->long_opt.virtual_strips = (int)value; return ANYSEQ_OK; }
   if (n == "long_profile") { ctx->long_opt.profile = (int)value; return ANYSEQ_OK; }
   if (n == "long_start_lag") { ctx->long_opt.start_lag = (int)value; return ANYSEQ_OK; }
+  if (n == "long_sleep_ns") { ctx->long_opt.sleep_ns = (int)value; return ANYSEQ_OK; }
   if (n == "long_narrow") { ctx->long_opt.narrow = (int)value; return ANYSEQ_OK; }
   if (n == "long_chunk_cols") { ctx->long_opt.chunk_cols = (int)value; return ANYSEQ_OK; }
   return fail(ctx, ANYSEQ_E_INVALID, "unknown option %s", name);

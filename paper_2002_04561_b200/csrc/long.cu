@@ -56,6 +56,7 @@ struct LongArgs {
   int32_t one;
   int32_t lag;
   int32_t keyed;  // local: 32 * (max score) fits in 31 bits -> packed (value, row) tracking
+  int32_t sleep_ns;  // long16: back-off of the row hand-off poll
   int32_t hopc;    // long16: packed -(G_o+G_e) for both halves, low-half borrow compensated
   int32_t neg16;   // long16: relative "-inf" (below every real relative value)
   int32_t margin;  // long16: the warp maximum is re-based to -margin
@@ -537,13 +538,16 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   // (d = G_o + G_e + max sigma bounds |H(x) - H(y)| per unit of Manhattan distance),
   // 2 bspan + margin (drift over 96 steps between re-basings) + slack inside the s16 range
   // above the relative -inf.
-  const int NR16 = opt.band_rows == 1024 ? 16 : 8;
   const int64_t d16 = (int64_t)P.go + P.ge + std::max(P.smax, 0);
-  const int64_t bspan16 = (int64_t)(64 * NR16 + 66) * d16;
   const int64_t margin16 = 100 * d16 + 16;
   const int NEG16C = -24576;
-  bool narrow = opt.narrow != 0 && P.kind == KLOCAL && P.gap == GAFFINE &&
-                2 * bspan16 + margin16 + 96 * d16 + P.go + P.ge + 256 < -NEG16C &&
+  auto fits16 = [&](int nr) {
+    return 2 * (int64_t)(64 * nr + 66) * d16 + margin16 + 96 * d16 + P.go + P.ge + 256 < -NEG16C;
+  };
+  int NR16 = opt.band_rows == 512 ? 8 : 16;  // 1024-row tasks by default, 512 if the range needs it
+  if (NR16 == 16 && !fits16(16)) NR16 = 8;
+  const int64_t bspan16 = (int64_t)(64 * NR16 + 66) * d16;
+  bool narrow = opt.narrow != 0 && P.kind == KLOCAL && P.gap == GAFFINE && fits16(NR16) &&
                 (int64_t)P.go + 2 * P.ge < 4096;
   if (narrow)
     for (uint64_t x = 0; x < m && narrow; ++x) narrow = (s[x] | 0x20) != 'n';
@@ -715,6 +719,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
       a.hopc = c == 0 ? 0 : (int32_t)((((uint32_t)(-c - 1) & 0xffffu) << 16) | (uint32_t)((65536 - c) & 0xffff));
     }
     a.neg16 = NEG16C;
+    a.sleep_ns = opt.sleep_ns;
     a.margin = (int32_t)margin16;
     a.bspan = (int32_t)bspan16;
     a.prof = nullptr;

@@ -16,6 +16,7 @@ struct LongOptions {
   int chunk_cols = 256;    // progress publication period (a release = full memory barrier)
   int start_lag = 0;       // columns the strip above must be ahead before a strip starts
   int profile = 0;         // print wait/task cycle counters to stderr
+  int sleep_ns = 64;       // long16: row hand-off poll back-off
   int narrow = 1;          // 1: 16-bit differential kernel where eligible (local affine)
 };
 

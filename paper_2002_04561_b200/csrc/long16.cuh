@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
     task = __shfl_sync(0xffffffffu, task, 0);
     if (task >= a.S * a.g_count) break;
     if (*(volatile int*)a.abort_flag) break;
+    const long long task_t0 = (a.prof && t == 0) ? clock64() : 0;
     const int s = task % a.S;
     const int g = a.g_first + task / a.S;
     const int c_lo = a.cb[g], c_hi = a.cb[g + 1], W = c_hi - c_lo;
@@ -100,13 +101,15 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
       int4 v = mine ? ld_row(src) : make_int4(0, s, 0, s);
       long long spins = 0;
       while (!__all_sync(0xffffffffu, v.y == s && v.w == s)) {
-        __nanosleep(64);
+        const long long t0 = (a.prof && t == 0) ? clock64() : 0;
+        __nanosleep(a.sleep_ns);
         if (v.y != s || v.w != s) v = ld_row(src);
         if ((++spins & 255) == 0 &&
             __any_sync(0xffffffffu, spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
           if (t == 0) atomicExch(a.abort_flag, 1);
           return false;
         }
+        if (a.prof && t == 0) atomicAdd(&a.prof[0], (unsigned long long)(clock64() - t0));
       }
       if (mine) ring_he[wb][c & (RING - 1)] = make_int2(v.x, v.z);
       return true;
@@ -280,6 +283,10 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
     if (!done) break;
     if (lkey_better(bv0, bi0, bj0, part.lv, part.li, part.lj)) { part.lv = bv0; part.li = bi0; part.lj = bj0; }
     if (lkey_better(bv1, bi1, bj1, part.lv, part.li, part.lj)) { part.lv = bv1; part.li = bi1; part.lj = bj1; }
+    if (a.prof && t == 0) {
+      atomicAdd(&a.prof[1], (unsigned long long)(clock64() - task_t0));
+      atomicAdd(&a.prof[2], 1ull);
+    }
     __syncwarp();
     if (br) {
       if (t == 0) {

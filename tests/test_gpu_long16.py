@@ -47,7 +47,7 @@ def _run(ctx, q, s, rows=0, strips=0, chunk=64, narrow=1, **kw):
     return (r["score"], r["q_end"], r["s_end"]), used
 
 
-@pytest.mark.parametrize("rows", [0, 1024])
+@pytest.mark.parametrize("rows", [0, 512])
 @pytest.mark.parametrize("strips", [1, 3])
 def test_long16_random_windows(ctx, rows, strips):
     """Unrelated i.i.d. sequences: small scores, the local floor active almost everywhere;
@@ -61,7 +61,7 @@ def test_long16_random_windows(ctx, rows, strips):
         assert got == _orc(q, s), (n, m)
 
 
-@pytest.mark.parametrize("rows", [0, 1024])
+@pytest.mark.parametrize("rows", [0, 512])
 def test_long16_mutated_beyond_16bit(ctx, rows):
     """C4 variant (a) shape, 40 kbp: optimum ~ 78k (far outside s16) -- the per-warp base
     and its re-basing carry the absolute value; strips exercise the boundary column."""
@@ -78,7 +78,7 @@ def test_long16_identical_closed_form(ctx):
     """G2 = G1: local score 2n at (n, n) (closed form), 300 kbp."""
     from synth import c4_genomes
     g1, g2 = c4_genomes(300_000, "c", seed=5)
-    for rows, strips in ((0, 1), (0, 3), (1024, 2)):
+    for rows, strips in ((0, 1), (0, 3), (512, 2)):
         got, used = _run(ctx, g1, g2, rows=rows, strips=strips)
         assert used == 1 and got == (600_000, 300_000, 300_000)
 
@@ -91,7 +91,7 @@ def test_long16_equals_s32(ctx):
         g1, g2 = c4_genomes(300_000, variant, seed=6)
         ref, used = _run(ctx, g1, g2, narrow=0)
         assert used == 0
-        for rows, strips in ((0, 0), (1024, 0), (0, 5)):
+        for rows, strips in ((0, 0), (512, 0), (0, 5)):
             got, used = _run(ctx, g1, g2, rows=rows, strips=strips)
             assert used == 1 and got == ref, (variant, rows, strips)
 
