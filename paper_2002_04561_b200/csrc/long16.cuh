@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
   constexpr int PER = 32;
   __shared__ int2 ring_he[4][RING];
   __shared__ uint16_t ring_sel[4][RING];  // subject code c of a column as c * 0x11
+  __shared__ int2 ring_out[4][64];        // the task's last row (H, E) awaiting publication
   const int t = threadIdx.x & 31;
   const int wb = threadIdx.x >> 5;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -165,11 +166,13 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
           const int id = ip0 + h * NR;
           diag = h16_set(diag, h, cv(id <= n ? bl[id].x : 0));
         }
-        if (t == 0) {  // row above the task: H(ip0, j), E(ip0 + 1, j)
+        {  // lane 0's low half: the row above the task, H(ip0, j) and E(ip0 + 1, j) (no branch)
           const int hx = FIRST ? 0 : he.x;
           const int ex = FIRST ? -cop : he.y;
-          hin = h16_set(hin, 0, cv(hx));
-          ein = h16_set(ein, 0, cv(ex));
+          const uint32_t h0 = prmt((uint32_t)cv(hx), hin, 0x7610u);
+          const uint32_t e0 = prmt((uint32_t)cv(ex), ein, 0x7610u);
+          hin = t == 0 ? h0 : hin;
+          ein = t == 0 ? e0 : ein;
         }
         uint32_t e = ein;
 #pragma unroll
@@ -184,8 +187,9 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
         diag = hin;
         Hbot = Hq[NR - 1];
         Ebot = e;
-        if (t == 31 && act1)  // the task's last row (high half), column lc - 1 -> strip s+1
-          st_row(a.rowbuf + c_lo + lc, h16_get(Hq[NR - 1], 1) + base, h16_get(e, 1) + base, s + 1);
+        if (t == 31 && act1)  // the task's last row (high half), column lc - 1: staged in
+          ring_out[wb][(lc - 1) & 63] =  // shared memory, published 32 columns at a time
+              make_int2(h16_get(Hq[NR - 1], 1) + base, h16_get(e, 1) + base);
         // local optimum: packed running maximum per half; strictly larger values only
         uint32_t cm;
         if (CHK) {
@@ -247,6 +251,18 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
         frame_consts();
       };
 
+      // publish staged columns [flushed, c_end) (at most 32) to the row buffer for strip s+1
+      int flushed = 0;
+      auto flush = [&](int c_end) {
+        __syncwarp();
+        const int c = flushed + t;
+        if (c < c_end) {
+          const int2 v = ring_out[wb][c & 63];
+          st_row(a.rowbuf + c_lo + c + 1, v.x, v.y, s + 1);
+        }
+        flushed = c_end;
+        __syncwarp();
+      };
       const std::integral_constant<bool, true> ON{};
       const std::integral_constant<bool, false> OFF{};
       const int K = W + 63;
@@ -267,16 +283,21 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
       }
       for (; k < kB; k += 2) {
         if (!maybe_refill(k)) return false;
-        if ((k % PER) == 0) reframe();
+        if ((k % PER) == 0) {
+          reframe();
+          flush(min(W, k - 63));  // columns <= k - 64 are complete
+        }
         step(OFF, k, HA, HB);
         step(OFF, k + 1, HB, HA);
       }
       for (; k + 1 < K; k += 2) {
         if (!maybe_refill(k)) return false;
+        if ((k % PER) == 0 && k >= 64) flush(min(W, k - 63));
         step(ON, k, HA, HB);
         step(ON, k + 1, HB, HA);
       }
       if (k < K) step(ON, k, HA, HB);
+      while (flushed < W) flush(min(W, flushed + 32));
       return true;
     };
     const bool done = (s == 0) ? sweep(std::true_type{}) : sweep(std::false_type{});
