@@ -544,8 +544,8 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   auto fits16 = [&](int nr) {
     return 2 * (int64_t)(64 * nr + 66) * d16 + margin16 + 96 * d16 + P.go + P.ge + 256 < -NEG16C;
   };
-  int NR16 = opt.band_rows == 512 ? 8 : 16;  // 1024-row tasks by default, 512 if the range needs it
-  if (NR16 == 16 && !fits16(16)) NR16 = 8;
+  int NR16 = opt.band_rows == 512 ? 8 : opt.band_rows == 768 ? 12 : 16;  // 1024-row tasks by
+  if (NR16 > 8 && !fits16(NR16)) NR16 = 8;  // default, 512 if the range needs it
   const int64_t bspan16 = (int64_t)(64 * NR16 + 66) * d16;
   bool narrow = opt.narrow != 0 && P.kind == KLOCAL && P.gap == GAFFINE && fits16(NR16) &&
                 (int64_t)P.go + 2 * P.ge < 4096;
@@ -553,7 +553,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     for (uint64_t x = 0; x < m && narrow; ++x) narrow = (s[x] | 0x20) != 'n';
   if (narrow) {
     HS = 64 * NR16;
-    fn = NR16 == 16 ? long16_kernel<16> : long16_kernel<8>;
+    fn = NR16 == 16 ? long16_kernel<16> : NR16 == 12 ? long16_kernel<12> : long16_kernel<8>;
   }
   out->narrow = narrow;
   const int S = (int)((n + HS - 1) / HS);

@@ -36,7 +36,7 @@ __device__ __forceinline__ uint32_t h16_pack(int lo, int hi) {
 }
 
 template <int NR>
-__global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
+__global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs a) {
   constexpr int HS = 64 * NR;  // rows per task: 32 lanes x 2 halves x NR
   constexpr int RING = 256;
   constexpr int PER = 32;
@@ -84,13 +84,13 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
       if (!warp_wait<true>(&a.bflag[g][s], 1, a)) break;
       if (s > 0 && !warp_wait<true>(&a.bflag[g][s - 1], 1, a)) break;
     }
-    uint32_t p0[NR], p1[NR], HA[NR], HB[NR], Ff[NR];
+    uint32_t p0[NR], p1[NR], H[NR], Ff[NR];  // H: the lane's rows at its last column (in place)
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const int iA = ip0 + r, iB = ip0 + NR + r;
       p0[r] = iA < n ? prof4(a.P, a.qc[iA]) : 0u;  // sigma rows of the low half
       p1[r] = iB < n ? prof4(a.P, a.qc[iB]) : 0u;  // ... and of the high half
-      HA[r] = HB[r] = VS16::splat(NEGc);
+      H[r] = VS16::splat(NEGc);
       Ff[r] = VS16::splat(NEGc);
     }
     auto refill = [&](int c0, int c1) -> bool {
@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
       uint32_t cur_nx = ring_sel[wb][(0 - 2 * t) & (RING - 1)];
       uint32_t prev = 0;
       int2 he_nx = ring_he[wb][0];
-      auto step = [&](auto chk, const int k, uint32_t (&Hi)[NR], uint32_t (&Hq)[NR]) {
+      auto step = [&](auto chk, const int k) {
+        uint32_t (&Hi)[NR] = H;
+        uint32_t (&Hq)[NR] = H;
         constexpr bool CHK = decltype(chk)::value;
         const uint32_t hs = __shfl_up_sync(0xffffffffu, Hbot, 1);
         const uint32_t es = __shfl_up_sync(0xffffffffu, Ebot, 1);
@@ -175,14 +177,16 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
           ein = t == 0 ? e0 : ein;
         }
         uint32_t e = ein;
+        uint32_t hd = diag;
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          const uint32_t hd = (r == 0) ? diag : Hi[r - 1];
+        for (int r = 0; r < NR; ++r) {  // in place: row r's previous column is row r+1's diagonal
+          const uint32_t old = Hi[r];
           const uint32_t sig = prmt(p0[r], p1[r], sel);
-          Ff[r] = __viaddmax_s16x2(Ff[r], NGE2, hop(Hi[r]));
+          Ff[r] = __viaddmax_s16x2(Ff[r], NGE2, hop(old));
           const uint32_t df = __viaddmax_s16x2(hd, sig, Ff[r]);
           Hq[r] = __vimax3_s16x2(df, e, Z);
           e = __viaddmax_s16x2(e, NGE2, hop(df));
+          hd = old;
         }
         diag = hin;
         Hbot = Hq[NR - 1];
@@ -231,17 +235,17 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
       };
       // re-choose the base: warp max of H over the (all active) halves -> -margin
       auto reframe = [&]() {
-        uint32_t mx = HA[0];
+        uint32_t mx = H[0];
 #pragma unroll
-        for (int r = 1; r + 1 < NR; r += 2) mx = __vimax3_s16x2(mx, HA[r], HA[r + 1]);
-        if ((NR % 2) == 0) mx = __vmaxs2(mx, HA[NR - 1]);
+        for (int r = 1; r + 1 < NR; r += 2) mx = __vimax3_s16x2(mx, H[r], H[r + 1]);
+        if ((NR % 2) == 0) mx = __vmaxs2(mx, H[NR - 1]);
         const int ml = max(h16_get(mx, 0), h16_get(mx, 1));
         const int M = __reduce_max_sync(0xffffffffu, ml);
         const int dl = M + a.margin;
         const uint32_t sub = VS16::splat(-dl);
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
-          HA[r] = __vadd2(HA[r], sub);
+          H[r] = __vadd2(H[r], sub);
           Ff[r] = __vadd2(Ff[r], sub);
         }
         Hbot = __vadd2(Hbot, sub);
@@ -278,8 +282,8 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
       };
       for (; k < kA; k += 2) {
         if (!maybe_refill(k)) return false;
-        step(ON, k, HA, HB);
-        step(ON, k + 1, HB, HA);
+        step(ON, k);
+        step(ON, k + 1);
       }
       for (; k < kB; k += 2) {
         if (!maybe_refill(k)) return false;
@@ -287,16 +291,16 @@ __global__ void __launch_bounds__(128) long16_kernel(LongArgs a) {
           reframe();
           flush(min(W, k - 63));  // columns <= k - 64 are complete
         }
-        step(OFF, k, HA, HB);
-        step(OFF, k + 1, HB, HA);
+        step(OFF, k);
+        step(OFF, k + 1);
       }
       for (; k + 1 < K; k += 2) {
         if (!maybe_refill(k)) return false;
         if ((k % PER) == 0 && k >= 64) flush(min(W, k - 63));
-        step(ON, k, HA, HB);
-        step(ON, k + 1, HB, HA);
+        step(ON, k);
+        step(ON, k + 1);
       }
-      if (k < K) step(ON, k, HA, HB);
+      if (k < K) step(ON, k);
       while (flushed < W) flush(min(W, flushed + 32));
       return true;
     };

@@ -8,7 +8,7 @@ variant = sys.argv[2] if len(sys.argv) > 2 else "a"
 g1, g2 = synth.c4_genomes(n, variant, seed=4)
 ctx = A.Context([0])
 sch = A.Scheme("local", "affine", 2, -1, 5, 1)
-for narrow, rows in ((0, 0), (1, 512), (1, 0)):
+for narrow, rows in ((0, 0), (1, 512), (1, 768), (1, 0)):
     ctx.set_option("long_narrow", narrow)
     ctx.set_option("long_band_rows", rows)
     r = ctx.align_long(sch, g1, g2)
