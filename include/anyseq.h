@@ -145,7 +145,9 @@ uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx);
    interval from the first start to the last end).  anyseq_get_stat reads "fill_ms"
    (summed device time of fill intervals), "fill_launches", "walk_ms"; anyseq_reset_stats
    clears them.  "timing" = 2 also prints a per-chunk event timeline of the host API to
-   stderr (debug).  Returns ANYSEQ_E_INVALID for unknown names. */
+   stderr (debug).  After anyseq_align_long: "long_kernel_ms" (device time of the long
+   kernel, max over devices) and "long_narrow" (1 if the 16-bit differential kernel ran).
+   Returns ANYSEQ_E_INVALID for unknown names. */
 anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value);
 anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
 
@@ -159,6 +161,12 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
                          round count; > 0 also exercises the multi-GPU boundary protocol)
      "long_blocks"       long pairs: cap on the persistent grid (0 = occupancy)
      "long_profile"      long pairs: print wait / task cycle counters to stderr
+     "long_narrow"       long pairs: 1 (default) runs local affine alignments whose scheme
+                         passes the range guard and whose subject has no N on the 16-bit
+                         differential kernel; 0 forces the 32-bit kernel
+     "long_band_rows"    long pairs, rows per warp task: 32-bit kernel 512 (default) or
+                         384; 16-bit kernel 1024 (default), 768 or 512
+     "long_sleep_ns"     long pairs (16-bit kernel): back-off of the row hand-off poll
      "timing"            see above */
 anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value);
 
