@@ -201,6 +201,36 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def long_pair_leg(ctx, A, n, n_sm, f_mhz):
+    """The metric's second half: C4 (two n-bp genomes, G2 = mutated copy of G1, local affine
+    5/1, +2/-1, score-only) through anyseq_align_long on this GPU, once (one call is ~9 s at
+    5 Mbp).  GCUPS = n*m / kernel time (CUDA events around the long kernel); wall includes
+    the upload and pack of both genomes.  Not a bench step: the headline value is C2."""
+    from synth import c4_genomes
+    g1, g2 = c4_genomes(n, "a", seed=4)
+    sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+    t0 = time.perf_counter()
+    r = ctx.align_long(sch, g1, g2)
+    wall = time.perf_counter() - t0
+    ms = ctx.stat("long_kernel_ms")
+    narrow = int(ctx.stat("long_narrow"))
+    cells = len(g1) * len(g2)
+    gcups = cells / (ms / 1e3) / 1e9
+    # DESIGN.md 5.4b: 5.5 ALU ops per two cells at 64 lane-ops/clk/SM (16-bit kernel);
+    # 5 ALU ops per cell (s32 kernel, 5.4)
+    cpc = 64 * 2 / 5.5 if narrow else 64 / 5.0
+    peak = n_sm * f_mhz * 1e6 * cpc / 1e9
+    return {"workload": f"C4: {len(g1)} bp x {len(g2)} bp (G2 = mutated copy of G1), local affine "
+                        "open 5 / extend 1, match 2 / mismatch -1, score-only, 1 GPU",
+            "value": round(gcups, 1), "unit": "GCUPS", "kernel_ms": round(ms, 1),
+            "wall_ms": round(wall * 1e3, 1),
+            "kernel": "long16_kernel<16> (16-bit differential)" if narrow else "long_kernel<LOCAL,AFFINE,16> (s32)",
+            "roofline": {"bound": "alu", "achieved": round(gcups, 1), "peak": round(peak, 1),
+                         "unit": "GCUPS", "frac": round(gcups / peak, 4),
+                         "peak_basis": f"{n_sm} SM x {f_mhz:.0f} MHz (C2 median under load) x {cpc:.2f} cells/clk/SM"},
+            "score": r["score"], "end": [r["q_end"], r["s_end"]]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -210,6 +240,8 @@ def main():
     ap.add_argument("--pairs", type=int, default=NUM_PAIRS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=3.0)
+    ap.add_argument("--long-bp", type=int, default=5_000_000,
+                    help="C4 long pair (second half of the metric) genome length; 0 skips it")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -338,6 +370,8 @@ def main():
             "parity_sample_ok": bool(parity)}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_baseline(qm, sm)
+    if rank == 0 and ws == 1 and args.long_bp > 0:
+        line["long_pair"] = long_pair_leg(ctx, A, args.long_bp, n_sm, f_mhz)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
