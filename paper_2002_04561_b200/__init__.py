@@ -61,6 +61,8 @@ _sig = {
     "anyseq_align_batch_device": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "anyseq_traceback": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _u64, _vp]),
     "anyseq_align_long": (ctypes.c_int, [_vp, _vp, ctypes.c_char_p, _u64, ctypes.c_char_p, _u64, _vp]),
+    "anyseq_traceback_long": (ctypes.c_int, [_vp, _vp, ctypes.c_char_p, _u64, ctypes.c_char_p, _u64,
+                                             _vp, _vp, _u64, _vp]),
     "anyseq_sync": (ctypes.c_int, [_vp]),
     "anyseq_kernel_launches": (ctypes.c_uint64, [_vp]),
     "anyseq_set_option": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64]),
@@ -240,6 +242,27 @@ class Context:
                                            out.ctypes.data))
         r = out[0]
         return {"score": int(r["score"]), "q_end": int(r["q_end"]), "s_end": int(r["s_end"])}
+
+    def traceback_long(self, scheme: Scheme, q, s, cigar_capacity: int | None = None) -> dict:
+        """Linear-space long-pair traceback (anyseq_traceback_long): score, begin/end cells
+        and the CIGAR as (length, op) tuples."""
+        q = bytes(q) if not isinstance(q, bytes) else q
+        s = bytes(s) if not isinstance(s, bytes) else s
+        out = np.zeros(1, dtype=ALIGNMENT_DTYPE)
+        cap = len(q) + len(s) + 1 if cigar_capacity is None else cigar_capacity
+        cig = np.empty(max(cap, 1), dtype=np.uint32)
+        used = ctypes.c_uint64(0)
+        p = scheme.c()
+        st = _lib.anyseq_traceback_long(self._h, ctypes.byref(p), q, len(q), s, len(s),
+                                        out.ctypes.data, cig.ctypes.data, cap, ctypes.byref(used))
+        if st != 0:
+            err = AnyseqError(st, _lib.anyseq_last_error(self._h).decode())
+            err.cigar_used = int(used.value)
+            raise err
+        r = out[0]
+        return {"score": int(r["score"]), "q_begin": int(r["q_begin"]), "s_begin": int(r["s_begin"]),
+                "q_end": int(r["q_end"]), "s_end": int(r["s_end"]),
+                "cigar": decode_cigar(cig[: used.value])}
 
     def align_batch_device(self, scheme: Scheme, d_q, d_q_off, d_s, d_s_off, d_scores,
                            d_ends=None, stream=None):

@@ -20,6 +20,7 @@
 #include "../../include/anyseq.h"
 #include "kernels.h"
 #include "long.h"
+#include "hirschberg.h"
 
 using namespace anyseq;
 
@@ -868,6 +869,217 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
   return ANYSEQ_OK;
 }
 
+// ---- linear-space long-pair traceback: Hirschberg's divide and conquer.
+// A problem (i0,i1) x (j0,j1) with more than kLeafCells cells is cut at mid = (i0+i1)/2:
+// a forward last-row pass over q[i0,mid) x s[j0,j1) and a reverse pass over q[mid,i1) x
+// s[j0,j1) (both on the GPU, all problems of one recursion level in one launch) give
+// F(j) = H(mid, j) and B(j) = the best score of q[mid,i1) x s[j0+j,j1); the optimal path
+// crosses row mid at the smallest j maximising F(j) + B(m'-j).  Leaves (in path order, so
+// their q and s ranges tile the alignment) run as ONE batched global traceback
+// (run_host_batch, the a4/a5 kernels); their CIGARs are concatenated.
+// Linear gaps only: an affine split must carry the gap state across the cut
+// (Myers-Miller), which the leaf traceback does not take as a boundary condition.
+struct HbNode {
+  int64_t i0, i1, j0, j1;
+};
+
+anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, const char* q,
+                                 uint64_t n, const char* s, uint64_t m, anyseq_alignment* out,
+                                 uint32_t* cigar, uint64_t cap, uint64_t* used) {
+  Device& D = ctx->devs[0];
+  CK(cudaSetDevice(D.id));
+  cudaStream_t st = D.stream;
+  const DevParams dp = dev_params(prm);
+  LrParams P;
+  P.g = prm->gap_extend;
+  for (int a = 0; a < 5; ++a)
+    for (int b = 0; b < 5; ++b)
+      P.sig[5 * a + b] = (int8_t)(prm->has_subst ? prm->subst[5 * a + b]
+                                                 : ((a == b && a < 4) ? prm->match : prm->mismatch));
+  (void)dp;
+  // range guard: |H| <= (n + m) * max(g, |sigma|) must stay inside int32
+  int64_t amax = P.g;
+  for (int k = 0; k < 25; ++k) amax = std::max<int64_t>(amax, std::abs((int)P.sig[k]));
+  if ((int64_t)(n + m + 2) * amax >= (1ll << 30))
+    return fail(ctx, ANYSEQ_E_UNSUPPORTED, "score range of the long traceback exceeds int32");
+  DevBuf asc, codes, bad, taskbuf, rows, best;
+  struct Guard {
+    DevBuf* b[6];
+    ~Guard() { for (auto* x : b) x->release(); }
+  } guard{{&asc, &codes, &bad, &taskbuf, &rows, &best}};
+  CK(asc.ensure(n + m + 16));
+  CK(codes.ensure(n + m + 16));
+  CK(bad.ensure(sizeof(int)));
+  CK(best.ensure(4 * sizeof(int32_t)));
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  if (n) CK(cudaMemcpyAsync(asc.as<char>(), q, n, cudaMemcpyHostToDevice, st));
+  if (m) CK(cudaMemcpyAsync(asc.as<char>() + n, s, m, cudaMemcpyHostToDevice, st));
+  launch_encode_codes(asc.as<char>(), codes.as<uint8_t>(), n + m, bad.as<int>(), st);
+  ctx->launches += n + m ? 1 : 0;
+  int h_bad = 0;
+  CK(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h_bad) return fail(ctx, ANYSEQ_E_BADSEQ, "long traceback: byte outside ACGTNacgtn");
+  const uint8_t* dq = codes.as<uint8_t>();
+  const uint8_t* ds = codes.as<uint8_t>() + n;
+
+  // region of the alignment: the whole matrix (global) or [begin, end) of a local optimum
+  int64_t qb = 0, sb = 0, qe = (int64_t)n, se = (int64_t)m;
+  int32_t want = 0;
+  if (prm->kind == ANYSEQ_LOCAL) {
+    anyseq_alignment e;
+    anyseq_status r = anyseq_align_long(ctx, prm, q, n, s, m, &e);
+    if (r != ANYSEQ_OK) return r;
+    want = e.score;
+    qe = e.q_end;
+    se = e.s_end;
+    qb = qe;
+    sb = se;
+    if (e.score > 0) {
+      // anchored reverse pass over the prefixes ending at the end cell: its optimum is the
+      // score of the best alignment ending there (= the local optimum), its cell the begin
+      CK(cudaSetDevice(D.id));
+      CK(rows.ensure((se + 1) * sizeof(int32_t)));
+      LrTask t{dq, ds, (int32_t)qe, (int32_t)se, 1, 1, rows.as<int32_t>(), best.as<int32_t>()};
+      CK(taskbuf.ensure(sizeof(LrTask)));
+      CK(cudaMemcpyAsync(taskbuf.p, &t, sizeof(t), cudaMemcpyHostToDevice, st));
+      launch_lastrow_anchored(taskbuf.as<LrTask>(), 1, P, st);
+      ctx->launches += 1;
+      int32_t hb[3];
+      CK(cudaMemcpyAsync(hb, best.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      CK(cudaGetLastError());
+      if (hb[0] != e.score)
+        return fail(ctx, ANYSEQ_E_CUDA, "anchored pass optimum %d != local optimum %d", hb[0],
+                    e.score);
+      qb = qe - hb[1];
+      sb = se - hb[2];
+    }
+  }
+
+  // Hirschberg levels; nodes stay in path order
+  const int64_t kLeafCells = 1 << 22;
+  std::vector<HbNode> nodes{{qb, qe, sb, se}};
+  std::vector<char> leaf(1, 0);
+  std::vector<int32_t> hrows;
+  for (;;) {
+    std::vector<LrTask> tasks;
+    std::vector<size_t> split_nodes, row_off;
+    size_t total = 0;
+    for (size_t k = 0; k < nodes.size(); ++k) {
+      if (leaf[k]) continue;
+      const HbNode& x = nodes[k];
+      const int64_t r = x.i1 - x.i0, c = x.j1 - x.j0;
+      if (r <= 1 || c <= 1 || r * c <= kLeafCells) {
+        leaf[k] = 1;
+        continue;
+      }
+      const int64_t mid = (x.i0 + x.i1) / 2;
+      split_nodes.push_back(k);
+      row_off.push_back(total);
+      tasks.push_back(LrTask{dq + x.i0, ds + x.j0, (int32_t)(mid - x.i0), (int32_t)c, 0, 0,
+                             nullptr, nullptr});
+      tasks.push_back(LrTask{dq + mid, ds + x.j0, (int32_t)(x.i1 - mid), (int32_t)c, 1, 0,
+                             nullptr, nullptr});
+      total += 2 * (size_t)(c + 1);
+    }
+    if (tasks.empty()) break;
+    CK(rows.ensure(total * sizeof(int32_t)));
+    for (size_t t = 0; t < split_nodes.size(); ++t) {
+      const int64_t c = nodes[split_nodes[t]].j1 - nodes[split_nodes[t]].j0;
+      tasks[2 * t].row = rows.as<int32_t>() + row_off[t];
+      tasks[2 * t + 1].row = rows.as<int32_t>() + row_off[t] + c + 1;
+    }
+    CK(taskbuf.ensure(tasks.size() * sizeof(LrTask)));
+    CK(cudaMemcpyAsync(taskbuf.p, tasks.data(), tasks.size() * sizeof(LrTask),
+                       cudaMemcpyHostToDevice, st));
+    launch_lastrow(taskbuf.as<LrTask>(), (int)tasks.size(), P, st);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    hrows.resize(total);
+    CK(cudaMemcpyAsync(hrows.data(), rows.p, total * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<HbNode> nn;
+    std::vector<char> nl;
+    size_t t = 0;
+    for (size_t k = 0; k < nodes.size(); ++k) {
+      if (t < split_nodes.size() && split_nodes[t] == k) {
+        const HbNode x = nodes[k];
+        const int64_t c = x.j1 - x.j0, mid = (x.i0 + x.i1) / 2;
+        const int32_t* F = hrows.data() + row_off[t];
+        const int32_t* B = F + c + 1;
+        const int64_t top = mid - x.i0, bot = x.i1 - mid;
+        int64_t bj = 0, bv = INT64_MIN;
+        for (int64_t j = 0; j <= c; ++j) {
+          const int64_t f = j == 0 ? -top * (int64_t)P.g : F[j];
+          const int64_t b = j == c ? -bot * (int64_t)P.g : B[c - j];
+          if (f + b > bv) {
+            bv = f + b;
+            bj = j;
+          }
+        }
+        nn.push_back({x.i0, mid, x.j0, x.j0 + bj});
+        nn.push_back({mid, x.i1, x.j0 + bj, x.j1});
+        nl.push_back(0);
+        nl.push_back(0);
+        ++t;
+      } else {
+        nn.push_back(nodes[k]);
+        nl.push_back(leaf[k]);
+      }
+    }
+    nodes.swap(nn);
+    leaf.swap(nl);
+  }
+
+  // leaves: one batched global traceback over consecutive q / s ranges
+  const uint64_t L = nodes.size();
+  std::vector<uint64_t> qo(L + 1), so(L + 1);
+  for (uint64_t k = 0; k < L; ++k) {
+    qo[k] = nodes[k].i0;
+    so[k] = nodes[k].j0;
+  }
+  qo[L] = nodes[L - 1].i1;
+  so[L] = nodes[L - 1].j1;
+  anyseq_batch lb{q, qo.data(), s, so.data(), L};
+  anyseq_params gp = *prm;
+  gp.kind = ANYSEQ_GLOBAL;
+  std::vector<anyseq_alignment> la(L);
+  const uint64_t lcap = (uint64_t)(qe - qb) + (uint64_t)(se - sb) + L;
+  std::vector<uint32_t> lc(std::max<uint64_t>(lcap, 1));
+  std::vector<int32_t> lsc(L);
+  uint64_t lused = 0;
+  anyseq_status r = run_host_batch(ctx, &gp, &lb, 1, lsc.data(), la.data(), lc.data(), lcap, &lused);
+  if (r != ANYSEQ_OK) return r;
+  int64_t score = 0;
+  std::vector<uint32_t> ops;
+  for (uint64_t k = 0; k < L; ++k) {
+    score += la[k].score;
+    for (uint32_t w = 0; w < la[k].cigar_len; ++w) {
+      const uint32_t word = lc[la[k].cigar_offset + w];
+      if (!ops.empty() && (ops.back() & 15) == (word & 15)) ops.back() += word & ~15u;
+      else ops.push_back(word);
+    }
+  }
+  if (prm->kind == ANYSEQ_LOCAL && score != want)
+    return fail(ctx, ANYSEQ_E_CUDA, "long traceback: path score %lld != optimum %d",
+                (long long)score, want);
+  if (used) *used = ops.size();
+  if (ops.size() > cap)
+    return fail(ctx, ANYSEQ_E_CAPACITY, "cigar needs %llu words, capacity %llu",
+                (unsigned long long)ops.size(), (unsigned long long)cap);
+  if (!ops.empty()) memcpy(cigar, ops.data(), ops.size() * sizeof(uint32_t));
+  memset(out, 0, sizeof(*out));
+  out->score = (int32_t)score;
+  out->q_begin = qb;
+  out->s_begin = sb;
+  out->q_end = qe;
+  out->s_end = se;
+  out->cigar_offset = 0;
+  out->cigar_len = (uint32_t)ops.size();
+  return ANYSEQ_OK;
+}
+
 }  // namespace
 
 // =========================================================================== C-ABI
@@ -1091,6 +1303,25 @@ anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, co
   out->q_end = out->q_begin = r.end_i;
   out->s_end = out->s_begin = r.end_j;
   return ANYSEQ_OK;
+}
+
+anyseq_status anyseq_traceback_long(anyseq_ctx* ctx, const anyseq_params* params, const char* q,
+                                    uint64_t n, const char* s, uint64_t m, anyseq_alignment* out,
+                                    uint32_t* cigar, uint64_t cigar_capacity,
+                                    uint64_t* cigar_used) {
+  if (!ctx) return ANYSEQ_E_INVALID;
+  anyseq_status st = validate_params(ctx, params);
+  if (st != ANYSEQ_OK) return st;
+  if (cigar_used) *cigar_used = 0;
+  if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
+  if (!cigar && cigar_capacity) return fail(ctx, ANYSEQ_E_INVALID, "cigar is NULL");
+  if ((n && !q) || (m && !s)) return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
+  if (n >= (1ull << 31) || m >= (1ull << 31))
+    return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long sequences must be shorter than 2^31");
+  if (params->gap != ANYSEQ_GAP_LINEAR || params->kind == ANYSEQ_SEMIGLOBAL)
+    return fail(ctx, ANYSEQ_E_UNSUPPORTED,
+                "long traceback: global and local alignments with linear gaps only");
+  return run_traceback_long(ctx, params, q, n, s, m, out, cigar, cigar_capacity, cigar_used);
 }
 
 anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) {

@@ -1,0 +1,137 @@
+// hirschberg.cu -- device passes of the linear-space long-pair traceback.
+//
+// Each CTA runs one last-row pass (hirschberg.h): threads own R consecutive rows of a
+// band of NT*R rows and sweep the columns with a skew of one step per thread; the bottom
+// row of a thread is handed to the next thread through a double-buffered shared-memory
+// slot (one barrier per step), and band to band through row[] in global memory, updated
+// in place (the band's thread 0 reads column j at step j-1, before the last thread of the
+// band overwrites it at step j+NT-2).  Recurrence: Eq. (1) with nu = -inf and the linear
+// gaps of Eqs. (2)-(3), H(i,0) = -i*g, H(0,j) = -j*g.  32-bit scores.
+#include "hirschberg.h"
+
+namespace {
+
+constexpr int NT = 256;  // threads per CTA
+constexpr int R = 16;    // rows per thread
+
+__global__ void encode_kernel(const char* __restrict__ ascii, uint8_t* __restrict__ codes,
+                              uint64_t len, int* bad) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < len;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned c = (unsigned char)ascii[k] & 0xDFu;  // upper case
+    uint8_t v = c == 'A' ? 0 : c == 'C' ? 1 : c == 'G' ? 2 : c == 'T' ? 3 : c == 'N' ? 4 : 0xff;
+    if (v == 0xff) {
+      *bad = 1;
+      v = 4;
+    }
+    codes[k] = v;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NT) lastrow_kernel(const LrTask* __restrict__ tasks,
+                                                     LrParams P) {
+  __shared__ int32_t xch[2][NT];
+  __shared__ int32_t ssig[25];
+  __shared__ int32_t rs[NT], ri[NT], rj[NT];
+  const LrTask T = tasks[blockIdx.x];
+  const int t = threadIdx.x;
+  if (t < 25) ssig[t] = P.sig[t];
+  __syncthreads();
+  const int g = P.g, n1 = T.n1, m1 = T.m1;
+  // running optimum of MODE 1: cell (0,0) holds 0 and beats every other border cell
+  int bs = 0, bi = 0, bj = 0;
+  for (int base = 0; base < n1; base += NT * R) {
+    const bool last_pass = base + NT * R >= n1;
+    const int i0 = base + t * R + 1;  // first row of this thread (1-based)
+    int ra[R], h[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = i0 + k;
+      ra[k] = i <= n1 ? 5 * (int)(T.rev ? T.a[n1 - i] : T.a[i - 1]) : 0;
+      h[k] = -i * g;  // H(i, 0)
+    }
+    int updiag = -(i0 - 1) * g;  // H(i0-1, 0)
+    const int own = last_pass ? n1 - i0 : -1;  // row n1 sits in h[own] of one thread
+    const int nsteps = m1 + NT - 1;
+    for (int s = 0; s < nsteps; ++s) {
+      const int j = s - t + 1;
+      if (j >= 1 && j <= m1) {
+        int up;  // H(i0-1, j)
+        if (t == 0) up = base == 0 ? -j * g : T.row[j];
+        else up = xch[(s - 1) & 1][t - 1];
+        const int bcode = T.rev ? T.b[m1 - j] : T.b[j - 1];
+        int diag = updiag, above = up;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const int nh = max(diag + ssig[ra[k] + bcode], max(above, h[k]) - g);
+          diag = h[k];
+          h[k] = nh;
+          above = nh;
+          if (MODE == 1 && nh > bs && i0 + k <= n1) {  // strict >: smallest j, then i
+            bs = nh;
+            bi = i0 + k;
+            bj = j;
+          }
+        }
+        updiag = up;
+        xch[s & 1][t] = h[R - 1];
+        if (last_pass) {
+          if (own >= 0 && own < R) {
+            int v = h[0];
+#pragma unroll
+            for (int k = 1; k < R; ++k) v = own == k ? h[k] : v;
+            T.row[j] = v;
+          }
+        } else if (t == NT - 1) {
+          T.row[j] = h[R - 1];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (MODE == 1) {
+    rs[t] = bs;
+    ri[t] = bi;
+    rj[t] = bj;
+    __syncthreads();
+    for (int w = NT / 2; w > 0; w >>= 1) {
+      if (t < w) {
+        const int s2 = rs[t + w], i2 = ri[t + w], j2 = rj[t + w];
+        const bool take = s2 > rs[t] || (s2 == rs[t] && (j2 < rj[t] || (j2 == rj[t] && i2 < ri[t])));
+        if (take) {
+          rs[t] = s2;
+          ri[t] = i2;
+          rj[t] = j2;
+        }
+      }
+      __syncthreads();
+    }
+    if (t == 0) {
+      T.best[0] = rs[0];
+      T.best[1] = ri[0];
+      T.best[2] = rj[0];
+    }
+  }
+}
+
+}  // namespace
+
+void launch_encode_codes(const char* ascii, uint8_t* codes, uint64_t len, int* bad,
+                         cudaStream_t st) {
+  if (!len) return;
+  const uint64_t blocks = (len + 255) / 256;
+  encode_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(ascii, codes,
+                                                                                   len, bad);
+}
+
+void launch_lastrow(const LrTask* d_tasks, int num_tasks, const LrParams& P, cudaStream_t st) {
+  if (num_tasks <= 0) return;
+  lastrow_kernel<0><<<num_tasks, NT, 0, st>>>(d_tasks, P);
+}
+
+void launch_lastrow_anchored(const LrTask* d_tasks, int num_tasks, const LrParams& P,
+                             cudaStream_t st) {
+  if (num_tasks <= 0) return;
+  lastrow_kernel<1><<<num_tasks, NT, 0, st>>>(d_tasks, P);
+}

@@ -1,0 +1,36 @@
+// hirschberg.h -- last-row score passes for the linear-space long-pair traceback
+// (Hirschberg's divide and conquer over the relaxation of Eqs. (1)-(3),
+// PAPER.md P:224-239, with the paper's linear-space score variant P:266-270 as the pass).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+// One score pass of a global, linear-gap DP over a[0..n1) (rows) x b[0..m1) (columns),
+// both as codes 0..4 (A,C,G,T,N).  rev != 0 reads both sequences back to front (the
+// reverse pass of Hirschberg).  n1 >= 1 and m1 >= 1.
+//  mode 0: row[j] = H(n1, j) for j = 1..m1 (row[0] is left to the host: -n1*g).
+//          row[] doubles as the band-to-band row buffer of the pass, so it needs m1+1 entries.
+//  mode 1: additionally best[0..2] = (max over all cells incl. row/col 0, i, j) with ties
+//          to the smallest j, then the smallest i (the anchored pass of a local alignment:
+//          reversed prefixes ending at the optimum's end cell).
+struct LrTask {
+  const uint8_t* a;
+  const uint8_t* b;
+  int32_t n1, m1;
+  int32_t rev, mode;
+  int32_t* row;
+  int32_t* best;
+};
+
+struct LrParams {
+  int32_t g;       // linear gap penalty magnitude (Eq. 2-3)
+  int8_t sig[25];  // sigma(a, b) = sig[5a + b]
+};
+
+// Encodes ASCII ACGTN (either case) to codes 0..4; any other byte sets *bad = 1.
+void launch_encode_codes(const char* ascii, uint8_t* codes, uint64_t len, int* bad,
+                         cudaStream_t st);
+// One CTA per task; every task of a launch runs the same mode.
+void launch_lastrow(const LrTask* d_tasks, int num_tasks, const LrParams& P, cudaStream_t st);
+void launch_lastrow_anchored(const LrTask* d_tasks, int num_tasks, const LrParams& P,
+                             cudaStream_t st);
