@@ -872,7 +872,8 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
 // ---- linear-space long-pair traceback: Hirschberg's divide and conquer.
 // A problem (i0,i1) x (j0,j1) with more than kLeafCells cells is cut at mid = (i0+i1)/2:
 // a forward last-row pass over q[i0,mid) x s[j0,j1) and a reverse pass over q[mid,i1) x
-// s[j0,j1) (both on the GPU, all problems of one recursion level in one launch) give
+// s[j0,j1) (both on the GPU, all problems of one recursion level in one launch, every
+// pass cut into pipelined 4096-row bands, one CTA each) give
 // F(j) = H(mid, j) and B(j) = the best score of q[mid,i1) x s[j0+j,j1); the optimal path
 // crosses row mid at the smallest j maximising F(j) + B(m'-j).  Leaves (in path order, so
 // their q and s ranges tile the alignment) run as ONE batched global traceback
@@ -902,15 +903,14 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
   for (int k = 0; k < 25; ++k) amax = std::max<int64_t>(amax, std::abs((int)P.sig[k]));
   if ((int64_t)(n + m + 2) * amax >= (1ll << 30))
     return fail(ctx, ANYSEQ_E_UNSUPPORTED, "score range of the long traceback exceeds int32");
-  DevBuf asc, codes, bad, taskbuf, rows, best;
+  DevBuf asc, codes, bad, taskbuf, rows, best, sync;
   struct Guard {
-    DevBuf* b[6];
+    DevBuf* b[7];
     ~Guard() { for (auto* x : b) x->release(); }
-  } guard{{&asc, &codes, &bad, &taskbuf, &rows, &best}};
+  } guard{{&asc, &codes, &bad, &taskbuf, &rows, &best, &sync}};
   CK(asc.ensure(n + m + 16));
   CK(codes.ensure(n + m + 16));
   CK(bad.ensure(sizeof(int)));
-  CK(best.ensure(4 * sizeof(int32_t)));
   CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
   if (n) CK(cudaMemcpyAsync(asc.as<char>(), q, n, cudaMemcpyHostToDevice, st));
   if (m) CK(cudaMemcpyAsync(asc.as<char>() + n, s, m, cudaMemcpyHostToDevice, st));
@@ -939,16 +939,33 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
       // anchored reverse pass over the prefixes ending at the end cell: its optimum is the
       // score of the best alignment ending there (= the local optimum), its cell the begin
       CK(cudaSetDevice(D.id));
+      const int nb = lastrow_bands((int)qe);
       CK(rows.ensure((se + 1) * sizeof(int32_t)));
+      CK(best.ensure(3 * (size_t)nb * sizeof(int32_t)));
+      CK(sync.ensure((1 + (size_t)nb) * sizeof(int)));
+      CK(cudaMemsetAsync(sync.p, 0, (1 + (size_t)nb) * sizeof(int), st));
       LrTask t{dq, ds, (int32_t)qe, (int32_t)se, 1, 1, rows.as<int32_t>(), best.as<int32_t>()};
-      CK(taskbuf.ensure(sizeof(LrTask)));
-      CK(cudaMemcpyAsync(taskbuf.p, &t, sizeof(t), cudaMemcpyHostToDevice, st));
-      launch_lastrow_anchored(taskbuf.as<LrTask>(), 1, P, st);
+      CK(taskbuf.ensure(sizeof(LrTask) + sizeof(int)));
+      struct {
+        LrTask t;
+        int bs;
+      } up{t, 0};
+      CK(cudaMemcpyAsync(taskbuf.p, &up, sizeof(up), cudaMemcpyHostToDevice, st));
+      launch_lastrow_anchored(taskbuf.as<LrTask>(),
+                              reinterpret_cast<const int*>(taskbuf.as<char>() + sizeof(LrTask)),
+                              1, nb, sync.as<int>(), P, st);
       ctx->launches += 1;
-      int32_t hb[3];
-      CK(cudaMemcpyAsync(hb, best.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+      std::vector<int32_t> hbb(3 * (size_t)nb);
+      CK(cudaMemcpyAsync(hbb.data(), best.p, hbb.size() * sizeof(int32_t),
+                         cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       CK(cudaGetLastError());
+      int32_t hb[3] = {hbb[0], hbb[1], hbb[2]};  // key: score desc, j asc, i asc (R10)
+      for (int b = 1; b < nb; ++b) {
+        const int32_t* x = hbb.data() + 3 * b;
+        if (x[0] > hb[0] || (x[0] == hb[0] && (x[2] < hb[2] || (x[2] == hb[2] && x[1] < hb[1]))))
+          hb[0] = x[0], hb[1] = x[1], hb[2] = x[2];
+      }
       if (hb[0] != e.score)
         return fail(ctx, ANYSEQ_E_CUDA, "anchored pass optimum %d != local optimum %d", hb[0],
                     e.score);
@@ -990,10 +1007,21 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
       tasks[2 * t].row = rows.as<int32_t>() + row_off[t];
       tasks[2 * t + 1].row = rows.as<int32_t>() + row_off[t] + c + 1;
     }
-    CK(taskbuf.ensure(tasks.size() * sizeof(LrTask)));
-    CK(cudaMemcpyAsync(taskbuf.p, tasks.data(), tasks.size() * sizeof(LrTask),
-                       cudaMemcpyHostToDevice, st));
-    launch_lastrow(taskbuf.as<LrTask>(), (int)tasks.size(), P, st);
+    // task array, then the first band of every task
+    const size_t tb = tasks.size() * sizeof(LrTask);
+    std::vector<char> up(tb + tasks.size() * sizeof(int));
+    memcpy(up.data(), tasks.data(), tb);
+    int nb = 0;
+    for (size_t k = 0; k < tasks.size(); ++k) {
+      memcpy(up.data() + tb + k * sizeof(int), &nb, sizeof(int));
+      nb += lastrow_bands(tasks[k].n1);
+    }
+    CK(taskbuf.ensure(up.size()));
+    CK(cudaMemcpyAsync(taskbuf.p, up.data(), up.size(), cudaMemcpyHostToDevice, st));
+    CK(sync.ensure((1 + (size_t)nb) * sizeof(int)));
+    CK(cudaMemsetAsync(sync.p, 0, (1 + (size_t)nb) * sizeof(int), st));
+    launch_lastrow(taskbuf.as<LrTask>(), reinterpret_cast<const int*>(taskbuf.as<char>() + tb),
+                   (int)tasks.size(), nb, sync.as<int>(), P, st);
     ctx->launches += 1;
     CK(cudaGetLastError());
     hrows.resize(total);

@@ -30,7 +30,12 @@ struct LrParams {
 // Encodes ASCII ACGTN (either case) to codes 0..4; any other byte sets *bad = 1.
 void launch_encode_codes(const char* ascii, uint8_t* codes, uint64_t len, int* bad,
                          cudaStream_t st);
-// One CTA per task; every task of a launch runs the same mode.
-void launch_lastrow(const LrTask* d_tasks, int num_tasks, const LrParams& P, cudaStream_t st);
-void launch_lastrow_anchored(const LrTask* d_tasks, int num_tasks, const LrParams& P,
-                             cudaStream_t st);
+// Row bands of one task (4096 rows each); band b of a task waits for band b-1's published
+// columns.  d_band_start[num_tasks] = first band of each task (exclusive prefix sum of
+// lastrow_bands), num_bands the total; d_sync = 1 + num_bands zeroed ints (ticket counter,
+// then per-band progress).  MODE 1 (anchored) writes best[3*band .. 3*band+2] per band.
+int lastrow_bands(int n1);
+void launch_lastrow(const LrTask* d_tasks, const int* d_band_start, int num_tasks,
+                    int num_bands, int* d_sync, const LrParams& P, cudaStream_t st);
+void launch_lastrow_anchored(const LrTask* d_tasks, const int* d_band_start, int num_tasks,
+                             int num_bands, int* d_sync, const LrParams& P, cudaStream_t st);
