@@ -231,6 +231,29 @@ def long_pair_leg(ctx, A, n, n_sm, f_mhz):
             "score": r["score"], "end": [r["q_end"], r["s_end"]]}
 
 
+def long_traceback_leg(ctx, A, n):
+    """linear-space traceback of a C4-shaped pair (n-bp genomes, G2 = mutated
+    copy of G1), global linear +2/-1/-1 (the paper's long traceback scheme, Fig. 5a), once,
+    through anyseq_traceback_long with host buffers.  GCUPS = n*m / wall time of the call
+    (the paper's convention: matrix cells over total time); pass_gcups = cells relaxed by
+    the Hirschberg last-row passes / their device time (CUDA events per level launch)."""
+    from synth import c4_genomes
+    g1, g2 = c4_genomes(n, "a", seed=4)
+    sch = A.Scheme("global", "linear", 2, -1, 0, 1)
+    ctx.traceback_long(sch, g1[:4096], g2[:4096])  # warm-up
+    t0 = time.perf_counter()
+    r = ctx.traceback_long(sch, g1, g2)
+    wall = time.perf_counter() - t0
+    pass_ms, pass_cells = ctx.stat("tb_pass_ms"), ctx.stat("tb_pass_cells")
+    cells = len(g1) * len(g2)
+    return {"workload": f"{len(g1)} bp x {len(g2)} bp (C4 variant a shape), global linear, "
+                        "match 2 / mismatch -1 / gap 1, traceback (Hirschberg), 1 GPU",
+            "value": round(cells / wall / 1e9, 1), "unit": "GCUPS", "wall_ms": round(wall * 1e3, 1),
+            "pass_ms": round(pass_ms, 1), "pass_cells": pass_cells,
+            "pass_gcups": round(pass_cells / (pass_ms / 1e3) / 1e9, 1),
+            "kernel": "lastrow_kernel<0>", "score": r["score"], "cigar_ops": len(r["cigar"])}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,6 +263,8 @@ def main():
     ap.add_argument("--pairs", type=int, default=NUM_PAIRS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=3.0)
+    ap.add_argument("--long-tb-bp", type=int, default=1_000_000,
+                    help="linear-space long traceback leg (8(f) f1) genome length; 0 skips it")
     ap.add_argument("--long-bp", type=int, default=5_000_000,
                     help="C4 long pair (second half of the metric) genome length; 0 skips it")
     args = ap.parse_args()
@@ -372,6 +397,8 @@ def main():
         line["cpu_baseline"] = cpu_oracle_baseline(qm, sm)
     if rank == 0 and ws == 1 and args.long_bp > 0:
         line["long_pair"] = long_pair_leg(ctx, A, args.long_bp, n_sm, f_mhz)
+    if rank == 0 and ws == 1 and args.long_tb_bp > 0:
+        line["long_traceback"] = long_traceback_leg(ctx, A, args.long_tb_bp)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

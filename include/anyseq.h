@@ -166,6 +166,8 @@ uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx);
    clears them.  "timing" = 2 also prints a per-chunk event timeline of the host API to
    stderr (debug).  After anyseq_align_long: "long_kernel_ms" (device time of the long
    kernel, max over devices) and "long_narrow" (1 if the 16-bit differential kernel ran).
+   After anyseq_traceback_long: "tb_pass_ms" (device time of the Hirschberg last-row
+   passes, summed over levels) and "tb_pass_cells" (cells those passes relaxed).
    Returns ANYSEQ_E_INVALID for unknown names. */
 anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value);
 anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);

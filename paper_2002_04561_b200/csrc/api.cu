@@ -109,6 +109,7 @@ struct anyseq_ctx {
   LongOptions long_opt;
   int long_narrow = 0;   // the last anyseq_align_long ran the 16-bit differential kernel
   double long_ms = 0;    // ... and its kernel time (max over devices)
+  double tb_pass_ms = 0, tb_pass_cells = 0;  // last anyseq_traceback_long: last-row passes
   int timing = 0;
   std::mutex ev_mu;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> fill_ev, walk_ev, pool;
@@ -975,6 +976,14 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
   }
 
   // Hirschberg levels; nodes stay in path order
+  ctx->tb_pass_ms = ctx->tb_pass_cells = 0;
+  cudaEvent_t ev0, ev1;
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  struct EvGuard {
+    cudaEvent_t a, b;
+    ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
+  } evg{ev0, ev1};
   const int64_t kLeafCells = 1 << 22;
   std::vector<HbNode> nodes{{qb, qe, sb, se}};
   std::vector<char> leaf(1, 0);
@@ -1020,13 +1029,19 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
     CK(cudaMemcpyAsync(taskbuf.p, up.data(), up.size(), cudaMemcpyHostToDevice, st));
     CK(sync.ensure((1 + (size_t)nb) * sizeof(int)));
     CK(cudaMemsetAsync(sync.p, 0, (1 + (size_t)nb) * sizeof(int), st));
+    CK(cudaEventRecord(ev0, st));
     launch_lastrow(taskbuf.as<LrTask>(), reinterpret_cast<const int*>(taskbuf.as<char>() + tb),
                    (int)tasks.size(), nb, sync.as<int>(), P, st);
+    CK(cudaEventRecord(ev1, st));
     ctx->launches += 1;
     CK(cudaGetLastError());
     hrows.resize(total);
     CK(cudaMemcpyAsync(hrows.data(), rows.p, total * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    float lvl_ms = 0;
+    CK(cudaEventElapsedTime(&lvl_ms, ev0, ev1));
+    ctx->tb_pass_ms += lvl_ms;
+    for (const LrTask& x : tasks) ctx->tb_pass_cells += (double)x.n1 * x.m1;
     std::vector<HbNode> nn;
     std::vector<char> nl;
     size_t t = 0;
@@ -1363,6 +1378,8 @@ anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) 
   if (n == "walk_ms") { *value = ctx->walk_ms; return ANYSEQ_OK; }
   if (n == "long_narrow") { *value = ctx->long_narrow; return ANYSEQ_OK; }
   if (n == "long_kernel_ms") { *value = ctx->long_ms; return ANYSEQ_OK; }
+  if (n == "tb_pass_ms") { *value = ctx->tb_pass_ms; return ANYSEQ_OK; }
+  if (n == "tb_pass_cells") { *value = ctx->tb_pass_cells; return ANYSEQ_OK; }
   if (n == "fill_launches") { *value = (double)ctx->fill_launches; return ANYSEQ_OK; }
   return fail(ctx, ANYSEQ_E_INVALID, "unknown stat %s", name);
 }

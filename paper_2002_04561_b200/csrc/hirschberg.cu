@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(NT) lastrow_kernel(const LrTask* __restrict__ 
       int diag = updiag, above = up;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        const int nh = max(diag + ssig[ra[k] + bcode], max(above, h[k]) - g);
+        const int nh = __viaddmax_s32(max(above, h[k]), -g, diag + ssig[ra[k] + bcode]);
         diag = h[k];
         h[k] = nh;
         above = nh;
