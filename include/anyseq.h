@@ -139,13 +139,13 @@ anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, co
    GPU forward / reverse last-row score passes (Eqs. (1)-(3)) cut the matrix at
    the middle row of every sub-problem until a piece has <= 2^22 cells; the pieces run as
    one batched global traceback (anyseq_traceback's kernels) and their CIGARs are joined.
-   LOCAL first finds the end cell with anyseq_align_long and the begin cell with an
-   anchored reverse pass.  Device memory O(n + m); host inputs as anyseq_align_long.
+   LOCAL and SEMIGLOBAL first find the end cell with anyseq_align_long and the begin cell
+   with an anchored reverse pass (best over all cells, resp. over row 0 / column 0).  Device memory O(n + m); host inputs as anyseq_align_long.
    out receives score, begin/end cells, cigar_offset 0 and cigar_len; cigar[] (host)
    receives the ops.  Among co-optimal paths the one returned may differ from
    anyseq_traceback's tie rule (the split takes the smallest crossing column); the
    score, end cell (LOCAL) and the path's rescored value are what is fixed.
-   Errors: ANYSEQ_E_UNSUPPORTED for affine gaps or SEMIGLOBAL (not built) and when the
+   Errors: ANYSEQ_E_UNSUPPORTED for affine gaps (Myers-Miller, not built) and when the
    score range could exceed int32; ANYSEQ_E_CAPACITY with *cigar_used = words required;
    ANYSEQ_E_BADSEQ for a byte outside ACGTNacgtn. */
 anyseq_status anyseq_traceback_long(anyseq_ctx* ctx, const anyseq_params* params, const char* q,

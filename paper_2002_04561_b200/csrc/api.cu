@@ -927,7 +927,7 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
   // region of the alignment: the whole matrix (global) or [begin, end) of a local optimum
   int64_t qb = 0, sb = 0, qe = (int64_t)n, se = (int64_t)m;
   int32_t want = 0;
-  if (prm->kind == ANYSEQ_LOCAL) {
+  if (prm->kind != ANYSEQ_GLOBAL) {
     anyseq_alignment e;
     anyseq_status r = anyseq_align_long(ctx, prm, q, n, s, m, &e);
     if (r != ANYSEQ_OK) return r;
@@ -936,9 +936,11 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
     se = e.s_end;
     qb = qe;
     sb = se;
-    if (e.score > 0) {
+    const bool local = prm->kind == ANYSEQ_LOCAL;
+    if (local ? e.score > 0 : (qe > 0 && se > 0)) {
       // anchored reverse pass over the prefixes ending at the end cell: its optimum is the
-      // score of the best alignment ending there (= the local optimum), its cell the begin
+      // score of the best alignment ending there (= the local optimum), its cell the begin;
+      // semi-global: the best over begins on row 0 / column 0 (the pass's last row / column)
       CK(cudaSetDevice(D.id));
       const int nb = lastrow_bands((int)qe);
       CK(rows.ensure((se + 1) * sizeof(int32_t)));
@@ -952,9 +954,9 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
         int bs;
       } up{t, 0};
       CK(cudaMemcpyAsync(taskbuf.p, &up, sizeof(up), cudaMemcpyHostToDevice, st));
-      launch_lastrow_anchored(taskbuf.as<LrTask>(),
-                              reinterpret_cast<const int*>(taskbuf.as<char>() + sizeof(LrTask)),
-                              1, nb, sync.as<int>(), P, st);
+      const int* bstart = reinterpret_cast<const int*>(taskbuf.as<char>() + sizeof(LrTask));
+      if (local) launch_lastrow_anchored(taskbuf.as<LrTask>(), bstart, 1, nb, sync.as<int>(), P, st);
+      else launch_lastrow_edges(taskbuf.as<LrTask>(), bstart, 1, nb, sync.as<int>(), P, st);
       ctx->launches += 1;
       std::vector<int32_t> hbb(3 * (size_t)nb);
       CK(cudaMemcpyAsync(hbb.data(), best.p, hbb.size() * sizeof(int32_t),
@@ -967,8 +969,14 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
         if (x[0] > hb[0] || (x[0] == hb[0] && (x[2] < hb[2] || (x[2] == hb[2] && x[1] < hb[1]))))
           hb[0] = x[0], hb[1] = x[1], hb[2] = x[2];
       }
+      if (!local) {  // border cells of the pass: all of q against nothing, or all of s
+        const int64_t cand[2][3] = {{-qe * (int64_t)P.g, qe, 0}, {-se * (int64_t)P.g, 0, se}};
+        for (auto& c : cand)
+          if (c[0] > hb[0] || (c[0] == hb[0] && (c[2] < hb[2] || (c[2] == hb[2] && c[1] < hb[1]))))
+            hb[0] = (int32_t)c[0], hb[1] = (int32_t)c[1], hb[2] = (int32_t)c[2];
+      }
       if (hb[0] != e.score)
-        return fail(ctx, ANYSEQ_E_CUDA, "anchored pass optimum %d != local optimum %d", hb[0],
+        return fail(ctx, ANYSEQ_E_CUDA, "anchored pass optimum %d != long-kernel optimum %d", hb[0],
                     e.score);
       qb = qe - hb[1];
       sb = se - hb[2];
@@ -1104,7 +1112,7 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
       else ops.push_back(word);
     }
   }
-  if (prm->kind == ANYSEQ_LOCAL && score != want)
+  if (prm->kind != ANYSEQ_GLOBAL && score != want)
     return fail(ctx, ANYSEQ_E_CUDA, "long traceback: path score %lld != optimum %d",
                 (long long)score, want);
   if (used) *used = ops.size();
@@ -1361,9 +1369,8 @@ anyseq_status anyseq_traceback_long(anyseq_ctx* ctx, const anyseq_params* params
   if ((n && !q) || (m && !s)) return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
   if (n >= (1ull << 31) || m >= (1ull << 31))
     return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long sequences must be shorter than 2^31");
-  if (params->gap != ANYSEQ_GAP_LINEAR || params->kind == ANYSEQ_SEMIGLOBAL)
-    return fail(ctx, ANYSEQ_E_UNSUPPORTED,
-                "long traceback: global and local alignments with linear gaps only");
+  if (params->gap != ANYSEQ_GAP_LINEAR)
+    return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long traceback: linear gaps only");
   return run_traceback_long(ctx, params, q, n, s, m, out, cigar, cigar_capacity, cigar_used);
 }
 

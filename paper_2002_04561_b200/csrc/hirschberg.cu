@@ -11,6 +11,8 @@
 // gaps of Eqs. (2)-(3), H(i,0) = -i*g, H(0,j) = -j*g.  32-bit scores.
 #include "hirschberg.h"
 
+#include <climits>
+
 namespace {
 
 constexpr int NT = 256;  // threads per CTA
@@ -62,7 +64,8 @@ __global__ void __launch_bounds__(NT) lastrow_kernel(const LrTask* __restrict__ 
   const int band = tk - band_start[lo];
   const int g = P.g, n1 = T.n1, m1 = T.m1;
   // running optimum of MODE 1: cell (0,0) holds 0 and beats every other border cell
-  int bs = 0, bi = 0, bj = 0;
+  // MODE 2 (semi-global begin): only cells of the last row or column count
+  int bs = MODE == 2 ? INT_MIN : 0, bi = 0, bj = 0;
   const int base = band * NT * R;
   const bool last_band = base + NT * R >= n1;
   const int i0 = base + t * R + 1;  // first row of this thread (1-based)
@@ -103,7 +106,8 @@ __global__ void __launch_bounds__(NT) lastrow_kernel(const LrTask* __restrict__ 
         diag = h[k];
         h[k] = nh;
         above = nh;
-        if (MODE == 1 && nh > bs && i0 + k <= n1) {  // strict >: smallest j, then i
+        if (MODE != 0 && nh > bs && i0 + k <= n1 &&  // strict >: smallest j, then i
+            (MODE == 1 || i0 + k == n1 || j == m1)) {
           bs = nh;
           bi = i0 + k;
           bj = j;
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(NT) lastrow_kernel(const LrTask* __restrict__ 
     }
     __syncthreads();
   }
-  if (MODE == 1) {
+  if (MODE != 0) {
     rs[t] = bs;
     ri[t] = bi;
     rj[t] = bj;
@@ -176,5 +180,12 @@ void launch_lastrow_anchored(const LrTask* d_tasks, const int* d_band_start, int
                              int num_bands, int* d_sync, const LrParams& P, cudaStream_t st) {
   if (num_tasks <= 0) return;
   lastrow_kernel<1><<<num_bands, NT, 0, st>>>(d_tasks, d_band_start, num_tasks, d_sync,
+                                              d_sync + 1, P);
+}
+
+void launch_lastrow_edges(const LrTask* d_tasks, const int* d_band_start, int num_tasks,
+                          int num_bands, int* d_sync, const LrParams& P, cudaStream_t st) {
+  if (num_tasks <= 0) return;
+  lastrow_kernel<2><<<num_bands, NT, 0, st>>>(d_tasks, d_band_start, num_tasks, d_sync,
                                               d_sync + 1, P);
 }

@@ -37,5 +37,10 @@ void launch_encode_codes(const char* ascii, uint8_t* codes, uint64_t len, int* b
 int lastrow_bands(int n1);
 void launch_lastrow(const LrTask* d_tasks, const int* d_band_start, int num_tasks,
                     int num_bands, int* d_sync, const LrParams& P, cudaStream_t st);
+// MODE 2: best over the cells of row n1 and column m1 only (the anchored pass of a
+// semi-global alignment, whose begin lies on row 0 or column 0); border cells (n1, 0) and
+// (0, m1) are left to the host.
+void launch_lastrow_edges(const LrTask* d_tasks, const int* d_band_start, int num_tasks,
+                          int num_bands, int* d_sync, const LrParams& P, cudaStream_t st);
 void launch_lastrow_anchored(const LrTask* d_tasks, const int* d_band_start, int num_tasks,
                              int num_bands, int* d_sync, const LrParams& P, cudaStream_t st);

@@ -1,4 +1,5 @@
-"""GPU parity of the linear-space long-pair traceback (anyseq_traceback_long)
+"""GPU parity of the linear-space long-pair traceback (anyseq_traceback_long, SURVEY 8(f) f1;
+global, local and semi-global kinds with linear gaps)
 against the oracle.  Several paths can be optimal, so the test compares what is unique --
 the optimum score (and, for local, the end cell under the tie rule of reading R10) -- with
 the oracle, and checks that the returned path is valid: it spans exactly the reported
@@ -95,3 +96,33 @@ def test_long_tb_errors(ctx):
         ctx.traceback_long(A.Scheme("global", "linear", 2, -1, 0, 1), b"ACGT" * 100,
                            b"TTGA" * 100, cigar_capacity=1)
     assert e.value.status == 4 and e.value.cigar_used > 1
+
+
+@pytest.mark.parametrize("n,m,seed", [(1, 1, 31), (5, 0, 32), (2000, 2600, 33), (9000, 400, 34),
+                                      (300, 7000, 35)])
+def test_long_tb_semi_linear(ctx, n, m, seed):
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    from synth import iid
+    q, s = iid(n, seed), iid(m, seed + 100)
+    so = O.Scheme("semi", "linear", 2, -1, 0, 1)
+    r = ctx.traceback_long(A.Scheme("semi", "linear", 2, -1, 0, 1), q, s)
+    o = O.score_rolling(so, q, s)
+    assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end)
+    assert r["q_begin"] == 0 or r["s_begin"] == 0          # begins on row 0 or column 0
+    assert r["q_end"] == n or r["s_end"] == m              # ends on the last row or column
+    _check_path(so, q, s, r)
+
+
+def test_long_tb_semi_read_in_reference(ctx):
+    """A 3 kbp read taken from a 40 kbp reference: semi-global places it with free end gaps."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    from synth import c4_genomes
+    g1, g2 = c4_genomes(40_000, "a", seed=9)
+    read = g2[12_000:15_000]
+    so = O.Scheme("semi", "linear", 2, -1, 0, 1)
+    r = ctx.traceback_long(A.Scheme("semi", "linear", 2, -1, 0, 1), read, g1)
+    o = O.score_rolling(so, read, g1)
+    assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end)
+    _check_path(so, read, g1, r)
