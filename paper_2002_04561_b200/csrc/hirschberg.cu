@@ -102,7 +102,10 @@ __global__ void __launch_bounds__(NT) lastrow_kernel(const LrTask* __restrict__ 
       int diag = updiag, above = up;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        const int nh = __viaddmax_s32(max(above, h[k]), -g, diag + ssig[ra[k] + bcode]);
+        // Eq. (1) reassociated: the off-chain part max(H_left - g, diag + sigma) first, so
+        // the dependency down the column is one VIADDMNMX per row (exact: max is associative)
+        const int x = __viaddmax_s32(h[k], -g, diag + ssig[ra[k] + bcode]);
+        const int nh = __viaddmax_s32(above, -g, x);
         diag = h[k];
         h[k] = nh;
         above = nh;
