@@ -874,7 +874,7 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
 // A problem (i0,i1) x (j0,j1) with more than kLeafCells cells is cut at mid = (i0+i1)/2:
 // a forward last-row pass over q[i0,mid) x s[j0,j1) and a reverse pass over q[mid,i1) x
 // s[j0,j1) (both on the GPU, all problems of one recursion level in one launch, every
-// pass cut into pipelined 4096-row bands, one CTA each) give
+// pass cut into pipelined 3072-row bands, one CTA each) give
 // F(j) = H(mid, j) and B(j) = the best score of q[mid,i1) x s[j0+j,j1); the optimal path
 // crosses row mid at the smallest j maximising F(j) + B(m'-j).  Leaves (in path order, so
 // their q and s ranges tile the alignment) run as ONE batched global traceback

@@ -15,8 +15,14 @@
 
 namespace {
 
-constexpr int NT = 256;  // threads per CTA
-constexpr int R = 16;    // rows per thread
+#ifndef HB_NT
+#define HB_NT 128
+#endif
+#ifndef HB_R
+#define HB_R 24
+#endif
+constexpr int NT = HB_NT;  // threads per CTA
+constexpr int R = HB_R;    // rows per thread
 
 __global__ void encode_kernel(const char* __restrict__ ascii, uint8_t* __restrict__ codes,
                               uint64_t len, int* bad) {

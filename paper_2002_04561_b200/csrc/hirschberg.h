@@ -30,7 +30,7 @@ struct LrParams {
 // Encodes ASCII ACGTN (either case) to codes 0..4; any other byte sets *bad = 1.
 void launch_encode_codes(const char* ascii, uint8_t* codes, uint64_t len, int* bad,
                          cudaStream_t st);
-// Row bands of one task (4096 rows each); band b of a task waits for band b-1's published
+// Row bands of one task (3072 rows each); band b of a task waits for band b-1's published
 // columns.  d_band_start[num_tasks] = first band of each task (exclusive prefix sum of
 // lastrow_bands), num_bands the total; d_sync = 1 + num_bands zeroed ints (ticket counter,
 // then per-band progress).  MODE 1 (anchored) writes best[3*band .. 3*band+2] per band.
