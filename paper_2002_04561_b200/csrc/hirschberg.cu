@@ -21,6 +21,9 @@ namespace {
 #ifndef HB_R
 #define HB_R 24
 #endif
+#ifndef HB_PUB
+#define HB_PUB 32
+#endif
 constexpr int NT = HB_NT;  // threads per CTA
 constexpr int R = HB_R;    // rows per thread
 
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(NT) lastrow_kernel(const LrTask* __restrict__ 
         }
       } else if (t == NT - 1) {
         __stcg(T.row + j, h[R - 1]);
-        if ((j & 31) == 0 || j == m1) {  // publish 32 columns at a time
+        if ((j & (HB_PUB - 1)) == 0 || j == m1) {  // publish HB_PUB columns at a time
           __threadfence();
           atomicExch(prog + tk, j);
         }
