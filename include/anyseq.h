@@ -137,7 +137,7 @@ anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, co
 /* Long-pair alignment WITH traceback in linear space (the paper's long
    genome traceback workload, Fig. 5a).  Hirschberg's divide and conquer:
    GPU forward / reverse last-row score passes (Eqs. (1)-(3)) cut the matrix at
-   the middle row of every sub-problem until a piece has <= 2^22 cells; the pieces run as
+   the middle row of every sub-problem until a piece has <= 2^20 cells; the pieces run as
    one batched global traceback (anyseq_traceback's kernels) and their CIGARs are joined.
    LOCAL and SEMIGLOBAL first find the end cell with anyseq_align_long and the begin cell
    with an anchored reverse pass (best over all cells, resp. over row 0 / column 0).  Device memory O(n + m); host inputs as anyseq_align_long.
@@ -167,7 +167,8 @@ uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx);
    stderr (debug).  After anyseq_align_long: "long_kernel_ms" (device time of the long
    kernel, max over devices) and "long_narrow" (1 if the 16-bit differential kernel ran).
    After anyseq_traceback_long: "tb_pass_ms" (device time of the Hirschberg last-row
-   passes, summed over levels) and "tb_pass_cells" (cells those passes relaxed).
+   passes, summed over levels), "tb_pass_cells" (cells those passes relaxed) and
+   "tb_leaf_ms" (host time of the batched leaf traceback).
    Returns ANYSEQ_E_INVALID for unknown names. */
 anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value);
 anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
@@ -188,6 +189,8 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
      "long_band_rows"    long pairs, rows per warp task: 32-bit kernel 512 (default) or
                          384; 16-bit kernel 1024 (default), 768 or 512
      "long_sleep_ns"     long pairs (16-bit kernel): back-off of the row hand-off poll
+     "tb_leaf_cells"     long traceback: Hirschberg recursion stops at <= this many cells
+                         per sub-problem (default 2^20)
      "timing"            see above */
 anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value);
 

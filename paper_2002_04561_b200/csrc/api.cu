@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -106,6 +107,8 @@ struct anyseq_ctx {
   int64_t chunk_bytes = 64ll << 20;  // host-API upload/compute pipelining granularity
   int64_t force_variant = -1;
   int64_t allow16 = 1;
+  int64_t tb_leaf_cells = 1 << 20;  // long traceback: Hirschberg leaf size (cells)
+  double tb_leaf_ms = 0;            // last anyseq_traceback_long: host time of the leaves
   LongOptions long_opt;
   int long_narrow = 0;   // the last anyseq_align_long ran the 16-bit differential kernel
   double long_ms = 0;    // ... and its kernel time (max over devices)
@@ -992,7 +995,7 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
     cudaEvent_t a, b;
     ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
   } evg{ev0, ev1};
-  const int64_t kLeafCells = 1 << 22;
+  const int64_t kLeafCells = ctx->tb_leaf_cells;
   std::vector<HbNode> nodes{{qb, qe, sb, se}};
   std::vector<char> leaf(1, 0);
   std::vector<int32_t> hrows;
@@ -1100,7 +1103,10 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
   std::vector<uint32_t> lc(std::max<uint64_t>(lcap, 1));
   std::vector<int32_t> lsc(L);
   uint64_t lused = 0;
+  const auto tl0 = std::chrono::steady_clock::now();
   anyseq_status r = run_host_batch(ctx, &gp, &lb, 1, lsc.data(), la.data(), lc.data(), lcap, &lused);
+  ctx->tb_leaf_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count();
   if (r != ANYSEQ_OK) return r;
   int64_t score = 0;
   std::vector<uint32_t> ops;
@@ -1313,6 +1319,11 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
   if (n == "force_variant") { ctx->force_variant = value; return ANYSEQ_OK; }
   if (n == "chunk_bytes") { ctx->chunk_bytes = std::max<int64_t>(value, 1 << 16); return ANYSEQ_OK; }
   if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }
+  if (n == "tb_leaf_cells") {
+    if (value < 1) return fail(ctx, ANYSEQ_E_INVALID, "tb_leaf_cells must be >= 1");
+    ctx->tb_leaf_cells = value;
+    return ANYSEQ_OK;
+  }
   if (n == "long_band_rows") { ctx->long_opt.band_rows = (int)value; return ANYSEQ_OK; }
   if (n == "long_blocks") { ctx->long_opt.blocks = (int)value; return ANYSEQ_OK; }
   if (n == "long_strips") { ctx->long_opt.virtual_strips = (int)value; return ANYSEQ_OK; }
@@ -1387,6 +1398,7 @@ anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) 
   if (n == "long_kernel_ms") { *value = ctx->long_ms; return ANYSEQ_OK; }
   if (n == "tb_pass_ms") { *value = ctx->tb_pass_ms; return ANYSEQ_OK; }
   if (n == "tb_pass_cells") { *value = ctx->tb_pass_cells; return ANYSEQ_OK; }
+  if (n == "tb_leaf_ms") { *value = ctx->tb_leaf_ms; return ANYSEQ_OK; }
   if (n == "fill_launches") { *value = (double)ctx->fill_launches; return ANYSEQ_OK; }
   return fail(ctx, ANYSEQ_E_INVALID, "unknown stat %s", name);
 }

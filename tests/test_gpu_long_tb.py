@@ -126,3 +126,23 @@ def test_long_tb_semi_read_in_reference(ctx):
     o = O.score_rolling(so, read, g1)
     assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end)
     _check_path(so, read, g1, r)
+
+
+@pytest.mark.parametrize("leaf", [64, 4096, 1 << 24])
+def test_long_tb_leaf_sizes(ctx, leaf):
+    """Deep recursion (tiny leaves: many levels, one-row and one-column pieces) and no
+    recursion at all give the same optimum and valid paths, for every kind."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    from synth import iid
+    q, s = iid(1800, 41), iid(1500, 42)
+    ctx.set_option("tb_leaf_cells", leaf)
+    try:
+        for kind in ("global", "local", "semi"):
+            so = O.Scheme(kind, "linear", 2, -1, 0, 1)
+            r = ctx.traceback_long(A.Scheme(kind, "linear", 2, -1, 0, 1), q, s)
+            o = O.score_rolling(so, q, s)
+            assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), kind
+            _check_path(so, q, s, r)
+    finally:
+        ctx.set_option("tb_leaf_cells", 1 << 20)

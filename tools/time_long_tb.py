@@ -11,7 +11,10 @@ from synth import c4_genomes
 
 
 def main(sizes):
+    import os
     ctx = A.Context([0])
+    if os.environ.get("TB_LEAF_CELLS"):
+        ctx.set_option("tb_leaf_cells", int(os.environ["TB_LEAF_CELLS"]))
     for kind in ("global", "local"):
         sch = A.Scheme(kind, "linear", 2, -1, 0, 1)
         for n in sizes:
@@ -26,7 +29,9 @@ def main(sizes):
                               "ops": len(r["cigar"]), "s": round(dt, 4),
                               "gcups": round(cells / dt / 1e9, 1),
                               "pass_gcups": round(ctx.stat("tb_pass_cells")
-                                                  / ctx.stat("tb_pass_ms") / 1e6, 1)}),
+                                                  / ctx.stat("tb_pass_ms") / 1e6, 1),
+                              "pass_ms": round(ctx.stat("tb_pass_ms"), 1),
+                              "leaf_ms": round(ctx.stat("tb_leaf_ms"), 1)}),
                   flush=True)
 
 
