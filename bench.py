@@ -112,12 +112,12 @@ def cpu_oracle_baseline(qm, sm, budget_s: float = 12.0, threads=None):
     q, qo = uniform_csr(qm[:k2])
     s, so = uniform_csr(sm[:k2])
     t0 = time.perf_counter()
-    O.batch(sch, q, qo, s, so, traceback=False, threads=th)
+    res, _ = O.batch(sch, q, qo, s, so, traceback=False, threads=th)
     dt = time.perf_counter() - t0
     cells = k2 * READ_LEN * READ_LEN
     return {"value": round(cells / dt / 1e9, 4), "unit": "GCUPS", "cores": th, "kind": "oracle",
             "sample": f"first {k2} of the {len(qm)} C2 pairs (150x150, semi-global affine 5/1), "
-                      f"{dt:.1f} s on {th} threads"}
+                      f"{dt:.1f} s on {th} threads"}, res["score"]
 
 
 def measured_alu_peak():
@@ -201,11 +201,15 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def long_pair_leg(ctx, A, n, n_sm, f_mhz):
+def long_pair_leg(ctx, A, n, n_sm, f_mhz, n_gpus=1):
     """The metric's second half: C4 (two n-bp genomes, G2 = mutated copy of G1, local affine
-    5/1, +2/-1, score-only) through anyseq_align_long on this GPU, once (one call is ~9 s at
-    5 Mbp).  GCUPS = n*m / kernel time (CUDA events around the long kernel); wall includes
-    the upload and pack of both genomes.  Not a bench step: the headline value is C2."""
+    5/1, +2/-1, score-only) through anyseq_align_long, once (one call is ~9 s at 5 Mbp on one
+    GPU).  With n_gpus > 1 the context spans GPUs 0..n_gpus-1 and the pair runs as n_gpus
+    column strips with the boundary column passed GPU to GPU over NVLink; rank
+    0 drives every device from one process (the other ranks wait on a CPU barrier).
+    GCUPS = n*m / kernel time (CUDA events around the long kernel, max over devices); wall
+    includes the upload and pack of both genomes.  Not a bench step: the headline value is
+    C2."""
     from synth import c4_genomes
     g1, g2 = c4_genomes(n, "a", seed=4)
     sch = A.Scheme("local", "affine", 2, -1, 5, 1)
@@ -219,15 +223,17 @@ def long_pair_leg(ctx, A, n, n_sm, f_mhz):
     # 5.5 ALU ops per two cells at 64 lane-ops/clk/SM (16-bit kernel);
     # 5 ALU ops per cell (s32 kernel, 5.4)
     cpc = 64 * 2 / 5.5 if narrow else 64 / 5.0
-    peak = n_sm * f_mhz * 1e6 * cpc / 1e9
+    peak = n_gpus * n_sm * f_mhz * 1e6 * cpc / 1e9
     return {"workload": f"C4: {len(g1)} bp x {len(g2)} bp (G2 = mutated copy of G1), local affine "
-                        "open 5 / extend 1, match 2 / mismatch -1, score-only, 1 GPU",
+                        f"open 5 / extend 1, match 2 / mismatch -1, score-only, {n_gpus} GPU"
+                        + ("s (column strips)" if n_gpus > 1 else ""),
+            "n_gpus": n_gpus,
             "value": round(gcups, 1), "unit": "GCUPS", "kernel_ms": round(ms, 1),
             "wall_ms": round(wall * 1e3, 1),
             "kernel": "long16_kernel<16> (16-bit differential)" if narrow else "long_kernel<LOCAL,AFFINE,16> (s32)",
             "roofline": {"bound": "alu", "achieved": round(gcups, 1), "peak": round(peak, 1),
                          "unit": "GCUPS", "frac": round(gcups / peak, 4),
-                         "peak_basis": f"{n_sm} SM x {f_mhz:.0f} MHz (C2 median under load) x {cpc:.2f} cells/clk/SM"},
+                         "peak_basis": f"{n_gpus} GPU x {n_sm} SM x {f_mhz:.0f} MHz (C2 median under load) x {cpc:.2f} cells/clk/SM"},
             "score": r["score"], "end": [r["q_end"], r["s_end"]]}
 
 
@@ -254,6 +260,20 @@ def long_traceback_leg(ctx, A, n):
             "kernel": "lastrow_kernel<0>", "score": r["score"], "cigar_ops": len(r["cigar"])}
 
 
+def time_device_steps(step, stream, steps):
+    """CUDA events around `steps` calls of step() on `stream` (after a synchronize)."""
+    import torch
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -278,13 +298,27 @@ def main():
     from synth import c2_reads, uniform_csr
 
     ws, rank, local = _dist()
+    if args.gpus != ws:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch N>1 under torchrun "
+              f"(one rank per GPU) -- reporting n_gpus={ws}", file=sys.stderr)
     torch.cuda.set_device(local)
+    cpu_group = None
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # CPU-side barrier for the legs where rank 0 alone drives every GPU (C4 column strips):
+        # an NCCL barrier would park a kernel on the GPUs that leg needs
+        cpu_group = dist.new_group(backend="gloo")
 
     def barrier():
         if ws > 1:
             dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=torch.device("cuda", local))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     qm, sm = c2_reads(args.pairs, seed=2 + 1000 * rank)
     q, qo = uniform_csr(qm)
@@ -313,35 +347,47 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    ms = time_device_steps(step, stream, args.steps)
     barrier()
     clocks = sampler.stop()
-    ms = e0.elapsed_time(e1)
     launches = ctx.launches - launches0
     fill_ms = ctx.stat("fill_ms")
     fill_launches = int(ctx.stat("fill_launches"))
     ctx.set_option("timing", 0)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms)
     value = cells * ws * args.steps / (ms_max / 1e3) / 1e9
-
-    # parity spot check of this run's output (oracle on a few pairs) -- not timed
-    from oracle import oracle as O
     got = d_sc.cpu().numpy()
-    osch = O.Scheme(SCHEME["kind"], SCHEME["gap"], SCHEME["match"], SCHEME["mismatch"],
-                    SCHEME["gap_open"], SCHEME["gap_extend"])
-    idx = np.random.default_rng(rank).choice(B, 64, replace=False)
-    parity = all(int(got[k]) == O.align(osch, qm[k].tobytes(), sm[k].tobytes(), False).score
-                 for k in idx)
+
+    # generic scheme (no compile-time scoring constants: open 6 / extend 1 has no specialised
+    # instance) on the same batch -- the rate of the fill without partial evaluation
+    gsch = A.Scheme("semi", "affine", 2, -1, 6, 1)
+    d_sc2 = torch.empty_like(d_sc)
+    gstep = lambda: ctx.align_batch_device(gsch, d_q, d_qo, d_s, d_so, d_sc2, stream=stream)
+    gstep()
+    g_ms = max_over_ranks(time_device_steps(gstep, stream, max(3, args.steps // 2)))
+    generic = {"scheme": "semi-global affine open 6 / extend 1, match 2 / mismatch -1 "
+                         "(no specialised instance)",
+               "value": round(cells * ws * max(3, args.steps // 2) / (g_ms / 1e3) / 1e9, 1),
+               "unit": "GCUPS"}
+
+    # strong scaling: the same 1M-pair batch split over the ranks
+    strong = None
+    if ws > 1:
+        k0, k1 = B * rank // ws, B * (rank + 1) // ws
+        sq, sqo = uniform_csr(qm[k0:k1])
+        ss_, sso = uniform_csr(sm[k0:k1])
+        t_q, t_s = torch.from_numpy(sq).to(dev), torch.from_numpy(ss_).to(dev)
+        t_qo = torch.from_numpy(sqo.view(np.int64)).to(dev)
+        t_so = torch.from_numpy(sso.view(np.int64)).to(dev)
+        t_sc = torch.empty(k1 - k0, dtype=torch.int32, device=dev)
+        sstep = lambda: ctx.align_batch_device(sch, t_q, t_qo, t_s, t_so, t_sc, stream=stream)
+        for _ in range(args.warmup):
+            sstep()
+        barrier()
+        s_ms = max_over_ranks(time_device_steps(sstep, stream, args.steps))
+        strong = {"workload": f"C2 1M pairs total split over {ws} ranks",
+                  "value": round(cells * args.steps / (s_ms / 1e3) / 1e9, 1), "unit": "GCUPS",
+                  "ms_per_step": round(s_ms / args.steps, 4), "scaling": "strong"}
 
     uniform_lengths = bool(np.all(np.diff(qo) == np.diff(qo)[0]) and
                            np.all(np.diff(so) == np.diff(so)[0]))
@@ -357,11 +403,9 @@ def main():
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         ctx.align_batch(sch, pq, pqo, ps, pso, out=pout)
-    e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = cells * ws * e2e_steps / float(te.item()) / 1e9
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = cells * ws * e2e_steps / e2e_s / 1e9
+    e2e_same = bool(np.array_equal(pout, got))
 
     # roofline of the dominant kernel (fill): cells per launch / mean launch time
     n_sm, cells_per_clk, rate_src = measured_alu_peak()
@@ -387,22 +431,52 @@ def main():
                     # the host API uploads the offsets only for non-uniform chunks
                     "h2d_bytes_per_step": int(q.nbytes + s.nbytes + (0 if uniform_lengths else
                                                                      qo.nbytes + so.nbytes)),
-                    "d2h_bytes_per_step": int(B * 4)},
+                    "d2h_bytes_per_step": int(B * 4), "same_scores_as_device_api": e2e_same},
             "gpu_launches": int(launches),
             "fill_launches": fill_launches,
             "roofline": roof,
             "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
-            "parity_sample_ok": bool(parity)}
+            "generic_scheme": generic}
+    if strong:
+        line["strong_scaling"] = strong
+
+    from oracle import oracle as O
+    osch = O.Scheme(SCHEME["kind"], SCHEME["gap"], SCHEME["match"], SCHEME["mismatch"],
+                    SCHEME["gap_open"], SCHEME["gap_extend"])
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_oracle_baseline(qm, sm)
-    if rank == 0 and ws == 1 and args.long_bp > 0:
-        line["long_pair"] = long_pair_leg(ctx, A, args.long_bp, n_sm, f_mhz)
-    if rank == 0 and ws == 1 and args.long_tb_bp > 0:
+        # the oracle baseline aligns (up to) the whole batch: compare every score it computed
+        cb, oscores = cpu_oracle_baseline(qm, sm)
+        line["cpu_baseline"] = cb
+        k = len(oscores)
+        mism = int(np.count_nonzero(got[:k] != oscores.astype(np.int32)))
+        line["parity"] = {"checked_pairs": k, "of": B, "mismatches": mism,
+                          "parity_full": bool(k == B and mism == 0)}
+    else:
+        # parity spot check of this rank's output (oracle on 64 pairs) -- not timed
+        idx = np.random.default_rng(rank).choice(B, 64, replace=False)
+        mism = sum(int(got[k]) != O.align(osch, qm[k].tobytes(), sm[k].tobytes(), False).score
+                   for k in idx)
+        line["parity"] = {"checked_pairs": 64, "of": B, "mismatches": int(mism),
+                          "parity_full": False}
+
+    # C4 long pair: on N GPUs through one N-device context driven by rank 0
+    if args.long_bp > 0:
+        if ws > 1:
+            dist.barrier(group=cpu_group)
+        if rank == 0:
+            lctx = ctx if ws == 1 else A.Context(list(range(ws)))
+            line["long_pair"] = long_pair_leg(lctx, A, args.long_bp, n_sm, f_mhz, n_gpus=ws)
+            if lctx is not ctx:
+                lctx.close()
+        if ws > 1:
+            dist.barrier(group=cpu_group)
+    if rank == 0 and args.long_tb_bp > 0:
         line["long_traceback"] = long_traceback_leg(ctx, A, args.long_tb_bp)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
     if ws > 1:
+        dist.barrier(group=cpu_group)
         dist.destroy_process_group()
 
 

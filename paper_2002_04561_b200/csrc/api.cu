@@ -157,8 +157,29 @@ anyseq_status fail(anyseq_ctx* c, anyseq_status s, const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(buf, sizeof(buf), fmt, ap);
   va_end(ap);
-  if (c) c->err = buf;
+  if (c) {
+    try {
+      c->err = buf;
+    } catch (...) {  // no exception crosses the ABI, not even from the error path
+    }
+  }
   return s;
+}
+
+// Every extern "C" body runs inside abi_guard: a host allocation failure (std::bad_alloc
+// from a vector, a string or a thread) becomes ANYSEQ_E_NOMEM and any other C++ exception
+// ANYSEQ_E_CUDA, so nothing but a status code crosses the C ABI (include/anyseq.h).
+template <class F>
+anyseq_status abi_guard(anyseq_ctx* c, F&& body) {
+  try {
+    return body();
+  } catch (const std::bad_alloc&) {
+    return fail(c, ANYSEQ_E_NOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(c, ANYSEQ_E_CUDA, "internal error: %s", e.what());
+  } catch (...) {
+    return fail(c, ANYSEQ_E_CUDA, "internal error");
+  }
 }
 
 #define CK(call)                                                                        \
@@ -590,16 +611,20 @@ anyseq_status check_batch_host(anyseq_ctx* ctx, const anyseq_batch* b) {
 // *uq / *us: the common q / s length when every pair of the range has the same lengths
 // (then the chunk's offsets are generated on the device instead of uploaded), else -1.
 anyseq_status check_pairs_host(anyseq_ctx* ctx, const anyseq_batch* b, uint64_t k0, uint64_t k1,
-                               int64_t* uq, int64_t* us) {
+                               int tb, int64_t* uq, int64_t* us) {
+  // traceback: a CIGAR word holds a run of at most 2^28 - 1 (len << 4 | op); an empty
+  // partner makes one gap run of the whole other sequence, so longer sequences are refused
+  const uint64_t lim = tb ? (1ull << 28) : (1ull << 31);
   const uint64_t lq = b->q_off[k0 + 1] - b->q_off[k0], ls = b->s_off[k0 + 1] - b->s_off[k0];
   bool uni = true;
   for (uint64_t k = k0; k < k1; ++k) {
     uni = uni && b->q_off[k + 1] - b->q_off[k] == lq && b->s_off[k + 1] - b->s_off[k] == ls;
     if (b->q_off[k + 1] < b->q_off[k] || b->s_off[k + 1] < b->s_off[k])
       return fail(ctx, ANYSEQ_E_INVALID, "pair %llu: offsets decrease", (unsigned long long)k);
-    if (b->q_off[k + 1] - b->q_off[k] >= (1ull << 31) || b->s_off[k + 1] - b->s_off[k] >= (1ull << 31))
-      return fail(ctx, ANYSEQ_E_INVALID, "pair %llu: sequence longer than 2^31-1",
-                  (unsigned long long)k);
+    if (b->q_off[k + 1] - b->q_off[k] >= lim || b->s_off[k + 1] - b->s_off[k] >= lim)
+      return fail(ctx, tb ? ANYSEQ_E_UNSUPPORTED : ANYSEQ_E_INVALID,
+                  "pair %llu: sequence longer than %s", (unsigned long long)k,
+                  tb ? "2^28-1 (traceback)" : "2^31-1");
   }
   *uq = uni ? (int64_t)lq : -1;
   *us = uni ? (int64_t)ls : -1;
@@ -684,7 +709,7 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
   auto upload = [&](int c) -> anyseq_status {
     const int set = c & 1;
     const uint64_t a0 = cb[c], a1 = cb[c + 1], B = a1 - a0;
-    const anyseq_status chk = check_pairs_host(ctx, b, a0, a1, &gen_q[set], &gen_s[set]);
+    const anyseq_status chk = check_pairs_host(ctx, b, a0, a1, tb, &gen_q[set], &gen_s[set]);
     if (chk != ANYSEQ_OK) return chk;
     const uint64_t q0 = b->q_off[a0], s0 = b->s_off[a0];
     const uint64_t qlen = b->q_off[a1] - q0, slen = b->s_off[a1] - s0;
@@ -829,6 +854,10 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
     std::vector<anyseq_ctx*> sub(G);
     std::vector<std::thread> th;
     std::mutex mu;
+    struct Joiner {  // a failed thread creation must not leave joinable threads behind
+      std::vector<std::thread>& v;
+      ~Joiner() { for (auto& t : v) if (t.joinable()) t.join(); }
+    } joiner{th};
     for (int g = 0; g < G; ++g) {
       th.emplace_back([&, g] {
         anyseq_ctx local;  // per-thread error string
@@ -837,9 +866,11 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
         local.allow16 = ctx->allow16;
         local.chunk_bytes = ctx->chunk_bytes;
         anyseq_status s = ANYSEQ_OK;
-        if (bounds[g + 1] > bounds[g])
-          s = run_host_shard(&local, ctx->devs[g], prm, b, bounds[g], bounds[g + 1], tb, scores,
-                             aln, nullptr, 0, &cigs[g], &words[g]);
+        if (bounds[g + 1] > bounds[g])  // an exception must not escape a std::thread either
+          s = abi_guard(&local, [&]() {
+            return run_host_shard(&local, ctx->devs[g], prm, b, bounds[g], bounds[g + 1], tb,
+                                  scores, aln, nullptr, 0, &cigs[g], &words[g]);
+          });
         std::lock_guard<std::mutex> lk(mu);
         st[g] = s;
         errs[g] = local.err;
@@ -884,6 +915,22 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
 // (run_host_batch, the a4/a5 kernels); their CIGARs are concatenated.
 // Linear gaps only: an affine split must carry the gap state across the cut
 // (Myers-Miller), which the leaf traceback does not take as a boundary condition.
+// Append a run of `len` ops to a CIGAR, merging with the last word when the op repeats;
+// a word holds at most 2^28 - 1 (len << 4 | op), so longer runs split into several words.
+void push_run(std::vector<uint32_t>& ops, uint32_t op, uint64_t len) {
+  constexpr uint64_t kMax = (1u << 28) - 1;
+  if (!ops.empty() && (ops.back() & 15) == op) {
+    const uint64_t room = kMax - (ops.back() >> 4), add = std::min(room, len);
+    ops.back() += (uint32_t)(add << 4);
+    len -= add;
+  }
+  for (; len > 0;) {
+    const uint64_t k = std::min(kMax, len);
+    ops.push_back((uint32_t)(k << 4) | op);
+    len -= k;
+  }
+}
+
 struct HbNode {
   int64_t i0, i1, j0, j1;
 };
@@ -1114,8 +1161,7 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
     score += la[k].score;
     for (uint32_t w = 0; w < la[k].cigar_len; ++w) {
       const uint32_t word = lc[la[k].cigar_offset + w];
-      if (!ops.empty() && (ops.back() & 15) == (word & 15)) ops.back() += word & ~15u;
-      else ops.push_back(word);
+      push_run(ops, word & 15, word >> 4);
     }
   }
   if (prm->kind != ANYSEQ_GLOBAL && score != want)
@@ -1142,9 +1188,21 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
 // =========================================================================== C-ABI
 extern "C" {
 
+static anyseq_status create_impl(anyseq_ctx** out, const int* device_ids, int num_devices);
+
 anyseq_status anyseq_create(anyseq_ctx** out, const int* device_ids, int num_devices) {
   if (!out) return ANYSEQ_E_INVALID;
   *out = nullptr;
+  try {
+    return create_impl(out, device_ids, num_devices);
+  } catch (const std::bad_alloc&) {
+    return ANYSEQ_E_NOMEM;
+  } catch (...) {
+    return ANYSEQ_E_CUDA;
+  }
+}
+
+static anyseq_status create_impl(anyseq_ctx** out, const int* device_ids, int num_devices) {
   if (num_devices < 1) return ANYSEQ_E_INVALID;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -1191,8 +1249,17 @@ anyseq_status anyseq_create(anyseq_ctx** out, const int* device_ids, int num_dev
   return ANYSEQ_OK;
 }
 
+static void destroy_impl(anyseq_ctx* c);
+
 void anyseq_destroy(anyseq_ctx* c) {
   if (!c) return;
+  try {
+    destroy_impl(c);
+  } catch (...) {  // nothing crosses the ABI; the context memory is released regardless
+  }
+}
+
+static void destroy_impl(anyseq_ctx* c) {
   resolve_events(c);
   for (auto& e : c->pool) {
     cudaEventDestroy(e.first);
@@ -1234,137 +1301,149 @@ anyseq_status anyseq_align_batch(anyseq_ctx* ctx, const anyseq_params* params,
                                  const anyseq_batch* batch, int32_t* scores,
                                  anyseq_alignment* ends) {
   if (!ctx) return ANYSEQ_E_INVALID;
-  anyseq_status s = validate_params(ctx, params);
-  if (s != ANYSEQ_OK) return s;
-  if ((s = check_batch_host(ctx, batch)) != ANYSEQ_OK) return s;
-  if (batch->num_pairs == 0) return ANYSEQ_OK;
-  if (!scores) return fail(ctx, ANYSEQ_E_INVALID, "scores is NULL");
-  return run_host_batch(ctx, params, batch, 0, scores, ends, nullptr, 0, nullptr);
+  return abi_guard(ctx, [&]() -> anyseq_status {
+    anyseq_status s = validate_params(ctx, params);
+    if (s != ANYSEQ_OK) return s;
+    if ((s = check_batch_host(ctx, batch)) != ANYSEQ_OK) return s;
+    if (batch->num_pairs == 0) return ANYSEQ_OK;
+    if (!scores) return fail(ctx, ANYSEQ_E_INVALID, "scores is NULL");
+    return run_host_batch(ctx, params, batch, 0, scores, ends, nullptr, 0, nullptr);
+  });
 }
 
 anyseq_status anyseq_traceback(anyseq_ctx* ctx, const anyseq_params* params,
                                const anyseq_batch* batch, anyseq_alignment* out, uint32_t* cigar,
                                uint64_t cigar_capacity, uint64_t* cigar_used) {
   if (!ctx) return ANYSEQ_E_INVALID;
-  anyseq_status s = validate_params(ctx, params);
-  if (s != ANYSEQ_OK) return s;
-  if ((s = check_batch_host(ctx, batch)) != ANYSEQ_OK) return s;
-  if (cigar_used) *cigar_used = 0;
-  if (batch->num_pairs == 0) return ANYSEQ_OK;
-  if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
-  if (!cigar && cigar_capacity) return fail(ctx, ANYSEQ_E_INVALID, "cigar is NULL");
-  std::vector<int32_t> scores(batch->num_pairs);
-  return run_host_batch(ctx, params, batch, 1, scores.data(), out, cigar, cigar_capacity,
-                        cigar_used);
+  return abi_guard(ctx, [&]() -> anyseq_status {
+    anyseq_status s = validate_params(ctx, params);
+    if (s != ANYSEQ_OK) return s;
+    if ((s = check_batch_host(ctx, batch)) != ANYSEQ_OK) return s;
+    if (cigar_used) *cigar_used = 0;
+    if (batch->num_pairs == 0) return ANYSEQ_OK;
+    if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
+    if (!cigar && cigar_capacity) return fail(ctx, ANYSEQ_E_INVALID, "cigar is NULL");
+    std::vector<int32_t> scores(batch->num_pairs);
+    return run_host_batch(ctx, params, batch, 1, scores.data(), out, cigar, cigar_capacity,
+                          cigar_used);
+  });
 }
 
 anyseq_status anyseq_align_batch_device(anyseq_ctx* ctx, const anyseq_params* params,
                                         const anyseq_batch* d_batch, int32_t* d_scores,
                                         anyseq_alignment* d_ends, void* stream) {
   if (!ctx) return ANYSEQ_E_INVALID;
-  anyseq_status s = validate_params(ctx, params);
-  if (s != ANYSEQ_OK) return s;
-  if (!d_batch) return fail(ctx, ANYSEQ_E_INVALID, "batch is NULL");
-  if (d_batch->num_pairs == 0) return ANYSEQ_OK;
-  if (!d_batch->q_off || !d_batch->s_off || !d_scores)
-    return fail(ctx, ANYSEQ_E_INVALID, "NULL device pointer");
-  if (d_batch->num_pairs >= (1ull << 31)) return fail(ctx, ANYSEQ_E_INVALID, "too many pairs");
-  Device& D = ctx->devs[0];
-  CK(cudaSetDevice(D.id));
-  cudaStream_t user = (cudaStream_t)stream;
-  // order the context stream after the caller's stream, run, then order the caller after us
-  cudaEvent_t ev;
-  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  CK(cudaEventRecord(ev, user));
-  CK(cudaStreamWaitEvent(D.stream, ev, 0));
-  // absolute ends of the CSR ranges
-  CK(cudaMemcpyAsync(D.h_small, d_batch->q_off + d_batch->num_pairs, 8, cudaMemcpyDeviceToHost, D.stream));
-  CK(cudaMemcpyAsync(D.h_small + 1, d_batch->s_off + d_batch->num_pairs, 8, cudaMemcpyDeviceToHost, D.stream));
-  CK(cudaStreamSynchronize(D.stream));
-  DeviceJob J;
-  J.d_q = d_batch->q;
-  J.d_qoff = d_batch->q_off;
-  J.d_s = d_batch->s;
-  J.d_soff = d_batch->s_off;
-  J.B = d_batch->num_pairs;
-  J.q_end = D.h_small[0];
-  J.s_end = D.h_small[1];
-  J.tb = 0;
-  J.want_ends = d_ends != nullptr;
-  J.d_scores_out = d_scores;
-  J.d_aln_out = d_ends;
-  s = run_device(ctx, D, params, J, nullptr, 0);
-  CK(cudaEventRecord(ev, D.stream));
-  CK(cudaStreamWaitEvent(user, ev, 0));
-  cudaEventDestroy(ev);
-  return s;
+  return abi_guard(ctx, [&]() -> anyseq_status {
+    anyseq_status s = validate_params(ctx, params);
+    if (s != ANYSEQ_OK) return s;
+    if (!d_batch) return fail(ctx, ANYSEQ_E_INVALID, "batch is NULL");
+    if (d_batch->num_pairs == 0) return ANYSEQ_OK;
+    if (!d_batch->q_off || !d_batch->s_off || !d_scores)
+      return fail(ctx, ANYSEQ_E_INVALID, "NULL device pointer");
+    if (d_batch->num_pairs >= (1ull << 31)) return fail(ctx, ANYSEQ_E_INVALID, "too many pairs");
+    Device& D = ctx->devs[0];
+    CK(cudaSetDevice(D.id));
+    cudaStream_t user = (cudaStream_t)stream;
+    // order the context stream after the caller's stream, run, then order the caller after us
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, user));
+    CK(cudaStreamWaitEvent(D.stream, ev, 0));
+    // absolute ends of the CSR ranges
+    CK(cudaMemcpyAsync(D.h_small, d_batch->q_off + d_batch->num_pairs, 8, cudaMemcpyDeviceToHost, D.stream));
+    CK(cudaMemcpyAsync(D.h_small + 1, d_batch->s_off + d_batch->num_pairs, 8, cudaMemcpyDeviceToHost, D.stream));
+    CK(cudaStreamSynchronize(D.stream));
+    DeviceJob J;
+    J.d_q = d_batch->q;
+    J.d_qoff = d_batch->q_off;
+    J.d_s = d_batch->s;
+    J.d_soff = d_batch->s_off;
+    J.B = d_batch->num_pairs;
+    J.q_end = D.h_small[0];
+    J.s_end = D.h_small[1];
+    J.tb = 0;
+    J.want_ends = d_ends != nullptr;
+    J.d_scores_out = d_scores;
+    J.d_aln_out = d_ends;
+    s = run_device(ctx, D, params, J, nullptr, 0);
+    CK(cudaEventRecord(ev, D.stream));
+    CK(cudaStreamWaitEvent(user, ev, 0));
+    cudaEventDestroy(ev);
+    return s;
+  });
 }
 
 anyseq_status anyseq_sync(anyseq_ctx* ctx) {
   if (!ctx) return ANYSEQ_E_INVALID;
-  for (auto& D : ctx->devs) {
-    CK(cudaSetDevice(D.id));
-    CK(cudaStreamSynchronize(D.stream));
-  }
-  return ANYSEQ_OK;
+  return abi_guard(ctx, [&]() -> anyseq_status {
+    for (auto& D : ctx->devs) {
+      CK(cudaSetDevice(D.id));
+      CK(cudaStreamSynchronize(D.stream));
+    }
+    return ANYSEQ_OK;
+  });
 }
 
 uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
 anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value) {
   if (!ctx || !name) return ANYSEQ_E_INVALID;
-  std::string n(name);
-  if (n == "tb_scratch_bytes") { ctx->tb_scratch_bytes = std::max<int64_t>(value, 1 << 20); return ANYSEQ_OK; }
-  if (n == "timing") { ctx->timing = (int)value; return ANYSEQ_OK; }
-  if (n == "force_variant") { ctx->force_variant = value; return ANYSEQ_OK; }
-  if (n == "chunk_bytes") { ctx->chunk_bytes = std::max<int64_t>(value, 1 << 16); return ANYSEQ_OK; }
-  if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }
-  if (n == "tb_leaf_cells") {
-    if (value < 1) return fail(ctx, ANYSEQ_E_INVALID, "tb_leaf_cells must be >= 1");
-    ctx->tb_leaf_cells = value;
-    return ANYSEQ_OK;
-  }
-  if (n == "long_band_rows") { ctx->long_opt.band_rows = (int)value; return ANYSEQ_OK; }
-  if (n == "long_blocks") { ctx->long_opt.blocks = (int)value; return ANYSEQ_OK; }
-  if (n == "long_strips") { ctx->long_opt.virtual_strips = (int)value; return ANYSEQ_OK; }
-  if (n == "long_profile") { ctx->long_opt.profile = (int)value; return ANYSEQ_OK; }
-  if (n == "long_start_lag") { ctx->long_opt.start_lag = (int)value; return ANYSEQ_OK; }
-  if (n == "long_sleep_ns") { ctx->long_opt.sleep_ns = (int)value; return ANYSEQ_OK; }
-  if (n == "long_narrow") { ctx->long_opt.narrow = (int)value; return ANYSEQ_OK; }
-  if (n == "long_chunk_cols") { ctx->long_opt.chunk_cols = (int)value; return ANYSEQ_OK; }
-  return fail(ctx, ANYSEQ_E_INVALID, "unknown option %s", name);
+  return abi_guard(ctx, [&]() -> anyseq_status {
+    std::string n(name);
+    if (n == "tb_scratch_bytes") { ctx->tb_scratch_bytes = std::max<int64_t>(value, 1 << 20); return ANYSEQ_OK; }
+    if (n == "timing") { ctx->timing = (int)value; return ANYSEQ_OK; }
+    if (n == "force_variant") { ctx->force_variant = value; return ANYSEQ_OK; }
+    if (n == "chunk_bytes") { ctx->chunk_bytes = std::max<int64_t>(value, 1 << 16); return ANYSEQ_OK; }
+    if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }
+    if (n == "tb_leaf_cells") {
+      if (value < 1) return fail(ctx, ANYSEQ_E_INVALID, "tb_leaf_cells must be >= 1");
+      ctx->tb_leaf_cells = value;
+      return ANYSEQ_OK;
+    }
+    if (n == "long_band_rows") { ctx->long_opt.band_rows = (int)value; return ANYSEQ_OK; }
+    if (n == "long_blocks") { ctx->long_opt.blocks = (int)value; return ANYSEQ_OK; }
+    if (n == "long_strips") { ctx->long_opt.virtual_strips = (int)value; return ANYSEQ_OK; }
+    if (n == "long_profile") { ctx->long_opt.profile = (int)value; return ANYSEQ_OK; }
+    if (n == "long_start_lag") { ctx->long_opt.start_lag = (int)value; return ANYSEQ_OK; }
+    if (n == "long_sleep_ns") { ctx->long_opt.sleep_ns = (int)value; return ANYSEQ_OK; }
+    if (n == "long_narrow") { ctx->long_opt.narrow = (int)value; return ANYSEQ_OK; }
+    if (n == "long_chunk_cols") { ctx->long_opt.chunk_cols = (int)value; return ANYSEQ_OK; }
+    return fail(ctx, ANYSEQ_E_INVALID, "unknown option %s", name);
+  });
 }
 
 anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, const char* q,
                                 uint64_t n, const char* s, uint64_t m, anyseq_alignment* out) {
   if (!ctx) return ANYSEQ_E_INVALID;
-  anyseq_status st = validate_params(ctx, params);
-  if (st != ANYSEQ_OK) return st;
-  if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
-  if ((n && !q) || (m && !s)) return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
-  if (n >= (1ull << 31) || m >= (1ull << 31))
-    return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long sequences must be shorter than 2^31");
-  std::vector<LongDevice> ld;
-  for (auto& D : ctx->devs) {
-    LongDevice x;
-    x.id = D.id;
-    x.stream = D.stream;
-    x.num_sms = D.num_sms;
-    ld.push_back(x);
-  }
-  std::string err;
-  uint64_t launches = 0;
-  LongResult r;
-  const int rc = run_long(ld, dev_params(params), q, n, s, m, ctx->long_opt, &r, &err, &launches);
-  ctx->launches += launches;
-  if (rc != 0) return fail(ctx, (anyseq_status)rc, "%s", err.c_str());
-  ctx->long_narrow = r.narrow ? 1 : 0;
-  ctx->long_ms = r.kernel_ms;
-  memset(out, 0, sizeof(*out));
-  out->score = r.score;
-  out->q_end = out->q_begin = r.end_i;
-  out->s_end = out->s_begin = r.end_j;
-  return ANYSEQ_OK;
+  return abi_guard(ctx, [&]() -> anyseq_status {
+    anyseq_status st = validate_params(ctx, params);
+    if (st != ANYSEQ_OK) return st;
+    if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
+    if ((n && !q) || (m && !s)) return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
+    if (n >= (1ull << 31) || m >= (1ull << 31))
+      return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long sequences must be shorter than 2^31");
+    std::vector<LongDevice> ld;
+    for (auto& D : ctx->devs) {
+      LongDevice x;
+      x.id = D.id;
+      x.stream = D.stream;
+      x.num_sms = D.num_sms;
+      ld.push_back(x);
+    }
+    std::string err;
+    uint64_t launches = 0;
+    LongResult r;
+    const int rc = run_long(ld, dev_params(params), q, n, s, m, ctx->long_opt, &r, &err, &launches);
+    ctx->launches += launches;
+    if (rc != 0) return fail(ctx, (anyseq_status)rc, "%s", err.c_str());
+    ctx->long_narrow = r.narrow ? 1 : 0;
+    ctx->long_ms = r.kernel_ms;
+    memset(out, 0, sizeof(*out));
+    out->score = r.score;
+    out->q_end = out->q_begin = r.end_i;
+    out->s_end = out->s_begin = r.end_j;
+    return ANYSEQ_OK;
+  });
 }
 
 anyseq_status anyseq_traceback_long(anyseq_ctx* ctx, const anyseq_params* params, const char* q,
@@ -1372,43 +1451,49 @@ anyseq_status anyseq_traceback_long(anyseq_ctx* ctx, const anyseq_params* params
                                     uint32_t* cigar, uint64_t cigar_capacity,
                                     uint64_t* cigar_used) {
   if (!ctx) return ANYSEQ_E_INVALID;
-  anyseq_status st = validate_params(ctx, params);
-  if (st != ANYSEQ_OK) return st;
-  if (cigar_used) *cigar_used = 0;
-  if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
-  if (!cigar && cigar_capacity) return fail(ctx, ANYSEQ_E_INVALID, "cigar is NULL");
-  if ((n && !q) || (m && !s)) return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
-  if (n >= (1ull << 31) || m >= (1ull << 31))
-    return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long sequences must be shorter than 2^31");
-  if (params->gap != ANYSEQ_GAP_LINEAR)
-    return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long traceback: linear gaps only");
-  return run_traceback_long(ctx, params, q, n, s, m, out, cigar, cigar_capacity, cigar_used);
+  return abi_guard(ctx, [&]() -> anyseq_status {
+    anyseq_status st = validate_params(ctx, params);
+    if (st != ANYSEQ_OK) return st;
+    if (cigar_used) *cigar_used = 0;
+    if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
+    if (!cigar && cigar_capacity) return fail(ctx, ANYSEQ_E_INVALID, "cigar is NULL");
+    if ((n && !q) || (m && !s)) return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
+    if (n >= (1ull << 31) || m >= (1ull << 31))
+      return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long sequences must be shorter than 2^31");
+    if (params->gap != ANYSEQ_GAP_LINEAR)
+      return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long traceback: linear gaps only");
+    return run_traceback_long(ctx, params, q, n, s, m, out, cigar, cigar_capacity, cigar_used);
+  });
 }
 
 anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) {
   if (!ctx || !name || !value) return ANYSEQ_E_INVALID;
-  for (auto& D : ctx->devs) {
-    cudaSetDevice(D.id);
-  }
-  resolve_events(ctx);
-  std::string n(name);
-  if (n == "fill_ms") { *value = ctx->fill_ms; return ANYSEQ_OK; }
-  if (n == "walk_ms") { *value = ctx->walk_ms; return ANYSEQ_OK; }
-  if (n == "long_narrow") { *value = ctx->long_narrow; return ANYSEQ_OK; }
-  if (n == "long_kernel_ms") { *value = ctx->long_ms; return ANYSEQ_OK; }
-  if (n == "tb_pass_ms") { *value = ctx->tb_pass_ms; return ANYSEQ_OK; }
-  if (n == "tb_pass_cells") { *value = ctx->tb_pass_cells; return ANYSEQ_OK; }
-  if (n == "tb_leaf_ms") { *value = ctx->tb_leaf_ms; return ANYSEQ_OK; }
-  if (n == "fill_launches") { *value = (double)ctx->fill_launches; return ANYSEQ_OK; }
-  return fail(ctx, ANYSEQ_E_INVALID, "unknown stat %s", name);
+  return abi_guard(ctx, [&]() -> anyseq_status {
+    for (auto& D : ctx->devs) {
+      cudaSetDevice(D.id);
+    }
+    resolve_events(ctx);
+    std::string n(name);
+    if (n == "fill_ms") { *value = ctx->fill_ms; return ANYSEQ_OK; }
+    if (n == "walk_ms") { *value = ctx->walk_ms; return ANYSEQ_OK; }
+    if (n == "long_narrow") { *value = ctx->long_narrow; return ANYSEQ_OK; }
+    if (n == "long_kernel_ms") { *value = ctx->long_ms; return ANYSEQ_OK; }
+    if (n == "tb_pass_ms") { *value = ctx->tb_pass_ms; return ANYSEQ_OK; }
+    if (n == "tb_pass_cells") { *value = ctx->tb_pass_cells; return ANYSEQ_OK; }
+    if (n == "tb_leaf_ms") { *value = ctx->tb_leaf_ms; return ANYSEQ_OK; }
+    if (n == "fill_launches") { *value = (double)ctx->fill_launches; return ANYSEQ_OK; }
+    return fail(ctx, ANYSEQ_E_INVALID, "unknown stat %s", name);
+  });
 }
 
 anyseq_status anyseq_reset_stats(anyseq_ctx* ctx) {
   if (!ctx) return ANYSEQ_E_INVALID;
-  resolve_events(ctx);
-  ctx->fill_ms = ctx->walk_ms = 0;
-  ctx->fill_launches = 0;
-  return ANYSEQ_OK;
+  return abi_guard(ctx, [&]() -> anyseq_status {
+    resolve_events(ctx);
+    ctx->fill_ms = ctx->walk_ms = 0;
+    ctx->fill_launches = 0;
+    return ANYSEQ_OK;
+  });
 }
 
 const char* anyseq_status_str(anyseq_status s) {

@@ -22,7 +22,7 @@ struct FillArgs {
   int32_t* end_j;
   uint4* strip_scratch;       // per resident lane group: strip_stride entries (H, E, bits)
   int64_t strip_stride;
-  uint32_t* dirs;             // TB: direction nibbles
+  uint32_t* dirs;             // TB: per-cell H store (one 32-bit word per lane, row, diagonal)
   int64_t dir_block_words;    // TB: words per slot block (fixed per launch)
   TbInfo* tb;                 // TB: per pair
   int32_t one;                // = 1 at run time (keeps IMAD-based adds on the FMA pipe)

@@ -1,4 +1,4 @@
-// csrc/fill_tb.cu -- traceback (direction nibble) instances.
+// csrc/fill_tb.cu -- traceback instances (the fill stores every cell's H for the walk).
 #include "fill_inst.cuh"
 namespace anyseq {
 FillFn fill_fn_tb(int v, int kind, int gap, bool pos) {

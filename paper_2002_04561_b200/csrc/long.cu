@@ -526,7 +526,25 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
       return ANYSEQ_E_UNSUPPORTED;
     }
   }
-  const int ND = (int)devs.size();
+  // Devices: one column strip per context entry; consecutive entries naming the same GPU
+  // form one group that runs its strips in ONE launch (column-strip-major tickets, the
+  // virtual-strip protocol) -- kernels that wait on each other are never launched side by
+  // side on one GPU (they need not be co-scheduled).  A GPU named twice non-adjacently is
+  // rejected for the same reason.
+  const int NE = (int)devs.size();
+  std::vector<int> gfirst, gcount;  // per group: first entry (= first strip), entries
+  for (int e = 0; e < NE; ++e) {
+    if (e > 0 && devs[e].id == devs[e - 1].id) { ++gcount.back(); continue; }
+    for (int f = 0; f < e; ++f)
+      if (devs[f].id == devs[e].id) {
+        *err = "long pairs: device " + std::to_string(devs[e].id) +
+               " is listed twice non-adjacently (its strips must run in one launch)";
+        return ANYSEQ_E_INVALID;
+      }
+    gfirst.push_back(e);
+    gcount.push_back(1);
+  }
+  const int ND = (int)gfirst.size();  // distinct devices (groups)
   // rows per lane: 16 (168 registers, 3 blocks/SM; default) or 12 (128 registers, 4
   // blocks/SM; option long_band_rows = 384) -- measured equal within noise on C4
   const int R = opt.band_rows == 384 ? 12 : 16;
@@ -557,8 +575,8 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   }
   out->narrow = narrow;
   const int S = (int)((n + HS - 1) / HS);
-  int Gtot = ND > 1 ? ND : std::max(1, opt.virtual_strips);
-  if (ND == 1 && opt.virtual_strips <= 0) {
+  int Gtot = NE > 1 ? NE : std::max(1, opt.virtual_strips);
+  if (NE == 1 && opt.virtual_strips <= 0) {
     // Auto: every task spans its column strip, so the last round of S*G tasks over W
     // resident warps idles the rest; G column passes (tickets column-strip major, so a
     // task's left edge was finished a pass earlier) shrink that round's share.
@@ -575,6 +593,10 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
       if (score > best + 1e-9) { best = score; Gtot = G; }
     }
   }
+  if (NE > 1 && (uint64_t)Gtot > m) {
+    *err = "long pairs: more devices than subject columns";
+    return ANYSEQ_E_INVALID;
+  }
   Gtot = (int)std::min<uint64_t>(Gtot, m);
   std::vector<int32_t> cb(Gtot + 1);
   for (int g = 0; g <= Gtot; ++g) cb[g] = (int32_t)((m * (uint64_t)g) / Gtot);
@@ -589,32 +611,33 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   std::vector<PerDev> pd(ND);
   std::vector<int2*> bcol_ptr(Gtot + 1, nullptr);  // edge g buffer lives on its consumer device
   std::vector<int32_t*> flag_ptr(Gtot + 1, nullptr);
-  // column strips per device
+  // column strips per device group (one strip per entry; a single entry: all Gtot strips)
+  std::vector<LongDevice> gdev(ND);
   for (int d = 0; d < ND; ++d) {
-    pd[d].g_first = ND > 1 ? d : 0;
-    pd[d].g_count = ND > 1 ? (d < Gtot ? 1 : 0) : Gtot;
+    gdev[d] = devs[gfirst[d]];
+    pd[d].g_first = NE > 1 ? gfirst[d] : 0;
+    pd[d].g_count = NE > 1 ? gcount[d] : Gtot;
   }
-  // peer access between neighbours
-  if (ND > 1) {
-    for (int d = 0; d + 1 < ND; ++d) {
-      int ok = 0;
-      LK(cudaDeviceCanAccessPeer(&ok, devs[d].id, devs[d + 1].id));
-      if (!ok) {
-        *err = "peer access unavailable between devices " + std::to_string(devs[d].id) + " and " +
-               std::to_string(devs[d + 1].id);
-        return ANYSEQ_E_PEER;
-      }
-      cudaSetDevice(devs[d].id);
-      cudaError_t e = cudaDeviceEnablePeerAccess(devs[d + 1].id, 0);
-      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) LK(e);
-      cudaGetLastError();
+  // peer access between neighbouring groups (distinct devices by construction): the producer
+  // of edge g stores into the consumer's column buffer and flags
+  for (int d = 0; d + 1 < ND; ++d) {
+    int ok = 0;
+    LK(cudaDeviceCanAccessPeer(&ok, gdev[d].id, gdev[d + 1].id));
+    if (!ok) {
+      *err = "peer access unavailable between devices " + std::to_string(gdev[d].id) + " and " +
+             std::to_string(gdev[d + 1].id);
+      return ANYSEQ_E_PEER;
     }
+    cudaSetDevice(gdev[d].id);
+    cudaError_t e = cudaDeviceEnablePeerAccess(gdev[d + 1].id, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) LK(e);
+    cudaGetLastError();
   }
   // allocation + upload + pack
   for (int d = 0; d < ND; ++d) {
     PerDev& D = pd[d];
-    LK(cudaSetDevice(devs[d].id));
-    cudaStream_t st = devs[d].stream;
+    LK(cudaSetDevice(gdev[d].id));
+    cudaStream_t st = gdev[d].stream;
     LK(cudaMalloc(&D.qa.p, n + 16));
     LK(cudaMalloc(&D.sa.p, m + 16));
     LK(cudaMalloc(&D.qc.p, n + 16));
@@ -634,7 +657,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     LK(cudaMemcpy(off.p, offs, 32, cudaMemcpyHostToDevice));
     LK(launch_pack((const char*)D.qa.p, n, (uint8_t*)D.qc.p, (const uint64_t*)off.p,
                    (const char*)D.sa.p, m, (uint8_t*)D.sc.p, (const uint64_t*)off.p + 2, 1,
-                   (uint32_t*)D.flg.p, (PlanSummary*)D.sum.p, st, devs[d].num_sms));
+                   (uint32_t*)D.flg.p, (PlanSummary*)D.sum.p, st, gdev[d].num_sms));
     *launches += 1;
     LK(cudaMemcpyAsync(&hs, D.sum.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
     LK(cudaStreamSynchronize(st));
@@ -667,7 +690,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     }
     int nb = 0;
     LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0));
-    D.grid = devs[d].num_sms * std::max(nb, 1);
+    D.grid = gdev[d].num_sms * std::max(nb, 1);
     if (opt.blocks > 0) D.grid = std::min(D.grid, opt.blocks);
     LK(cudaMalloc(&D.parts.p, (size_t)D.grid * 4 * sizeof(LongPart)));
   }
@@ -675,23 +698,23 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   // flags of edge g live on the consumer as well (producer stores over NVLink).
   for (int d = 0; d < ND; ++d) {
     PerDev& D = pd[d];
-    LK(cudaSetDevice(devs[d].id));
+    LK(cudaSetDevice(gdev[d].id));
     LK(cudaMemcpyAsync(D.bptr.p, bcol_ptr.data(), (Gtot + 1) * sizeof(int2*), cudaMemcpyHostToDevice,
-                       devs[d].stream));
+                       gdev[d].stream));
     LK(cudaMemcpyAsync(D.fptr.p, flag_ptr.data(), (Gtot + 1) * sizeof(int32_t*), cudaMemcpyHostToDevice,
-                       devs[d].stream));
-    long_init_kernel<<<devs[d].num_sms * 4, 256, 0, devs[d].stream>>>(
+                       gdev[d].stream));
+    long_init_kernel<<<gdev[d].num_sms * 4, 256, 0, gdev[d].stream>>>(
         P, (int)n, (int)m, (int4*)D.rowbuf.p, D.g_first == 0 && D.g_count > 0 ? bcol_ptr[0] : nullptr,
         (int2* const*)D.bptr.p, (const int*)D.cbuf.p, Gtot, D.g_first, D.g_count);
     LK(cudaGetLastError());
     *launches += 1;
-    LK(cudaStreamSynchronize(devs[d].stream));
+    LK(cudaStreamSynchronize(gdev[d].stream));
   }
   // launch (all devices concurrently; their kernels wait on each other only via flags)
   for (int d = 0; d < ND; ++d) {
     PerDev& D = pd[d];
     if (D.g_count == 0) continue;
-    LK(cudaSetDevice(devs[d].id));
+    LK(cudaSetDevice(gdev[d].id));
     LongArgs a;
     a.P = P;
     a.qc = (const uint8_t*)D.qc.p;
@@ -731,10 +754,10 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     a.spin_limit = 1ll << 28;
     LK(cudaEventCreate(&D.e0));
     LK(cudaEventCreate(&D.e1));
-    LK(cudaEventRecord(D.e0, devs[d].stream));
-    fn<<<D.grid, 128, 0, devs[d].stream>>>(a);
+    LK(cudaEventRecord(D.e0, gdev[d].stream));
+    fn<<<D.grid, 128, 0, gdev[d].stream>>>(a);
     LK(cudaGetLastError());
-    LK(cudaEventRecord(D.e1, devs[d].stream));
+    LK(cudaEventRecord(D.e1, gdev[d].stream));
     *launches += 1;
   }
   // gather
@@ -746,8 +769,8 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   for (int d = 0; d < ND; ++d) {
     PerDev& D = pd[d];
     if (D.g_count == 0) continue;
-    LK(cudaSetDevice(devs[d].id));
-    LK(cudaStreamSynchronize(devs[d].stream));
+    LK(cudaSetDevice(gdev[d].id));
+    LK(cudaStreamSynchronize(gdev[d].stream));
     float ms = 0;
     cudaEventElapsedTime(&ms, D.e0, D.e1);
     out->kernel_ms = std::max(out->kernel_ms, (double)ms);
@@ -759,7 +782,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
       unsigned long long pr[3];
       LK(cudaMemcpy(pr, D.profbuf.p, 24, cudaMemcpyDeviceToHost));
       fprintf(stderr, "[anyseq long] device %d: wait cycles %llu, task cycles %llu, tasks %llu, wait share %.3f, grid %d\n",
-              devs[d].id, pr[0], pr[1], pr[2], pr[1] ? (double)pr[0] / pr[1] : 0.0, D.grid);
+              gdev[d].id, pr[0], pr[1], pr[2], pr[1] ? (double)pr[0] / pr[1] : 0.0, D.grid);
     }
     aborted |= ab;
     std::vector<LongPart> parts((size_t)D.grid * 4);

@@ -11,7 +11,7 @@ struct VariantDesc {
   int pairs;  // 2 = VS16 (two alignments per register), 1 = VS32
   int L;      // lanes per group
   int R;      // rows per lane
-  int tb;     // 1 = writes direction nibbles
+  int tb;     // 1 = traceback fill (stores every cell's H)
 };
 
 constexpr int NV = 8;

@@ -194,3 +194,72 @@ def c5_mixed(num_pairs: int, seed: int = 5, lo: int = 100, hi: int = 1000,
     q, qo = csr(qs)
     s, so = csr(ss)
     return q, qo, s, so
+
+
+def _ragged_gather(src: np.ndarray, starts: np.ndarray, lens: np.ndarray) -> np.ndarray:
+    """Concatenation of src[starts[k] : starts[k] + lens[k]] over k (vectorised)."""
+    lens = lens.astype(np.int32)
+    tot = int(lens.sum())
+    it = np.int32 if tot + len(src) < 2**31 else np.int64
+    base = np.repeat((starts.astype(it) - (np.cumsum(lens, dtype=it) - lens)), lens)
+    base += np.arange(tot, dtype=it)
+    return src[base]
+
+
+def c5_mixed_large(num_pairs: int, seed: int = 5, lo: int = 100, hi: int = 1000,
+                   ref_len: int = 10_000_000, chunk: int = 50_000):
+    """C5 at scale (vectorised; same recipe as c5_mixed, its own draw order): L ~ U{lo..hi};
+    s = R window of length L; q = copy of R[pos : pos + L + 32] with 1 % substitutions, then
+    indel events at 0.1 % of positions (insertion or deletion by coin flip, geometric length
+    with mean 1.5, deletions clipped at the copy's end), cut or extended with i.i.d. bases to
+    length L + U{-5..5} (at least 1).  Returns CSR (q, q_off, s, s_off)."""
+    rng = _rng(seed)
+    ref = iid_codes(rng, ref_len)
+    qs, ss, qlens, slens = [], [], [], []
+    for k0 in range(0, num_pairs, chunk):
+        B = min(chunk, num_pairs - k0)
+        L = rng.integers(lo, hi + 1, size=B)
+        dl = rng.integers(-5, 6, size=B)
+        pos = rng.integers(0, ref_len - hi - 64, size=B)
+        ss.append(ALPHA[_ragged_gather(ref, pos, L)])
+        slens.append(L)
+        span = L + 32
+        src = _ragged_gather(ref, pos, span)
+        N = len(src)
+        sub = rng.random(N) < 0.01
+        src[sub] = (src[sub] + rng.integers(1, 4, size=int(sub.sum()), dtype=np.uint8)) % 4
+        pair_end = np.repeat(np.cumsum(span), span)  # exclusive end of each element's pair
+        ev = np.flatnonzero(rng.random(N) < 0.001)
+        glen = rng.geometric(1.0 / 1.5, size=len(ev))
+        is_del = rng.random(len(ev)) < 0.5
+        keep = np.ones(N, dtype=np.int32)
+        d0, dg = ev[is_del], glen[is_del]
+        if len(d0):
+            di = np.repeat(d0, dg) + (np.arange(int(dg.sum())) -
+                                      np.repeat(np.cumsum(dg) - dg, dg))
+            di = di[di < np.repeat(pair_end[d0], dg)]
+            keep[di] = 0
+        ins = np.zeros(N, dtype=np.int32)
+        np.add.at(ins, ev[~is_del], glen[~is_del])
+        cnt = ins + keep  # output symbols per source element: inserted bases, then the element
+        tot = int(cnt.sum())
+        grp = np.repeat(np.arange(N, dtype=np.int32), cnt)
+        r = np.arange(tot, dtype=np.int32) - np.repeat(np.cumsum(cnt, dtype=np.int32) - cnt, cnt)
+        y = np.where(r < ins[grp], iid_codes(rng, tot), src[grp]).astype(np.uint8)
+        newlen = np.add.reduceat(cnt, np.concatenate([[0], np.cumsum(span)[:-1]]))
+        ql = np.maximum(1, L + dl)
+        take = np.minimum(newlen, ql)
+        ystart = np.concatenate([[0], np.cumsum(newlen)[:-1]])
+        qstart = np.concatenate([[0], np.cumsum(ql)[:-1]])
+        out = iid_codes(rng, int(ql.sum()))  # the extension bases where a copy is too short
+        out[_ragged_gather(np.arange(len(out), dtype=np.int32), qstart, take)] = \
+            _ragged_gather(y, ystart, take)
+        qs.append(ALPHA[out])
+        qlens.append(ql)
+    q = np.concatenate(qs)
+    s = np.concatenate(ss)
+    qo = np.zeros(num_pairs + 1, dtype=np.uint64)
+    so = np.zeros(num_pairs + 1, dtype=np.uint64)
+    np.cumsum(np.concatenate(qlens), out=qo[1:])
+    np.cumsum(np.concatenate(slens), out=so[1:])
+    return q, qo, s, so

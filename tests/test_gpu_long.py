@@ -83,19 +83,23 @@ def test_long_bad_byte(ctx):
     assert e.value.status_name == "E_BADSEQ"
 
 
-def test_long_multi_device():
-    """Column strips across real GPUs (peer stores of the boundary column)."""
+@pytest.mark.parametrize("kind,gap,go", [("local", "affine", 5), ("global", "linear", 0),
+                                         ("semi", "affine", 2)])
+def test_long_multi_device(kind, gap, go):
+    """A multi-device context: one column strip per entry.  With several GPUs the boundary
+    column goes over NVLink (peer stores + system-scope flags); on a one-GPU box the entries
+    name GPU 0 repeatedly and form one device group whose strips run in ONE launch (kernels
+    that wait on each other are never launched side by side on one GPU)."""
     import torch
     import paper_2002_04561_b200 as A
     from synth import c4_genomes
     n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     g1, g2 = c4_genomes(60_000, "a", seed=4)
-    o = _orc("local", "affine", 5, g1, g2)
-    with A.Context(list(range(n))) as c:
-        r = c.align_long(A.Scheme("local", "affine", 2, -1, 5, 1), g1, g2)
-    assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end)
+    o = _orc(kind, gap, go, g1, g2)
+    for devs in ([0, 0], [0, 0, 0, 0], list(range(n)) if n >= 2 else [0] * 8):
+        with A.Context(devs) as c:
+            r = c.align_long(A.Scheme(kind, gap, 2, -1, go, 1), g1, g2)
+        assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), devs
 
 
 def test_long_kinds_and_gaps_small_strips(ctx):

@@ -287,3 +287,47 @@ def test_batch_matches_single():
             assert (res["q_end"][k], res["s_end"][k]) == (a.q_end, a.s_end)
             assert (res["q_begin"][k], res["s_begin"][k]) == (a.q_begin, a.s_begin)
             assert cigs[k] == a.cigar
+
+
+def test_lowercase_branch_vs_brute():
+    """oracle_code's lowercase branch (reading R12: ACGTN case-insensitive): mixed-case
+    inputs, including lowercase n, scored against brute force (which maps case itself) and
+    equal to the uppercase spelling -- score, cells and CIGAR."""
+    rng = random.Random(13)
+    for t in range(120):
+        sch = O.Scheme(rng.choice(["global", "local", "semi"]), rng.choice(["linear", "affine"]),
+                       2, -1, rng.randint(0, 4), 1)
+        q = "".join(rng.choice("ACGTNacgtn") for _ in range(rng.randint(0, 5)))
+        s = "".join(rng.choice("ACGTNacgtn") for _ in range(rng.randint(0, 5)))
+        _check_vs_brute(sch, q, s)
+        a, u = O.align(sch, q, s), O.align(sch, q.upper(), s.upper())
+        assert (a.score, a.q_begin, a.s_begin, a.q_end, a.s_end, a.cigar) == \
+               (u.score, u.q_begin, u.s_begin, u.q_end, u.s_end, u.cigar)
+
+
+def test_invalid_bytes_rejected():
+    """oracle_code's reject branch (R12): every byte outside ACGTNacgtn, at the first, a
+    middle and the last position of q or of s, makes align, score_rolling and batch fail;
+    every byte inside the alphabet is accepted."""
+    import numpy as np
+    ok = set(b"ACGTNacgtn")
+    sch = O.Scheme("local", "affine", 2, -1, 5, 1)
+    for byte in range(256):
+        for pos in (0, 2, 4):
+            bad = bytearray(b"ACGTA")
+            bad[pos] = byte
+            for q, s in ((bytes(bad), b"ACGTA"), (b"ACGTA", bytes(bad))):
+                if byte in ok:
+                    O.align(sch, q, s)
+                    O.score_rolling(sch, q, s)
+                    continue
+                with pytest.raises(ValueError):
+                    O.align(sch, q, s)
+                with pytest.raises(ValueError):
+                    O.score_rolling(sch, q, s)
+        if byte not in ok:
+            qa = np.frombuffer(b"ACGT" + bytes([byte]) + b"GG", np.uint8)
+            sa = np.frombuffer(b"ACGTGG", np.uint8)
+            with pytest.raises(ValueError):
+                O.batch(sch, qa, np.array([0, 3, 7], np.uint64), np.concatenate([sa, sa]),
+                        np.array([0, 6, 12], np.uint64))

@@ -2,7 +2,7 @@
 # then the launch list of the same bench command under ncu (one ncu tool per call)
 set -x
 ./paper_2002_04561_b200/lib/dpx_bench > gpurun_out/dpx.json 2> gpurun_out/dpx.err
-./tools/pipebench > gpurun_out/pipebench.txt 2>&1
+bash tools/build_tools.sh && ./tools/bin/pipebench > gpurun_out/pipebench.txt 2>&1
 CMD="python bench.py"
 $CMD > gpurun_out/bench_full.log 2>&1
 tail -1 gpurun_out/bench_full.log
