@@ -169,6 +169,8 @@ uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx);
    After anyseq_traceback_long: "tb_pass_ms" (device time of the Hirschberg last-row
    passes, summed over levels), "tb_pass_cells" (cells those passes relaxed) and
    "tb_leaf_ms" (host time of the batched leaf traceback).
+   "h2d_bytes" / "d2h_bytes": bytes the host API copied host -> device (sequences as
+   2-bit codes or ASCII, offsets) and device -> host (results) since the last reset.
    Returns ANYSEQ_E_INVALID for unknown names. */
 anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value);
 anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
@@ -176,6 +178,10 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
 /* Tunables; returns ANYSEQ_E_INVALID for unknown names.
      "chunk_bytes"       host API: bytes of sequence per upload chunk (default 64 MiB;
                          the first and last chunks are smaller)
+     "pack2"             host API: 1 (default) packs ACGT-only chunks to 2-bit codes on
+                         host threads and uploads those (a quarter of the bytes; the device
+                         expands them); chunks with N or other bytes go up as ASCII.  0 =
+                         always ASCII
      "tb_scratch_bytes"  traceback: device bytes of the per-cell H store per fill/walk
                          chunk (default 16 GiB; 2 B per cell for s16x2 slots)
      "allow16"           0 forces 32-bit arithmetic (debug); "force_variant" (debug)

@@ -22,7 +22,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["api.cu", "kernels.cu", "fill_dispatch.cu", "fill_s16.cu", "fill_s16_spec.cu", "fill_s32.cu",
            "fill_tb.cu",
-           "long.cu", "hirschberg.cu"]
+           "long.cu", "long16_global.cu", "long16_local.cu", "long16_semi.cu",
+           "long16_dispatch.cu", "long_tb.cu", "hirschberg.cu", "hostpack.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]

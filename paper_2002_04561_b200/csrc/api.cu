@@ -10,9 +10,11 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -22,6 +24,8 @@
 #include "kernels.h"
 #include "long.h"
 #include "hirschberg.h"
+#include "hostpack.h"
+#include "long_tb.h"
 
 using namespace anyseq;
 
@@ -89,6 +93,7 @@ struct Device {
   cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   PlanSummary* h_sum = nullptr;  // pinned, mapped (written by the publish kernel)
   HostBuf h_stage;               // pinned staging of score-mode results
+  HostBuf h_pack[3];             // pinned 2-bit packed chunks (host API, ACGT-only chunks)
   // score-mode variant launches of one plan run concurrently (each with its own strip
   // scratch): small per-variant launches of mixed-length batches then share the GPU
   DevBuf strip_v[NV], dirs_v[NV];
@@ -107,16 +112,32 @@ struct anyseq_ctx {
   int64_t chunk_bytes = 64ll << 20;  // host-API upload/compute pipelining granularity
   int64_t force_variant = -1;
   int64_t allow16 = 1;
+  int64_t pack2 = 1;        // host API: upload ACGT-only chunks as 2-bit codes
+  std::unique_ptr<PackPool> packpool;  // host packing threads (created on first use)
+  PackPool* shared_pool = nullptr;  // per-device shard contexts use the parent's pool
+  std::mutex pool_mu;
+  PackPool* packer() {
+    if (shared_pool) return shared_pool;
+    std::lock_guard<std::mutex> lk(pool_mu);
+    // one core stays with the thread that drives the device (it waits on the plan summary)
+    if (!packpool)
+      packpool.reset(new PackPool((int)std::max(1u, std::thread::hardware_concurrency() - 1)));
+    return packpool.get();
+  }
   int64_t tb_leaf_cells = 1 << 20;  // long traceback: Hirschberg leaf size (cells)
   double tb_leaf_ms = 0;            // last anyseq_traceback_long: host time of the leaves
   LongOptions long_opt;
   int long_narrow = 0;   // the last anyseq_align_long ran the 16-bit differential kernel
   double long_ms = 0;    // ... and its kernel time (max over devices)
-  double tb_pass_ms = 0, tb_pass_cells = 0;  // last anyseq_traceback_long: last-row passes
+  double tb_pass_ms = 0, tb_pass_cells = 0;  // last anyseq_traceback_long: forward pass(es)
+  double tb_walk_ms = 0, tb_ckpt_bytes = 0;   // ... checkpointed walk time, checkpoint bytes
+  int64_t tb_budget = 0, tb_kc_shift = 0, tb_ck_every = 0;  // options (0 = automatic)
+  int tb_method = 0;  // last anyseq_traceback_long: 1 = checkpoints, 2 = Hirschberg
   int timing = 0;
   std::mutex ev_mu;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> fill_ev, walk_ev, pool;
   double fill_ms = 0, walk_ms = 0;
+  std::atomic<uint64_t> h2d_bytes{0}, d2h_bytes{0};  // host API sequence / result traffic
   uint64_t fill_launches = 0;
   // timing >= 2: labelled events on the device streams, printed by the host API (debug)
   std::vector<std::pair<std::string, cudaEvent_t>> trace;
@@ -275,6 +296,7 @@ struct DeviceJob {
   uint64_t* rebase_soff = nullptr;
   uint64_t rebase_q0 = 0, rebase_s0 = 0;
   int64_t gen_q = -1, gen_s = -1;   // >= 0: offsets are k * gen (not uploaded), see prep
+  int packed2 = 0;                  // d_q / d_s hold 2-bit codes (host-packed ACGT-only chunk)
   uint64_t cig_base = 0;            // traceback: added to every cigar_offset of this job
   int32_t* d_scores_out;      // score mode output (device) or null => ctx buffer
   anyseq_alignment* d_aln_out;  // alignment structs (device) or null => ctx buffer
@@ -329,9 +351,13 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   L(1);
   // byte codes are indexed by absolute CSR position; pack the whole [0, end) range the
   // caller's offsets cover (bytes before off[0] are never read by a pair)
-  CK(launch_pack(J.d_q, J.q_end, D.q_code.as<uint8_t>(), J.d_qoff, J.d_s, J.s_end,
-                 D.s_code.as<uint8_t>(), J.d_soff, B, D.flags.as<uint32_t>(),
-                 D.sum.as<PlanSummary>(), st, D.num_sms));
+  if (J.packed2)
+    CK(launch_unpack2((const uint8_t*)J.d_q, J.q_end, D.q_code.as<uint8_t>(),
+                      (const uint8_t*)J.d_s, J.s_end, D.s_code.as<uint8_t>(), st, D.num_sms));
+  else
+    CK(launch_pack(J.d_q, J.q_end, D.q_code.as<uint8_t>(), J.d_qoff, J.d_s, J.s_end,
+                   D.s_code.as<uint8_t>(), J.d_soff, B, D.flags.as<uint32_t>(),
+                   D.sum.as<PlanSummary>(), st, D.num_sms));
   L(1);
   ctx->mark(st, "packed");
 
@@ -655,12 +681,18 @@ void describe_badseq(anyseq_ctx* ctx, const anyseq_batch* b, uint64_t k0) {
 // Traceback cigar words go straight into the caller's buffer when cig_direct is set (one
 // device: offsets are final), else into *cig (multi-device: rebased after all shards finish).
 // *cig_words receives the shard's total cigar words either way.
+PackPool* pool_of(anyseq_ctx* ctx) { return ctx->packer(); }
+
 anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* prm,
                              const anyseq_batch* b, uint64_t k0, uint64_t k1, int tb,
                              int32_t* scores, anyseq_alignment* aln, uint32_t* cig_direct,
                              uint64_t cig_cap, std::vector<uint32_t>* cig, uint64_t* cig_words) {
   CK(cudaSetDevice(D.id));
   cudaStream_t st = D.stream, cs = D.copy_stream;
+  const auto t_call = std::chrono::steady_clock::now();  // timing >= 2: host timeline
+  auto ms_since = [t_call]() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();
+  };
   // chunk boundaries by cumulative sequence bytes (offsets are monotone)
   std::vector<uint64_t> cb{k0};
   {
@@ -706,6 +738,84 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     if (stage_a) memcpy(aln + a0, h_al + a0, B * sizeof(anyseq_alignment));
   };
   int64_t gen_q[2] = {-1, -1}, gen_s[2] = {-1, -1};  // per buffer set (see check_pairs_host)
+  int packed[2] = {0, 0};       // per buffer set: the chunk went up as 2-bit codes
+  uint64_t s2off[2] = {0, 0};   // ... and its s codes start at this byte of the blob
+  // a1, 2-bit path: a pack-ahead thread packs chunk after chunk on the host pool (validation
+  // fused) into a ring of three pinned staging slots while this thread drives the device;
+  // chunk c waits only for its own packing, and the packer reuses a slot once the upload of
+  // the chunk three back has completed.  A chunk with any byte outside ACGTacgt (N
+  // included) goes up as ASCII instead; the device pack then validates it and flags N.
+  PackPool* pool = ctx->pack2 ? pool_of(ctx) : nullptr;
+  struct Ahead {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<int> state;   // per chunk: 0 pending, 1 packed, 2 take the ASCII path
+    std::vector<char> issued; // per chunk: its upload was issued (slot event recorded)
+    bool stop = false;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    std::thread th;
+    ~Ahead() {
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        stop = true;
+      }
+      cv.notify_all();
+      if (th.joinable()) th.join();
+      for (auto e : ev) if (e) cudaEventDestroy(e);
+    }
+  } ahead;
+  auto chunk_sizes = [&](int c, uint64_t* qb, uint64_t* sb) {
+    const uint64_t qlen = b->q_off[cb[c + 1]] - b->q_off[cb[c]];
+    const uint64_t slen = b->s_off[cb[c + 1]] - b->s_off[cb[c]];
+    *qb = ((qlen + 3) / 4 + 15) & ~15ull;
+    *sb = ((slen + 3) / 4 + 15) & ~15ull;
+  };
+  if (pool && NC > 0) {
+    uint64_t need = 0;
+    for (int c = 0; c < NC; ++c) {
+      uint64_t qb, sb;
+      chunk_sizes(c, &qb, &sb);
+      need = std::max(need, qb + sb + 16);
+    }
+    for (int k = 0; k < 3; ++k) {
+      CK(D.h_pack[k].ensure(need));
+      CK(cudaEventCreateWithFlags(&ahead.ev[k], cudaEventDisableTiming));
+    }
+    ahead.state.assign(NC, 0);
+    ahead.issued.assign(NC, 0);
+    const int dev = D.id;
+    ahead.th = std::thread([&, dev, ms_since] {
+      cudaSetDevice(dev);
+      for (int c = 0; c < NC; ++c) {
+        const int slot = c % 3;
+        if (c >= 3) {  // the slot's previous upload (chunk c - 3) must have completed
+          std::unique_lock<std::mutex> lk(ahead.mu);
+          ahead.cv.wait(lk, [&] { return ahead.stop || ahead.issued[c - 3]; });
+          if (ahead.stop) return;
+          lk.unlock();
+          cudaEventSynchronize(ahead.ev[slot]);
+        }
+        uint64_t qb, sb;
+        chunk_sizes(c, &qb, &sb);
+        const uint64_t q0 = b->q_off[cb[c]], s0 = b->s_off[cb[c]];
+        uint8_t* hp = (uint8_t*)D.h_pack[slot].p;
+        bool ok2 = false;
+        const double tp0 = ms_since();
+        try {
+          ok2 = pool->pack2(b->q + q0, b->q_off[cb[c + 1]] - q0, hp) &&
+                pool->pack2(b->s + s0, b->s_off[cb[c + 1]] - s0, hp + qb);
+        } catch (...) {
+          ok2 = false;  // (allocation failure in the pool) -> the ASCII path
+        }
+        if (ctx->timing >= 2)
+          fprintf(stderr, "[host] pack %d: %.3f -> %.3f ms\n", c, tp0, ms_since());
+        std::lock_guard<std::mutex> lk(ahead.mu);
+        ahead.state[c] = ok2 ? 1 : 2;
+        ahead.cv.notify_all();
+        if (ahead.stop) return;
+      }
+    });
+  }
   auto upload = [&](int c) -> anyseq_status {
     const int set = c & 1;
     const uint64_t a0 = cb[c], a1 = cb[c + 1], B = a1 - a0;
@@ -713,18 +823,47 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     if (chk != ANYSEQ_OK) return chk;
     const uint64_t q0 = b->q_off[a0], s0 = b->s_off[a0];
     const uint64_t qlen = b->q_off[a1] - q0, slen = b->s_off[a1] - s0;
-    CK(D.q_ascii2[set].ensure(qlen + 16));
+    CK(D.q_ascii2[set].ensure(qlen + 64));
     CK(D.s_ascii2[set].ensure(slen + 16));
     CK(D.q_off2[set].ensure((B + 1) * 8));
     CK(D.s_off2[set].ensure((B + 1) * 8));
     // the previous user of this set (chunk c-2) is finished: its offsets are read up to the
     // last kernel of the chunk, not just by the pack kernels
     CK(cudaStreamWaitEvent(cs, D.ev_free[set], 0));
-    if (qlen) CK(cudaMemcpyAsync(D.q_ascii2[set].p, b->q + q0, qlen, cudaMemcpyHostToDevice, cs));
-    if (slen) CK(cudaMemcpyAsync(D.s_ascii2[set].p, b->s + s0, slen, cudaMemcpyHostToDevice, cs));
+    packed[set] = 0;
+    if (pool) {
+      int stt;
+      {
+        std::unique_lock<std::mutex> lk(ahead.mu);
+        ahead.cv.wait(lk, [&] { return ahead.state[c] != 0; });
+        stt = ahead.state[c];
+      }
+      if (ctx->timing >= 2) fprintf(stderr, "[host] chunk %d packed-wait done %.3f ms\n", c, ms_since());
+      const int slot = c % 3;
+      if (stt == 1) {
+        uint64_t qb, sb;
+        chunk_sizes(c, &qb, &sb);
+        packed[set] = 1;
+        s2off[set] = qb;
+        CK(cudaMemcpyAsync(D.q_ascii2[set].p, D.h_pack[slot].p, qb + sb, cudaMemcpyHostToDevice, cs));
+        ctx->h2d_bytes += qb + sb;
+      }
+      CK(cudaEventRecord(ahead.ev[slot], cs));
+      {
+        std::lock_guard<std::mutex> lk(ahead.mu);
+        ahead.issued[c] = 1;
+      }
+      ahead.cv.notify_all();
+    }
+    if (!packed[set]) {
+      if (qlen) CK(cudaMemcpyAsync(D.q_ascii2[set].p, b->q + q0, qlen, cudaMemcpyHostToDevice, cs));
+      if (slen) CK(cudaMemcpyAsync(D.s_ascii2[set].p, b->s + s0, slen, cudaMemcpyHostToDevice, cs));
+      ctx->h2d_bytes += qlen + slen;
+    }
     if (gen_q[set] < 0) {  // uniform chunks: offsets generated on the device (prep kernel)
       CK(cudaMemcpyAsync(D.q_off2[set].p, b->q_off + a0, (B + 1) * 8, cudaMemcpyHostToDevice, cs));
       CK(cudaMemcpyAsync(D.s_off2[set].p, b->s_off + a0, (B + 1) * 8, cudaMemcpyHostToDevice, cs));
+      ctx->h2d_bytes += 2 * (B + 1) * 8;
     }
     CK(cudaEventRecord(D.ev_up[set], cs));
     return ANYSEQ_OK;
@@ -737,17 +876,24 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
   if (s != ANYSEQ_OK) return s;
   mark(cs, "up-end", 0);
   uint64_t cig_base = 0;
+  // ASCII path: the upload of chunk c+1 is issued before chunk c's compute (the copy engine
+  // is the bottleneck); 2-bit path: after it, so that chunk c's kernels never wait for the
+  // packing of chunk c+1 (the packer thread runs ahead on its own)
+  auto upload_next = [&](int c) -> anyseq_status {
+    if (c + 1 >= NC) return ANYSEQ_OK;
+    mark(cs, "up-begin", c + 1);
+    const anyseq_status u = upload(c + 1);
+    if (u != ANYSEQ_OK) {
+      cudaStreamSynchronize(cs);  // chunk c may be in flight: leave the device idle
+      cudaStreamSynchronize(st);
+      return u;
+    }
+    mark(cs, "up-end", c + 1);
+    return ANYSEQ_OK;
+  };
   for (int c = 0; c < NC; ++c) {
     const int set = c & 1;
-    if (c + 1 < NC) {
-      mark(cs, "up-begin", c + 1);
-      if ((s = upload(c + 1)) != ANYSEQ_OK) {
-        cudaStreamSynchronize(cs);  // chunk c may be in flight: leave the device idle
-        cudaStreamSynchronize(st);
-        return s;
-      }
-      mark(cs, "up-end", c + 1);
-    }
+    if (!pool && (s = upload_next(c)) != ANYSEQ_OK) return s;
     mark(st, "compute-begin", c);
     const uint64_t a0 = cb[c], a1 = cb[c + 1], B = a1 - a0;
     const uint64_t q0 = b->q_off[a0], s0 = b->s_off[a0];
@@ -758,7 +904,8 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     DeviceJob J;
     J.d_q = D.q_ascii2[set].as<char>();
     J.d_qoff = D.q_off2[set].as<uint64_t>();
-    J.d_s = D.s_ascii2[set].as<char>();
+    J.d_s = packed[set] ? D.q_ascii2[set].as<char>() + s2off[set] : D.s_ascii2[set].as<char>();
+    J.packed2 = packed[set];
     J.d_soff = D.s_off2[set].as<uint64_t>();
     J.rebase_qoff = D.q_off2[set].as<uint64_t>();
     J.rebase_soff = D.s_off2[set].as<uint64_t>();
@@ -779,7 +926,13 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
       cap_words = qlen + slen + 1;  // worst case sum(n+m); exact total known after the walk
       CK(D.cigar.ensure(cap_words * 4));
     }
+    const double tr0 = ms_since();
     s = run_device(ctx, D, prm, J, tb ? D.cigar.as<uint32_t>() : nullptr, cap_words);
+    if (ctx->timing >= 2) fprintf(stderr, "[host] chunk %d run_device %.3f -> %.3f ms\n", c, tr0, ms_since());
+    if (s == ANYSEQ_OK && pool) {
+      const anyseq_status u = upload_next(c);
+      if (u != ANYSEQ_OK) return u;
+    }
     if (s == ANYSEQ_OK && c > 0) copy_out(c - 1);  // run_device synchronised past it
     if (s != ANYSEQ_OK) {
       if (s == ANYSEQ_E_BADSEQ) describe_badseq(ctx, b, a0);
@@ -789,11 +942,13 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     }
     if (!tb) {
       CK(cudaMemcpyAsync(h_sc + a0, D.scores.p, B * 4, cudaMemcpyDeviceToHost, st));
+      ctx->d2h_bytes += B * 4 + (aln ? B * sizeof(anyseq_alignment) : 0);
       mark(st, "scores-d2h-issued", c);
       if (aln) CK(cudaMemcpyAsync(h_al + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
     } else {
       // cigar offsets already include cig_base (finalize adds J.cig_base on the device)
       CK(cudaMemcpyAsync(h_al + a0, D.aln.p, B * sizeof(anyseq_alignment), cudaMemcpyDeviceToHost, st));
+      ctx->d2h_bytes += B * sizeof(anyseq_alignment) + J.cigar_total * 4;
       if (J.cigar_total && cig_direct) {
         if (cig_base + J.cigar_total <= cig_cap)
           CK(cudaMemcpyAsync(cig_direct + cig_base, D.cigar.p, J.cigar_total * 4,
@@ -865,6 +1020,8 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
         local.force_variant = ctx->force_variant;
         local.allow16 = ctx->allow16;
         local.chunk_bytes = ctx->chunk_bytes;
+        local.pack2 = ctx->pack2;
+        local.shared_pool = ctx->pack2 ? ctx->packer() : nullptr;
         anyseq_status s = ANYSEQ_OK;
         if (bounds[g + 1] > bounds[g])  // an exception must not escape a std::thread either
           s = abi_guard(&local, [&]() {
@@ -875,6 +1032,8 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
         st[g] = s;
         errs[g] = local.err;
         ctx->launches += local.launches.load();
+        ctx->h2d_bytes += local.h2d_bytes.load();
+        ctx->d2h_bytes += local.d2h_bytes.load();
       });
     }
     for (auto& t : th) t.join();
@@ -935,7 +1094,7 @@ struct HbNode {
   int64_t i0, i1, j0, j1;
 };
 
-anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, const char* q,
+anyseq_status run_traceback_long_hirschberg(anyseq_ctx* ctx, const anyseq_params* prm, const char* q,
                                  uint64_t n, const char* s, uint64_t m, anyseq_alignment* out,
                                  uint32_t* cigar, uint64_t cap, uint64_t* used) {
   Device& D = ctx->devs[0];
@@ -1183,6 +1342,80 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
   return ANYSEQ_OK;
 }
 
+// Linear-space long traceback from checkpoints (long_tb.cu): ONE forward pass of the 16-bit
+// long kernel keeps the DP rows at row-block and the DP columns at column-block boundaries
+// (and finds the optimum); the walk recomputes one tile at a time from them, so every
+// decision is the full-matrix one (bit-exact with the oracle's traceback), for every kind
+// and both gap models.  Falls back to Hirschberg (linear gaps only) when the 16-bit kernel
+// cannot run the pair (an N in the subject, or the range guard).
+anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, const char* q,
+                                 uint64_t n, const char* s, uint64_t m, anyseq_alignment* out,
+                                 uint32_t* cigar, uint64_t cap, uint64_t* used) {
+  ctx->tb_pass_ms = ctx->tb_pass_cells = ctx->tb_walk_ms = ctx->tb_ckpt_bytes = 0;
+  ctx->tb_leaf_ms = 0;
+  ctx->tb_method = 1;
+  const DevParams dp = dev_params(prm);
+  memset(out, 0, sizeof(*out));
+  std::vector<uint32_t> ops;
+  if (n == 0 || m == 0) {  // one gap run (global) or the empty alignment
+    if (prm->kind == ANYSEQ_GLOBAL && n + m) {
+      push_run(ops, n ? 1u : 2u, n + m);
+      out->score = (int32_t)(-(dp.go + (int64_t)(n + m) * dp.ge));
+      out->q_end = (int64_t)n;
+      out->s_end = (int64_t)m;
+    }
+  } else {
+    Device& D = ctx->devs[0];
+    CK(cudaSetDevice(D.id));
+    LongDevice ld{D.id, D.stream, D.num_sms};
+    std::vector<LongDevice> one{ld};
+    LongCkpt ck;
+    ck.want = 1;
+    ck.budget = ctx->tb_budget;
+    ck.force_kc_shift = (int)ctx->tb_kc_shift;
+    ck.force_ck_every = (int)ctx->tb_ck_every;
+    LongResult r;
+    std::string err;
+    uint64_t launches = 0;
+    int rc = run_long(one, dp, q, n, s, m, ctx->long_opt, &r, &err, &launches, &ck);
+    ctx->launches += launches;
+    if (rc == ANYSEQ_E_UNSUPPORTED && prm->gap == ANYSEQ_GAP_LINEAR) {
+      ctx->tb_method = 2;
+      return run_traceback_long_hirschberg(ctx, prm, q, n, s, m, out, cigar, cap, used);
+    }
+    if (rc != 0) return fail(ctx, (anyseq_status)rc, "%s", err.c_str());
+    ctx->tb_pass_ms = r.kernel_ms;
+    ctx->tb_pass_cells = (double)n * (double)m;
+    ctx->tb_ckpt_bytes = (double)ck.bytes;
+    int8_t sig[25];
+    for (int a = 0; a < 5; ++a)
+      for (int b = 0; b < 5; ++b)
+        sig[5 * a + b] = (int8_t)(prm->has_subst ? prm->subst[5 * a + b]
+                                                 : ((a == b && a < 4) ? prm->match : prm->mismatch));
+    int64_t bi = 0, bj = 0;
+    double wms = 0;
+    launches = 0;
+    rc = run_long_traceback(ld, dp, sig, ck, r.end_i, r.end_j, (int64_t)n, (int64_t)m, &ops, &bi,
+                            &bj, &wms, &err, &launches);
+    ctx->launches += launches;
+    if (rc != 0) return fail(ctx, (anyseq_status)rc, "%s", err.c_str());
+    ctx->tb_walk_ms = wms;
+    out->score = r.score;
+    out->q_begin = bi;
+    out->s_begin = bj;
+    out->q_end = r.end_i;
+    out->s_end = r.end_j;
+  }
+  if (used) *used = ops.size();
+  if (ops.size() > cap)
+    return fail(ctx, ANYSEQ_E_CAPACITY, "cigar needs %llu words, capacity %llu",
+                (unsigned long long)ops.size(), (unsigned long long)cap);
+  if (!ops.empty()) memcpy(cigar, ops.data(), ops.size() * sizeof(uint32_t));
+  out->cigar_offset = 0;
+  out->cigar_len = (uint32_t)ops.size();
+  return ANYSEQ_OK;
+}
+
 }  // namespace
 
 // =========================================================================== C-ABI
@@ -1274,6 +1507,7 @@ static void destroy_impl(anyseq_ctx* c) {
                       &D.cigar,   &D.temp,    &D.sum,    &D.long_ws, &D.tickets};
     for (DevBuf* b : bufs) b->release();
     D.h_stage.release();
+    for (auto& hp : D.h_pack) hp.release();
     if (D.h_sum) cudaFreeHost(D.h_sum);
     if (D.h_small) cudaFreeHost(D.h_small);
     for (int i = 0; i < 2; ++i) {
@@ -1395,6 +1629,19 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
     if (n == "force_variant") { ctx->force_variant = value; return ANYSEQ_OK; }
     if (n == "chunk_bytes") { ctx->chunk_bytes = std::max<int64_t>(value, 1 << 16); return ANYSEQ_OK; }
     if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }
+    if (n == "pack2") { ctx->pack2 = value ? 1 : 0; return ANYSEQ_OK; }
+    if (n == "tb_ckpt_bytes") { ctx->tb_budget = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
+    if (n == "tb_kc_shift") {
+      if (value != 0 && (value < 8 || value > 12))
+        return fail(ctx, ANYSEQ_E_INVALID, "tb_kc_shift must be 0 or in [8, 12]");
+      ctx->tb_kc_shift = value;
+      return ANYSEQ_OK;
+    }
+    if (n == "tb_ck_every") {
+      if (value < 0 || value > 8) return fail(ctx, ANYSEQ_E_INVALID, "tb_ck_every must be in [0, 8]");
+      ctx->tb_ck_every = value;
+      return ANYSEQ_OK;
+    }
     if (n == "tb_leaf_cells") {
       if (value < 1) return fail(ctx, ANYSEQ_E_INVALID, "tb_leaf_cells must be >= 1");
       ctx->tb_leaf_cells = value;
@@ -1460,8 +1707,6 @@ anyseq_status anyseq_traceback_long(anyseq_ctx* ctx, const anyseq_params* params
     if ((n && !q) || (m && !s)) return fail(ctx, ANYSEQ_E_INVALID, "sequence pointer is NULL");
     if (n >= (1ull << 31) || m >= (1ull << 31))
       return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long sequences must be shorter than 2^31");
-    if (params->gap != ANYSEQ_GAP_LINEAR)
-      return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long traceback: linear gaps only");
     return run_traceback_long(ctx, params, q, n, s, m, out, cigar, cigar_capacity, cigar_used);
   });
 }
@@ -1481,7 +1726,12 @@ anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) 
     if (n == "tb_pass_ms") { *value = ctx->tb_pass_ms; return ANYSEQ_OK; }
     if (n == "tb_pass_cells") { *value = ctx->tb_pass_cells; return ANYSEQ_OK; }
     if (n == "tb_leaf_ms") { *value = ctx->tb_leaf_ms; return ANYSEQ_OK; }
+    if (n == "tb_walk_ms") { *value = ctx->tb_walk_ms; return ANYSEQ_OK; }
+    if (n == "tb_ckpt_bytes") { *value = ctx->tb_ckpt_bytes; return ANYSEQ_OK; }
+    if (n == "tb_method") { *value = ctx->tb_method; return ANYSEQ_OK; }
     if (n == "fill_launches") { *value = (double)ctx->fill_launches; return ANYSEQ_OK; }
+    if (n == "h2d_bytes") { *value = (double)ctx->h2d_bytes.load(); return ANYSEQ_OK; }
+    if (n == "d2h_bytes") { *value = (double)ctx->d2h_bytes.load(); return ANYSEQ_OK; }
     return fail(ctx, ANYSEQ_E_INVALID, "unknown stat %s", name);
   });
 }
@@ -1492,6 +1742,8 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx) {
     resolve_events(ctx);
     ctx->fill_ms = ctx->walk_ms = 0;
     ctx->fill_launches = 0;
+    ctx->h2d_bytes = 0;
+    ctx->d2h_bytes = 0;
     return ANYSEQ_OK;
   });
 }

@@ -113,6 +113,44 @@ cudaError_t launch_pack(const char* d_q, uint64_t q_len, uint8_t* d_qcode, const
   return cudaGetLastError();
 }
 
+// One thread per 16 bases: a 32-bit word of 2-bit codes -> 16 byte codes (one 16-byte store).
+__global__ void __launch_bounds__(256) unpack2_kernel(const uint8_t* __restrict__ q2, uint64_t qn,
+                                                      uint8_t* __restrict__ qc,
+                                                      const uint8_t* __restrict__ s2, uint64_t sn,
+                                                      uint8_t* __restrict__ sc) {
+  const uint64_t u0 = (qn + 15) / 16, units = u0 + (sn + 15) / 16;
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < units;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const bool isq = u < u0;
+    const uint64_t b = (isq ? u : u - u0) * 16, len = isq ? qn : sn;
+    const uint8_t* in = isq ? q2 : s2;
+    uint8_t* out = isq ? qc : sc;
+    // the packed buffers are padded to a 4-byte multiple by the host API
+    const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(in + b / 4));
+    uint32_t o[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t x = w >> (8 * t);  // bases 4t .. 4t+3
+      o[t] = (x & 3u) | ((x << 6) & 0x300u) | ((x << 12) & 0x30000u) | ((x << 18) & 0x3000000u);
+    }
+    if (b + 16 <= len) {
+      *reinterpret_cast<uint4*>(out + b) = make_uint4(o[0], o[1], o[2], o[3]);
+    } else {
+      for (uint64_t k = 0; b + k < len; ++k) out[b + k] = (uint8_t)(o[k >> 2] >> (8 * (k & 3)));
+    }
+  }
+}
+
+cudaError_t launch_unpack2(const uint8_t* d_q2, uint64_t q_len, uint8_t* d_qcode,
+                           const uint8_t* d_s2, uint64_t s_len, uint8_t* d_scode,
+                           cudaStream_t st, int num_sms) {
+  const uint64_t units = (q_len + 15) / 16 + (s_len + 15) / 16;
+  if (units == 0) return cudaSuccess;
+  unpack2_kernel<<<grid_for((int64_t)units, 256, num_sms, 16), 256, 0, st>>>(d_q2, q_len, d_qcode,
+                                                                             d_s2, s_len, d_scode);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------ prep / publish
 __global__ void prep_kernel(uint32_t* flags, uint64_t n, PlanSummary* sum, uint64_t* qoff,
                             uint64_t* soff, uint64_t q0, uint64_t s0, int64_t gq, int64_t gs,

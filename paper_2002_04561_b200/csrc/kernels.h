@@ -15,6 +15,13 @@ cudaError_t launch_pack(const char* d_q, uint64_t q_len, uint8_t* d_qcode, const
                         uint64_t num_pairs, uint32_t* d_flags, PlanSummary* d_sum,
                         cudaStream_t st, int num_sms);
 
+// a1, 2-bit path (host API, ACGT-only chunks): expand 2-bit codes (base p in bits 2 (p % 4)
+// of byte p / 4, packed on the host) into byte codes 0..3; q and s in one launch.  No
+// validation is needed (the host packer admits only ACGTacgt) and no pair has an N.
+cudaError_t launch_unpack2(const uint8_t* d_q2, uint64_t q_len, uint8_t* d_qcode,
+                           const uint8_t* d_s2, uint64_t s_len, uint8_t* d_scode,
+                           cudaStream_t st, int num_sms);
+
 // per-call plan state: clear the per-pair flags, initialise the device summary and (host-API
 // chunks, qoff != null) rebase the verbatim-uploaded offsets to the chunk's first byte
 // fill-launch slot counters zeroed by prep (one per fill launch of a call; more launches

@@ -26,124 +26,9 @@
 #include "../../include/anyseq.h"
 #include "kernels.h"
 #include "long.h"
+#include "long_dev.cuh"
 
 namespace anyseq {
-
-struct LongPart {
-  int32_t lv, li, lj;  // local best (value, i, j)
-  int32_t rv, rj;      // semi: best on row n, j in [0, m-1]
-  int32_t cv, ci;      // semi: best on column m, i in [0, n]
-  int32_t gv, gset;    // global H(n,m)
-  int32_t pad_;
-};
-
-struct LongArgs {
-  DevParams P;
-  const uint8_t* qc;
-  const uint8_t* sc;
-  int32_t n, m;
-  int32_t Gtot, g_first, g_count;
-  const int32_t* cb;  // [Gtot+1]
-  int32_t S;
-  int32_t* ticket;
-  int32_t* rowprog;   // [Gtot * S]
-  int32_t* const* bflag;  // [Gtot+1] per-edge flag arrays of S ints (on the consumer)
-  int2* const* bcol;  // [Gtot+1] column buffers: (H(i, cb[g]), F(i, cb[g])), i = 0..n
-  int4* rowbuf;       // [m+1]: (H, tag, E, tag) of the last completed row at column j
-  LongPart* parts;
-  int32_t* abort_flag;
-  int32_t chunk;
-  int32_t one;
-  int32_t lag;
-  int32_t keyed;  // local: 32 * (max score) fits in 31 bits -> packed (value, row) tracking
-  int32_t sleep_ns;  // long16: back-off of the row hand-off poll
-  int32_t hopc;    // long16: packed -(G_o+G_e) for both halves, low-half borrow compensated
-  int32_t neg16;   // long16: relative "-inf" (below every real relative value)
-  int32_t margin;  // long16: the warp maximum is re-based to -margin
-  int32_t bspan;   // long16: bound on |H(x) - H(y)| over one task window (Lipschitz, d * dist)
-  unsigned long long* prof;  // optional: [0] cycles waiting, [1] cycles in tasks, [2] tasks
-  long long spin_limit;
-};
-
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_sys(const int* p) {
-  int v;
-  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(int* p, int v) {
-  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Row hand-off words: (value, tag) pairs in one 8-byte access each, so a reader that sees
-// the tag of the strip it waits for also sees the value (single-copy atomicity of aligned
-// 8-byte accesses) -- no fences, no progress counters (the LL idea of NCCL's protocols).
-__device__ __forceinline__ void st_row(int4* p, int h, int e, int tag) {
-  asm volatile("st.relaxed.gpu.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(h), "r"(tag),
-               "r"(e), "r"(tag)
-               : "memory");
-}
-__device__ __forceinline__ int4 ld_row(const int4* p) {
-  int4 v;
-  asm volatile("ld.relaxed.gpu.global.v4.s32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p)
-               : "memory");
-  return v;
-}
-
-__device__ __forceinline__ bool lkey_better(int v, int i, int j, int bv, int bi, int bj) {
-  return v > bv || (v == bv && (j < bj || (j == bj && i < bi)));
-}
-
-__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ int ld_relaxed_sys(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// lane 0 polls *p >= need with relaxed loads (no L1 invalidation per poll) and closes with
-// one acquire fence; returns false on timeout/abort (warp-uniform).
-template <bool SYS>
-__device__ __forceinline__ bool warp_wait(const int* p, int need, const LongArgs& a) {
-  int ok = 1;
-  if ((threadIdx.x & 31) == 0) {
-    const long long t0 = a.prof ? clock64() : 0;
-    long long spins = 0;
-    // relaxed polls, then one acquire load once the value is there (no full fence)
-    while (true) {
-      if ((SYS ? ld_relaxed_sys(p) : ld_relaxed_gpu(p)) >= need &&
-          (SYS ? ld_acquire_sys(p) : ld_acquire_gpu(p)) >= need)
-        break;
-      if ((++spins & 255) == 0 && (spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
-        atomicExch(a.abort_flag, 1);
-        ok = 0;
-        break;
-      }
-      __nanosleep(32);
-    }
-    if (a.prof) atomicAdd(&a.prof[0], (unsigned long long)(clock64() - t0));
-  }
-  return __shfl_sync(0xffffffffu, ok, 0) != 0;
-}
-
-__device__ __forceinline__ int imad_add_s(int x, uint32_t one, int k) {
-  int d;
-  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(one), "r"(k));
-  return d;
-}
 
 template <int KIND, int GAP, int R>
 __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
@@ -460,8 +345,44 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
   if (t == 0) a.parts[wg] = part;
 }
 
-#include "long16.cuh"
 
+
+// SEMI optimum after a 16-bit long kernel (reading R5): candidates (n, j) for j in
+// [j0, j1) ∩ [1, m-1] from the row buffer (the last row strip's published row = row n),
+// then -- on the device owning column m -- (i, m) for i = 0..n from the boundary column the
+// last strip wrote.  Key = (value, then the earliest candidate: seq = j for row n, m + i for
+// column m); strict '>' in that order = the largest key with the smallest seq.  (n, 0) = 0
+// is merged on the host.
+__global__ void semi_reduce_kernel(const int4* __restrict__ rowbuf, int j0, int j1, int m,
+                                   const int2* __restrict__ colm, int n,
+                                   unsigned long long* out) {
+  unsigned long long best = 0;
+  const int64_t nrow = j1 > j0 ? j1 - j0 : 0;
+  const int64_t tot = nrow + (colm ? (int64_t)n + 1 : 0);
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int v;
+    uint32_t seq;
+    if (x < nrow) {
+      const int j = j0 + (int)x;
+      v = rowbuf[j].x;
+      seq = (uint32_t)j;
+    } else {
+      const int i = (int)(x - nrow);
+      v = colm[i].x;
+      seq = (uint32_t)m + (uint32_t)i;
+    }
+    const unsigned long long key =
+        ((unsigned long long)((uint32_t)v ^ 0x80000000u) << 32) | (0xFFFFFFFFu - seq);
+    best = key > best ? key : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+    best = y > best ? y : best;
+  }
+  if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
 
 __global__ void long_init_kernel(DevParams P, int n, int m, int4* rowbuf, int2* bcol0,
                                  int2* const* bcol, const int* cb, int Gtot, int g_first,
@@ -473,16 +394,15 @@ __global__ void long_init_kernel(DevParams P, int n, int m, int4* rowbuf, int2* 
     if (x <= m) rowbuf[x] = make_int4(0, 0, NEG, 0);  // tag 0: no strip has written yet
     if (bcol0 && x <= n) bcol0[x] = make_int2(glob && x > 0 ? -(P.go + (int)x * P.ge) : 0, NEG);  // H(i,0), F(i,0)
     if (x == 0) {
-      for (int g = g_first; g < g_first + g_count; ++g) {
-        if (g == 0) continue;
+      for (int g = g_first; g <= g_first + g_count; ++g) {
+        // the group's own edges; plus column m (edge Gtot) when the group keeps it (SEMI)
+        if (g == 0 || (g == g_first + g_count && !(g == Gtot && bcol[g]))) continue;
         const int c = cb[g];
         bcol[g][0] = make_int2(glob ? -(P.go + c * P.ge) : 0, NEG);  // H(0, c_g)
       }
     }
   }
 }
-
-typedef void (*LongFn)(LongArgs);
 
 template <int R>
 static LongFn long_fn(int kind, int gap) {
@@ -506,9 +426,17 @@ struct Buf {
   } while (0)
 }  // namespace
 
+void LongCkpt::release() {
+  for (void* p : {(void*)qc, (void*)sc, (void*)rowck, (void*)colck})
+    if (p) cudaFree(p);
+  qc = sc = nullptr;
+  rowck = colck = nullptr;
+  bytes = 0;
+}
+
 int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, uint64_t n,
              const char* s, uint64_t m, const LongOptions& opt, LongResult* out, std::string* err,
-             uint64_t* launches) {
+             uint64_t* launches, LongCkpt* ck) {
   out->kernel_ms = 0;
   out->narrow = false;
   if (n == 0 || m == 0) {  // empty sequences: one gap run (global) or the empty alignment
@@ -562,18 +490,24 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   auto fits16 = [&](int nr) {
     return 2 * (int64_t)(64 * nr + 66) * d16 + margin16 + 96 * d16 + P.go + P.ge + 256 < -NEG16C;
   };
-  int NR16 = opt.band_rows == 512 ? 8 : opt.band_rows == 768 ? 12 : 16;  // 1024-row tasks by
-  if (NR16 > 8 && !fits16(NR16)) NR16 = 8;  // default, 512 if the range needs it
+  int NR16 = opt.band_rows == 512 ? 8 : 16;  // 1024-row tasks by default, 512 if the range
+  if (NR16 > 8 && !fits16(NR16)) NR16 = 8;    // guard needs it
   const int64_t bspan16 = (int64_t)(64 * NR16 + 66) * d16;
-  bool narrow = opt.narrow != 0 && P.kind == KLOCAL && P.gap == GAFFINE && fits16(NR16) &&
-                (int64_t)P.go + 2 * P.ge < 4096;
+  // every kind and gap model (linear = affine with G_o = 0, exact for scores); the subject's
+  // selector has four codes, so a subject with N takes the 32-bit kernel
+  bool narrow = opt.narrow != 0 && fits16(NR16) && (int64_t)P.go + 2 * P.ge < 4096;
   if (narrow)
     for (uint64_t x = 0; x < m && narrow; ++x) narrow = (s[x] | 0x20) != 'n';
   if (narrow) {
     HS = 64 * NR16;
-    fn = NR16 == 16 ? long16_kernel<16> : NR16 == 12 ? long16_kernel<12> : long16_kernel<8>;
+    fn = long16_fn(NR16, P.kind, ck && ck->want);
   }
   out->narrow = narrow;
+  if (ck && ck->want && (!narrow || NE != 1)) {
+    *err = narrow ? "long traceback: one device only"
+                  : "long traceback: needs the 16-bit kernel (subject without N, range guard)";
+    return ANYSEQ_E_UNSUPPORTED;
+  }
   const int S = (int)((n + HS - 1) / HS);
   int Gtot = NE > 1 ? NE : std::max(1, opt.virtual_strips);
   if (NE == 1 && opt.virtual_strips <= 0) {
@@ -610,6 +544,42 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   };
   std::vector<PerDev> pd(ND);
   std::vector<int2*> bcol_ptr(Gtot + 1, nullptr);  // edge g buffer lives on its consumer device
+  const int pad_top = (narrow && P.kind == KSEMI) ? (int)((uint64_t)S * HS - n) : 0;
+  // checkpoint geometry: row checkpoints every ck_every strips (row blocks of HS * ck_every
+  // <= 4096 rows), column checkpoints every 2^kc_shift columns (<= 4096), the finest that
+  // fits the budget (the traceback's tile recompute shrinks with the tile)
+  if (ck && ck->want) {
+    size_t fr = 0, tot = 0;
+    LK(cudaSetDevice(devs[0].id));
+    LK(cudaMemGetInfo(&fr, &tot));
+    const int64_t budget = ck->budget > 0 ? ck->budget : (int64_t)(0.4 * (double)fr);
+    auto bytes_of = [&](int every, int kcs) -> int64_t {
+      const int64_t rows = (int64_t)(S - 1) / every, cols = (int64_t)(m - 1) >> kcs;
+      return (rows * (int64_t)(m + 1) + cols * (int64_t)(n + 1)) * (int64_t)sizeof(int2);
+    };
+    const int cands[][2] = {{1, 10}, {1, 11}, {2, 11}, {2, 12}, {4, 12}, {8, 12}};
+    int every = 0, kcs = 0;
+    for (auto& c : cands) {
+      if (HS * c[0] > 4096) continue;
+      if (bytes_of(c[0], c[1]) <= budget) { every = c[0]; kcs = c[1]; break; }
+    }
+    if (ck->force_ck_every > 0) every = ck->force_ck_every;
+    if (ck->force_kc_shift > 0) kcs = ck->force_kc_shift;
+    if (every == 0) {
+      *err = "long traceback: checkpoints exceed the device memory budget";
+      return ANYSEQ_E_NOMEM;
+    }
+    ck->release();
+    ck->HS = HS;
+    ck->ck_every = every;
+    ck->kc_shift = kcs;
+    ck->PT = pad_top;
+    ck->S = S;
+    const int64_t rows = (int64_t)(S - 1) / every, cols = (int64_t)(m - 1) >> kcs;
+    ck->bytes = (size_t)bytes_of(every, kcs);
+    if (rows > 0) LK(cudaMalloc(&ck->rowck, (size_t)rows * (m + 1) * sizeof(int2)));
+    if (cols > 0) LK(cudaMalloc(&ck->colck, (size_t)cols * (n + 1) * sizeof(int2)));
+  }
   std::vector<int32_t*> flag_ptr(Gtot + 1, nullptr);
   // column strips per device group (one strip per entry; a single entry: all Gtot strips)
   std::vector<LongDevice> gdev(ND);
@@ -680,9 +650,12 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     LK(cudaMemcpyAsync(D.cbuf.p, cb.data(), (Gtot + 1) * 4, cudaMemcpyHostToDevice, st));
     // column buffers consumed on this device: edges g_first .. g_first+g_count-1 (edge 0 = init)
     if (D.g_count > 0) {
-      const size_t bytes = (size_t)D.g_count * (n + 1) * sizeof(int2);
+      // 16-bit SEMI: the group owning the last column strip also keeps column m (H(i, m),
+      // written by the last strip's right edge) for the optimum's column candidates
+      const int extra = (narrow && P.kind == KSEMI && D.g_first + D.g_count == Gtot) ? 1 : 0;
+      const size_t bytes = (size_t)(D.g_count + extra) * (n + 1) * sizeof(int2);
       LK(cudaMalloc(&D.bcol_own.p, bytes));
-      for (int k = 0; k < D.g_count; ++k)
+      for (int k = 0; k < D.g_count + extra; ++k)
         bcol_ptr[D.g_first + k] = (int2*)D.bcol_own.p + (size_t)k * (n + 1);
       LK(cudaMalloc(&D.flags.p, (size_t)D.g_count * S * 4));
       LK(cudaMemsetAsync(D.flags.p, 0, (size_t)D.g_count * S * 4, st));
@@ -745,6 +718,12 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     a.sleep_ns = opt.sleep_ns;
     a.margin = (int32_t)margin16;
     a.bspan = (int32_t)bspan16;
+    a.pad_top = pad_top;
+    a.rowck = ck && ck->want ? ck->rowck : nullptr;
+    a.colck = ck && ck->want ? ck->colck : nullptr;
+    a.ck_every = ck && ck->want ? ck->ck_every : 1;
+    a.kc_shift = ck && ck->want ? ck->kc_shift : 30;
+    if (narrow) a.lag = opt.start_lag;  // 16-bit kernel: start slack off unless asked for
     a.prof = nullptr;
     if (opt.profile) {
       LK(cudaMalloc(&D.profbuf.p, 64));
@@ -794,9 +773,46 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
       if (p.gset) { gv = p.gv; have_g = true; }
     }
   }
+  auto handoff = [&]() {  // CKPT: the traceback walk reads the codes after this returns
+    if (ck && ck->want) {
+      ck->qc = (uint8_t*)pd[0].qc.p;
+      ck->sc = (uint8_t*)pd[0].sc.p;
+      pd[0].qc.p = pd[0].sc.p = nullptr;
+    }
+  };
   if (aborted) {
     *err = "long kernel: a boundary wait exceeded its bound";
     return ANYSEQ_E_TIMEOUT;
+  }
+  if (narrow && P.kind == KSEMI) {
+    // row n from each group's row buffer (its own column strips), column m from the last
+    // group's extra boundary column; (n, 0) = 0 is the first candidate (seq 0)
+    unsigned long long key = ((unsigned long long)0x80000000u << 32) | 0xFFFFFFFFu;
+    for (int d = 0; d < ND; ++d) {
+      PerDev& D = pd[d];
+      if (D.g_count == 0) continue;
+      LK(cudaSetDevice(gdev[d].id));
+      Buf kb;
+      LK(cudaMalloc(&kb.p, 8));
+      LK(cudaMemsetAsync(kb.p, 0, 8, gdev[d].stream));
+      const int j0 = std::max(1, cb[D.g_first]), j1 = std::min<int>((int)m, cb[D.g_first + D.g_count]);
+      const bool lastg = D.g_first + D.g_count == Gtot;
+      semi_reduce_kernel<<<gdev[d].num_sms * 4, 256, 0, gdev[d].stream>>>(
+          (const int4*)D.rowbuf.p, j0, j1, (int)m, lastg ? bcol_ptr[Gtot] : nullptr, (int)n,
+          (unsigned long long*)kb.p);
+      LK(cudaGetLastError());
+      *launches += 1;
+      unsigned long long kd = 0;
+      LK(cudaMemcpyAsync(&kd, kb.p, 8, cudaMemcpyDeviceToHost, gdev[d].stream));
+      LK(cudaStreamSynchronize(gdev[d].stream));
+      key = std::max(key, kd);
+    }
+    handoff();
+    const uint32_t seq = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
+    out->score = (int32_t)((uint32_t)(key >> 32) ^ 0x80000000u);
+    if (seq < m) { out->end_i = (int64_t)n; out->end_j = seq; }
+    else { out->end_i = (int64_t)(seq - m); out->end_j = (int64_t)m; }
+    return 0;
   }
   if (P.kind == KLOCAL) {
     out->score = lv; out->end_i = li; out->end_j = lj;
@@ -810,6 +826,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     }
     out->score = gv; out->end_i = (int64_t)n; out->end_j = (int64_t)m;
   }
+  handoff();
   return 0;
 }
 

@@ -33,9 +33,28 @@ struct LongResult {
   bool narrow;             // the 16-bit differential kernel ran
 };
 
+// Checkpoints for the linear-space traceback (long_tb.h): with want set, run_long runs the
+// 16-bit kernel's CKPT instance on ONE device and hands back (owned here, freed by release()
+// or the destructor) the device codes of q and s and the checkpoint rows / columns.
+struct LongCkpt {
+  int want = 0;
+  int64_t budget = 0;         // max device bytes for the checkpoints (0 = 40 % of free)
+  int force_kc_shift = 0;     // > 0: column block 2^k (tests); else chosen from the budget
+  int force_ck_every = 0;     // > 0: row checkpoint every k strips (tests)
+  // outputs
+  uint8_t* qc = nullptr;
+  uint8_t* sc = nullptr;
+  int2* rowck = nullptr;
+  int2* colck = nullptr;
+  int HS = 0, ck_every = 1, kc_shift = 10, PT = 0, S = 0;
+  size_t bytes = 0;           // checkpoint bytes allocated
+  void release();
+  ~LongCkpt() { release(); }
+};
+
 // Returns 0 or an anyseq_status code; err receives a message.
 int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, uint64_t n,
              const char* s, uint64_t m, const LongOptions& opt, LongResult* out, std::string* err,
-             uint64_t* launches);
+             uint64_t* launches, LongCkpt* ck = nullptr);
 
 }  // namespace anyseq

@@ -1,11 +1,13 @@
-// csrc/long16.cuh -- long-pair local affine score-only kernel in 16-bit differential
-// arithmetic (included by long.cu after the s32 kernel's helpers).
+// csrc/long16.cuh -- long-pair score-only kernel in 16-bit differential arithmetic, every
+// kind and gap model (included inside namespace anyseq by the
+// long16_*.cu instance files after long_dev.cuh).
 //
 // Paper: 16-bit scores where the value range allows (SIMD lanes of half
 // width double the cells per instruction).  Long pairs exceed 16 bits absolutely, so the
 // kernel keeps every value relative to a per-warp base: the DP only compares sums of
 // neighbouring cells, and neighbouring H values differ by at most d = G_o + G_e + max(σ,0)
-// (DESIGN.md §5.4b), so the 576 (or 1088) cells a warp holds at one step fit in s16.
+// (the Lipschitz bound holds for the local, global and semi-global
+// recurrences alike), so the cells a warp holds at one step fit in s16.
 //
 // Same task shell as long_kernel (tickets, tagged row hand-off, boundary columns, flags,
 // bounded waits).  What changes is the warp's inner layout: lane t owns 2·NR rows of the
@@ -19,10 +21,19 @@
 // Values are kept strictly negative (rel = abs − base ∈ [−24576, −1]): then H − (G_o+G_e)
 // can be formed on the FMA pipe as one 32-bit IMAD on the packed register (the low half
 // always borrows, the constant pre-compensates the high half), leaving the ALU pipe per two
-// cells: PRMT (σ of both halves), 3 VIADDMNMX.S16x2, VIMNMX3.S16x2 (local floor).
+// cells: PRMT (σ of both halves), 3 VIADDMNMX.S16x2 and one max (VIMNMX3.S16x2 with the
+// local floor, VIMNMX.S16x2 otherwise).  Linear gaps run as affine with G_o = 0: the
+// reassociated recurrence below is then exactly Eqs. (2)-(3) (E = H_up − g, F = H_left − g).
 // The base is re-chosen every 32 steps once all virtual lanes are active (warp max of H →
-// −margin); the local optimum is tracked per half as a packed running maximum (one
-// VIMNMX3 per two registers) and resolved to (value, i, j) in a rare branch.
+// −margin).
+//
+// Optimum (readings R5/R10): LOCAL tracks a packed running maximum per half (one
+// VIMNMX3 per two registers) resolved to (value, i, j) in a rare branch.  SEMI places its
+// pad rows at the TOP of the first strip (σ = 0 rows that reproduce the zero row 0
+// exactly), so the matrix's last row n is the last row strip's published row: after the
+// kernel the row buffer holds H(n, j) for every j, the last column strip writes H(i, m) to
+// one more boundary column, and semi_reduce_kernel scans both in the candidate order of
+// R5.  GLOBAL reads H(n, m) at the last task's last column.
 #pragma once
 
 __device__ __forceinline__ uint32_t h16_set(uint32_t x, int h, int v) {
@@ -35,7 +46,11 @@ __device__ __forceinline__ uint32_t h16_pack(int lo, int hi) {
   return ((uint32_t)lo & 0xffffu) | ((uint32_t)hi << 16);
 }
 
-template <int NR>
+// CKPT (linear-space traceback): the pass also keeps the
+// checkpoints the traceback's tile recompute starts from -- every ck_every-th row strip's
+// last row, (H, E) of that row (a.rowck), and every 2^kc_shift-th column, (H, F) of every
+// row (a.colck) -- in absolute 32-bit values.
+template <int NR, int KIND, bool CKPT = false>
 __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs a) {
   constexpr int HS = 64 * NR;  // rows per task: 32 lanes x 2 halves x NR
   constexpr int RING = 256;
@@ -43,6 +58,7 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
   __shared__ int2 ring_he[4][RING];
   __shared__ uint16_t ring_sel[4][RING];  // subject code c of a column as c * 0x11
   __shared__ int2 ring_out[4][64];        // the task's last row (H, E) awaiting publication
+  __shared__ int ring_eck[CKPT ? 4 : 1][64];  // CKPT: E of that row itself (not of the next)
   const int t = threadIdx.x & 31;
   const int wb = threadIdx.x >> 5;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -76,9 +92,11 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
     const int s = task % a.S;
     const int g = a.g_first + task / a.S;
     const int c_lo = a.cb[g], c_hi = a.cb[g + 1], W = c_hi - c_lo;
-    const int ip0 = s * HS + t * 2 * NR;
+    // real row of the lane's first row, minus 1 (SEMI: a.pad_top pad rows above row 1)
+    const int ip0 = s * HS + t * 2 * NR - a.pad_top;
     const int2* bl = a.bcol[g];
-    int2* br = (g + 1 < a.Gtot) ? a.bcol[g + 1] : nullptr;
+    // right edge: the next strip's left boundary; SEMI's last strip: column m (candidates)
+    int2* br = (g + 1 < a.Gtot || KIND == KSEMI) ? a.bcol[g + 1] : nullptr;
 
     if (g > 0) {
       if (!warp_wait<true>(&a.bflag[g][s], 1, a)) break;
@@ -87,9 +105,9 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
     uint32_t p0[NR], p1[NR], H[NR], Ff[NR];  // H: the lane's rows at its last column (in place)
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      const int iA = ip0 + r, iB = ip0 + NR + r;
-      p0[r] = iA < n ? prof4(a.P, a.qc[iA]) : 0u;  // sigma rows of the low half
-      p1[r] = iB < n ? prof4(a.P, a.qc[iB]) : 0u;  // ... and of the high half
+      const int iA = ip0 + r + 1, iB = ip0 + NR + r + 1;  // real rows (1-based)
+      p0[r] = (iA >= 1 && iA <= n) ? prof4(a.P, a.qc[iA - 1]) : 0u;  // sigma rows, low half
+      p1[r] = (iB >= 1 && iB <= n) ? prof4(a.P, a.qc[iB - 1]) : 0u;  // ... and high half
       H[r] = VS16::splat(NEGc);
       Ff[r] = VS16::splat(NEGc);
     }
@@ -120,13 +138,17 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
 
     // frame: every value of the task lies within a.bspan of H(ip0, c_lo + 1) (the row
     // above, first column), so base = that + bspan puts them all in [-2 bspan, -margin]
-    int base = (s > 0 ? ring_he[wb][0].x : 0) + a.bspan;
+    const int h00 = (s > 0) ? ring_he[wb][0].x
+                            : (KIND == KGLOBAL ? -(P.go + (c_lo + 1) * P.ge) : 0);
+    int base = h00 + a.bspan;
     auto cv = [&](int x) -> int { return max(x - base, NEGc); };  // absolute -> relative
     int bv0 = 0, bi0 = 0, bj0 = 0, bv1 = 0, bi1 = 0, bj1 = 0;   // per-half best (absolute)
-    uint32_t Z, best;  // the local floor (absolute 0) and the running maxima, relative
+    uint32_t Z = 0, best = 0;  // LOCAL: the floor (absolute 0) and the running maxima, relative
     auto frame_consts = [&]() {
-      Z = VS16::splat(max(-base, NEGc));
-      best = h16_pack(min(max(bv0 - base, -32768), 32767), min(max(bv1 - base, -32768), 32767));
+      if (KIND == KLOCAL) {
+        Z = VS16::splat(max(-base, NEGc));
+        best = h16_pack(min(max(bv0 - base, -32768), 32767), min(max(bv1 - base, -32768), 32767));
+      }
     };
     frame_consts();
     uint32_t diag = VS16::splat(NEGc), Hbot = VS16::splat(NEGc), Ebot = VS16::splat(NEGc);
@@ -159,77 +181,117 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
           const int h = lc;
 #pragma unroll
           for (int r = 0; r < NR; ++r) {
-            const int ip = ip0 + h * NR + r;
+            const int i = ip0 + h * NR + r + 1;  // real row; pad rows: H = 0 (SEMI), F = -inf
             int2 b = make_int2(0, NEG32);
-            if (ip < n) b = bl[ip + 1];
+            // (SEMI pad rows read bl[0] = (H(0, c_lo), F) = (0, -inf): their own boundary)
+            if (i <= n) b = bl[KIND == KSEMI ? max(i, 0) : i];
             Hi[r] = h16_set(Hi[r], h, cv(b.x));
             Ff[r] = h16_set(Ff[r], h, cv(b.y));
           }
-          const int id = ip0 + h * NR;
-          diag = h16_set(diag, h, cv(id <= n ? bl[id].x : 0));
+          const int id = ip0 + h * NR;  // the row above the half's first row
+          diag = h16_set(diag, h, cv(id <= n ? bl[KIND == KSEMI ? max(id, 0) : id].x : 0));
         }
         {  // lane 0's low half: the row above the task, H(ip0, j) and E(ip0 + 1, j) (no branch)
-          const int hx = FIRST ? 0 : he.x;
-          const int ex = FIRST ? -cop : he.y;
-          const uint32_t h0 = prmt((uint32_t)cv(hx), hin, 0x7610u);
-          const uint32_t e0 = prmt((uint32_t)cv(ex), ein, 0x7610u);
-          hin = t == 0 ? h0 : hin;
-          ein = t == 0 ? e0 : ein;
+          // (first strip: row 0 -- 0 for LOCAL / SEMI, -(G_o + j G_e) for GLOBAL)
+          const int h0 = KIND == KGLOBAL ? -(P.go + (c_lo + lc + 1) * P.ge) : 0;
+          const int hx = FIRST ? h0 : he.x;
+          const int ex = FIRST ? h0 - cop : he.y;
+          const uint32_t hl = prmt((uint32_t)cv(hx), hin, 0x7610u);
+          const uint32_t el = prmt((uint32_t)cv(ex), ein, 0x7610u);
+          hin = t == 0 ? hl : hin;
+          ein = t == 0 ? el : ein;
         }
         uint32_t e = ein;
         uint32_t hd = diag;
+        uint32_t elast = 0;  // CKPT: E of the last row
 #pragma unroll
         for (int r = 0; r < NR; ++r) {  // in place: row r's previous column is row r+1's diagonal
+          if (CKPT && r == NR - 1) elast = e;
           const uint32_t old = Hi[r];
           const uint32_t sig = prmt(p0[r], p1[r], sel);
           Ff[r] = __viaddmax_s16x2(Ff[r], NGE2, hop(old));
           const uint32_t df = __viaddmax_s16x2(hd, sig, Ff[r]);
-          Hq[r] = __vimax3_s16x2(df, e, Z);
+          Hq[r] = KIND == KLOCAL ? __vimax3_s16x2(df, e, Z) : __vmaxs2(df, e);
           e = __viaddmax_s16x2(e, NGE2, hop(df));
           hd = old;
         }
         diag = hin;
         Hbot = Hq[NR - 1];
         Ebot = e;
-        if (t == 31 && act1)  // the task's last row (high half), column lc - 1: staged in
+        if (t == 31 && act1) {  // the task's last row (high half), column lc - 1: staged in
           ring_out[wb][(lc - 1) & 63] =  // shared memory, published 32 columns at a time
               make_int2(h16_get(Hq[NR - 1], 1) + base, h16_get(e, 1) + base);
-        // local optimum: packed running maximum per half; strictly larger values only
-        uint32_t cm;
-        if (CHK) {
-          uint32_t mx = Hq[0];
-#pragma unroll
-          for (int r = 1; r + 1 < NR; r += 2) mx = __vimax3_s16x2(mx, Hq[r], Hq[r + 1]);
-          if ((NR % 2) == 0) mx = __vmaxs2(mx, Hq[NR - 1]);
-          mx = VS16::select_mask(mx, (act0 ? 1u : 0u) | (act1 ? 2u : 0u), VS16::splat(-32768));
-          cm = __vmaxs2(mx, best);
-        } else {
-          cm = __vimax3_s16x2(best, Hq[0], Hq[1]);
-#pragma unroll
-          for (int r = 2; r + 1 < NR; r += 2) cm = __vimax3_s16x2(cm, Hq[r], Hq[r + 1]);
-          if ((NR % 2) == 1) cm = __vmaxs2(cm, Hq[NR - 1]);
+          if (CKPT) ring_eck[wb][(lc - 1) & 63] = h16_get(elast, 1) + base;
         }
-        if (cm != best) {  // rare: resolve (value, first row, column) of the improved half(s)
+        if (CKPT) {  // column checkpoints: (H, F) of every real row at columns j = k 2^kc_shift
+          const int kcm = (1 << a.kc_shift) - 1;
+          const int jl = c_lo + lc + 1;  // the low half's column; the high half's is jl - 1
+          if ((((jl & kcm) == 0) && act0) || ((((jl - 1) & kcm) == 0) && act1)) {
+            const int h = ((jl & kcm) == 0) ? 0 : 1;
+            const int jj = jl - h;
+            if (jj < a.m) {
+              int2* dst = a.colck + (size_t)((jj >> a.kc_shift) - 1) * (a.n + 1);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int v = h16_get(cm, h);
-            if (v != h16_get(best, h)) {
-              int rr = NR - 1;
-#pragma unroll
-              for (int r = NR - 1; r >= 0; --r)
-                if (h16_get(Hq[r], h) == v) rr = r;
-              if (h == 0) { bv0 = v + base; bi0 = ip0 + rr + 1; bj0 = c_lo + lc + 1; }
-              else { bv1 = v + base; bi1 = ip0 + NR + rr + 1; bj1 = c_lo + lc; }
+              for (int r = 0; r < NR; ++r) {
+                const int i = ip0 + h * NR + r + 1;
+                if (i >= 1 && i <= n)
+                  dst[i] = make_int2(h16_get(Hq[r], h) + base, h16_get(Ff[r], h) + base);
+              }
             }
           }
-          best = cm;
         }
-        if (CHK && br && (lc == W - 1 || lc == W)) {  // half h's last column: right edge
-          const int h = lc - (W - 1);
+        if (KIND == KLOCAL) {
+          // local optimum: packed running maximum per half; strictly larger values only
+          uint32_t cm;
+          if (CHK) {
+            uint32_t mx = Hq[0];
 #pragma unroll
-          for (int r = 0; r < NR; ++r) {
-            const int ip = ip0 + h * NR + r;
-            if (ip < n) br[ip + 1] = make_int2(h16_get(Hq[r], h) + base, h16_get(Ff[r], h) + base);
+            for (int r = 1; r + 1 < NR; r += 2) mx = __vimax3_s16x2(mx, Hq[r], Hq[r + 1]);
+            if ((NR % 2) == 0) mx = __vmaxs2(mx, Hq[NR - 1]);
+            mx = VS16::select_mask(mx, (act0 ? 1u : 0u) | (act1 ? 2u : 0u), VS16::splat(-32768));
+            cm = __vmaxs2(mx, best);
+          } else {
+            cm = __vimax3_s16x2(best, Hq[0], Hq[1]);
+#pragma unroll
+            for (int r = 2; r + 1 < NR; r += 2) cm = __vimax3_s16x2(cm, Hq[r], Hq[r + 1]);
+            if ((NR % 2) == 1) cm = __vmaxs2(cm, Hq[NR - 1]);
+          }
+          if (cm != best) {  // rare: resolve (value, first row, column) of the improved half(s)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int v = h16_get(cm, h);
+              if (v != h16_get(best, h)) {
+                int rr = NR - 1;
+#pragma unroll
+                for (int r = NR - 1; r >= 0; --r)
+                  if (h16_get(Hq[r], h) == v) rr = r;
+                if (h == 0) { bv0 = v + base; bi0 = ip0 + rr + 1; bj0 = c_lo + lc + 1; }
+                else { bv1 = v + base; bi1 = ip0 + NR + rr + 1; bj1 = c_lo + lc; }
+              }
+            }
+            best = cm;
+          }
+        }
+        if (CHK && (lc == W - 1 || lc == W)) {  // half h's last column
+          const int h = lc - (W - 1);
+          if (br) {  // right edge (H, F) of the half's real rows
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+              const int i = ip0 + h * NR + r + 1;
+              if ((KIND != KSEMI || i >= 1) && i <= n)
+                br[i] = make_int2(h16_get(Hq[r], h) + base, h16_get(Ff[r], h) + base);
+            }
+          }
+          if (KIND == KGLOBAL && s == a.S - 1 && c_hi == a.m) {  // H(n, m): the global optimum
+            const int rr = n - 1 - ip0 - h * NR;
+            if (rr >= 0 && rr < NR) {
+              int v = 0;
+#pragma unroll
+              for (int r = 0; r < NR; ++r)
+                if (r == rr) v = h16_get(Hq[r], h);
+              part.gv = v + base;
+              part.gset = 1;
+            }
           }
         }
       };
@@ -257,12 +319,16 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
 
       // publish staged columns [flushed, c_end) (at most 32) to the row buffer for strip s+1
       int flushed = 0;
+      const int ck_slot =
+          (CKPT && s + 1 < a.S && ((s + 1) % a.ck_every) == 0) ? (s + 1) / a.ck_every - 1 : -1;
       auto flush = [&](int c_end) {
         __syncwarp();
         const int c = flushed + t;
         if (c < c_end) {
           const int2 v = ring_out[wb][c & 63];
           st_row(a.rowbuf + c_lo + c + 1, v.x, v.y, s + 1);
+          if (CKPT && ck_slot >= 0)  // row checkpoint: (H, E) of the strip's last row
+            a.rowck[(size_t)ck_slot * (a.m + 1) + c_lo + c + 1] = make_int2(v.x, ring_eck[wb][c & 63]);
         }
         flushed = c_end;
         __syncwarp();
@@ -306,14 +372,16 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
     };
     const bool done = (s == 0) ? sweep(std::true_type{}) : sweep(std::false_type{});
     if (!done) break;
-    if (lkey_better(bv0, bi0, bj0, part.lv, part.li, part.lj)) { part.lv = bv0; part.li = bi0; part.lj = bj0; }
-    if (lkey_better(bv1, bi1, bj1, part.lv, part.li, part.lj)) { part.lv = bv1; part.li = bi1; part.lj = bj1; }
+    if (KIND == KLOCAL) {
+      if (lkey_better(bv0, bi0, bj0, part.lv, part.li, part.lj)) { part.lv = bv0; part.li = bi0; part.lj = bj0; }
+      if (lkey_better(bv1, bi1, bj1, part.lv, part.li, part.lj)) { part.lv = bv1; part.li = bi1; part.lj = bj1; }
+    }
     if (a.prof && t == 0) {
       atomicAdd(&a.prof[1], (unsigned long long)(clock64() - task_t0));
       atomicAdd(&a.prof[2], 1ull);
     }
     __syncwarp();
-    if (br) {
+    if (br && g + 1 < a.Gtot) {
       if (t == 0) {
         __threadfence_system();
         st_release_sys(&a.bflag[g + 1][s], 1);
@@ -326,6 +394,10 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
     const int li = __shfl_xor_sync(0xffffffffu, part.li, o);
     const int lj = __shfl_xor_sync(0xffffffffu, part.lj, o);
     if (lkey_better(lv, li, lj, part.lv, part.li, part.lj)) { part.lv = lv; part.li = li; part.lj = lj; }
+    const int gv = __shfl_xor_sync(0xffffffffu, part.gv, o);
+    const int gs = __shfl_xor_sync(0xffffffffu, part.gset, o);
+    if (gs && !part.gset) { part.gv = gv; part.gset = 1; }
   }
   if (t == 0) a.parts[wg] = part;
 }
+

@@ -1,0 +1,15 @@
+// csrc/long16_dispatch.cu -- 16-bit long kernel instance by kind (long_dev.cuh).
+#include "long_dev.cuh"
+
+namespace anyseq {
+
+LongFn long16_fn_global(int nr, bool ckpt);
+LongFn long16_fn_local(int nr, bool ckpt);
+LongFn long16_fn_semi(int nr, bool ckpt);
+
+LongFn long16_fn(int nr, int kind, bool ckpt) {
+  return kind == KGLOBAL ? long16_fn_global(nr, ckpt)
+       : kind == KLOCAL ? long16_fn_local(nr, ckpt) : long16_fn_semi(nr, ckpt);
+}
+
+}  // namespace anyseq

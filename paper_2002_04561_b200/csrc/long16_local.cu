@@ -1,0 +1,15 @@
+// csrc/long16_local.cu -- instances of the 16-bit differential long kernel
+// (long16.cuh) for KLOCAL alignments; one translation unit per kind so they compile in
+// parallel.
+#include "long_dev.cuh"
+
+namespace anyseq {
+
+#include "long16.cuh"
+
+LongFn long16_fn_local(int nr, bool ckpt) {
+  if (ckpt) return nr == 8 ? long16_kernel<8, KLOCAL, true> : long16_kernel<16, KLOCAL, true>;
+  return nr == 8 ? long16_kernel<8, KLOCAL> : long16_kernel<16, KLOCAL>;
+}
+
+}  // namespace anyseq

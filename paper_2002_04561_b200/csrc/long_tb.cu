@@ -1,0 +1,386 @@
+// csrc/long_tb.cu -- linear-space long-pair traceback from checkpoints.
+//
+// The forward pass (long16_kernel<.., CKPT = true>, one pass over the whole matrix, which
+// also finds the optimum of Eqs. (1)-(5)) keeps the DP rows at every row-block
+// boundary and the DP columns at every column-block boundary.  The traceback then walks
+// the path of the relax listing (the oracle's walk of SURVEY 8(c) step 7) from
+// the end cell back, one tile (row block x column block) at a time: the tile region
+// up-left of the current cell is recomputed from its top checkpoint row and left
+// checkpoint column into per-cell direction bytes (H source DIAG/UP/LEFT/STOP with the tie
+// order DIAG > E > F, plus the E / F extension bits with extension winning ties -- readings
+// R7-R9), and one warp walks them with 32-cell lookahead until the path leaves the tile.
+// Every decision is taken from exact full-matrix values, so the CIGAR is the one the
+// full-matrix traceback (the oracle) produces: bit-exact, affine or linear, every kind.
+//
+// The recompute: thread t of 256 owns TR consecutive rows of the tile and sweeps its
+// columns with a skew of one step per thread (the anti-diagonal wavefront of P:274); the
+// row above a thread's first row arrives from thread t-1 through a double-buffered shared
+// slot (one barrier per step).  Direction bytes go to a global scratch in step-major order
+// (word (step * 256 + t) holds the thread's TR rows), so every step's stores are one
+// coalesced row of words and the walk reads a diagonal run as consecutive words.
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/anyseq.h"
+#include "common.cuh"
+#include "long.h"
+#include "long_tb.h"
+
+namespace anyseq {
+
+namespace {
+
+constexpr int NT = 256;  // recompute threads (rows: NT * TR per tile)
+constexpr int NEGI = -(1 << 29);
+
+struct WalkArgs {
+  int32_t kind, affine;
+  int32_t go, ge, cop;
+  int8_t sig[25];
+  const uint8_t* qc;  // codes of q (rows), s (columns)
+  const uint8_t* sc;
+  int32_t n, m;
+  const int2* rowck;  // (H, E) of checkpoint rows
+  const int2* colck;  // (H, F) of checkpoint columns
+  int32_t TH;         // rows per row block (padded coordinates)
+  int32_t PT;         // pad rows above row 1 (SEMI)
+  int32_t kc_shift;   // columns per column block = 1 << kc_shift
+  int32_t end_i, end_j;
+  uint8_t* scratch;   // direction bytes of one tile, (kc + NT) * NT * TR
+  uint32_t* ops;      // reversed RLE words (len << 4 | op)
+  uint64_t ops_cap;
+  unsigned long long* out;  // [0] ops written (or required), [1] begin i, [2] begin j, [3] tiles
+};
+
+__device__ __forceinline__ int h_row0(const WalkArgs& a, int j) {  // H(0, j)
+  return a.kind == KGLOBAL ? (j ? -(a.go + j * a.ge) : 0) : 0;
+}
+__device__ __forceinline__ int h_col0(const WalkArgs& a, int i) {  // H(i, 0)
+  return a.kind == KGLOBAL ? (i ? -(a.go + i * a.ge) : 0) : 0;
+}
+
+template <int TR>
+__global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
+  __shared__ int xh[2][NT], xe[2][NT];
+  __shared__ int ssig[25];
+  __shared__ int sh_i, sh_j, sh_st, sh_done;
+  __shared__ unsigned long long sh_nops;
+  __shared__ uint32_t sh_run;  // the RLE word being accumulated (len << 4 | op), 0 = none
+  const int t = threadIdx.x;
+  if (t < 25) ssig[t] = a.sig[t];
+  if (t == 0) {
+    sh_i = a.end_i;
+    sh_j = a.end_j;
+    sh_st = 0;  // 0 = H, 1 = E (vertical, I), 2 = F (horizontal, D)
+    sh_done = 0;
+    sh_nops = 0;
+    sh_run = 0;
+  }
+  __syncthreads();
+  const int kc = 1 << a.kc_shift;
+  unsigned long long tiles = 0;
+  // append a run of ops (walk order = reversed alignment order); warp 0 lane 0 only
+  auto emit = [&](uint32_t op, uint64_t len) {
+    while (len > 0) {
+      uint32_t r = sh_run;
+      if (r && (r & 15) == op && (r >> 4) < (1u << 28) - 1) {
+        const uint64_t room = ((1u << 28) - 1) - (r >> 4), add = len < room ? len : room;
+        sh_run = r + (uint32_t)(add << 4);
+        len -= add;
+      } else {
+        if (r) {
+          if (sh_nops < a.ops_cap) a.ops[sh_nops] = r;
+          ++sh_nops;
+        }
+        const uint64_t add = len < (1u << 28) - 1 ? len : (1u << 28) - 1;
+        sh_run = (uint32_t)(add << 4) | op;
+        len -= add;
+      }
+    }
+  };
+
+  for (;;) {
+    __syncthreads();
+    if (sh_done) break;
+    const int i = sh_i, j = sh_j;
+    if (i == 0 || j == 0) {  // boundary: global emits the leading gap run (R16), else stop
+      if (t == 0) {
+        if (a.kind == KGLOBAL) {
+          if (i) emit(1, (uint64_t)i);
+          if (j) emit(2, (uint64_t)j);
+          sh_i = 0;
+          sh_j = 0;
+        }
+        sh_done = 1;
+      }
+      continue;
+    }
+    // the tile holding (i, j): row block b (padded rows [b TH, (b+1) TH)), column block k
+    const int b = (i - 1 + a.PT) / a.TH;
+    const int R = max(0, b * a.TH - a.PT);  // top boundary row of the tile
+    const int kb = (j - 1) >> a.kc_shift;
+    const int C = kb << a.kc_shift;         // left boundary column
+    const int nr = i - R, nc = j - C;       // the region up-left of (i, j)
+    ++tiles;
+    // ---- recompute the region into direction bytes ----
+    const int row0 = R + t * TR;  // the row above this thread's first row
+    const bool tact = t * TR < nr;
+    int h[TR], f[TR];
+    int qcode[TR];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int ii = row0 + r + 1;
+      const bool real = ii <= i;
+      int2 lb = make_int2(h_col0(a, ii), NEGI);  // column 0: H(i, 0), F = -inf
+      if (real && kb > 0) lb = a.colck[(size_t)(kb - 1) * (a.n + 1) + ii];
+      h[r] = lb.x;
+      f[r] = lb.y;
+      qcode[r] = real ? 5 * (int)a.qc[ii - 1] : 0;
+    }
+    // the diagonal of the first row at the first column: H(row0, C)
+    int hprev;
+    if (t == 0) {
+      hprev = (b == 0 || R == 0) ? h_row0(a, C)
+            : (kb == 0 ? h_col0(a, R) : a.rowck[(size_t)(b - 1) * (a.m + 1) + C].x);
+    } else {
+      hprev = (kb == 0) ? h_col0(a, row0) : a.colck[(size_t)(kb - 1) * (a.n + 1) + row0].x;
+    }
+    const int nthreads = (nr + TR - 1) / TR;
+    const int steps = nc + nthreads - 1;
+    for (int k = 0; k < steps; ++k) {
+      const int c = k - t;  // column index in the region (jj = C + 1 + c)
+      if (tact && c >= 0 && c < nc) {
+        const int jj = C + 1 + c;
+        int hup, eup;  // H(row0, jj), E(row0, jj)
+        if (t == 0) {
+          if (R == 0) {
+            hup = h_row0(a, jj);
+            eup = NEGI;
+          } else {
+            const int2 v = a.rowck[(size_t)(b - 1) * (a.m + 1) + jj];
+            hup = v.x;
+            eup = v.y;
+          }
+        } else {
+          hup = xh[(k - 1) & 1][t - 1];
+          eup = xe[(k - 1) & 1][t - 1];
+        }
+        const int scode = a.sc[jj - 1];
+        int dg = hprev;
+        hprev = hup;
+        uint32_t word = 0;
+#pragma unroll
+        for (int r = 0; r < TR; ++r) {
+          int E, F;
+          uint32_t eext = 0, fext = 0;
+          if (a.affine) {  // Eqs. (4)-(5): extension first, extension wins ties (R8)
+            const int ex = eup - a.ge, eo = hup - a.cop;
+            E = max(ex, eo);
+            eext = ex >= eo;
+            const int fx = f[r] - a.ge, fo = h[r] - a.cop;
+            F = max(fx, fo);
+            fext = fx >= fo;
+          } else {  // Eqs. (2)-(3)
+            E = hup - a.ge;
+            F = h[r] - a.ge;
+          }
+          // Eq. (1) in the relax listing's order: strict '>' replacement, DIAG > E > F (R7)
+          int H = dg + ssig[qcode[r] + scode];
+          uint32_t src = 0;
+          if (E > H) { H = E; src = 1; }
+          if (F > H) { H = F; src = 2; }
+          if (a.kind == KLOCAL && H <= 0) { H = 0; src = 3; }  // nu = 0 wins ties at 0 (R9)
+          word |= (src | (eext << 2) | (fext << 3)) << (8 * (r & 3));
+          if ((r & 3) == 3 || r == TR - 1) {
+            reinterpret_cast<uint32_t*>(a.scratch)[((size_t)k * NT + t) * ((TR + 3) / 4) + (r >> 2)] = word;
+            word = 0;
+          }
+          dg = h[r];
+          h[r] = H;
+          f[r] = F;
+          hup = H;
+          eup = E;
+        }
+        xh[k & 1][t] = hup;
+        xe[k & 1][t] = eup;
+      }
+      __syncthreads();
+    }
+    // ---- walk the region (warp 0) until the path leaves it ----
+    if (t < 32) {
+      const int lane = t;
+      int ci = i, cj = j, st = sh_st;
+      auto dir_at = [&](int ii, int jj) -> uint32_t {  // direction byte of cell (ii, jj)
+        const int rr = ii - R - 1, tt = rr / TR, step = (jj - C - 1) + tt;
+        return a.scratch[((size_t)step * NT + tt) * (((TR + 3) / 4) * 4) + (rr % TR)];
+      };
+      bool done = false;
+      while (!done && ci > R && cj > C) {
+        if (st == 0) {  // H state: a diagonal run, then the first non-DIAG cell
+          const int ii = ci - lane, jj = cj - lane;
+          const bool in = ii > R && jj > C;
+          const uint32_t d = in ? dir_at(ii, jj) : 0xFFu;
+          const uint32_t stopm = __ballot_sync(0xffffffffu, !in || (d & 3) != 0);
+          const int l = stopm ? __ffs(stopm) - 1 : 32;  // cells [0, l) are DIAG
+          if (l > 0 && lane == 0) emit(0, (uint64_t)l);
+          ci -= l;
+          cj -= l;
+          if (l < 32) {
+            const uint32_t dl = __shfl_sync(0xffffffffu, d, l);
+            const bool inl = (ci > R && cj > C);
+            if (inl) {
+              const uint32_t src = dl & 3;
+              if (src == 3) done = true;           // local STOP
+              else st = (int)src;                  // UP -> E state, LEFT -> F state
+            }
+          }
+        } else if (st == 1) {  // E state: I ops up the column while E extends
+          const int ii = ci - lane;
+          const bool in = ii > R;
+          const uint32_t d = in ? dir_at(ii, cj) : 0;
+          const uint32_t endm = __ballot_sync(0xffffffffu, in && !((d >> 2) & 1));
+          const uint32_t outm = __ballot_sync(0xffffffffu, !in);
+          const int le = endm ? __ffs(endm) - 1 : 32, lo = outm ? __ffs(outm) - 1 : 32;
+          if (le < lo) {  // the run ends inside: cells [0, le] emit I, then the H state
+            if (lane == 0) emit(1, (uint64_t)le + 1);
+            ci -= le + 1;
+            st = 0;
+          } else {        // all extend up to the region's edge (or 32 cells): stay in E
+            if (lane == 0) emit(1, (uint64_t)lo);
+            ci -= lo;
+          }
+        } else {  // F state: D ops along the row while F extends
+          const int jj = cj - lane;
+          const bool in = jj > C;
+          const uint32_t d = in ? dir_at(ci, jj) : 0;
+          const uint32_t endm = __ballot_sync(0xffffffffu, in && !((d >> 3) & 1));
+          const uint32_t outm = __ballot_sync(0xffffffffu, !in);
+          const int le = endm ? __ffs(endm) - 1 : 32, lo = outm ? __ffs(outm) - 1 : 32;
+          if (le < lo) {
+            if (lane == 0) emit(2, (uint64_t)le + 1);
+            cj -= le + 1;
+            st = 0;
+          } else {
+            if (lane == 0) emit(2, (uint64_t)lo);
+            cj -= lo;
+          }
+        }
+      }
+      if (lane == 0) {
+        sh_i = ci;
+        sh_j = cj;
+        sh_st = st;
+        if (done) sh_done = 1;
+      }
+    }
+  }
+  if (t == 0) {
+    if (sh_run) {
+      if (sh_nops < a.ops_cap) a.ops[sh_nops] = sh_run;
+      ++sh_nops;
+    }
+    a.out[0] = sh_nops;
+    a.out[1] = (unsigned long long)sh_i;
+    a.out[2] = (unsigned long long)sh_j;
+    a.out[3] = tiles;
+  }
+}
+
+struct DBuf {
+  void* p = nullptr;
+  ~DBuf() { if (p) cudaFree(p); }
+};
+
+}  // namespace
+
+#define TK(call)                                                        \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) {                                            \
+      *err = std::string(#call) + ": " + cudaGetErrorString(e_);        \
+      return e_ == cudaErrorMemoryAllocation ? ANYSEQ_E_NOMEM : ANYSEQ_E_CUDA; \
+    }                                                                   \
+  } while (0)
+
+int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t sig[25],
+                       const LongCkpt& ck, int64_t end_i, int64_t end_j, int64_t n, int64_t m,
+                       std::vector<uint32_t>* ops, int64_t* begin_i, int64_t* begin_j,
+                       double* walk_ms, std::string* err, uint64_t* launches) {
+  TK(cudaSetDevice(dev.id));
+  cudaStream_t st = dev.stream;
+  ops->clear();
+  *begin_i = end_i;
+  *begin_j = end_j;
+  if (end_i == 0 && end_j == 0) return 0;
+  const int TH = ck.HS * ck.ck_every;
+  const int TR = TH / NT;
+  if (TR != 2 && TR != 4 && TR != 8 && TR != 16) {
+    *err = "long traceback: unsupported row block height";
+    return ANYSEQ_E_UNSUPPORTED;
+  }
+  WalkArgs a;
+  memset(&a, 0, sizeof(a));
+  a.kind = P.kind;
+  a.affine = P.gap == GAFFINE;
+  a.go = P.go;
+  a.ge = P.ge;
+  a.cop = P.go + P.ge;
+  memcpy(a.sig, sig, 25);
+  a.qc = ck.qc;
+  a.sc = ck.sc;
+  a.n = (int)n;
+  a.m = (int)m;
+  a.rowck = ck.rowck;
+  a.colck = ck.colck;
+  a.TH = TH;
+  a.PT = ck.PT;
+  a.kc_shift = ck.kc_shift;
+  a.end_i = (int)end_i;
+  a.end_j = (int)end_j;
+  const size_t scratch = ((size_t)(1 << ck.kc_shift) + NT) * NT * (((TR + 3) / 4) * 4);
+  DBuf sb, ob, outb;
+  TK(cudaMalloc(&sb.p, scratch));
+  const uint64_t cap = (uint64_t)(n + m + 2);
+  TK(cudaMalloc(&ob.p, cap * sizeof(uint32_t)));
+  TK(cudaMalloc(&outb.p, 4 * sizeof(unsigned long long)));
+  a.scratch = (uint8_t*)sb.p;
+  a.ops = (uint32_t*)ob.p;
+  a.ops_cap = cap;
+  a.out = (unsigned long long*)outb.p;
+  cudaEvent_t e0, e1;
+  TK(cudaEventCreate(&e0));
+  TK(cudaEventCreate(&e1));
+  TK(cudaEventRecord(e0, st));
+  switch (TR) {
+    case 2: tile_walk_kernel<2><<<1, NT, 0, st>>>(a); break;
+    case 4: tile_walk_kernel<4><<<1, NT, 0, st>>>(a); break;
+    case 8: tile_walk_kernel<8><<<1, NT, 0, st>>>(a); break;
+    default: tile_walk_kernel<16><<<1, NT, 0, st>>>(a); break;
+  }
+  TK(cudaGetLastError());
+  TK(cudaEventRecord(e1, st));
+  *launches += 1;
+  unsigned long long out[4];
+  TK(cudaMemcpyAsync(out, outb.p, sizeof(out), cudaMemcpyDeviceToHost, st));
+  TK(cudaStreamSynchronize(st));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *walk_ms = ms;
+  if (out[0] > cap) {
+    *err = "long traceback: walk overflowed its op buffer";
+    return ANYSEQ_E_CUDA;
+  }
+  ops->resize(out[0]);
+  if (out[0]) TK(cudaMemcpy(ops->data(), ob.p, out[0] * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  // walk order is end -> begin: reverse into alignment order
+  for (size_t x = 0, y = ops->size(); x + 1 < y; ++x, --y) std::swap((*ops)[x], (*ops)[y - 1]);
+  *begin_i = (int64_t)out[1];
+  *begin_j = (int64_t)out[2];
+  return 0;
+}
+
+}  // namespace anyseq

@@ -468,3 +468,57 @@ def test_c5_one_percent_of_1m_mixed():
             sspan = np.bincount(pair, weights=ln * (op != 1), minlength=B)
             assert np.array_equal(qspan.astype(np.int64), aln["q_end"] - aln["q_begin"]), kind
             assert np.array_equal(sspan.astype(np.int64), aln["s_end"] - aln["s_begin"]), kind
+
+
+def test_pack2_mixed_chunks(ctx):
+    """The host API's 2-bit upload (a1): ACGT-only chunks (upper and lower case) go up as
+    2-bit codes, chunks with an N -- or a bad byte -- take the byte path.  With small
+    chunks the same batch mixes both; scores, ends and CIGARs equal the oracle's and the
+    byte-path-only run (option pack2 = 0); a bad byte is still reported with its pair."""
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs, csr
+    q, qo, s, so = random_pairs(1200, 0, 300, seed=90, lower_frac=0.3)
+    q = q.copy()
+    # an N in pair 700's query and in pair 1100's subject: their chunks take the byte path
+    for arr, off, k in ((q, qo, 700), (s, so, 1100)):
+        if off[k + 1] > off[k]:
+            arr[int(off[k])] = ord("N")
+    res, ocig = _oracle("local", "affine", 5, 1, q, qo, s, so, tb=True)
+    sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+    ctx.set_option("chunk_bytes", 1 << 16)
+    try:
+        for p2 in (1, 0):
+            ctx.set_option("pack2", p2)
+            _check_scores(ctx, sch, q, qo, s, so, res)
+            _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+        ctx.set_option("pack2", 1)
+        bad = q.copy()
+        bad[int(qo[900]) + 1 if qo[901] - qo[900] > 1 else int(qo[901])] = ord("x")
+        with pytest.raises(A.AnyseqError) as e:
+            ctx.align_batch(sch, bad, qo, s, so)
+        assert e.value.status_name == "E_BADSEQ"
+    finally:
+        ctx.set_option("pack2", 1)
+        ctx.set_option("chunk_bytes", 64 << 20)
+
+
+def test_pack2_all_lengths(ctx):
+    """2-bit upload edge cases: every length 0..70 (partial last code byte, chunk ends
+    mid-byte) in one uniform-free batch, global linear, against the oracle."""
+    import paper_2002_04561_b200 as A
+    from synth import csr
+    rng = np.random.default_rng(3)
+    qs = [rng.choice(list(b"ACGTacgt"), size=L).astype(np.uint8).tobytes() for L in range(71)]
+    ss = [rng.choice(list(b"ACGT"), size=(L * 7) % 71).astype(np.uint8).tobytes()
+          for L in range(71)]
+    q, qo = csr(qs)
+    s, so = csr(ss)
+    res, ocig = _oracle("global", "linear", 0, 1, q, qo, s, so, tb=True)
+    sch = A.Scheme("global", "linear", 2, -1, 0, 1)
+    for cb in (1 << 12, 64 << 20):
+        ctx.set_option("chunk_bytes", cb)
+        try:
+            _check_scores(ctx, sch, q, qo, s, so, res)
+            _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+        finally:
+            ctx.set_option("chunk_bytes", 64 << 20)

@@ -1,9 +1,15 @@
-"""GPU parity of the linear-space long-pair traceback (anyseq_traceback_long, SURVEY 8(f) f1;
-global, local and semi-global kinds with linear gaps)
-against the oracle.  Several paths can be optimal, so the test compares what is unique --
-the optimum score (and, for local, the end cell under the tie rule of reading R10) -- with
-the oracle, and checks that the returned path is valid: it spans exactly the reported
-cells and rescoring it by P:241 (oracle/brute.rescore_cigar) gives the optimum."""
+"""GPU parity of the linear-space long-pair traceback (anyseq_traceback_long).
+
+Checkpointed path (every kind, linear and affine gaps): the walk takes every decision from
+exact full-matrix values, so score, begin cell, end cell and CIGAR are compared
+ELEMENT BY ELEMENT with the oracle's full-matrix traceback (oracle.align), at checkpoint
+geometries that put many tile boundaries on the path.  Larger pairs (beyond the oracle's
+full matrix) are checked against the oracle's linear-space score (score and end cell) and
+by rescoring the path.
+
+Hirschberg fallback (linear gaps, subjects with N): several paths can be optimal, so those
+tests compare what is unique -- the optimum score and end cell -- and check that the path
+is valid and rescores to the optimum."""
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -28,6 +34,98 @@ def _check_path(scheme_o, q, s, r):
     assert brute.rescore_cigar(scheme_o, qs, ss, r["q_begin"], r["s_begin"], cig) == r["score"]
 
 
+KINDS = ("global", "local", "semi")
+GAPS = (("linear", 0), ("affine", 5), ("affine", 2))
+# (long_band_rows, tb_ck_every, tb_kc_shift): 512-row strips with tiles 512 x 256 and
+# 1024 x 512, and the automatic geometry (1024-row strips, 1024-column blocks)
+GEOMS = ((512, 1, 8), (512, 2, 9), (0, 0, 0))
+
+
+def _set_geom(ctx, geom):
+    rows, every, kcs = geom
+    ctx.set_option("long_band_rows", rows)
+    ctx.set_option("tb_ck_every", every)
+    ctx.set_option("tb_kc_shift", kcs)
+
+
+def _pairs():
+    from synth import iid, c4_genomes
+    g1, g2 = c4_genomes(9000, "a", seed=21)
+    return [(iid(3000, 1), iid(2800, 2)),              # unrelated: gappy, many ties
+            (g1[:3100], g2[:2900]),                    # mutated copy, indels
+            (g1[5000:5400], g2[200:5200]),             # wide, a long free-end / gap run
+            (iid(1, 3), iid(1, 4)), (iid(70, 5), iid(1, 6)), (iid(1, 7), iid(700, 8))]
+
+
+@pytest.mark.parametrize("geom", GEOMS, ids=["512x256", "1024x512", "auto"])
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("gap,go", GAPS, ids=["lin", "aff5", "aff2"])
+def test_long_tb_ckpt_bit_exact(ctx, geom, kind, gap, go):
+    """Checkpointed traceback == the oracle's full-matrix traceback: score, begin, end and
+    CIGAR, for every kind and gap model, across checkpoint geometries."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    so = O.Scheme(kind, gap, 2, -1, go, 1)
+    _set_geom(ctx, geom)
+    try:
+        for q, s in _pairs():
+            r = ctx.traceback_long(A.Scheme(kind, gap, 2, -1, go, 1), q, s)
+            assert ctx.stat("tb_method") == 1
+            o = O.align(so, q, s)
+            got = (r["score"], r["q_begin"], r["s_begin"], r["q_end"], r["s_end"])
+            assert got == (o.score, o.q_begin, o.s_begin, o.q_end, o.s_end), (len(q), len(s))
+            assert r["cigar"] == o.cigar, (len(q), len(s))
+    finally:
+        _set_geom(ctx, (0, 0, 0))
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_long_tb_ckpt_matrix_scoring(ctx, kind):
+    """Matrix scoring through the checkpointed traceback, bit-exact."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    from synth import c4_genomes
+    mat = ((3, -2, -1, -2, -1), (-2, 2, -2, -1, -1), (-1, -2, 3, -2, -1),
+           (-2, -1, -2, 2, -1), (-1, -1, -1, -1, -1))
+    g1, g2 = c4_genomes(4000, "a", seed=23)
+    so = O.Scheme(kind, "affine", 0, 0, 4, 1, matrix=mat)
+    ctx.set_option("tb_kc_shift", 8)
+    try:
+        r = ctx.traceback_long(A.Scheme(kind, "affine", 0, 0, 4, 1, matrix=mat), g1, g2)
+    finally:
+        ctx.set_option("tb_kc_shift", 0)
+    o = O.align(so, g1, g2)
+    assert (r["score"], r["q_begin"], r["s_begin"], r["q_end"], r["s_end"]) == \
+           (o.score, o.q_begin, o.s_begin, o.q_end, o.s_end)
+    assert r["cigar"] == o.cigar
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("gap,go", [("affine", 5), ("linear", 0)])
+def test_long_tb_ckpt_large(ctx, kind, gap, go):
+    """120 kbp mutated pair (C4 variant-a shape): score and end cell equal the oracle's
+    linear-space score; the path spans begin -> end and rescores to the optimum."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    from synth import c4_genomes
+    g1, g2 = c4_genomes(120_000, "a", seed=24)
+    so = O.Scheme(kind, gap, 2, -1, go, 1)
+    r = ctx.traceback_long(A.Scheme(kind, gap, 2, -1, go, 1), g1, g2)
+    assert ctx.stat("tb_method") == 1
+    o = O.score_rolling(so, g1, g2)
+    assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end)
+    _check_path(so, g1, g2, r)
+
+
+def _with_n(x: bytes) -> bytes:
+    """The same sequence with one base replaced by N (sends the subject to the 32-bit kernel
+    and the traceback to the Hirschberg fallback)."""
+    b = bytearray(x)
+    if b:
+        b[len(b) // 2] = ord("N")
+    return bytes(b)
+
+
 @pytest.mark.parametrize("n,m,seed", [(1, 1, 1), (0, 9, 2), (7, 0, 3), (300, 280, 4),
                                       (3000, 2500, 5), (9000, 8700, 6), (1, 5000, 7),
                                       (6000, 3, 8)])
@@ -35,7 +133,7 @@ def test_long_tb_global_linear(ctx, n, m, seed):
     import paper_2002_04561_b200 as A
     from oracle import oracle as O
     from synth import iid
-    q, s = iid(n, seed), iid(m, seed + 100)
+    q, s = iid(n, seed), _with_n(iid(m, seed + 100))
     r = ctx.traceback_long(A.Scheme("global", "linear", 2, -1, 0, 1), q, s)
     so = O.Scheme("global", "linear", 2, -1, 0, 1)
     o = O.score_rolling(so, q, s)
@@ -62,6 +160,7 @@ def test_long_tb_local_linear_mutated(ctx, length, seed):
     from oracle import oracle as O
     from synth import c4_genomes
     g1, g2 = c4_genomes(length, "a", seed=seed)
+    g2 = _with_n(g2)
     so = O.Scheme("local", "linear", 2, -1, 0, 1)
     r = ctx.traceback_long(A.Scheme("local", "linear", 2, -1, 0, 1), g1, g2)
     o = O.score_rolling(so, g1, g2)
@@ -73,7 +172,7 @@ def test_long_tb_local_random_and_zero(ctx):
     import paper_2002_04561_b200 as A
     from oracle import oracle as O
     from synth import iid
-    q, s = iid(2500, 21), iid(2700, 22)
+    q, s = iid(2500, 21), _with_n(iid(2700, 22))
     so = O.Scheme("local", "linear", 2, -1, 0, 1)
     r = ctx.traceback_long(A.Scheme("local", "linear", 2, -1, 0, 1), q, s)
     o = O.align(so, q, s)
@@ -86,8 +185,10 @@ def test_long_tb_local_random_and_zero(ctx):
 
 def test_long_tb_errors(ctx):
     import paper_2002_04561_b200 as A
+    # affine gaps with an N in the subject: neither the 16-bit kernel nor Hirschberg (linear)
     with pytest.raises(A.AnyseqError) as e:
-        ctx.traceback_long(A.Scheme("global", "affine", 2, -1, 5, 1), b"ACGT", b"ACGT")
+        ctx.traceback_long(A.Scheme("global", "affine", 2, -1, 5, 1), b"ACGT" * 300,
+                           b"ACNT" * 300)
     assert e.value.status == 6
     with pytest.raises(A.AnyseqError) as e:
         ctx.traceback_long(A.Scheme("global", "linear", 2, -1, 0, 1), b"ACXT", b"ACGT")
@@ -104,7 +205,7 @@ def test_long_tb_semi_linear(ctx, n, m, seed):
     import paper_2002_04561_b200 as A
     from oracle import oracle as O
     from synth import iid
-    q, s = iid(n, seed), iid(m, seed + 100)
+    q, s = iid(n, seed), _with_n(iid(m, seed + 100))
     so = O.Scheme("semi", "linear", 2, -1, 0, 1)
     r = ctx.traceback_long(A.Scheme("semi", "linear", 2, -1, 0, 1), q, s)
     o = O.score_rolling(so, q, s)
@@ -121,6 +222,7 @@ def test_long_tb_semi_read_in_reference(ctx):
     from synth import c4_genomes
     g1, g2 = c4_genomes(40_000, "a", seed=9)
     read = g2[12_000:15_000]
+    g1 = _with_n(g1)
     so = O.Scheme("semi", "linear", 2, -1, 0, 1)
     r = ctx.traceback_long(A.Scheme("semi", "linear", 2, -1, 0, 1), read, g1)
     o = O.score_rolling(so, read, g1)
@@ -135,7 +237,7 @@ def test_long_tb_leaf_sizes(ctx, leaf):
     import paper_2002_04561_b200 as A
     from oracle import oracle as O
     from synth import iid
-    q, s = iid(1800, 41), iid(1500, 42)
+    q, s = iid(1800, 41), _with_n(iid(1500, 42))
     ctx.set_option("tb_leaf_cells", leaf)
     try:
         for kind in ("global", "local", "semi"):
