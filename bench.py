@@ -237,27 +237,32 @@ def long_pair_leg(ctx, A, n, n_sm, f_mhz, n_gpus=1):
             "score": r["score"], "end": [r["q_end"], r["s_end"]]}
 
 
-def long_traceback_leg(ctx, A, n):
-    """linear-space traceback of a C4-shaped pair (n-bp genomes, G2 = mutated
-    copy of G1), global linear +2/-1/-1 (the paper's long traceback scheme, Fig. 5a), once,
-    through anyseq_traceback_long with host buffers.  GCUPS = n*m / wall time of the call
-    (the paper's convention: matrix cells over total time); pass_gcups = cells relaxed by
-    the Hirschberg last-row passes / their device time (CUDA events per level launch)."""
+def long_traceback_leg(ctx, A, n, kind="global", gap="linear", go=0):
+    """linear-space traceback of a C4-shaped pair (n-bp genomes, G2 =
+    mutated copy of G1), once, through anyseq_traceback_long with host buffers: one
+    checkpointing forward pass of the 16-bit long kernel, then the tile-recompute walk
+    (DESIGN.md 5.4c).  Schemes: global linear +2/-1/-1 (the paper's long traceback scheme,
+    Fig. 5a) and local affine 5/1 (C4's scheme).  GCUPS = n*m / wall time of the call (the
+    paper's convention: matrix cells over total time); pass_gcups = n*m / the forward pass's
+    device time; walk_ms = the walk kernel's device time."""
     from synth import c4_genomes
     g1, g2 = c4_genomes(n, "a", seed=4)
-    sch = A.Scheme("global", "linear", 2, -1, 0, 1)
-    ctx.traceback_long(sch, g1, g2)  # warm-up: one-time device allocations of the leaves
+    sch = A.Scheme(kind, gap, 2, -1, go, 1)
+    ctx.traceback_long(sch, g1, g2)  # warm-up: one-time allocations
     t0 = time.perf_counter()
     r = ctx.traceback_long(sch, g1, g2)
     wall = time.perf_counter() - t0
-    pass_ms, pass_cells = ctx.stat("tb_pass_ms"), ctx.stat("tb_pass_cells")
+    pass_ms, walk_ms = ctx.stat("tb_pass_ms"), ctx.stat("tb_walk_ms")
     cells = len(g1) * len(g2)
-    return {"workload": f"{len(g1)} bp x {len(g2)} bp (C4 variant a shape), global linear, "
-                        "match 2 / mismatch -1 / gap 1, traceback (Hirschberg), 1 GPU",
+    return {"workload": f"{len(g1)} bp x {len(g2)} bp (C4 variant a shape), {kind} {gap}"
+                        + (f" open {go} / extend 1" if gap == "affine" else " gap 1")
+                        + ", match 2 / mismatch -1, traceback (checkpoints + tile walk), 1 GPU",
             "value": round(cells / wall / 1e9, 1), "unit": "GCUPS", "wall_ms": round(wall * 1e3, 1),
-            "pass_ms": round(pass_ms, 1), "pass_cells": pass_cells,
-            "pass_gcups": round(pass_cells / (pass_ms / 1e3) / 1e9, 1),
-            "kernel": "lastrow_kernel<0>", "score": r["score"], "cigar_ops": len(r["cigar"])}
+            "pass_ms": round(pass_ms, 1), "pass_gcups": round(cells / (pass_ms / 1e3) / 1e9, 1),
+            "walk_ms": round(walk_ms, 1), "ckpt_bytes": int(ctx.stat("tb_ckpt_bytes")),
+            "method": "checkpoints" if ctx.stat("tb_method") == 1 else "hirschberg",
+            "score": r["score"], "begin": [r["q_begin"], r["s_begin"]],
+            "end": [r["q_end"], r["s_end"]], "cigar_ops": len(r["cigar"])}
 
 
 def time_device_steps(step, stream, steps):
@@ -475,6 +480,8 @@ def main():
             dist.barrier(group=cpu_group)
     if rank == 0 and args.long_tb_bp > 0:
         line["long_traceback"] = long_traceback_leg(ctx, A, args.long_tb_bp)
+        line["long_traceback_local_affine"] = long_traceback_leg(ctx, A, args.long_tb_bp,
+                                                                 "local", "affine", 5)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -113,6 +113,7 @@ struct anyseq_ctx {
   int64_t force_variant = -1;
   int64_t allow16 = 1;
   int64_t pack2 = 1;        // host API: upload ACGT-only chunks as 2-bit codes
+  int64_t pack2_percent = 0;  // share of the bytes packed (0 = auto: 60 % from pinned sources)
   std::unique_ptr<PackPool> packpool;  // host packing threads (created on first use)
   PackPool* shared_pool = nullptr;  // per-device shard contexts use the parent's pool
   std::mutex pool_mu;
@@ -784,9 +785,26 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     ahead.state.assign(NC, 0);
     ahead.issued.assign(NC, 0);
     const int dev = D.id;
-    ahead.th = std::thread([&, dev, ms_since] {
+    // Host packing (~60-75 GB/s of ASCII on 16 host threads) and the copy engine (~50-55
+    // GB/s) are both ~the GPU's fill rate: from pinned sources the chunks are split between
+    // them -- a share goes up as 2-bit codes, the rest as ASCII DMA -- greedily by bytes.
+    const bool pinned_src = host_pinned(b->q) && host_pinned(b->s);
+    const double share = ctx->pack2_percent > 0 ? std::min<int64_t>(ctx->pack2_percent, 100) / 100.0
+                                                : (pinned_src ? 0.6 : 1.0);
+    ahead.th = std::thread([&, dev, ms_since, share] {
       cudaSetDevice(dev);
+      double packed_bytes = 0, all_bytes = 0;
       for (int c = 0; c < NC; ++c) {
+        const double cbytes = (double)(b->q_off[cb[c + 1]] - b->q_off[cb[c]] +
+                                       b->s_off[cb[c + 1]] - b->s_off[cb[c]]);
+        all_bytes += cbytes;
+        if (packed_bytes + cbytes > share * all_bytes + 1.0) {  // this one goes as ASCII
+          std::lock_guard<std::mutex> lk(ahead.mu);
+          ahead.state[c] = 2;
+          ahead.cv.notify_all();
+          continue;
+        }
+        packed_bytes += cbytes;
         const int slot = c % 3;
         if (c >= 3) {  // the slot's previous upload (chunk c - 3) must have completed
           std::unique_lock<std::mutex> lk(ahead.mu);
@@ -1021,6 +1039,7 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
         local.allow16 = ctx->allow16;
         local.chunk_bytes = ctx->chunk_bytes;
         local.pack2 = ctx->pack2;
+        local.pack2_percent = ctx->pack2_percent;
         local.shared_pool = ctx->pack2 ? ctx->packer() : nullptr;
         anyseq_status s = ANYSEQ_OK;
         if (bounds[g + 1] > bounds[g])  // an exception must not escape a std::thread either
@@ -1630,6 +1649,11 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
     if (n == "chunk_bytes") { ctx->chunk_bytes = std::max<int64_t>(value, 1 << 16); return ANYSEQ_OK; }
     if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "pack2") { ctx->pack2 = value ? 1 : 0; return ANYSEQ_OK; }
+    if (n == "pack2_percent") {
+      if (value < 0 || value > 100) return fail(ctx, ANYSEQ_E_INVALID, "pack2_percent in [0, 100]");
+      ctx->pack2_percent = value;
+      return ANYSEQ_OK;
+    }
     if (n == "tb_ckpt_bytes") { ctx->tb_budget = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
     if (n == "tb_kc_shift") {
       if (value != 0 && (value < 8 || value > 12))

@@ -103,12 +103,12 @@ def test_long_tb_ckpt_matrix_scoring(ctx, kind):
 @pytest.mark.parametrize("kind", KINDS)
 @pytest.mark.parametrize("gap,go", [("affine", 5), ("linear", 0)])
 def test_long_tb_ckpt_large(ctx, kind, gap, go):
-    """120 kbp mutated pair (C4 variant-a shape): score and end cell equal the oracle's
+    """30 kbp mutated pair (C4 variant-a shape): score and end cell equal the oracle's
     linear-space score; the path spans begin -> end and rescores to the optimum."""
     import paper_2002_04561_b200 as A
     from oracle import oracle as O
     from synth import c4_genomes
-    g1, g2 = c4_genomes(120_000, "a", seed=24)
+    g1, g2 = c4_genomes(30_000, "a", seed=24)
     so = O.Scheme(kind, gap, 2, -1, go, 1)
     r = ctx.traceback_long(A.Scheme(kind, gap, 2, -1, go, 1), g1, g2)
     assert ctx.stat("tb_method") == 1
