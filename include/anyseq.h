@@ -183,7 +183,7 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
                          expands them); chunks with N or other bytes go up as ASCII.  0 =
                          always ASCII
      "pack2_percent"     share (by bytes) of the chunks that are packed; the rest go up as
-                         ASCII DMA in parallel (0 = auto: 60 from pinned sources, else 100)
+                         ASCII DMA in parallel (0 = 100, the default)
      "tb_scratch_bytes"  traceback: device bytes of the per-cell H store per fill/walk
                          chunk (default 16 GiB; 2 B per cell for s16x2 slots)
      "allow16"           0 forces 32-bit arithmetic (debug); "force_variant" (debug)

@@ -112,8 +112,9 @@ struct anyseq_ctx {
   int64_t chunk_bytes = 64ll << 20;  // host-API upload/compute pipelining granularity
   int64_t force_variant = -1;
   int64_t allow16 = 1;
+  int64_t tb8 = 1;          // traceback: 1-byte H store where the range allows
   int64_t pack2 = 1;        // host API: upload ACGT-only chunks as 2-bit codes
-  int64_t pack2_percent = 0;  // share of the bytes packed (0 = auto: 60 % from pinned sources)
+  int64_t pack2_percent = 0;  // share of the bytes packed (0 = all)
   std::unique_ptr<PackPool> packpool;  // host packing threads (created on first use)
   PackPool* shared_pool = nullptr;  // per-device shard contexts use the parent's pool
   std::mutex pool_mu;
@@ -436,6 +437,21 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     L(1);
   }
 
+  // Traceback H store in low bytes: the walk rebuilds H from neighbour
+  // differences, exact when |H(x) - H(y)| < 128 for adjacent cells and a diagonal test
+  // |H(i-1,j-1) - (H(i,j) - sigma)| < 256 -- both hold when 2 d + max |sigma| < 256, d =
+  // G_o + G_e + max(sigma, 0) being the Lipschitz bound of the recurrence
+  int tb8 = 0;
+  if (J.tb && ctx->tb8) {
+    int smaxabs = 0;
+    for (int a = 0; a < 25; ++a) {
+      const int v = prm->has_subst ? prm->subst[a] : ((a % 6 == 0 && a < 24) ? prm->match : prm->mismatch);
+      smaxabs = std::max(smaxabs, std::abs(v));
+    }
+    const int64_t dl = (int64_t)P.go + P.ge + std::max(P.smax, 0);
+    tb8 = (2 * dl + smaxabs < 256 && dl < 128) ? 1 : 0;
+  }
+
   // ---- a3/a4: fill (+ a5 walk) per variant ----
   // score mode with several variants: fork the variant launches onto their own streams
   int nvar = 0;
@@ -507,14 +523,18 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     } else {
       const int64_t ns = (S.maxn[v] + HS - 1) / HS;
       const int64_t dk = S.maxm[v] + d.L - 1 + d.R - 1;  // diagonals (step - row) per strip
-      const int64_t block_words = ns * dk * d.R * d.L;    // one H word per (diag, row, lane)
+      const int64_t block_words = ns * dk * d.R * d.L;    // one H element per (diag, row, lane)
       DevBuf& dirs = fork ? D.dirs_v[v] : D.dirs;
-      const int64_t cap_words = std::max<int64_t>(ctx->tb_scratch_bytes / 4, block_words);
+      // element size: the full H word (4 B), or -- when neighbouring H values provably
+      // differ by less than 128 -- its low byte per alignment (2 B for s16x2, 1 B for s32)
+      const int64_t esz = tb8 ? (d.pairs == 2 ? 2 : 1) : 4;
+      const int64_t cap_words = std::max<int64_t>(ctx->tb_scratch_bytes / esz, block_words);
       int64_t chunk = std::max<int64_t>(1, cap_words / block_words);
       chunk = std::min<int64_t>(chunk, nslot[v]);
-      CK(dirs.ensure((size_t)(chunk * block_words) * 4));
+      CK(dirs.ensure((size_t)(chunk * block_words) * esz + 16));
       fa.dirs = dirs.as<uint32_t>();
       fa.dir_block_words = block_words;
+      fa.tb8 = tb8;
       fa.tb = D.tb.as<TbInfo>();
       for (int64_t lo = 0; lo < nslot[v]; lo += chunk) {
         const int64_t hi = std::min<int64_t>(nslot[v], lo + chunk);
@@ -544,6 +564,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
         wa.pairs_per_slot = d.pairs;
         wa.tb = D.tb.as<TbInfo>();
         wa.dirs = dirs.as<uint32_t>();
+        wa.tb8 = tb8;
         wa.q_off = J.d_qoff;
         wa.s_off = J.d_soff;
         wa.ops = D.ops.as<uint32_t>();
@@ -785,12 +806,11 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     ahead.state.assign(NC, 0);
     ahead.issued.assign(NC, 0);
     const int dev = D.id;
-    // Host packing (~60-75 GB/s of ASCII on 16 host threads) and the copy engine (~50-55
-    // GB/s) are both ~the GPU's fill rate: from pinned sources the chunks are split between
-    // them -- a share goes up as 2-bit codes, the rest as ASCII DMA -- greedily by bytes.
-    const bool pinned_src = host_pinned(b->q) && host_pinned(b->s);
+    // Share of the chunks (by bytes) packed on the host; the rest go up as ASCII DMA
+    // (option pack2_percent; all by default: splitting between host packing and ASCII DMA
+    // measured slower on B200 hosts -- both read host memory)
     const double share = ctx->pack2_percent > 0 ? std::min<int64_t>(ctx->pack2_percent, 100) / 100.0
-                                                : (pinned_src ? 0.6 : 1.0);
+                                                : 1.0;
     ahead.th = std::thread([&, dev, ms_since, share] {
       cudaSetDevice(dev);
       double packed_bytes = 0, all_bytes = 0;
@@ -1039,6 +1059,7 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
         local.allow16 = ctx->allow16;
         local.chunk_bytes = ctx->chunk_bytes;
         local.pack2 = ctx->pack2;
+        local.tb8 = ctx->tb8;
         local.pack2_percent = ctx->pack2_percent;
         local.shared_pool = ctx->pack2 ? ctx->packer() : nullptr;
         anyseq_status s = ANYSEQ_OK;
@@ -1649,6 +1670,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
     if (n == "chunk_bytes") { ctx->chunk_bytes = std::max<int64_t>(value, 1 << 16); return ANYSEQ_OK; }
     if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "pack2") { ctx->pack2 = value ? 1 : 0; return ANYSEQ_OK; }
+    if (n == "tb8") { ctx->tb8 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "pack2_percent") {
       if (value < 0 || value > 100) return fail(ctx, ANYSEQ_E_INVALID, "pack2_percent in [0, 100]");
       ctx->pack2_percent = value;

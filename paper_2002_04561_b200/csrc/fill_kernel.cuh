@@ -363,10 +363,26 @@ __global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) 
         if (TB && valid && sact && k < M + L - 1) {
           // word ((st * DK + k - r + R - 1) * R + r) * L + t: diagonal-major per lane (the
           // walk's diagonal runs are sequential), lanes of a group contiguous (32 B/row)
-          uint32_t* wp = a.dirs + dbase +
-                         (((int64_t)st * (M + L - 1 + R - 1) + k + R - 1) * R) * L + t;
+          const int64_t w0 = (((int64_t)st * (M + L - 1 + R - 1) + k + R - 1) * R) * L + t;
+          if (a.tb8) {
+            // 1 B per cell: the low byte of H of each alignment (both halves of an s16x2
+            // register in one 16-bit store); same element order, elements of 2 B (s16x2)
+            // or 1 B (s32) instead of 4 B words
+            if (V::P == 2) {
+              uint16_t* bp = reinterpret_cast<uint16_t*>(a.dirs) + dbase + w0;
 #pragma unroll
-          for (int r = 0; r < R; ++r) wp[-(int64_t)r * (R - 1) * L] = (uint32_t)Hq[r];
+              for (int r = 0; r < R; ++r)
+                bp[-(int64_t)r * (R - 1) * L] = (uint16_t)prmt((uint32_t)Hq[r], 0u, 0x0020u);
+            } else {
+              uint8_t* bp = reinterpret_cast<uint8_t*>(a.dirs) + dbase + w0;
+#pragma unroll
+              for (int r = 0; r < R; ++r) bp[-(int64_t)r * (R - 1) * L] = (uint8_t)Hq[r];
+            }
+          } else {
+            uint32_t* wp = a.dirs + dbase + w0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) wp[-(int64_t)r * (R - 1) * L] = (uint32_t)Hq[r];
+          }
         }
         diag = hin;
         Hbot = Hq[R - 1];

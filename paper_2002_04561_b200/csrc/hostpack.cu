@@ -45,42 +45,69 @@ bool pack_scalar(const uint8_t* in, size_t n, uint8_t* out) {
   return ok;
 }
 
+// Per byte x (either case): the low nibble of 'a','c','g','t' is 1, 3, 7, 4; a 16-entry
+// table indexed by the low nibble gives the lowercase letter that nibble must come from
+// (0 = none) and a second one its 2-bit code, so validation is one table lookup and one
+// compare of (x | 0x20) and the code one more lookup.  Four codes per byte: maddubs
+// (c0 + 4 c1), madd (p0 + 16 p1), then the low byte of every 32-bit lane.
 __attribute__((target("avx2"))) bool pack_avx2(const uint8_t* in, size_t n, uint8_t* out) {
   const size_t n32 = n / 32;
-  __m256i bad = _mm256_setzero_si256();
-  const __m256i m20 = _mm256_set1_epi8(0x20), ca = _mm256_set1_epi8('a'),
-                cc = _mm256_set1_epi8('c'), cg = _mm256_set1_epi8('g'),
-                ct = _mm256_set1_epi8('t'), m3 = _mm256_set1_epi8(3),
-                ones = _mm256_set1_epi8(-1);
+  const __m256i lowtab = _mm256_setr_epi8(0, 'a', 0, 'c', 't', 0, 0, 'g', 0, 0, 0, 0, 0, 0, 0, 0,
+                                          0, 'a', 0, 'c', 't', 0, 0, 'g', 0, 0, 0, 0, 0, 0, 0, 0);
+  const __m256i codetab = _mm256_setr_epi8(0, 0, 0, 1, 3, 0, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0,
+                                           0, 0, 0, 1, 3, 0, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0);
+  const __m256i m0f = _mm256_set1_epi8(0x0f), m20 = _mm256_set1_epi8(0x20);
   const __m256i w2 = _mm256_set1_epi16(0x0401), w4 = _mm256_set1_epi32(0x00100001);
   const __m256i gather = _mm256_setr_epi8(0, 4, 8, 12, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
                                           -1, -1, 0, 4, 8, 12, -1, -1, -1, -1, -1, -1, -1, -1,
                                           -1, -1, -1, -1);
+  uint32_t bad = 0;
   for (size_t i = 0; i < n32; ++i) {
     const __m256i x = _mm256_loadu_si256((const __m256i*)(in + 32 * i));
-    const __m256i l = _mm256_or_si256(x, m20);
-    const __m256i ok =
-        _mm256_or_si256(_mm256_or_si256(_mm256_cmpeq_epi8(l, ca), _mm256_cmpeq_epi8(l, cc)),
-                        _mm256_or_si256(_mm256_cmpeq_epi8(l, cg), _mm256_cmpeq_epi8(l, ct)));
-    bad = _mm256_or_si256(bad, _mm256_xor_si256(ok, ones));
-    const __m256i c =
-        _mm256_and_si256(_mm256_xor_si256(_mm256_srli_epi16(x, 1), _mm256_srli_epi16(x, 2)), m3);
-    // 4 codes per byte: pairs (c0 + 4 c1) with maddubs, then (p0 + 16 p1) with madd
+    const __m256i lo = _mm256_and_si256(x, m0f);
+    const __m256i ok = _mm256_cmpeq_epi8(_mm256_or_si256(x, m20), _mm256_shuffle_epi8(lowtab, lo));
+    bad |= ~(uint32_t)_mm256_movemask_epi8(ok);
+    const __m256i c = _mm256_shuffle_epi8(codetab, lo);
     const __m256i p4 = _mm256_madd_epi16(_mm256_maddubs_epi16(c, w2), w4);
     const __m256i sh = _mm256_shuffle_epi8(p4, gather);
-    const uint32_t lo = (uint32_t)_mm256_extract_epi32(sh, 0);
-    const uint32_t hi = (uint32_t)_mm256_extract_epi32(sh, 4);
-    memcpy(out + 8 * i, &lo, 4);
-    memcpy(out + 8 * i + 4, &hi, 4);
+    const uint32_t a0 = (uint32_t)_mm256_extract_epi32(sh, 0);
+    const uint32_t a1 = (uint32_t)_mm256_extract_epi32(sh, 4);
+    memcpy(out + 8 * i, &a0, 4);
+    memcpy(out + 8 * i + 4, &a1, 4);
   }
-  bool ok = _mm256_testz_si256(bad, bad);
-  if (n32 * 32 < n) ok &= pack_scalar(in + n32 * 32, n - n32 * 32, out + n32 * 8);
-  return ok;
+  bool okall = bad == 0;
+  if (n32 * 32 < n) okall &= pack_scalar(in + n32 * 32, n - n32 * 32, out + n32 * 8);
+  return okall;
+}
+
+__attribute__((target("avx512f,avx512bw"))) bool pack_avx512(const uint8_t* in, size_t n,
+                                                                uint8_t* out) {
+  const size_t n64 = n / 64;
+  const __m512i lowtab = _mm512_broadcast_i32x4(
+      _mm_setr_epi8(0, 'a', 0, 'c', 't', 0, 0, 'g', 0, 0, 0, 0, 0, 0, 0, 0));
+  const __m512i codetab = _mm512_broadcast_i32x4(
+      _mm_setr_epi8(0, 0, 0, 1, 3, 0, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0));
+  const __m512i m0f = _mm512_set1_epi8(0x0f), m20 = _mm512_set1_epi8(0x20);
+  const __m512i w2 = _mm512_set1_epi16(0x0401), w4 = _mm512_set1_epi32(0x00100001);
+  __mmask64 bad = 0;
+  for (size_t i = 0; i < n64; ++i) {
+    const __m512i x = _mm512_loadu_si512((const void*)(in + 64 * i));
+    const __m512i lo = _mm512_and_si512(x, m0f);
+    bad |= _mm512_cmpneq_epi8_mask(_mm512_or_si512(x, m20), _mm512_shuffle_epi8(lowtab, lo));
+    const __m512i c = _mm512_shuffle_epi8(codetab, lo);
+    const __m512i p4 = _mm512_madd_epi16(_mm512_maddubs_epi16(c, w2), w4);
+    _mm_storeu_si128((__m128i*)(out + 16 * i), _mm512_cvtepi32_epi8(p4));  // low byte of each lane
+  }
+  bool okall = bad == 0;
+  if (n64 * 64 < n) okall &= pack_scalar(in + n64 * 64, n - n64 * 64, out + n64 * 16);
+  return okall;
 }
 
 const bool kHaveAvx2 = __builtin_cpu_supports("avx2");
+const bool kHaveAvx512 = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
 
 bool pack_range(const uint8_t* in, size_t n, uint8_t* out) {
+  if (kHaveAvx512) return pack_avx512(in, n, out);
   return kHaveAvx2 ? pack_avx2(in, n, out) : pack_scalar(in, n, out);
 }
 

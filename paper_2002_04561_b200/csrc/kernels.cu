@@ -415,7 +415,7 @@ __global__ void walk_kernel(WalkArgs a) {
     const TbInfo ti = a.tb[pair];
     const uint64_t base = a.q_off[pair] + a.s_off[pair] + (uint64_t)pair;
     walk_pair(a.P, a.dirs, ti, a.qcode + a.q_off[pair] - 1, a.scode + a.s_off[pair] - 1,
-              a.ops + base, a.n_ops + pair, a.beg_i + pair, a.beg_j + pair);
+              a.ops + base, a.n_ops + pair, a.beg_i + pair, a.beg_j + pair, a.tb8 != 0);
   }
 }
 

@@ -82,6 +82,7 @@ struct WalkArgs {
   int32_t pairs_per_slot;
   const TbInfo* tb;
   const uint32_t* dirs;
+  int32_t tb8;     // the H store holds low bytes (FillArgs::tb8)
   const uint64_t* q_off;
   const uint64_t* s_off;
   uint32_t* ops;   // per-pair run region (reversed run order)

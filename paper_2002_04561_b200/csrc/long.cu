@@ -758,10 +758,12 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     int ab = 0;
     LK(cudaMemcpy(&ab, D.abort_.p, 4, cudaMemcpyDeviceToHost));
     if (opt.profile && D.profbuf.p) {
-      unsigned long long pr[3];
-      LK(cudaMemcpy(pr, D.profbuf.p, 24, cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[anyseq long] device %d: wait cycles %llu, task cycles %llu, tasks %llu, wait share %.3f, grid %d\n",
-              gdev[d].id, pr[0], pr[1], pr[2], pr[1] ? (double)pr[0] / pr[1] : 0.0, D.grid);
+      unsigned long long pr[5];
+      LK(cudaMemcpy(pr, D.profbuf.p, sizeof(pr), cudaMemcpyDeviceToHost));
+      const double tc = pr[1] ? (double)pr[1] : 1.0;
+      fprintf(stderr, "[anyseq long] device %d: task cycles %llu, tasks %llu, grid %d; wait share: "
+              "mid-task refills %.3f, task-start refills %.3f, column-edge flags %.3f\n",
+              gdev[d].id, pr[1], pr[2], D.grid, pr[0] / tc, pr[3] / tc, pr[4] / tc);
     }
     aborted |= ab;
     std::vector<LongPart> parts((size_t)D.grid * 4);

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
   __shared__ int2 ring_he[4][RING];
   __shared__ uint16_t ring_sel[4][RING];  // subject code c of a column as c * 0x11
   __shared__ int2 ring_out[4][64];        // the task's last row (H, E) awaiting publication
+  __shared__ int4 ring_pf[4][64];         // row hand-off entries prefetched a period early
   __shared__ int ring_eck[CKPT ? 4 : 1][64];  // CKPT: E of that row itself (not of the next)
   const int t = threadIdx.x & 31;
   const int wb = threadIdx.x >> 5;
@@ -128,12 +129,70 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
           if (t == 0) atomicExch(a.abort_flag, 1);
           return false;
         }
+        if (a.prof && t == 0)  // [0]: mid-task refills, [3]: the task's first two refills
+          atomicAdd(&a.prof[c0 < 2 * PER ? 3 : 0], (unsigned long long)(clock64() - t0));
+      }
+      if (mine) ring_he[wb][c & (RING - 1)] = make_int2(v.x, v.z);
+      return true;
+    };
+    // Software-pipelined refill: one period (32 steps) before the ring needs them, the row
+    // hand-off entries of the next 32 columns are copied global -> shared with cp.async (and
+    // their subject codes loaded into a register), so the L2 latency of the hand-off hides
+    // behind the period's relaxation; at the refill point the tags are checked in shared
+    // memory and only entries not yet published by the strip above are polled.
+    int pf_code = 0;
+    auto prefetch = [&](int c0) {
+      const int c = c0 + t;
+      if (s > 0 && c < W) cp_async16(&ring_pf[wb][c & 63], a.rowbuf + c_lo + c + 1);
+      cp_async_commit();
+      pf_code = c < W ? a.sc[c_lo + c] : 0;
+    };
+    auto consume = [&](int c0, int c1) -> bool {
+      const int c = c0 + t;
+      const bool mine = c < c1;
+      if (mine) ring_sel[wb][c & (RING - 1)] = (uint16_t)(pf_code * 0x11u);
+      if (s == 0) return true;
+      cp_async_wait_all();
+      const int4* src = a.rowbuf + c_lo + c + 1;
+      int4 v = mine ? ring_pf[wb][c & 63] : make_int4(0, s, 0, s);
+      long long spins = 0;
+      while (!__all_sync(0xffffffffu, v.y == s && v.w == s)) {
+        const long long t0 = (a.prof && t == 0) ? clock64() : 0;
+        if (v.y != s || v.w != s) v = ld_row(src);
+        if (!__all_sync(0xffffffffu, v.y == s && v.w == s)) __nanosleep(a.sleep_ns);
+        if ((++spins & 255) == 0 &&
+            __any_sync(0xffffffffu, spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
+          if (t == 0) atomicExch(a.abort_flag, 1);
+          return false;
+        }
         if (a.prof && t == 0) atomicAdd(&a.prof[0], (unsigned long long)(clock64() - t0));
       }
       if (mine) ring_he[wb][c & (RING - 1)] = make_int2(v.x, v.z);
       return true;
     };
+    // start slack (option long_start_lag, columns): tickets are taken in strip order, so the
+    // strips of a round start one after the other and would run at the minimum distance the
+    // hand-off allows (~4 refill periods) -- any hiccup of a strip then stalls the chain
+    // below it.  Starting `lag` columns further behind gives every strip that much slack.
+    if (s > 0 && a.lag > 0 && W > a.lag) {
+      const int4* p = a.rowbuf + c_lo + a.lag;
+      int ok = 1;
+      if (t == 0) {
+        long long spins = 0;
+        while (ok) {
+          const int4 v = ld_row(p);
+          if (v.y == s && v.w == s) break;
+          if ((++spins & 255) == 0 && (spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
+            atomicExch(a.abort_flag, 1);
+            ok = 0;
+          }
+          __nanosleep(256);
+        }
+      }
+      if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+    }
     if (!refill(0, min(W, PER)) || !refill(PER, min(W, 2 * PER))) break;
+    prefetch(2 * PER);
     __syncwarp();
 
     // frame: every value of the task lies within a.bspan of H(ip0, c_lo + 1) (the row
@@ -341,7 +400,8 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
       int k = 0;
       auto maybe_refill = [&](int kk) -> bool {
         if ((kk % PER) == 0 && kk > 0 && kk + PER < W) {
-          if (!refill(kk + PER, min(W, kk + 2 * PER))) return false;
+          if (!consume(kk + PER, min(W, kk + 2 * PER))) return false;
+          prefetch(kk + 2 * PER);
           __syncwarp();
         }
         return true;

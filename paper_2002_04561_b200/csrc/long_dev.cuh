@@ -83,6 +83,14 @@ __device__ __forceinline__ int4 ld_row(const int4* p) {
   return v;
 }
 
+// 16-byte global -> shared copy that bypasses L1 (cp.async.cg), committed as a group
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ bool lkey_better(int v, int i, int j, int bv, int bi, int bj) {
   return v > bv || (v == bv && (j < bj || (j == bj && i < bi)));
 }
@@ -118,7 +126,7 @@ __device__ __forceinline__ bool warp_wait(const int* p, int need, const LongArgs
       }
       __nanosleep(32);
     }
-    if (a.prof) atomicAdd(&a.prof[0], (unsigned long long)(clock64() - t0));
+    if (a.prof) atomicAdd(&a.prof[4], (unsigned long long)(clock64() - t0));  // [4]: flags
   }
   return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }

@@ -13,16 +13,19 @@
 namespace anyseq {
 
 // H(i, j) of a pair from the traceback H store (fill_kernel.cuh, traceback mode): one
-// 32-bit word per (strip, diagonal d = step - row, row, lane) of the slot -- a diagonal
-// run of the walk reads consecutive 32-byte sectors -- both alignments of an s16x2 slot
-// in its halves (global/semi s16x2 values biased by 2^14); row 0 / column 0 are the
-// initial values of P:259-264.
-__device__ __forceinline__ int hval(const DevParams& P, const uint32_t* __restrict__ dirs,
-                                    const TbInfo& ti, int i, int j) {
-  if (i == 0 || j == 0) {
-    if (P.kind != KGLOBAL || (i == 0 && j == 0)) return 0;
-    return -(P.go + (i + j) * P.ge);
-  }
+// element per (strip, diagonal d = step - row, row, lane) of the slot -- a diagonal run of
+// the walk reads consecutive 32-byte sectors.  Full store: 32-bit words with both
+// alignments of an s16x2 slot in their halves (global/semi s16x2 values biased by 2^14).
+// Low-byte store (tb8): 16-bit elements holding the low byte of each alignment's H (s16x2)
+// or bytes (s32); the walk rebuilds exact values from neighbour differences (see below).
+// Row 0 / column 0 are the initial values of P:259-264, always exact.
+__device__ __forceinline__ int hbound(const DevParams& P, int i, int j) {
+  if (P.kind != KGLOBAL || (i == 0 && j == 0)) return 0;
+  return -(P.go + (i + j) * P.ge);
+}
+
+__device__ __forceinline__ int hraw(const DevParams& P, const uint32_t* __restrict__ dirs,
+                                    const TbInfo& ti, int i, int j, bool tb8) {
   const int L = ti.L, R = ti.R;
   const int ip = i - 1 + ti.pad;
   int st, tt, r;
@@ -36,12 +39,28 @@ __device__ __forceinline__ int hval(const DevParams& P, const uint32_t* __restri
   const int DK = ti.slot_M + L - 1 + R - 1;   // diagonal index range per strip
   const int64_t w =
       ti.dir_base + ((((int64_t)st * DK + (k - r + R - 1)) * R + r) * L + tt);
+  if (tb8) {
+    if (ti.P == 2)
+      return (int)((__ldg(reinterpret_cast<const unsigned short*>(dirs) + w) >> (8 * ti.half)) & 0xffu);
+    return (int)__ldg(reinterpret_cast<const unsigned char*>(dirs) + w);
+  }
   const uint32_t word = dirs[w];
   if (ti.P == 2) {
     const int v = (int)(int16_t)(uint16_t)(ti.half ? (word >> 16) : (word & 0xffffu));
     return P.kind == KLOCAL ? v : v - (1 << 14);
   }
   return (int)word;
+}
+
+// Does cell (i, j) hold the value `want`?  Exact for the full store; for the low-byte store
+// exact whenever |H(i,j) - want| < 256 (the host admits tb8 only then).
+__device__ __forceinline__ bool hmatch(int raw, int want, bool tb8) {
+  return tb8 ? (raw == (want & 0xff)) : (raw == want);
+}
+// The exact value of cell (i, j) from its stored element and the exact value `ref` of an
+// adjacent cell (|difference| < 128 for the low-byte store).
+__device__ __forceinline__ int hnear(int raw, int ref, bool tb8) {
+  return tb8 ? ref + (int)(int8_t)(uint8_t)(raw - (ref & 0xff)) : raw;
 }
 
 struct RunWriter {
@@ -62,16 +81,29 @@ struct RunWriter {
 
 // Walk one pair from its end cell; runs in walk order (reversed) at ops_out, the number of
 // runs and the begin cell to the pointers.  qc / sc: 1-based code pointers of the pair.
+// The walk keeps the exact H of its current cell (starting from the optimum's score) and
+// takes every other value either as a test against an expected value (hmatch) or rebuilt
+// from the adjacent cell just visited (hnear): both exact for either store format.
 static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t* __restrict__ dirs,
                                        const TbInfo& ti, const uint8_t* qc, const uint8_t* sc,
                                        uint32_t* ops_out, int32_t* n_ops, int32_t* beg_i,
-                                       int32_t* beg_j) {
+                                       int32_t* beg_j, bool tb8) {
   const int go = P.go, ge = P.ge;
   const int kind = P.kind;
   RunWriter rw{ops_out, 0, 0, 0};
   int i = ti.end_i, j = ti.end_j;
-  int h = hval(P, dirs, ti, i, j);
+  int h = ti.score;
   const bool linear = P.gap == GLINEAR;
+  // the exact value of (i2, j2) given the exact value ref of an adjacent cell
+  auto hget = [&](int i2, int j2, int ref) -> int {
+    if (i2 == 0 || j2 == 0) return hbound(P, i2, j2);
+    return hnear(hraw(P, dirs, ti, i2, j2, tb8), ref, tb8);
+  };
+  // does (i2, j2) hold `want`
+  auto hhas = [&](int i2, int j2, int want) -> bool {
+    if (i2 == 0 || j2 == 0) return hbound(P, i2, j2) == want;
+    return hmatch(hraw(P, dirs, ti, i2, j2, tb8), want, tb8);
+  };
   for (;;) {
     if (i == 0 || j == 0) {
       if (kind == KGLOBAL) {  // reading R16: boundary runs
@@ -105,7 +137,8 @@ static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t
 #pragma unroll
       for (int l = 0; l < DW; ++l) {
         if (l < lim) {
-          hv[l] = hval(P, dirs, ti, i - 1 - l, j - 1 - l);
+          const int i2 = i - 1 - l, j2 = j - 1 - l;
+          hv[l] = (i2 == 0 || j2 == 0) ? hbound(P, i2, j2) : hraw(P, dirs, ti, i2, j2, tb8);
           const uint32_t cq = vec ? (uint32_t)(vq >> (8 * (DW - 1 - l))) & 0xffu : qc[i - l];
           const uint32_t cs = vec ? (uint32_t)(vs >> (8 * (DW - 1 - l))) & 0xffu : sc[j - l];
           sg[l] = sigma_of(P, cq, cs);
@@ -114,9 +147,13 @@ static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t
       int taken = 0;
 #pragma unroll
       for (int l = 0; l < DW; ++l) {
-        if (l == taken && l < lim && !(kind == KLOCAL && h <= 0) && h == hv[l] + sg[l]) {
-          h = hv[l];
-          ++taken;
+        if (l == taken && l < lim && !(kind == KLOCAL && h <= 0)) {
+          const int want = h - sg[l];  // DIAG iff H(i-1-l, j-1-l) = H - sigma
+          const bool bnd = (i - 1 - l == 0) || (j - 1 - l == 0);
+          if (bnd ? hv[l] == want : hmatch(hv[l], want, tb8)) {
+            h = want;
+            ++taken;
+          }
         }
       }
       if (taken) {
@@ -126,38 +163,45 @@ static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t
         continue;  // re-examine (i, j): boundary, STOP or the next run
       }
     }
-    const int hd = hval(P, dirs, ti, i - 1, j - 1);
     const int sig = sigma_of(P, qc[i], sc[j]);
-    if (h == hd + sig) {  // DIAG
+    if (hhas(i - 1, j - 1, h - sig)) {  // DIAG
       rw.push(0u, 1);
       --i; --j;
-      h = hd;
+      h -= sig;
       continue;
     }
     if (linear) {
-      const int hu = hval(P, dirs, ti, i - 1, j);
-      if (h == hu - ge) { rw.push(1u, 1); --i; h = hu; continue; }
-      rw.push(2u, 1);
+      if (hhas(i - 1, j, h + ge)) { rw.push(1u, 1); --i; h += ge; continue; }
+      rw.push(2u, 1);  // LEFT: H(i, j-1) = H(i, j) + g
       --j;
-      h = hval(P, dirs, ti, i, j);
+      h += ge;
       continue;
     }
     // UP iff E(i,j) = h, E(i,j) = max_k H(i-k,j) - Go - k Ge <= h; the gap is the largest
     // k with H(i-k,j) - Go - k Ge = h.  H(i',j') <= match * min(i',j') bounds the scan
-    // (no k with match * min(i-k, j) - Go - k Ge < h can reach h); loads go in batches.
+    // (no k with match * min(i-k, j) - Go - k Ge < h can reach h); loads go in batches and
+    // values are rebuilt cell by cell up the column.
     int kb = 0, hb = 0;
     {
       constexpr int SB = 8;
       const int mt = max(P.smax, 0);
+      int ref = h;  // exact value of (i - k0 + 1, j)
       for (int k0 = 1; k0 <= i; k0 += SB) {
         if (mt * min(i - k0, j) - go - k0 * ge < h) break;
         int hv[SB];
 #pragma unroll
         for (int l = 0; l < SB; ++l)
-          if (k0 + l <= i) hv[l] = hval(P, dirs, ti, i - k0 - l, j);
+          if (k0 + l <= i) {
+            const int i2 = i - k0 - l;
+            hv[l] = (i2 == 0) ? hbound(P, 0, j) : hraw(P, dirs, ti, i2, j, tb8);
+          }
 #pragma unroll
         for (int l = 0; l < SB; ++l)
-          if (k0 + l <= i && hv[l] - go - (k0 + l) * ge == h) { kb = k0 + l; hb = hv[l]; }
+          if (k0 + l <= i) {
+            const int i2 = i - k0 - l;
+            ref = (i2 == 0) ? hv[l] : hnear(hv[l], ref, tb8);
+            if (ref - go - (k0 + l) * ge == h) { kb = k0 + l; hb = ref; }
+          }
       }
     }
     if (kb) {
@@ -169,15 +213,23 @@ static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t
     {  // LEFT: F(i,j) = h, the largest such k along the row
       constexpr int SB = 8;
       const int mt = max(P.smax, 0);
+      int ref = h;
       for (int k0 = 1; k0 <= j; k0 += SB) {
         if (mt * min(i, j - k0) - go - k0 * ge < h) break;
         int hv[SB];
 #pragma unroll
         for (int l = 0; l < SB; ++l)
-          if (k0 + l <= j) hv[l] = hval(P, dirs, ti, i, j - k0 - l);
+          if (k0 + l <= j) {
+            const int j2 = j - k0 - l;
+            hv[l] = (j2 == 0) ? hbound(P, i, 0) : hraw(P, dirs, ti, i, j2, tb8);
+          }
 #pragma unroll
         for (int l = 0; l < SB; ++l)
-          if (k0 + l <= j && hv[l] - go - (k0 + l) * ge == h) { kb = k0 + l; hb = hv[l]; }
+          if (k0 + l <= j) {
+            const int j2 = j - k0 - l;
+            ref = (j2 == 0) ? hv[l] : hnear(hv[l], ref, tb8);
+            if (ref - go - (k0 + l) * ge == h) { kb = k0 + l; hb = ref; }
+          }
       }
     }
     if (!kb) break;  // unreachable for a consistent H store (no predecessor found)
@@ -185,6 +237,7 @@ static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t
     j -= kb;
     h = hb;
   }
+  (void)hget;
   rw.flush();
   *n_ops = rw.n;
   *beg_i = i;

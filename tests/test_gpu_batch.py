@@ -522,3 +522,25 @@ def test_pack2_all_lengths(ctx):
             _check_tb(ctx, sch, q, qo, s, so, res, ocig)
         finally:
             ctx.set_option("chunk_bytes", 64 << 20)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_tb8_low_byte_store(ctx, kind):
+    """Traceback H store in low bytes: identical alignments to the full
+    store and to the oracle, for s16x2 and s32 slots; a scheme whose neighbour differences
+    can reach 128 (open 60 / extend 10) keeps the full store and is still exact."""
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs
+    q, qo, s, so = random_pairs(400, 0, 360, seed=91)
+    for go, ge in ((5, 1), (60, 10)):
+        res, ocig = _oracle(kind, "affine", go, ge, q, qo, s, so, tb=True)
+        sch = A.Scheme(kind, "affine", 2, -1, go, ge)
+        for allow16 in (1, 0):
+            ctx.set_option("allow16", allow16)
+            try:
+                for tb8 in (1, 0):
+                    ctx.set_option("tb8", tb8)
+                    _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+            finally:
+                ctx.set_option("tb8", 1)
+                ctx.set_option("allow16", 1)
