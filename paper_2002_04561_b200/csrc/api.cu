@@ -106,6 +106,7 @@ struct Device {
 
 struct anyseq_ctx {
   std::vector<Device> devs;
+  std::vector<std::unique_ptr<LongWs>> lws;  // per device entry: long-pair buffers kept across calls
   std::string err;
   std::atomic<uint64_t> launches{0};
   int64_t tb_scratch_bytes = 16ll << 30;  // traceback H store per fill/walk chunk
@@ -1194,8 +1195,8 @@ anyseq_status run_traceback_long_hirschberg(anyseq_ctx* ctx, const anyseq_params
       const int nb = lastrow_bands((int)qe);
       CK(rows.ensure((se + 1) * sizeof(int32_t)));
       CK(best.ensure(3 * (size_t)nb * sizeof(int32_t)));
-      CK(sync.ensure((1 + (size_t)nb) * sizeof(int)));
-      CK(cudaMemsetAsync(sync.p, 0, (1 + (size_t)nb) * sizeof(int), st));
+      CK(sync.ensure((2 + (size_t)nb) * sizeof(int)));
+      CK(cudaMemsetAsync(sync.p, 0, (2 + (size_t)nb) * sizeof(int), st));
       LrTask t{dq, ds, (int32_t)qe, (int32_t)se, 1, 1, rows.as<int32_t>(), best.as<int32_t>()};
       CK(taskbuf.ensure(sizeof(LrTask) + sizeof(int)));
       struct {
@@ -1210,8 +1211,11 @@ anyseq_status run_traceback_long_hirschberg(anyseq_ctx* ctx, const anyseq_params
       std::vector<int32_t> hbb(3 * (size_t)nb);
       CK(cudaMemcpyAsync(hbb.data(), best.p, hbb.size() * sizeof(int32_t),
                          cudaMemcpyDeviceToHost, st));
+      int h_abort = 0;
+      CK(cudaMemcpyAsync(&h_abort, sync.as<int>() + 1 + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       CK(cudaGetLastError());
+      if (h_abort) return fail(ctx, ANYSEQ_E_TIMEOUT, "long traceback: a band wait exceeded its bound");
       int32_t hb[3] = {hbb[0], hbb[1], hbb[2]};  // key: score desc, j asc, i asc (R10)
       for (int b = 1; b < nb; ++b) {
         const int32_t* x = hbb.data() + 3 * b;
@@ -1284,8 +1288,8 @@ anyseq_status run_traceback_long_hirschberg(anyseq_ctx* ctx, const anyseq_params
     }
     CK(taskbuf.ensure(up.size()));
     CK(cudaMemcpyAsync(taskbuf.p, up.data(), up.size(), cudaMemcpyHostToDevice, st));
-    CK(sync.ensure((1 + (size_t)nb) * sizeof(int)));
-    CK(cudaMemsetAsync(sync.p, 0, (1 + (size_t)nb) * sizeof(int), st));
+    CK(sync.ensure((2 + (size_t)nb) * sizeof(int)));
+    CK(cudaMemsetAsync(sync.p, 0, (2 + (size_t)nb) * sizeof(int), st));
     CK(cudaEventRecord(ev0, st));
     launch_lastrow(taskbuf.as<LrTask>(), reinterpret_cast<const int*>(taskbuf.as<char>() + tb),
                    (int)tasks.size(), nb, sync.as<int>(), P, st);
@@ -1294,7 +1298,10 @@ anyseq_status run_traceback_long_hirschberg(anyseq_ctx* ctx, const anyseq_params
     CK(cudaGetLastError());
     hrows.resize(total);
     CK(cudaMemcpyAsync(hrows.data(), rows.p, total * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    int h_abort = 0;
+    CK(cudaMemcpyAsync(&h_abort, sync.as<int>() + 1 + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (h_abort) return fail(ctx, ANYSEQ_E_TIMEOUT, "long traceback: a band wait exceeded its bound");
     float lvl_ms = 0;
     CK(cudaEventElapsedTime(&lvl_ms, ev0, ev1));
     ctx->tb_pass_ms += lvl_ms;
@@ -1332,35 +1339,94 @@ anyseq_status run_traceback_long_hirschberg(anyseq_ctx* ctx, const anyseq_params
     leaf.swap(nl);
   }
 
-  // leaves: one batched global traceback over consecutive q / s ranges
+  // leaves: one batched global traceback over consecutive q / s ranges.  One-row and
+  // one-column leaves (a long indel crossing a cut) can be arbitrarily long and would size
+  // the batch's per-variant scratch by their length: they are solved here in closed form
+  // (global, linear gaps: the best single match plus gaps, or the all-gap path).
   const uint64_t L = nodes.size();
-  std::vector<uint64_t> qo(L + 1), so(L + 1);
+  auto code_of = [](char ch) -> int {
+    const int x = ch | 0x20;
+    return x == 'a' ? 0 : x == 'c' ? 1 : x == 'g' ? 2 : x == 't' ? 3 : 4;
+  };
+  auto sig_of = [&](int a, int b) -> int64_t {
+    return prm->has_subst ? prm->subst[5 * a + b] : ((a == b && a < 4) ? prm->match : prm->mismatch);
+  };
+  const int64_t g = prm->gap_extend;
+  std::vector<char> thin(L, 0);
+  std::vector<uint64_t> thick;
   for (uint64_t k = 0; k < L; ++k) {
-    qo[k] = nodes[k].i0;
-    so[k] = nodes[k].j0;
+    const HbNode& x = nodes[k];
+    if (x.i1 - x.i0 <= 1 || x.j1 - x.j0 <= 1) thin[k] = 1;
+    else thick.push_back(k);
   }
-  qo[L] = nodes[L - 1].i1;
-  so[L] = nodes[L - 1].j1;
-  anyseq_batch lb{q, qo.data(), s, so.data(), L};
-  anyseq_params gp = *prm;
-  gp.kind = ANYSEQ_GLOBAL;
-  std::vector<anyseq_alignment> la(L);
-  const uint64_t lcap = (uint64_t)(qe - qb) + (uint64_t)(se - sb) + L;
-  std::vector<uint32_t> lc(std::max<uint64_t>(lcap, 1));
-  std::vector<int32_t> lsc(L);
+  std::vector<anyseq_alignment> la(thick.size());
+  std::vector<uint32_t> lc;
   uint64_t lused = 0;
   const auto tl0 = std::chrono::steady_clock::now();
-  anyseq_status r = run_host_batch(ctx, &gp, &lb, 1, lsc.data(), la.data(), lc.data(), lcap, &lused);
+  if (!thick.empty()) {
+    // the thick leaves' ranges, copied back to back into one CSR batch (thin leaves between
+    // them leave gaps in q and s, so the original buffers cannot serve as the CSR)
+    std::vector<uint64_t> bq{0}, bs{0};
+    std::string cq, cs;
+    for (uint64_t k : thick) {
+      const HbNode& x = nodes[k];
+      cq.append(q + x.i0, (size_t)(x.i1 - x.i0));
+      cs.append(s + x.j0, (size_t)(x.j1 - x.j0));
+      bq.push_back(cq.size());
+      bs.push_back(cs.size());
+    }
+    const uint64_t B = thick.size();
+    anyseq_batch lb{cq.data(), bq.data(), cs.data(), bs.data(), B};
+    anyseq_params gp = *prm;
+    gp.kind = ANYSEQ_GLOBAL;
+    const uint64_t lcap = cq.size() + cs.size() + B;
+    lc.resize(std::max<uint64_t>(lcap, 1));
+    std::vector<int32_t> lsc(B);
+    anyseq_status r = run_host_batch(ctx, &gp, &lb, 1, lsc.data(), la.data(), lc.data(), lcap, &lused);
+    if (r != ANYSEQ_OK) return r;
+  }
   ctx->tb_leaf_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count();
-  if (r != ANYSEQ_OK) return r;
   int64_t score = 0;
   std::vector<uint32_t> ops;
+  size_t tk = 0;
   for (uint64_t k = 0; k < L; ++k) {
-    score += la[k].score;
-    for (uint32_t w = 0; w < la[k].cigar_len; ++w) {
-      const uint32_t word = lc[la[k].cigar_offset + w];
-      push_run(ops, word & 15, word >> 4);
+    const HbNode& x = nodes[k];
+    if (!thin[k]) {
+      const anyseq_alignment& a = la[tk++];
+      score += a.score;
+      for (uint32_t w = 0; w < a.cigar_len; ++w) {
+        const uint32_t word = lc[a.cigar_offset + w];
+        push_run(ops, word & 15, word >> 4);
+      }
+      continue;
+    }
+    const int64_t r = x.i1 - x.i0, c = x.j1 - x.j0;
+    if (r == 0 || c == 0) {  // one gap run
+      if (r) push_run(ops, 1u, (uint64_t)r);
+      if (c) push_run(ops, 2u, (uint64_t)c);
+      score -= (r + c) * g;
+      continue;
+    }
+    // r == 1 or c == 1: the best single match (first maximiser) or the all-gap path
+    const bool row = r == 1;
+    const int64_t len = row ? c : r;
+    int64_t bv = INT64_MIN, bk = 0;
+    for (int64_t k2 = 0; k2 < len; ++k2) {
+      const int64_t v = row ? sig_of(code_of(q[x.i0]), code_of(s[x.j0 + k2]))
+                            : sig_of(code_of(q[x.i0 + k2]), code_of(s[x.j0]));
+      if (v > bv) { bv = v; bk = k2; }
+    }
+    const uint32_t gapop = row ? 2u : 1u;  // the long side's gaps
+    if (bv - (len - 1) * g >= -(len + 1) * g) {
+      push_run(ops, gapop, (uint64_t)bk);
+      push_run(ops, 0u, 1);
+      push_run(ops, gapop, (uint64_t)(len - 1 - bk));
+      score += bv - (len - 1) * g;
+    } else {
+      push_run(ops, row ? 1u : 2u, 1);
+      push_run(ops, gapop, (uint64_t)len);
+      score -= (len + 1) * g;
     }
   }
   if (prm->kind != ANYSEQ_GLOBAL && score != want)
@@ -1407,7 +1473,7 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
   } else {
     Device& D = ctx->devs[0];
     CK(cudaSetDevice(D.id));
-    LongDevice ld{D.id, D.stream, D.num_sms};
+    LongDevice ld{D.id, D.stream, D.num_sms, ctx->lws[0].get()};
     std::vector<LongDevice> one{ld};
     LongCkpt ck;
     ck.want = 1;
@@ -1517,6 +1583,7 @@ static anyseq_status create_impl(anyseq_ctx** out, const int* device_ids, int nu
       return ANYSEQ_E_CUDA;
     }
   }
+  for (size_t d = 0; d < c->devs.size(); ++d) c->lws.emplace_back(new LongWs());
   cudaSetDevice(c->devs[0].id);
   *out = c;
   return ANYSEQ_OK;
@@ -1534,6 +1601,10 @@ void anyseq_destroy(anyseq_ctx* c) {
 
 static void destroy_impl(anyseq_ctx* c) {
   resolve_events(c);
+  for (size_t d = 0; d < c->lws.size(); ++d) {
+    cudaSetDevice(c->devs[d].id);
+    c->lws[d]->release();
+  }
   for (auto& e : c->pool) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -1716,11 +1787,13 @@ anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, co
     if (n >= (1ull << 31) || m >= (1ull << 31))
       return fail(ctx, ANYSEQ_E_UNSUPPORTED, "long sequences must be shorter than 2^31");
     std::vector<LongDevice> ld;
-    for (auto& D : ctx->devs) {
+    for (size_t d = 0; d < ctx->devs.size(); ++d) {
+      const Device& D = ctx->devs[d];
       LongDevice x;
       x.id = D.id;
       x.stream = D.stream;
       x.num_sms = D.num_sms;
+      x.ws = ctx->lws[d].get();
       ld.push_back(x);
     }
     std::string err;

@@ -53,7 +53,7 @@ template <int MODE>
 __global__ void __launch_bounds__(NT) lastrow_kernel(const LrTask* __restrict__ tasks,
                                                      const int* __restrict__ band_start,
                                                      int num_tasks, int* ticket, int* prog,
-                                                     LrParams P) {
+                                                     int num_bands_total, LrParams P) {
   __shared__ int32_t xch[2][NT];
   __shared__ int32_t ssig[25];
   __shared__ int32_t rs[NT], ri[NT], rj[NT];
@@ -98,9 +98,17 @@ __global__ void __launch_bounds__(NT) lastrow_kernel(const LrTask* __restrict__ 
         if (band == 0) {
           up = -j * g;
         } else {
+          long long spins = 0;  // bounded like every device-side wait (-> ANYSEQ_E_TIMEOUT)
           while (ready < j) {
             ready = ld_acquire(wait_on);
-            if (ready < j) __nanosleep(64);
+            if (ready < j) {
+              __nanosleep(64);
+              if ((++spins & 1023) == 0 &&
+                  (spins > (1ll << 26) || *(volatile int*)(prog - 1 + num_bands_total + 1))) {
+                atomicExch((int*)(prog - 1 + num_bands_total + 1), 1);
+                ready = j;  // abandon the band: the host discards the pass
+              }
+            }
           }
           up = __ldcg(T.row + j);
         }
@@ -185,19 +193,19 @@ void launch_lastrow(const LrTask* d_tasks, const int* d_band_start, int num_task
                     int num_bands, int* d_sync, const LrParams& P, cudaStream_t st) {
   if (num_tasks <= 0) return;
   lastrow_kernel<0><<<num_bands, NT, 0, st>>>(d_tasks, d_band_start, num_tasks, d_sync,
-                                              d_sync + 1, P);
+                                              d_sync + 1, num_bands, P);
 }
 
 void launch_lastrow_anchored(const LrTask* d_tasks, const int* d_band_start, int num_tasks,
                              int num_bands, int* d_sync, const LrParams& P, cudaStream_t st) {
   if (num_tasks <= 0) return;
   lastrow_kernel<1><<<num_bands, NT, 0, st>>>(d_tasks, d_band_start, num_tasks, d_sync,
-                                              d_sync + 1, P);
+                                              d_sync + 1, num_bands, P);
 }
 
 void launch_lastrow_edges(const LrTask* d_tasks, const int* d_band_start, int num_tasks,
                           int num_bands, int* d_sync, const LrParams& P, cudaStream_t st) {
   if (num_tasks <= 0) return;
   lastrow_kernel<2><<<num_bands, NT, 0, st>>>(d_tasks, d_band_start, num_tasks, d_sync,
-                                              d_sync + 1, P);
+                                              d_sync + 1, num_bands, P);
 }

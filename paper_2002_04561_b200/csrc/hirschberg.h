@@ -32,8 +32,8 @@ void launch_encode_codes(const char* ascii, uint8_t* codes, uint64_t len, int* b
                          cudaStream_t st);
 // Row bands of one task (3072 rows each); band b of a task waits for band b-1's published
 // columns.  d_band_start[num_tasks] = first band of each task (exclusive prefix sum of
-// lastrow_bands), num_bands the total; d_sync = 1 + num_bands zeroed ints (ticket counter,
-// then per-band progress).  MODE 1 (anchored) writes best[3*band .. 3*band+2] per band.
+// lastrow_bands), num_bands the total; d_sync = 2 + num_bands zeroed ints (ticket counter,
+// per-band progress, then an abort flag set when a band-to-band wait exceeds its bound).  MODE 1 (anchored) writes best[3*band .. 3*band+2] per band.
 int lastrow_bands(int n1);
 void launch_lastrow(const LrTask* d_tasks, const int* d_band_start, int num_tasks,
                     int num_bands, int* d_sync, const LrParams& P, cudaStream_t st);

@@ -414,8 +414,21 @@ static LongFn long_fn(int kind, int gap) {
 namespace {
 struct Buf {
   void* p = nullptr;
-  ~Buf() { if (p) cudaFree(p); }
+  bool own = true;
+  ~Buf() { if (p && own) cudaFree(p); }
 };
+// a buffer from the device's persistent workspace slot, or a call-local allocation
+cudaError_t get_buf(Buf& b, LongWs* ws, int slot, size_t bytes) {
+  if (ws) {
+    b.own = false;
+    return ws->get(slot, bytes, &b.p);
+  }
+  b.own = true;
+  return cudaMalloc(&b.p, bytes < 256 ? 256 : bytes);
+}
+enum { WS_QA, WS_SA, WS_QC, WS_SC, WS_SUM, WS_FLG, WS_OFF, WS_ROWBUF, WS_PROG, WS_TICKET,
+       WS_ABORT, WS_CB, WS_BPTR, WS_FPTR, WS_BCOL, WS_FLAGS, WS_PARTS, WS_PROF, WS_KEY,
+       WS_ROWCK, WS_COLCK };
 #define LK(call)                                                      \
   do {                                                                \
     cudaError_t e_ = (call);                                          \
@@ -427,8 +440,9 @@ struct Buf {
 }  // namespace
 
 void LongCkpt::release() {
-  for (void* p : {(void*)qc, (void*)sc, (void*)rowck, (void*)colck})
-    if (p) cudaFree(p);
+  if (owns)
+    for (void* p : {(void*)qc, (void*)sc, (void*)rowck, (void*)colck})
+      if (p) cudaFree(p);
   qc = sc = nullptr;
   rowck = colck = nullptr;
   bytes = 0;
@@ -490,8 +504,20 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   auto fits16 = [&](int nr) {
     return 2 * (int64_t)(64 * nr + 66) * d16 + margin16 + 96 * d16 + P.go + P.ge + 256 < -NEG16C;
   };
-  int NR16 = opt.band_rows == 512 ? 8 : 16;  // 1024-row tasks by default, 512 if the range
+  // 1024-row tasks by default, 512 if the range guard needs it -- or across >= 4 devices:
+  // a device keeps (resident warps x rows per task) rows in flight, and the last of G
+  // devices trails the first by G - 1 such pipelines (tools/scaling_model.py)
+  int NR16 = (opt.band_rows == 512 || (opt.band_rows == 0 && NE >= 4)) ? 8 : 16;  // (range
   if (NR16 > 8 && !fits16(NR16)) NR16 = 8;    // guard needs it
+  if (NR16 > 8 && opt.band_rows == 0) {
+    // short pairs: fewer 1024-row strips than ~1.5x the resident warps leave warps idle
+    // through the first pass of every column strip -- 512-row strips double the strips
+    int nb = 0;
+    cudaSetDevice(devs[0].id);
+    LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, long16_fn(16, P.kind, ck && ck->want), 128, 0));
+    const double warps = 4.0 * devs[0].num_sms * std::max(nb, 1);
+    if ((double)((n + 1023) / 1024) < 1.5 * warps) NR16 = 8;
+  }
   const int64_t bspan16 = (int64_t)(64 * NR16 + 66) * d16;
   // every kind and gap model (linear = affine with G_o = 0, exact for scores); the subject's
   // selector has four codes, so a subject with N takes the 32-bit kernel
@@ -577,8 +603,20 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     ck->S = S;
     const int64_t rows = (int64_t)(S - 1) / every, cols = (int64_t)(m - 1) >> kcs;
     ck->bytes = (size_t)bytes_of(every, kcs);
-    if (rows > 0) LK(cudaMalloc(&ck->rowck, (size_t)rows * (m + 1) * sizeof(int2)));
-    if (cols > 0) LK(cudaMalloc(&ck->colck, (size_t)cols * (n + 1) * sizeof(int2)));
+    LongWs* ws = devs[0].ws;
+    ck->owns = ws == nullptr;
+    if (rows > 0) {
+      void* p = nullptr;
+      LK(ws ? ws->get(WS_ROWCK, (size_t)rows * (m + 1) * sizeof(int2), &p)
+            : cudaMalloc(&p, (size_t)rows * (m + 1) * sizeof(int2)));
+      ck->rowck = (int2*)p;
+    }
+    if (cols > 0) {
+      void* p = nullptr;
+      LK(ws ? ws->get(WS_COLCK, (size_t)cols * (n + 1) * sizeof(int2), &p)
+            : cudaMalloc(&p, (size_t)cols * (n + 1) * sizeof(int2)));
+      ck->colck = (int2*)p;
+    }
   }
   std::vector<int32_t*> flag_ptr(Gtot + 1, nullptr);
   // column strips per device group (one strip per entry; a single entry: all Gtot strips)
@@ -608,12 +646,12 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     PerDev& D = pd[d];
     LK(cudaSetDevice(gdev[d].id));
     cudaStream_t st = gdev[d].stream;
-    LK(cudaMalloc(&D.qa.p, n + 16));
-    LK(cudaMalloc(&D.sa.p, m + 16));
-    LK(cudaMalloc(&D.qc.p, n + 16));
-    LK(cudaMalloc(&D.sc.p, m + 16));
-    LK(cudaMalloc(&D.sum.p, sizeof(PlanSummary)));
-    LK(cudaMalloc(&D.flg.p, 16));
+    LK(get_buf(D.qa, gdev[d].ws, WS_QA, n + 16));
+    LK(get_buf(D.sa, gdev[d].ws, WS_SA, m + 16));
+    LK(get_buf(D.qc, gdev[d].ws, WS_QC, n + 16));
+    LK(get_buf(D.sc, gdev[d].ws, WS_SC, m + 16));
+    LK(get_buf(D.sum, gdev[d].ws, WS_SUM, sizeof(PlanSummary)));
+    LK(get_buf(D.flg, gdev[d].ws, WS_FLG, 16));
     LK(cudaMemcpyAsync(D.qa.p, q, n, cudaMemcpyHostToDevice, st));
     LK(cudaMemcpyAsync(D.sa.p, s, m, cudaMemcpyHostToDevice, st));
     PlanSummary hs;
@@ -623,7 +661,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     LK(cudaStreamSynchronize(st));
     uint64_t offs[4] = {0, n, 0, m};
     Buf off;
-    LK(cudaMalloc(&off.p, 32));
+    LK(get_buf(off, gdev[d].ws, WS_OFF, 32));
     LK(cudaMemcpy(off.p, offs, 32, cudaMemcpyHostToDevice));
     LK(launch_pack((const char*)D.qa.p, n, (uint8_t*)D.qc.p, (const uint64_t*)off.p,
                    (const char*)D.sa.p, m, (uint8_t*)D.sc.p, (const uint64_t*)off.p + 2, 1,
@@ -637,13 +675,13 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
              std::to_string(in_s ? hs.err_pos - (1ull << 62) : hs.err_pos);
       return ANYSEQ_E_BADSEQ;
     }
-    LK(cudaMalloc(&D.rowbuf.p, (m + 1) * sizeof(int4)));
-    LK(cudaMalloc(&D.prog.p, (size_t)Gtot * S * 4));
-    LK(cudaMalloc(&D.ticket.p, 4));
-    LK(cudaMalloc(&D.abort_.p, 4));
-    LK(cudaMalloc(&D.cbuf.p, (Gtot + 1) * 4));
-    LK(cudaMalloc(&D.bptr.p, (Gtot + 1) * sizeof(int2*)));
-    LK(cudaMalloc(&D.fptr.p, (Gtot + 1) * sizeof(int32_t*)));
+    LK(get_buf(D.rowbuf, gdev[d].ws, WS_ROWBUF, (m + 1) * sizeof(int4)));
+    LK(get_buf(D.prog, gdev[d].ws, WS_PROG, (size_t)Gtot * S * 4));
+    LK(get_buf(D.ticket, gdev[d].ws, WS_TICKET, 4));
+    LK(get_buf(D.abort_, gdev[d].ws, WS_ABORT, 4));
+    LK(get_buf(D.cbuf, gdev[d].ws, WS_CB, (Gtot + 1) * 4));
+    LK(get_buf(D.bptr, gdev[d].ws, WS_BPTR, (Gtot + 1) * sizeof(int2*)));
+    LK(get_buf(D.fptr, gdev[d].ws, WS_FPTR, (Gtot + 1) * sizeof(int32_t*)));
     LK(cudaMemsetAsync(D.prog.p, 0, (size_t)Gtot * S * 4, st));
     LK(cudaMemsetAsync(D.ticket.p, 0, 4, st));
     LK(cudaMemsetAsync(D.abort_.p, 0, 4, st));
@@ -654,10 +692,10 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
       // written by the last strip's right edge) for the optimum's column candidates
       const int extra = (narrow && P.kind == KSEMI && D.g_first + D.g_count == Gtot) ? 1 : 0;
       const size_t bytes = (size_t)(D.g_count + extra) * (n + 1) * sizeof(int2);
-      LK(cudaMalloc(&D.bcol_own.p, bytes));
+      LK(get_buf(D.bcol_own, gdev[d].ws, WS_BCOL, bytes));
       for (int k = 0; k < D.g_count + extra; ++k)
         bcol_ptr[D.g_first + k] = (int2*)D.bcol_own.p + (size_t)k * (n + 1);
-      LK(cudaMalloc(&D.flags.p, (size_t)D.g_count * S * 4));
+      LK(get_buf(D.flags, gdev[d].ws, WS_FLAGS, (size_t)D.g_count * S * 4));
       LK(cudaMemsetAsync(D.flags.p, 0, (size_t)D.g_count * S * 4, st));
       for (int k = 0; k < D.g_count; ++k) flag_ptr[D.g_first + k] = (int32_t*)D.flags.p + (size_t)k * S;
     }
@@ -665,7 +703,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0));
     D.grid = gdev[d].num_sms * std::max(nb, 1);
     if (opt.blocks > 0) D.grid = std::min(D.grid, opt.blocks);
-    LK(cudaMalloc(&D.parts.p, (size_t)D.grid * 4 * sizeof(LongPart)));
+    LK(get_buf(D.parts, gdev[d].ws, WS_PARTS, (size_t)D.grid * 4 * sizeof(LongPart)));
   }
   // In multi-GPU mode edge g (g >= 1) is produced on device g-1 and consumed on device g;
   // flags of edge g live on the consumer as well (producer stores over NVLink).
@@ -726,7 +764,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     if (narrow) a.lag = opt.start_lag;  // 16-bit kernel: start slack off unless asked for
     a.prof = nullptr;
     if (opt.profile) {
-      LK(cudaMalloc(&D.profbuf.p, 64));
+      LK(get_buf(D.profbuf, gdev[d].ws, WS_PROF, 64));
       LK(cudaMemset(D.profbuf.p, 0, 64));
       a.prof = (unsigned long long*)D.profbuf.p;
     }
@@ -779,7 +817,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
     if (ck && ck->want) {
       ck->qc = (uint8_t*)pd[0].qc.p;
       ck->sc = (uint8_t*)pd[0].sc.p;
-      pd[0].qc.p = pd[0].sc.p = nullptr;
+      if (pd[0].qc.own) pd[0].qc.p = pd[0].sc.p = nullptr;  // ownership moves to ck
     }
   };
   if (aborted) {
@@ -795,7 +833,7 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
       if (D.g_count == 0) continue;
       LK(cudaSetDevice(gdev[d].id));
       Buf kb;
-      LK(cudaMalloc(&kb.p, 8));
+      LK(get_buf(kb, gdev[d].ws, WS_KEY, 8));
       LK(cudaMemsetAsync(kb.p, 0, 8, gdev[d].stream));
       const int j0 = std::max(1, cb[D.g_first]), j1 = std::min<int>((int)m, cb[D.g_first + D.g_count]);
       const bool lastg = D.g_first + D.g_count == Gtot;

@@ -20,10 +20,40 @@ struct LongOptions {
   int narrow = 1;          // 1: 16-bit differential kernel where eligible (local affine)
 };
 
+// Device buffers of the long-pair path kept across calls (a context owns one per device):
+// slot k grows on demand, so repeated calls skip cudaMalloc / cudaFree of the row buffer,
+// the boundary columns and the traceback checkpoints (tens of GB for 1 Mbp pairs).
+struct LongWs {
+  static constexpr int kSlots = 24;
+  void* p[kSlots] = {};
+  size_t cap[kSlots] = {};
+  cudaError_t get(int slot, size_t bytes, void** out) {
+    if (cap[slot] < bytes) {
+      if (p[slot]) cudaFree(p[slot]);
+      p[slot] = nullptr;
+      cap[slot] = 0;
+      cudaError_t e = cudaMalloc(&p[slot], bytes < 256 ? 256 : bytes);
+      if (e != cudaSuccess) return e;
+      cap[slot] = bytes < 256 ? 256 : bytes;
+    }
+    *out = p[slot];
+    return cudaSuccess;
+  }
+  void release() {
+    for (int k = 0; k < kSlots; ++k) {
+      if (p[k]) cudaFree(p[k]);
+      p[k] = nullptr;
+      cap[k] = 0;
+    }
+  }
+  ~LongWs() { release(); }
+};
+
 struct LongDevice {
   int id;
   cudaStream_t stream;
   int num_sms;
+  LongWs* ws = nullptr;  // persistent buffers (nullptr: allocate per call)
 };
 
 struct LongResult {
@@ -48,6 +78,7 @@ struct LongCkpt {
   int2* colck = nullptr;
   int HS = 0, ck_every = 1, kc_shift = 10, PT = 0, S = 0;
   size_t bytes = 0;           // checkpoint bytes allocated
+  bool owns = true;           // false: the buffers live in a LongWs
   void release();
   ~LongCkpt() { release(); }
 };

@@ -56,9 +56,13 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
   constexpr int RING = 256;
   constexpr int PER = 32;
   __shared__ int2 ring_he[4][RING];
-  __shared__ uint16_t ring_sel[4][RING];  // subject code c of a column as c * 0x11
+  // full PRMT selector of a column c for the two halves: codes of c (low half) and c - 1
+  // (high half, one column behind), sign-replicating (VS16::selector)
+  __shared__ uint32_t ring_sel[4][RING];
+  // OFF-phase steps: lane 0's input (H, E of the row above) already in the warp's relative
+  // frame, packed (h | e << 16), converted once per refill period right after re-basing
+  __shared__ uint32_t ring_rel[4][RING];
   __shared__ int2 ring_out[4][64];        // the task's last row (H, E) awaiting publication
-  __shared__ int4 ring_pf[4][64];         // row hand-off entries prefetched a period early
   __shared__ int ring_eck[CKPT ? 4 : 1][64];  // CKPT: E of that row itself (not of the next)
   const int t = threadIdx.x & 31;
   const int wb = threadIdx.x >> 5;
@@ -74,8 +78,9 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
   // subject codes of columns past a task's end are read (and ignored) by the warp's last
   // steps: keep every ring entry a valid code so the active half's selector stays intact
   for (int x = t; x < RING; x += 32) {
-    ring_sel[wb][x] = 0;
+    ring_sel[wb][x] = 0xC480u;
     ring_he[wb][x] = make_int2(0, 0);
+    ring_rel[wb][x] = 0;
   }
   __syncwarp();
 
@@ -112,11 +117,26 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
       H[r] = VS16::splat(NEGc);
       Ff[r] = VS16::splat(NEGc);
     }
+    int last_code = 0;  // subject code of the column before the next refill's first
     auto refill = [&](int c0, int c1) -> bool {
+      if (c0 >= c1) return true;  // (the task's second initial refill when W <= 32)
       const int c = c0 + t;
       const bool mine = c < c1;
-      if (mine) ring_sel[wb][c & (RING - 1)] = (uint16_t)(a.sc[c_lo + c] * 0x11u);
-      if (s == 0) return true;
+      const int code = mine ? a.sc[c_lo + c] : 0;
+      int pcode = __shfl_up_sync(0xffffffffu, code, 1);
+      if (t == 0) pcode = last_code;
+      last_code = __shfl_sync(0xffffffffu, code, (c1 - 1 - c0) & 31);  // code of column c1 - 1
+      if (mine) ring_sel[wb][c & (RING - 1)] = (uint32_t)code * 0x11u + (uint32_t)pcode * 0x1100u + 0xC480u;
+      // the high half relaxes column W - 1 one step after the low half left the task: its
+      // selector (entry W) carries code(W - 1) in the high nibbles
+      if (c1 == W && t == 0) ring_sel[wb][W & (RING - 1)] = (uint32_t)last_code * 0x1100u + 0xC480u;
+      if (s == 0) {  // first strip: lane 0's input is row 0
+        if (mine) {
+          const int h0 = KIND == KGLOBAL ? -(P.go + (c_lo + c + 1) * P.ge) : 0;
+          ring_he[wb][c & (RING - 1)] = make_int2(h0, h0 - cop);
+        }
+        return true;
+      }
       const int4* src = a.rowbuf + c_lo + c + 1;
       int4 v = mine ? ld_row(src) : make_int4(0, s, 0, s);
       long long spins = 0;
@@ -131,41 +151,6 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
         }
         if (a.prof && t == 0)  // [0]: mid-task refills, [3]: the task's first two refills
           atomicAdd(&a.prof[c0 < 2 * PER ? 3 : 0], (unsigned long long)(clock64() - t0));
-      }
-      if (mine) ring_he[wb][c & (RING - 1)] = make_int2(v.x, v.z);
-      return true;
-    };
-    // Software-pipelined refill: one period (32 steps) before the ring needs them, the row
-    // hand-off entries of the next 32 columns are copied global -> shared with cp.async (and
-    // their subject codes loaded into a register), so the L2 latency of the hand-off hides
-    // behind the period's relaxation; at the refill point the tags are checked in shared
-    // memory and only entries not yet published by the strip above are polled.
-    int pf_code = 0;
-    auto prefetch = [&](int c0) {
-      const int c = c0 + t;
-      if (s > 0 && c < W) cp_async16(&ring_pf[wb][c & 63], a.rowbuf + c_lo + c + 1);
-      cp_async_commit();
-      pf_code = c < W ? a.sc[c_lo + c] : 0;
-    };
-    auto consume = [&](int c0, int c1) -> bool {
-      const int c = c0 + t;
-      const bool mine = c < c1;
-      if (mine) ring_sel[wb][c & (RING - 1)] = (uint16_t)(pf_code * 0x11u);
-      if (s == 0) return true;
-      cp_async_wait_all();
-      const int4* src = a.rowbuf + c_lo + c + 1;
-      int4 v = mine ? ring_pf[wb][c & 63] : make_int4(0, s, 0, s);
-      long long spins = 0;
-      while (!__all_sync(0xffffffffu, v.y == s && v.w == s)) {
-        const long long t0 = (a.prof && t == 0) ? clock64() : 0;
-        if (v.y != s || v.w != s) v = ld_row(src);
-        if (!__all_sync(0xffffffffu, v.y == s && v.w == s)) __nanosleep(a.sleep_ns);
-        if ((++spins & 255) == 0 &&
-            __any_sync(0xffffffffu, spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
-          if (t == 0) atomicExch(a.abort_flag, 1);
-          return false;
-        }
-        if (a.prof && t == 0) atomicAdd(&a.prof[0], (unsigned long long)(clock64() - t0));
       }
       if (mine) ring_he[wb][c & (RING - 1)] = make_int2(v.x, v.z);
       return true;
@@ -192,7 +177,6 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
       if (!__shfl_sync(0xffffffffu, ok, 0)) break;
     }
     if (!refill(0, min(W, PER)) || !refill(PER, min(W, 2 * PER))) break;
-    prefetch(2 * PER);
     __syncwarp();
 
     // frame: every value of the task lies within a.bspan of H(ip0, c_lo + 1) (the row
@@ -212,28 +196,40 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
     frame_consts();
     uint32_t diag = VS16::splat(NEGc), Hbot = VS16::splat(NEGc), Ebot = VS16::splat(NEGc);
 
-    auto sweep = [&](auto first_c) -> bool {
-      constexpr bool FIRST = decltype(first_c)::value;
-      uint32_t cur_nx = ring_sel[wb][(0 - 2 * t) & (RING - 1)];
-      uint32_t prev = 0;
+    auto sweep = [&]() -> bool {
+      uint32_t sel_nx = ring_sel[wb][(0 - 2 * t) & (RING - 1)];
       int2 he_nx = ring_he[wb][0];
+      uint32_t rel_nx = 0;
       auto step = [&](auto chk, const int k) {
         uint32_t (&Hi)[NR] = H;
         uint32_t (&Hq)[NR] = H;
         constexpr bool CHK = decltype(chk)::value;
-        const uint32_t hs = __shfl_up_sync(0xffffffffu, Hbot, 1);
-        const uint32_t es = __shfl_up_sync(0xffffffffu, Ebot, 1);
-        // low half <- lane t-1's high half (row above, same column); high half <- own low
-        // half of the previous step (row above, one column behind)
-        uint32_t hin = __byte_perm(hs, Hbot, 0x5432);
-        uint32_t ein = __byte_perm(es, Ebot, 0x5432);
         const int lc = k - 2 * t;  // low half's column (task-relative); high half: lc - 1
-        const uint32_t cur = cur_nx;
-        cur_nx = ring_sel[wb][(lc + 1) & (RING - 1)];
-        const uint32_t sel = cur | (prev << 8) | 0xC480u;  // VS16::selector(c(lc), c(lc-1))
-        prev = cur;
-        const int2 he = he_nx;
-        if (!FIRST) he_nx = ring_he[wb][(k + 1) & (RING - 1)];  // lane 0's next column
+        const uint32_t sel = sel_nx;
+        sel_nx = ring_sel[wb][(lc + 1) & (RING - 1)];
+        uint32_t hin, ein;
+        int2 he = make_int2(0, 0);
+        if (CHK) {
+          const uint32_t hs = __shfl_up_sync(0xffffffffu, Hbot, 1);
+          const uint32_t es = __shfl_up_sync(0xffffffffu, Ebot, 1);
+          // low half <- lane t-1's high half (row above, same column); high half <- own
+          // low half of the previous step (row above, one column behind)
+          hin = __byte_perm(hs, Hbot, 0x5432);
+          ein = __byte_perm(es, Ebot, 0x5432);
+          he = he_nx;
+          he_nx = ring_he[wb][(k + 1) & (RING - 1)];  // lane 0's next column
+        } else {
+          // lane 31's high half is nobody's input: it carries lane 0's input (pre-converted
+          // ring entry) through the same rotating shuffle, so lane 0 needs no select
+          const uint32_t rel = rel_nx;
+          rel_nx = ring_rel[wb][(k + 1) & (RING - 1)];
+          const uint32_t vh = prmt(Hbot, rel, t == 31 ? 0x5410u : 0x3210u);
+          const uint32_t ve = prmt(Ebot, rel, t == 31 ? 0x7610u : 0x3210u);
+          const uint32_t hs = __shfl_sync(0xffffffffu, vh, (t + 31) & 31);
+          const uint32_t es = __shfl_sync(0xffffffffu, ve, (t + 31) & 31);
+          hin = __byte_perm(hs, Hbot, 0x5432);
+          ein = __byte_perm(es, Ebot, 0x5432);
+        }
         const bool act0 = !CHK || (lc >= 0 && lc < W);
         const bool act1 = !CHK || (lc >= 1 && lc <= W);
         if (CHK && (lc == 0 || lc == 1)) {  // half h reaches the left boundary column
@@ -250,13 +246,9 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
           const int id = ip0 + h * NR;  // the row above the half's first row
           diag = h16_set(diag, h, cv(id <= n ? bl[KIND == KSEMI ? max(id, 0) : id].x : 0));
         }
-        {  // lane 0's low half: the row above the task, H(ip0, j) and E(ip0 + 1, j) (no branch)
-          // (first strip: row 0 -- 0 for LOCAL / SEMI, -(G_o + j G_e) for GLOBAL)
-          const int h0 = KIND == KGLOBAL ? -(P.go + (c_lo + lc + 1) * P.ge) : 0;
-          const int hx = FIRST ? h0 : he.x;
-          const int ex = FIRST ? h0 - cop : he.y;
-          const uint32_t hl = prmt((uint32_t)cv(hx), hin, 0x7610u);
-          const uint32_t el = prmt((uint32_t)cv(ex), ein, 0x7610u);
+        if (CHK) {  // lane 0's low half: the row above the task, H(ip0, j), E(ip0 + 1, j)
+          const uint32_t hl = prmt((uint32_t)cv(he.x), hin, 0x7610u);
+          const uint32_t el = prmt((uint32_t)cv(he.y), ein, 0x7610u);
           hin = t == 0 ? hl : hin;
           ein = t == 0 ? el : ein;
         }
@@ -375,6 +367,13 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
         base += dl;
         frame_consts();
       };
+      // lane 0's inputs of columns [c0, c0 + 32) in the current frame, packed (h | e << 16)
+      auto convert = [&](int c0) {
+        const int2 v = ring_he[wb][(c0 + t) & (RING - 1)];
+        ring_rel[wb][(c0 + t) & (RING - 1)] = h16_pack(cv(v.x), cv(v.y));
+        __syncwarp();
+        rel_nx = ring_rel[wb][c0 & (RING - 1)];
+      };
 
       // publish staged columns [flushed, c_end) (at most 32) to the row buffer for strip s+1
       int flushed = 0;
@@ -400,8 +399,7 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
       int k = 0;
       auto maybe_refill = [&](int kk) -> bool {
         if ((kk % PER) == 0 && kk > 0 && kk + PER < W) {
-          if (!consume(kk + PER, min(W, kk + 2 * PER))) return false;
-          prefetch(kk + 2 * PER);
+          if (!refill(kk + PER, min(W, kk + 2 * PER))) return false;
           __syncwarp();
         }
         return true;
@@ -415,11 +413,13 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
         if (!maybe_refill(k)) return false;
         if ((k % PER) == 0) {
           reframe();
+          convert(k);
           flush(min(W, k - 63));  // columns <= k - 64 are complete
         }
         step(OFF, k);
         step(OFF, k + 1);
       }
+      he_nx = ring_he[wb][k & (RING - 1)];  // the CHK path's lane-0 input again
       for (; k + 1 < K; k += 2) {
         if (!maybe_refill(k)) return false;
         if ((k % PER) == 0 && k >= 64) flush(min(W, k - 63));
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
       while (flushed < W) flush(min(W, flushed + 32));
       return true;
     };
-    const bool done = (s == 0) ? sweep(std::true_type{}) : sweep(std::false_type{});
+    const bool done = sweep();
     if (!done) break;
     if (KIND == KLOCAL) {
       if (lkey_better(bv0, bi0, bj0, part.lv, part.li, part.lj)) { part.lv = bv0; part.li = bi0; part.lj = bj0; }

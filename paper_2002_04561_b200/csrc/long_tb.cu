@@ -61,9 +61,15 @@ __device__ __forceinline__ int h_col0(const WalkArgs& a, int i) {  // H(i, 0)
   return a.kind == KGLOBAL ? (i ? -(a.go + i * a.ge) : 0) : 0;
 }
 
+constexpr int KC_MAX = 4096;  // widest column block
+
 template <int TR>
 __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
   __shared__ int xh[2][NT], xe[2][NT];
+  // the region's top boundary row (H, E) and subject codes, staged once per tile: the
+  // recompute's per-step inputs then come from shared memory, not from L2 round trips
+  extern __shared__ int2 top[];  // [KC_MAX]
+  __shared__ uint8_t scode_s[KC_MAX];
   __shared__ int ssig[25];
   __shared__ int sh_i, sh_j, sh_st, sh_done;
   __shared__ unsigned long long sh_nops;
@@ -149,25 +155,27 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
     }
     const int nthreads = (nr + TR - 1) / TR;
     const int steps = nc + nthreads - 1;
+    for (int c = t; c < nc; c += NT) {
+      const int jj = C + 1 + c;
+      top[c] = R == 0 ? make_int2(h_row0(a, jj), NEGI) : a.rowck[(size_t)(b - 1) * (a.m + 1) + jj];
+      scode_s[c] = a.sc[jj - 1];
+    }
+    __syncthreads();
     for (int k = 0; k < steps; ++k) {
       const int c = k - t;  // column index in the region (jj = C + 1 + c)
       if (tact && c >= 0 && c < nc) {
         const int jj = C + 1 + c;
         int hup, eup;  // H(row0, jj), E(row0, jj)
         if (t == 0) {
-          if (R == 0) {
-            hup = h_row0(a, jj);
-            eup = NEGI;
-          } else {
-            const int2 v = a.rowck[(size_t)(b - 1) * (a.m + 1) + jj];
-            hup = v.x;
-            eup = v.y;
-          }
+          const int2 v = top[c];
+          hup = v.x;
+          eup = v.y;
         } else {
           hup = xh[(k - 1) & 1][t - 1];
           eup = xe[(k - 1) & 1][t - 1];
         }
-        const int scode = a.sc[jj - 1];
+        (void)jj;
+        const int scode = scode_s[c];
         int dg = hprev;
         hprev = hup;
         uint32_t word = 0;
@@ -353,11 +361,24 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
   TK(cudaEventCreate(&e0));
   TK(cudaEventCreate(&e1));
   TK(cudaEventRecord(e0, st));
+  const size_t smem = (size_t)KC_MAX * sizeof(int2);
   switch (TR) {
-    case 2: tile_walk_kernel<2><<<1, NT, 0, st>>>(a); break;
-    case 4: tile_walk_kernel<4><<<1, NT, 0, st>>>(a); break;
-    case 8: tile_walk_kernel<8><<<1, NT, 0, st>>>(a); break;
-    default: tile_walk_kernel<16><<<1, NT, 0, st>>>(a); break;
+    case 2:
+      TK(cudaFuncSetAttribute(tile_walk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      tile_walk_kernel<2><<<1, NT, smem, st>>>(a);
+      break;
+    case 4:
+      TK(cudaFuncSetAttribute(tile_walk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      tile_walk_kernel<4><<<1, NT, smem, st>>>(a);
+      break;
+    case 8:
+      TK(cudaFuncSetAttribute(tile_walk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      tile_walk_kernel<8><<<1, NT, smem, st>>>(a);
+      break;
+    default:
+      TK(cudaFuncSetAttribute(tile_walk_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      tile_walk_kernel<16><<<1, NT, smem, st>>>(a);
+      break;
   }
   TK(cudaGetLastError());
   TK(cudaEventRecord(e1, st));

@@ -9,3 +9,4 @@ NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3"
 $NV -o bin/mixbench mixbench.cu
 $NV -o bin/pipebench pipebench.cu
 g++ -O3 -march=native -pthread -o bin/hostpack_bench hostpack_bench.cpp
+$NV -o bin/dpx_latency dpx_latency.cu
