@@ -197,8 +197,15 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
      "long_band_rows"    long pairs, rows per warp task: 32-bit kernel 512 (default) or
                          384; 16-bit kernel 1024 (default), 768 or 512
      "long_sleep_ns"     long pairs (16-bit kernel): back-off of the row hand-off poll
-     "tb_leaf_cells"     long traceback: Hirschberg recursion stops at <= this many cells
-                         per sub-problem (default 2^20)
+     "tb_leaf_cells"     long traceback, Hirschberg fallback: recursion stops at <= this
+                         many cells per sub-problem (default 2^20)
+     "tb_ckpt_bytes"     long traceback: device memory budget of the checkpoints (default
+                         0 = 40 % of free memory); "tb_kc_shift" (8..12) / "tb_ck_every"
+                         (1..8) force the column / row checkpoint spacing (tests)
+     "tb8"               batch traceback: 1 (default) stores the low byte of H per cell when
+                         the scheme allows it exactly (R23); 0 = full H
+     "batch_long_cells"  a batch pair with n*m >= this (and n, m >= 2048) is aligned by the
+                         long-pair path instead of the batch kernel (default 2^26; 0 = never)
      "timing"            see above */
 anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value);
 

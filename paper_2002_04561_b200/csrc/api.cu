@@ -113,6 +113,7 @@ struct anyseq_ctx {
   int64_t chunk_bytes = 64ll << 20;  // host-API upload/compute pipelining granularity
   int64_t force_variant = -1;
   int64_t allow16 = 1;
+  int64_t batch_long_cells = 1ll << 26;  // batch pairs this large take the long-pair path
   int64_t tb8 = 1;          // traceback: 1-byte H store where the range allows
   int64_t pack2 = 1;        // host API: upload ACGT-only chunks as 2-bit codes
   int64_t pack2_percent = 0;  // share of the bytes packed (0 = all)
@@ -134,6 +135,8 @@ struct anyseq_ctx {
   double long_ms = 0;    // ... and its kernel time (max over devices)
   double tb_pass_ms = 0, tb_pass_cells = 0;  // last anyseq_traceback_long: forward pass(es)
   double tb_walk_ms = 0, tb_ckpt_bytes = 0;   // ... checkpointed walk time, checkpoint bytes
+  double tb_tiles = 0, tb_hits = 0;           // ... tiles walked, found precomputed by helpers
+  int64_t walk_helpers = 96;                  // helper CTAs of the walk
   int64_t tb_budget = 0, tb_kc_shift = 0, tb_ck_every = 0;  // options (0 = automatic)
   int tb_method = 0;  // last anyseq_traceback_long: 1 = checkpoints, 2 = Hirschberg
   int timing = 0;
@@ -1032,9 +1035,9 @@ std::vector<uint64_t> shard_bounds(const anyseq_batch* b, int G) {
   return bounds;
 }
 
-anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const anyseq_batch* b,
-                             int tb, int32_t* scores, anyseq_alignment* aln, uint32_t* cigar,
-                             uint64_t cap, uint64_t* used) {
+anyseq_status run_host_batch_core(anyseq_ctx* ctx, const anyseq_params* prm, const anyseq_batch* b,
+                                  int tb, int32_t* scores, anyseq_alignment* aln, uint32_t* cigar,
+                                  uint64_t cap, uint64_t* used) {
   const int G = (int)ctx->devs.size();
   std::vector<uint64_t> bounds = shard_bounds(b, G);
   std::vector<anyseq_status> st(G, ANYSEQ_OK);
@@ -1115,6 +1118,116 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
 // (run_host_batch, the a4/a5 kernels); their CIGARs are concatenated.
 // Linear gaps only: an affine split must carry the gap state across the cut
 // (Myers-Miller), which the leaf traceback does not take as a boundary condition.
+anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, const char* q,
+                                 uint64_t n, const char* s, uint64_t m, anyseq_alignment* out,
+                                 uint32_t* cigar, uint64_t cap, uint64_t* used);
+
+// Mixed batches (host-side form): a pair whose matrix is large (n·m >=
+// option batch_long_cells, both sides >= 2048) would tie one 8-lane group of the batch
+// kernel up for seconds; it goes to the long-pair path instead (the tiled wavefront over all
+// SMs, §5.4 / §5.4c), the rest of the batch to the batch path, and the results are merged in
+// pair order (both paths follow the same optimum and traceback rules, so the results are the
+// ones the batch path would give).
+anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const anyseq_batch* b,
+                             int tb, int32_t* scores, anyseq_alignment* aln, uint32_t* cigar,
+                             uint64_t cap, uint64_t* used) {
+  std::vector<uint64_t> longs;
+  if (ctx->batch_long_cells > 0)
+    for (uint64_t k = 0; k < b->num_pairs; ++k) {
+      const uint64_t n = b->q_off[k + 1] - b->q_off[k], m = b->s_off[k + 1] - b->s_off[k];
+      if (n >= 2048 && m >= 2048 && (long double)n * m >= (long double)ctx->batch_long_cells)
+        longs.push_back(k);
+    }
+  if (longs.empty()) return run_host_batch_core(ctx, prm, b, tb, scores, aln, cigar, cap, used);
+  // the other pairs, compacted
+  const uint64_t B = b->num_pairs, BL = longs.size(), BS = B - BL;
+  std::vector<uint64_t> rest;
+  rest.reserve(BS);
+  {
+    size_t x = 0;
+    for (uint64_t k = 0; k < B; ++k) {
+      if (x < BL && longs[x] == k) { ++x; continue; }
+      rest.push_back(k);
+    }
+  }
+  std::string cq, cs;
+  std::vector<uint64_t> qo{0}, so{0};
+  for (uint64_t k : rest) {
+    cq.append(b->q + b->q_off[k], (size_t)(b->q_off[k + 1] - b->q_off[k]));
+    cs.append(b->s + b->s_off[k], (size_t)(b->s_off[k + 1] - b->s_off[k]));
+    qo.push_back(cq.size());
+    so.push_back(cs.size());
+  }
+  const anyseq_batch b2{cq.data(), qo.data(), cs.data(), so.data(), BS};
+  std::vector<int32_t> sc2(BS);
+  std::vector<anyseq_alignment> al2((aln || tb) ? BS : 0);
+  std::vector<uint32_t> cg2;
+  uint64_t used2 = 0;
+  if (BS) {
+    if (tb) cg2.resize(std::max<uint64_t>(cq.size() + cs.size() + BS, 1));
+    const anyseq_status r = run_host_batch_core(ctx, prm, &b2, tb, sc2.data(),
+                                                al2.empty() ? nullptr : al2.data(),
+                                                tb ? cg2.data() : nullptr, cg2.size(), &used2);
+    if (r != ANYSEQ_OK) return r;
+  }
+  // the long pairs
+  std::vector<anyseq_alignment> al3(BL);
+  std::vector<std::vector<uint32_t>> cg3(BL);
+  for (uint64_t x = 0; x < BL; ++x) {
+    const uint64_t k = longs[x];
+    const char* qk = b->q + b->q_off[k];
+    const char* sk = b->s + b->s_off[k];
+    const uint64_t n = b->q_off[k + 1] - b->q_off[k], m = b->s_off[k + 1] - b->s_off[k];
+    anyseq_status r;
+    if (tb) {
+      cg3[x].resize(n + m + 1);
+      uint64_t u = 0;
+      r = run_traceback_long(ctx, prm, qk, n, sk, m, &al3[x], cg3[x].data(), cg3[x].size(), &u);
+      cg3[x].resize(u);
+    } else {
+      r = anyseq_align_long(ctx, prm, qk, n, sk, m, &al3[x]);
+    }
+    if (r != ANYSEQ_OK) {
+      ctx->err = "pair " + std::to_string(k) + " (long-pair path): " + ctx->err;
+      return r;
+    }
+  }
+  // merge in pair order
+  uint64_t off = 0;
+  size_t xl = 0, xs = 0;
+  for (uint64_t k = 0; k < B; ++k) {
+    const bool isl = xl < BL && longs[xl] == k;
+    anyseq_alignment a;
+    memset(&a, 0, sizeof(a));
+    const uint32_t* ops = nullptr;
+    if (isl) {
+      a = al3[xl];
+      ops = cg3[xl].data();
+      ++xl;
+    } else {
+      if (!al2.empty()) a = al2[xs];
+      a.score = sc2[xs];
+      if (tb) ops = cg2.data() + al2[xs].cigar_offset;
+      ++xs;
+    }
+    scores[k] = a.score;
+    if (tb) {
+      const uint32_t len = a.cigar_len;
+      if (off + len <= cap && len) memcpy(cigar + off, ops, (size_t)len * sizeof(uint32_t));
+      a.cigar_offset = off;
+      off += len;
+    }
+    if (aln) aln[k] = a;
+  }
+  if (tb) {
+    if (used) *used = off;
+    if (off > cap)
+      return fail(ctx, ANYSEQ_E_CAPACITY, "cigar needs %llu words, capacity %llu",
+                  (unsigned long long)off, (unsigned long long)cap);
+  }
+  return ANYSEQ_OK;
+}
+
 // Append a run of `len` ops to a CIGAR, merging with the last word when the op repeats;
 // a word holds at most 2^28 - 1 (len << 4 | op), so longer runs split into several words.
 void push_run(std::vector<uint32_t>& ops, uint32_t op, uint64_t len) {
@@ -1501,8 +1614,11 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
     int64_t bi = 0, bj = 0;
     double wms = 0;
     launches = 0;
+    int64_t tiles = 0, hits = 0;
     rc = run_long_traceback(ld, dp, sig, ck, r.end_i, r.end_j, (int64_t)n, (int64_t)m, &ops, &bi,
-                            &bj, &wms, &err, &launches);
+                            &bj, &wms, &err, &launches, (int)ctx->walk_helpers, &tiles, &hits);
+    ctx->tb_tiles = (double)tiles;
+    ctx->tb_hits = (double)hits;
     ctx->launches += launches;
     if (rc != 0) return fail(ctx, (anyseq_status)rc, "%s", err.c_str());
     ctx->tb_walk_ms = wms;
@@ -1742,12 +1858,14 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
     if (n == "allow16") { ctx->allow16 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "pack2") { ctx->pack2 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "tb8") { ctx->tb8 = value ? 1 : 0; return ANYSEQ_OK; }
+    if (n == "batch_long_cells") { ctx->batch_long_cells = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
     if (n == "pack2_percent") {
       if (value < 0 || value > 100) return fail(ctx, ANYSEQ_E_INVALID, "pack2_percent in [0, 100]");
       ctx->pack2_percent = value;
       return ANYSEQ_OK;
     }
     if (n == "tb_ckpt_bytes") { ctx->tb_budget = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
+    if (n == "walk_helpers") { ctx->walk_helpers = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
     if (n == "tb_kc_shift") {
       if (value != 0 && (value < 8 || value > 12))
         return fail(ctx, ANYSEQ_E_INVALID, "tb_kc_shift must be 0 or in [8, 12]");
@@ -1848,6 +1966,8 @@ anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) 
     if (n == "tb_walk_ms") { *value = ctx->tb_walk_ms; return ANYSEQ_OK; }
     if (n == "tb_ckpt_bytes") { *value = ctx->tb_ckpt_bytes; return ANYSEQ_OK; }
     if (n == "tb_method") { *value = ctx->tb_method; return ANYSEQ_OK; }
+    if (n == "tb_tiles") { *value = ctx->tb_tiles; return ANYSEQ_OK; }
+    if (n == "tb_hits") { *value = ctx->tb_hits; return ANYSEQ_OK; }
     if (n == "fill_launches") { *value = (double)ctx->fill_launches; return ANYSEQ_OK; }
     if (n == "h2d_bytes") { *value = (double)ctx->h2d_bytes.load(); return ANYSEQ_OK; }
     if (n == "d2h_bytes") { *value = (double)ctx->d2h_bytes.load(); return ANYSEQ_OK; }

@@ -51,7 +51,12 @@ struct WalkArgs {
   uint8_t* scratch;   // direction bytes of one tile, (kc + NT) * NT * TR
   uint32_t* ops;      // reversed RLE words (len << 4 | op)
   uint64_t ops_cap;
-  unsigned long long* out;  // [0] ops written (or required), [1] begin i, [2] begin j, [3] tiles
+  unsigned long long* out;  // [0] ops written, [1] begin i, [2] begin j, [3] tiles, [4] hits
+  uint8_t* slots;     // NSLOT helper scratches, slot_bytes each (whole tiles)
+  size_t slot_bytes;
+  int* sync;          // [0] jobs queued (walker), [1] jobs taken (helpers), [2] done, [3] abort
+  int* slot_job;      // [NSLOT]: the job whose bytes the slot holds (-1: none yet)
+  int2* jobs;         // [JMAX]: tile (row block, column block) of each job
 };
 
 __device__ __forceinline__ int h_row0(const WalkArgs& a, int j) {  // H(0, j)
@@ -62,30 +67,187 @@ __device__ __forceinline__ int h_col0(const WalkArgs& a, int i) {  // H(i, 0)
 }
 
 constexpr int KC_MAX = 4096;  // widest column block
+constexpr int NSLOT = 64;     // tile scratch slots of the helper CTAs
+constexpr int JMAX = 1 << 20; // job queue entries (a job = one tile)
 
+__device__ __forceinline__ int ld_acq(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Shared memory of one CTA's recompute.
+struct RecompSmem {
+  int xh[2][NT], xe[2][NT];
+  uint8_t scode[KC_MAX];
+  int sig[25];
+};
+
+// Recompute rows (R, R + nr] x columns (C, C + nc] of tile (b, kb) into direction bytes at
+// `dirs` (word (step * NT + t) * WPT + r/4 holds the thread's rows r), block-wide.  `top`
+// (dynamic shared memory, nc entries) receives the tile's top boundary row.
+template <int TR>
+__device__ void recompute(const WalkArgs& a, int b, int kb, int R, int C, int nr, int nc,
+                          uint8_t* dirs, RecompSmem& sm, int2* top) {
+  const int t = threadIdx.x;
+  const int row0 = R + t * TR;  // the row above this thread's first row
+  const bool tact = t * TR < nr;
+  int h[TR], f[TR];
+  int qcode[TR];
+#pragma unroll
+  for (int r = 0; r < TR; ++r) {
+    const int ii = row0 + r + 1;
+    const bool real = ii <= R + nr;
+    int2 lb = make_int2(h_col0(a, ii), NEGI);  // column 0: H(i, 0), F = -inf
+    if (real && kb > 0) lb = a.colck[(size_t)(kb - 1) * (a.n + 1) + ii];
+    h[r] = lb.x;
+    f[r] = lb.y;
+    qcode[r] = real ? 5 * (int)a.qc[ii - 1] : 0;
+  }
+  // the diagonal of the first row at the first column: H(row0, C)
+  int hprev;
+  if (t == 0) {
+    hprev = R == 0 ? h_row0(a, C)
+                   : (kb == 0 ? h_col0(a, R) : a.rowck[(size_t)(b - 1) * (a.m + 1) + C].x);
+  } else {
+    hprev = (kb == 0) ? h_col0(a, row0) : a.colck[(size_t)(kb - 1) * (a.n + 1) + row0].x;
+  }
+  const int nthreads = (nr + TR - 1) / TR;
+  const int steps = nc + nthreads - 1;
+  for (int c = t; c < nc; c += NT) {
+    const int jj = C + 1 + c;
+    top[c] = R == 0 ? make_int2(h_row0(a, jj), NEGI) : a.rowck[(size_t)(b - 1) * (a.m + 1) + jj];
+    sm.scode[c] = a.sc[jj - 1];
+  }
+  __syncthreads();
+  for (int k = 0; k < steps; ++k) {
+    const int c = k - t;  // column index in the region (jj = C + 1 + c)
+    if (tact && c >= 0 && c < nc) {
+      int hup, eup;  // H(row0, jj), E(row0, jj)
+      if (t == 0) {
+        const int2 v = top[c];
+        hup = v.x;
+        eup = v.y;
+      } else {
+        hup = sm.xh[(k - 1) & 1][t - 1];
+        eup = sm.xe[(k - 1) & 1][t - 1];
+      }
+      const int scode = sm.scode[c];
+      int dg = hprev;
+      hprev = hup;
+      uint32_t word = 0;
+#pragma unroll
+      for (int r = 0; r < TR; ++r) {
+        int E, F;
+        uint32_t eext = 0, fext = 0;
+        if (a.affine) {  // Eqs. (4)-(5): extension first, extension wins ties (R8)
+          const int ex = eup - a.ge, eo = hup - a.cop;
+          E = max(ex, eo);
+          eext = ex >= eo;
+          const int fx = f[r] - a.ge, fo = h[r] - a.cop;
+          F = max(fx, fo);
+          fext = fx >= fo;
+        } else {  // Eqs. (2)-(3)
+          E = hup - a.ge;
+          F = h[r] - a.ge;
+        }
+        // Eq. (1) in the relax listing's order: strict '>' replacement, DIAG > E > F (R7)
+        int H = dg + sm.sig[qcode[r] + scode];
+        uint32_t src = 0;
+        if (E > H) { H = E; src = 1; }
+        if (F > H) { H = F; src = 2; }
+        if (a.kind == KLOCAL && H <= 0) { H = 0; src = 3; }  // nu = 0 wins ties at 0 (R9)
+        word |= (src | (eext << 2) | (fext << 3)) << (8 * (r & 3));
+        if ((r & 3) == 3 || r == TR - 1) {
+          reinterpret_cast<uint32_t*>(dirs)[((size_t)k * NT + t) * ((TR + 3) / 4) + (r >> 2)] = word;
+          word = 0;
+        }
+        dg = h[r];
+        h[r] = H;
+        f[r] = F;
+        hup = H;
+        eup = E;
+      }
+      sm.xh[k & 1][t] = hup;
+      sm.xe[k & 1][t] = eup;
+    }
+    __syncthreads();
+  }
+}
+
+// Block 0 walks; blocks 1.. are helpers that recompute whole tiles the walker is predicted
+// to enter next (the path is monotone: up, left or up-left), so the walker mostly finds its
+// next tile's direction bytes ready instead of recomputing them on one SM.
 template <int TR>
 __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
-  __shared__ int xh[2][NT], xe[2][NT];
-  // the region's top boundary row (H, E) and subject codes, staged once per tile: the
-  // recompute's per-step inputs then come from shared memory, not from L2 round trips
+  __shared__ RecompSmem sm;
   extern __shared__ int2 top[];  // [KC_MAX]
-  __shared__ uint8_t scode_s[KC_MAX];
-  __shared__ int ssig[25];
-  __shared__ int sh_i, sh_j, sh_st, sh_done;
-  __shared__ unsigned long long sh_nops;
+  __shared__ int sh_i, sh_j, sh_st, sh_done, sh_slot, sh_job;
+  __shared__ unsigned long long sh_nops, sh_hits;
   __shared__ uint32_t sh_run;  // the RLE word being accumulated (len << 4 | op), 0 = none
+  __shared__ long long sched_tile[NSLOT];  // walker: tile (b << 32 | kb) of the slot's last job
+  __shared__ int sched_job[NSLOT];
+  __shared__ int sh_tail;
   const int t = threadIdx.x;
-  if (t < 25) ssig[t] = a.sig[t];
+  if (t < 25) sm.sig[t] = a.sig[t];
+  const int kc = 1 << a.kc_shift;
+  const size_t wpt_bytes = ((TR + 3) / 4) * 4;
+  if (blockIdx.x > 0) {  // ---------------------------------------------------- helper
+    __shared__ int hj, hexit;
+    for (;;) {
+      __syncthreads();
+      if (t == 0) {
+        hexit = 0;
+        hj = atomicAdd(&a.sync[1], 1);
+        long long spins = 0;
+        while (ld_acq(&a.sync[0]) <= hj) {
+          if (*(volatile int*)&a.sync[2]) { hexit = 1; break; }
+          __nanosleep(256);
+          if (++spins > (1ll << 26)) { atomicExch(&a.sync[3], 1); hexit = 1; break; }
+        }
+        if (!hexit && hj >= NSLOT) {  // the slot's previous job must be complete
+          const int s = hj % NSLOT;
+          while (ld_acq(&a.slot_job[s]) != hj - NSLOT) {
+            if (*(volatile int*)&a.sync[3]) { hexit = 1; break; }
+            __nanosleep(128);
+          }
+        }
+      }
+      __syncthreads();
+      if (hexit) return;
+      const int j = hj, s = j % NSLOT;
+      const int2 tile = a.jobs[j];
+      const int b = tile.x, kb = tile.y;
+      const int R = max(0, b * a.TH - a.PT);
+      const int R1 = min(a.n, (b + 1) * a.TH - a.PT);
+      const int C = kb << a.kc_shift;
+      const int C1 = min(a.m, C + kc);
+      recompute<TR>(a, b, kb, R, C, R1 - R, C1 - C, a.slots + (size_t)s * a.slot_bytes, sm, top);
+      if (t == 0) {
+        __threadfence();
+        st_rel(&a.slot_job[s], j);
+      }
+    }
+  }
+  // ------------------------------------------------------------------------- walker
   if (t == 0) {
     sh_i = a.end_i;
     sh_j = a.end_j;
     sh_st = 0;  // 0 = H, 1 = E (vertical, I), 2 = F (horizontal, D)
     sh_done = 0;
     sh_nops = 0;
+    sh_hits = 0;
     sh_run = 0;
+    sh_tail = 0;
+  }
+  if (t < NSLOT) {
+    sched_tile[t] = -1;
+    sched_job[t] = -1;
   }
   __syncthreads();
-  const int kc = 1 << a.kc_shift;
   unsigned long long tiles = 0;
   // append a run of ops (walk order = reversed alignment order); warp 0 lane 0 only
   auto emit = [&](uint32_t op, uint64_t len) {
@@ -106,6 +268,7 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
       }
     }
   };
+  const bool helpers = gridDim.x > 1;
 
   for (;;) {
     __syncthreads();
@@ -128,93 +291,56 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
     const int R = max(0, b * a.TH - a.PT);  // top boundary row of the tile
     const int kb = (j - 1) >> a.kc_shift;
     const int C = kb << a.kc_shift;         // left boundary column
-    const int nr = i - R, nc = j - C;       // the region up-left of (i, j)
     ++tiles;
-    // ---- recompute the region into direction bytes ----
-    const int row0 = R + t * TR;  // the row above this thread's first row
-    const bool tact = t * TR < nr;
-    int h[TR], f[TR];
-    int qcode[TR];
-#pragma unroll
-    for (int r = 0; r < TR; ++r) {
-      const int ii = row0 + r + 1;
-      const bool real = ii <= i;
-      int2 lb = make_int2(h_col0(a, ii), NEGI);  // column 0: H(i, 0), F = -inf
-      if (real && kb > 0) lb = a.colck[(size_t)(kb - 1) * (a.n + 1) + ii];
-      h[r] = lb.x;
-      f[r] = lb.y;
-      qcode[r] = real ? 5 * (int)a.qc[ii - 1] : 0;
-    }
-    // the diagonal of the first row at the first column: H(row0, C)
-    int hprev;
     if (t == 0) {
-      hprev = (b == 0 || R == 0) ? h_row0(a, C)
-            : (kb == 0 ? h_col0(a, R) : a.rowck[(size_t)(b - 1) * (a.m + 1) + C].x);
-    } else {
-      hprev = (kb == 0) ? h_col0(a, row0) : a.colck[(size_t)(kb - 1) * (a.n + 1) + row0].x;
-    }
-    const int nthreads = (nr + TR - 1) / TR;
-    const int steps = nc + nthreads - 1;
-    for (int c = t; c < nc; c += NT) {
-      const int jj = C + 1 + c;
-      top[c] = R == 0 ? make_int2(h_row0(a, jj), NEGI) : a.rowck[(size_t)(b - 1) * (a.m + 1) + jj];
-      scode_s[c] = a.sc[jj - 1];
+      sh_slot = -1;
+      if (helpers) {
+        const long long key = ((long long)b << 32) | (unsigned)kb;
+        int found = -1;
+        for (int x = 0; x < NSLOT; ++x)
+          if (sched_tile[x] == key) found = x;
+        // predict the next tiles (up, left, up-left and the diagonal band two and three
+        // tiles ahead) and queue those not yet queued; a slot is reused only when its
+        // tile lies behind the walker (not up-left of or equal to the current tile)
+        const int pred[9][2] = {{1, 1}, {1, 0}, {0, 1}, {2, 2}, {2, 1}, {1, 2}, {3, 3}, {3, 2}, {2, 3}};
+        for (int x = 0; x < 9; ++x) {
+          const int tb = b - pred[x][0], tk = kb - pred[x][1];
+          if (tb < 0 || tk < 0) continue;
+          const long long k2 = ((long long)tb << 32) | (unsigned)tk;
+          bool have = false;
+          for (int y = 0; y < NSLOT; ++y) have |= sched_tile[y] == k2;
+          if (have) continue;
+          const int jn = sh_tail;
+          if (jn >= JMAX) break;
+          const int sl = jn % NSLOT;
+          const long long old = sched_tile[sl];
+          if (old >= 0 && (int)(old >> 32) <= b && (int)(old & 0xffffffff) <= kb) continue;
+          a.jobs[jn] = make_int2(tb, tk);
+          sched_tile[sl] = k2;
+          sched_job[sl] = jn;
+          sh_tail = jn + 1;
+          st_rel(&a.sync[0], jn + 1);
+        }
+        if (found >= 0) {  // its bytes are (or will be) in slot `found`
+          const int jf = sched_job[found];
+          long long spins = 0;
+          while (ld_acq(&a.slot_job[found]) != jf) {
+            __nanosleep(64);
+            if (++spins > (1ll << 26)) { atomicExch(&a.sync[3], 1); break; }
+          }
+          sh_slot = found;
+          ++sh_hits;
+        }
+      }
     }
     __syncthreads();
-    for (int k = 0; k < steps; ++k) {
-      const int c = k - t;  // column index in the region (jj = C + 1 + c)
-      if (tact && c >= 0 && c < nc) {
-        const int jj = C + 1 + c;
-        int hup, eup;  // H(row0, jj), E(row0, jj)
-        if (t == 0) {
-          const int2 v = top[c];
-          hup = v.x;
-          eup = v.y;
-        } else {
-          hup = xh[(k - 1) & 1][t - 1];
-          eup = xe[(k - 1) & 1][t - 1];
-        }
-        (void)jj;
-        const int scode = scode_s[c];
-        int dg = hprev;
-        hprev = hup;
-        uint32_t word = 0;
-#pragma unroll
-        for (int r = 0; r < TR; ++r) {
-          int E, F;
-          uint32_t eext = 0, fext = 0;
-          if (a.affine) {  // Eqs. (4)-(5): extension first, extension wins ties (R8)
-            const int ex = eup - a.ge, eo = hup - a.cop;
-            E = max(ex, eo);
-            eext = ex >= eo;
-            const int fx = f[r] - a.ge, fo = h[r] - a.cop;
-            F = max(fx, fo);
-            fext = fx >= fo;
-          } else {  // Eqs. (2)-(3)
-            E = hup - a.ge;
-            F = h[r] - a.ge;
-          }
-          // Eq. (1) in the relax listing's order: strict '>' replacement, DIAG > E > F (R7)
-          int H = dg + ssig[qcode[r] + scode];
-          uint32_t src = 0;
-          if (E > H) { H = E; src = 1; }
-          if (F > H) { H = F; src = 2; }
-          if (a.kind == KLOCAL && H <= 0) { H = 0; src = 3; }  // nu = 0 wins ties at 0 (R9)
-          word |= (src | (eext << 2) | (fext << 3)) << (8 * (r & 3));
-          if ((r & 3) == 3 || r == TR - 1) {
-            reinterpret_cast<uint32_t*>(a.scratch)[((size_t)k * NT + t) * ((TR + 3) / 4) + (r >> 2)] = word;
-            word = 0;
-          }
-          dg = h[r];
-          h[r] = H;
-          f[r] = F;
-          hup = H;
-          eup = E;
-        }
-        xh[k & 1][t] = hup;
-        xe[k & 1][t] = eup;
-      }
-      __syncthreads();
+    const int slot = sh_slot;
+    const uint8_t* dirs;
+    if (slot >= 0) {
+      dirs = a.slots + (size_t)slot * a.slot_bytes;
+    } else {  // not predicted: recompute the region up-left of (i, j) here
+      recompute<TR>(a, b, kb, R, C, i - R, j - C, a.scratch, sm, top);
+      dirs = a.scratch;
     }
     // ---- walk the region (warp 0) until the path leaves it ----
     if (t < 32) {
@@ -222,7 +348,7 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
       int ci = i, cj = j, st = sh_st;
       auto dir_at = [&](int ii, int jj) -> uint32_t {  // direction byte of cell (ii, jj)
         const int rr = ii - R - 1, tt = rr / TR, step = (jj - C - 1) + tt;
-        return a.scratch[((size_t)step * NT + tt) * (((TR + 3) / 4) * 4) + (rr % TR)];
+        return dirs[((size_t)step * NT + tt) * wpt_bytes + (rr % TR)];
       };
       bool done = false;
       while (!done && ci > R && cj > C) {
@@ -285,6 +411,7 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
     }
   }
   if (t == 0) {
+    st_rel(&a.sync[2], 1);  // helpers: no more jobs
     if (sh_run) {
       if (sh_nops < a.ops_cap) a.ops[sh_nops] = sh_run;
       ++sh_nops;
@@ -293,6 +420,7 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
     a.out[1] = (unsigned long long)sh_i;
     a.out[2] = (unsigned long long)sh_j;
     a.out[3] = tiles;
+    a.out[4] = sh_hits;
   }
 }
 
@@ -315,7 +443,8 @@ struct DBuf {
 int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t sig[25],
                        const LongCkpt& ck, int64_t end_i, int64_t end_j, int64_t n, int64_t m,
                        std::vector<uint32_t>* ops, int64_t* begin_i, int64_t* begin_j,
-                       double* walk_ms, std::string* err, uint64_t* launches) {
+                       double* walk_ms, std::string* err, uint64_t* launches, int walk_helpers,
+                       int64_t* tiles, int64_t* hits) {
   TK(cudaSetDevice(dev.id));
   cudaStream_t st = dev.stream;
   ops->clear();
@@ -348,11 +477,26 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
   a.end_i = (int)end_i;
   a.end_j = (int)end_j;
   const size_t scratch = ((size_t)(1 << ck.kc_shift) + NT) * NT * (((TR + 3) / 4) * 4);
-  DBuf sb, ob, outb;
+  DBuf sb, ob, outb, slotb, syncb, jobb;
   TK(cudaMalloc(&sb.p, scratch));
   const uint64_t cap = (uint64_t)(n + m + 2);
   TK(cudaMalloc(&ob.p, cap * sizeof(uint32_t)));
-  TK(cudaMalloc(&outb.p, 4 * sizeof(unsigned long long)));
+  TK(cudaMalloc(&outb.p, 8 * sizeof(unsigned long long)));
+  TK(cudaMemsetAsync(outb.p, 0, 8 * sizeof(unsigned long long), st));
+  // helper CTAs: whole-tile recomputes of the predicted next tiles (option walk_helpers)
+  const int helpers = std::max(0, std::min(walk_helpers, dev.num_sms - 1));
+  if (helpers > 0) {
+    TK(cudaMalloc(&slotb.p, (size_t)NSLOT * scratch));
+    TK(cudaMalloc(&syncb.p, (4 + NSLOT) * sizeof(int)));
+    TK(cudaMemsetAsync(syncb.p, 0, 4 * sizeof(int), st));
+    TK(cudaMemsetAsync((int*)syncb.p + 4, 0xFF, NSLOT * sizeof(int), st));
+    TK(cudaMalloc(&jobb.p, (size_t)JMAX * sizeof(int2)));
+  }
+  a.slots = (uint8_t*)slotb.p;
+  a.slot_bytes = scratch;
+  a.sync = (int*)syncb.p;
+  a.slot_job = helpers > 0 ? (int*)syncb.p + 4 : nullptr;
+  a.jobs = (int2*)jobb.p;
   a.scratch = (uint8_t*)sb.p;
   a.ops = (uint32_t*)ob.p;
   a.ops_cap = cap;
@@ -365,25 +509,25 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
   switch (TR) {
     case 2:
       TK(cudaFuncSetAttribute(tile_walk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      tile_walk_kernel<2><<<1, NT, smem, st>>>(a);
+      tile_walk_kernel<2><<<1 + helpers, NT, smem, st>>>(a);
       break;
     case 4:
       TK(cudaFuncSetAttribute(tile_walk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      tile_walk_kernel<4><<<1, NT, smem, st>>>(a);
+      tile_walk_kernel<4><<<1 + helpers, NT, smem, st>>>(a);
       break;
     case 8:
       TK(cudaFuncSetAttribute(tile_walk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      tile_walk_kernel<8><<<1, NT, smem, st>>>(a);
+      tile_walk_kernel<8><<<1 + helpers, NT, smem, st>>>(a);
       break;
     default:
       TK(cudaFuncSetAttribute(tile_walk_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      tile_walk_kernel<16><<<1, NT, smem, st>>>(a);
+      tile_walk_kernel<16><<<1 + helpers, NT, smem, st>>>(a);
       break;
   }
   TK(cudaGetLastError());
   TK(cudaEventRecord(e1, st));
   *launches += 1;
-  unsigned long long out[4];
+  unsigned long long out[8];
   TK(cudaMemcpyAsync(out, outb.p, sizeof(out), cudaMemcpyDeviceToHost, st));
   TK(cudaStreamSynchronize(st));
   float ms = 0;
@@ -401,6 +545,16 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
   for (size_t x = 0, y = ops->size(); x + 1 < y; ++x, --y) std::swap((*ops)[x], (*ops)[y - 1]);
   *begin_i = (int64_t)out[1];
   *begin_j = (int64_t)out[2];
+  if (tiles) *tiles = (int64_t)out[3];
+  if (hits) *hits = (int64_t)out[4];
+  if (helpers > 0) {
+    int ab = 0;
+    TK(cudaMemcpy(&ab, (int*)syncb.p + 3, sizeof(int), cudaMemcpyDeviceToHost));
+    if (ab) {
+      *err = "long traceback: a walk wait exceeded its bound";
+      return ANYSEQ_E_TIMEOUT;
+    }
+  }
   return 0;
 }
 

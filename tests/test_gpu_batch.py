@@ -544,3 +544,33 @@ def test_tb8_low_byte_store(ctx, kind):
             finally:
                 ctx.set_option("tb8", 1)
                 ctx.set_option("allow16", 1)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_mixed_batch_routes_long_pairs(ctx, kind):
+    """Mixed batch (host-side form): pairs at or above batch_long_cells go
+    to the long-pair path; scores, cells and CIGARs of every pair still equal the oracle's,
+    in pair order, with cigar offsets contiguous."""
+    import paper_2002_04561_b200 as A
+    from synth import random_pairs, c4_genomes, csr
+    q0, qo0, s0, so0 = random_pairs(40, 0, 300, seed=92)
+    g1, g2 = c4_genomes(6000, "a", seed=93)
+    qs = [q0[qo0[k]:qo0[k + 1]].tobytes() for k in range(40)]
+    ss = [s0[so0[k]:so0[k + 1]].tobytes() for k in range(40)]
+    for pos, (a, b) in ((3, (g1[:2500], g2[:2600])), (17, (g1[3000:5600], g2[3000:5500])),
+                        (39, (g2[:2100], g1[:3000]))):
+        qs.insert(pos, a)
+        ss.insert(pos, b)
+    q, qo = csr(qs)
+    s, so = csr(ss)
+    res, ocig = _oracle(kind, "affine", 5, 1, q, qo, s, so, tb=True)
+    sch = A.Scheme(kind, "affine", 2, -1, 5, 1)
+    ctx.set_option("batch_long_cells", 1 << 22)
+    try:
+        _check_scores(ctx, sch, q, qo, s, so, res)
+        _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+        aln, words = ctx.traceback(sch, q, qo, s, so)
+        cl = aln["cigar_len"].astype(np.uint64)
+        assert np.array_equal(aln["cigar_offset"], np.cumsum(cl) - cl)
+    finally:
+        ctx.set_option("batch_long_cells", 1 << 26)

@@ -36,16 +36,18 @@ def _check_path(scheme_o, q, s, r):
 
 KINDS = ("global", "local", "semi")
 GAPS = (("linear", 0), ("affine", 5), ("affine", 2))
-# (long_band_rows, tb_ck_every, tb_kc_shift): 512-row strips with tiles 512 x 256 and
-# 1024 x 512, and the automatic geometry (1024-row strips, 1024-column blocks)
-GEOMS = ((512, 1, 8), (512, 2, 9), (0, 0, 0))
+# (long_band_rows, tb_ck_every, tb_kc_shift, walk_helpers): 512-row strips with tiles
+# 512 x 256 (the walker alone) and 1024 x 512 (helper CTAs recomputing predicted tiles), and
+# the automatic geometry with helpers
+GEOMS = ((512, 1, 8, 0), (512, 2, 9, 96), (0, 0, 0, 96))
 
 
 def _set_geom(ctx, geom):
-    rows, every, kcs = geom
+    rows, every, kcs, helpers = geom
     ctx.set_option("long_band_rows", rows)
     ctx.set_option("tb_ck_every", every)
     ctx.set_option("tb_kc_shift", kcs)
+    ctx.set_option("walk_helpers", helpers)
 
 
 def _pairs():
@@ -76,7 +78,7 @@ def test_long_tb_ckpt_bit_exact(ctx, geom, kind, gap, go):
             assert got == (o.score, o.q_begin, o.s_begin, o.q_end, o.s_end), (len(q), len(s))
             assert r["cigar"] == o.cigar, (len(q), len(s))
     finally:
-        _set_geom(ctx, (0, 0, 0))
+        _set_geom(ctx, (0, 0, 0, 96))
 
 
 @pytest.mark.parametrize("kind", KINDS)

@@ -41,7 +41,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c1,c3,c5,c4")
     ap.add_argument("--c4n", type=int, default=5_000_000)
-    ap.add_argument("--c5pairs", type=int, default=200_000)
+    ap.add_argument("--c5pairs", type=int, default=1_000_000)
     args = ap.parse_args()
     ctx = A.Context([0])
     res = []
@@ -65,6 +65,10 @@ def main():
             paln = pin(np.zeros(len(qo) - 1, A.ALIGNMENT_DTYPE))
             pcig = pin(np.zeros(32 * (len(qo) - 1), np.uint32))
             sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+            ctx.set_option("tb8", 0)  # the round-1 store (full H, 2 B per cell) for comparison
+            _, wall16, fill16, walk16 = timed(
+                ctx, lambda: ctx.traceback(sch, q, qo, s, so, out_aln=paln, out_cigar=pcig), 2)
+            ctx.set_option("tb8", 1)
             (aln, cig), wall, fill, walk = timed(
                 ctx, lambda: ctx.traceback(sch, q, qo, s, so, out_aln=paln, out_cigar=pcig), 2)
             idx = np.random.default_rng(0).choice(len(qm), 300, replace=False)
@@ -76,15 +80,18 @@ def main():
             cells = 1e6 * 150 * 150
             res.append({"config": "C3 1M x 150bp SW affine traceback (CIGAR)", "cells": cells,
                         "wall_ms": wall * 1e3, "fill_ms": fill, "walk_ms": walk,
+                        "fill_gcups": cells / (fill / 1e3) / 1e9,
+                        "full_h_store": {"wall_ms": wall16 * 1e3, "fill_ms": fill16,
+                                         "walk_ms": walk16},
                         "gcups_wall": cells / wall / 1e9,
                         "gcups_fill_walk": cells / ((fill + walk) / 1e3) / 1e9, "parity_300": ok})
         elif c == "c5":
-            q, qo, s, so = synth.c5_mixed(args.c5pairs, seed=5)
+            q, qo, s, so = synth.c5_mixed_large(args.c5pairs, seed=5)
             q, qo, s, so = pin(q), pin(qo), pin(s), pin(so)
             B = len(qo) - 1
             psc = pin(np.zeros(B, np.int32))
             paln = pin(np.zeros(B, A.ALIGNMENT_DTYPE))
-            pcig = pin(np.zeros(int(qo[-1] + so[-1]) + B, np.uint32))
+            pcig = pin(np.zeros(24 * B, np.uint32))
             cells = float(np.sum(np.diff(qo).astype(np.float64) * np.diff(so).astype(np.float64)))
             for kind in ("global", "semi", "local"):
                 sch = A.Scheme(kind, "affine", 2, -1, 5, 1)
@@ -109,11 +116,13 @@ def main():
                 t0 = time.perf_counter()
                 r = ctx.align_long(sch, g1, g2)
                 wall = time.perf_counter() - t0
+                kms = ctx.stat("long_kernel_ms")
                 cells = float(len(g1)) * len(g2)
                 ok = (r["score"], r["q_end"], r["s_end"]) == (2 * len(g1), len(g1), len(g1)) \
                     if variant == "c" else None
                 res.append({"config": f"C4 {args.c4n}bp x {len(g2)}bp SW affine variant {variant}",
-                            "cells": cells, "wall_ms": wall * 1e3,
+                            "cells": cells, "wall_ms": wall * 1e3, "kernel_ms": kms,
+                            "gcups_kernel": cells / (kms / 1e3) / 1e9,
                             "gcups_wall": cells / wall / 1e9, "result": r, "closed_form_ok": ok})
         while printed < len(res):
             print(json.dumps(res[printed]), flush=True)
