@@ -18,7 +18,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libanyseq.so")
+# ANYSEQ_LIB: another build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("ANYSEQ_LIB") or os.path.join(HERE, "lib", "libanyseq.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "anyseq.h")
 
 if not os.path.exists(LIB_PATH):

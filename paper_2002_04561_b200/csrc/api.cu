@@ -1206,7 +1206,7 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
       ++xl;
     } else {
       if (!al2.empty()) a = al2[xs];
-      a.score = sc2[xs];
+      if (!tb) a.score = sc2[xs];  // (traceback mode: the score is in the alignment struct)
       if (tb) ops = cg2.data() + al2[xs].cigar_offset;
       ++xs;
     }

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
   __shared__ uint32_t ring_rel[4][RING];
   __shared__ int2 ring_out[4][64];        // the task's last row (H, E) awaiting publication
   __shared__ int ring_eck[CKPT ? 4 : 1][64];  // CKPT: E of that row itself (not of the next)
+  __shared__ int4 ring_pf[4][64];  // row hand-off entries fetched (cp.async) ahead of need
   const int t = threadIdx.x & 31;
   const int wb = threadIdx.x >> 5;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -118,8 +119,9 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
       Ff[r] = VS16::splat(NEGc);
     }
     int last_code = 0;  // subject code of the column before the next refill's first
-    auto refill = [&](int c0, int c1) -> bool {
-      if (c0 >= c1) return true;  // (the task's second initial refill when W <= 32)
+    // subject codes of columns [c0, c1) -> full selectors in the ring (first strip: lane 0's
+    // input row 0 as well)
+    auto codes = [&](int c0, int c1) {
       const int c = c0 + t;
       const bool mine = c < c1;
       const int code = mine ? a.sc[c_lo + c] : 0;
@@ -130,29 +132,74 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
       // the high half relaxes column W - 1 one step after the low half left the task: its
       // selector (entry W) carries code(W - 1) in the high nibbles
       if (c1 == W && t == 0) ring_sel[wb][W & (RING - 1)] = (uint32_t)last_code * 0x1100u + 0xC480u;
-      if (s == 0) {  // first strip: lane 0's input is row 0
-        if (mine) {
-          const int h0 = KIND == KGLOBAL ? -(P.go + (c_lo + c + 1) * P.ge) : 0;
-          ring_he[wb][c & (RING - 1)] = make_int2(h0, h0 - cop);
-        }
-        return true;
+      if (s == 0 && mine) {
+        const int h0 = KIND == KGLOBAL ? -(P.go + (c_lo + c + 1) * P.ge) : 0;
+        ring_he[wb][c & (RING - 1)] = make_int2(h0, h0 - cop);
       }
+    };
+    // the hand-off entries of [c0, c1) (s > 0): poll until every entry carries tag s
+    auto handoff = [&](int c0, int c1, int4 v) -> bool {
+      const int c = c0 + t;
+      const bool mine = c < c1;
+      if (!mine) v = make_int4(0, s, 0, s);
       const int4* src = a.rowbuf + c_lo + c + 1;
-      int4 v = mine ? ld_row(src) : make_int4(0, s, 0, s);
       long long spins = 0;
       while (!__all_sync(0xffffffffu, v.y == s && v.w == s)) {
         const long long t0 = (a.prof && t == 0) ? clock64() : 0;
-        __nanosleep(a.sleep_ns);
         if (v.y != s || v.w != s) v = ld_row(src);
+        if (!__all_sync(0xffffffffu, v.y == s && v.w == s)) __nanosleep(a.sleep_ns);
         if ((++spins & 255) == 0 &&
             __any_sync(0xffffffffu, spins > a.spin_limit || *(volatile int*)a.abort_flag)) {
           if (t == 0) atomicExch(a.abort_flag, 1);
           return false;
         }
-        if (a.prof && t == 0)  // [0]: mid-task refills, [3]: the task's first two refills
+        if (a.prof && t == 0)  // [0]: mid-task waits, [3]: the task's first two refills
           atomicAdd(&a.prof[c0 < 2 * PER ? 3 : 0], (unsigned long long)(clock64() - t0));
       }
       if (mine) ring_he[wb][c & (RING - 1)] = make_int2(v.x, v.z);
+      return true;
+    };
+    auto refill = [&](int c0, int c1) -> bool {  // synchronous (the task's first two periods)
+      if (c0 >= c1) return true;  // (the task's second initial refill when W <= 32)
+      codes(c0, c1);
+      if (s == 0) return true;
+      const int c = c0 + t;
+      return handoff(c0, c1, c < c1 ? ld_row(a.rowbuf + c_lo + c + 1) : make_int4(0, s, 0, s));
+    };
+    // Non-blocking hand-off for the rest of the task: the next period's 32 entries are
+    // requested (cp.async into ring_pf) two periods before lane 0 needs them and checked every
+    // other step; entries the strip above has not published yet are requested again, and
+    // the warp blocks (polls) only when the batch is due.  A strip that runs close behind
+    // the strip above thereby keeps computing instead of spinning on the hand-off.
+    int pf_next = 2 * PER;  // first column of the next batch to request
+    int pf_b0 = -1;         // first column of the batch in flight (-1: none)
+    auto pump = [&](int kk) -> bool {
+      if (pf_b0 >= 0) {
+        const int c1 = min(W, pf_b0 + PER), c = pf_b0 + t;
+        cp_async_wait_all();
+        int4 v = c < c1 ? ring_pf[wb][c & 63] : make_int4(0, s, 0, s);
+        const bool ok = __all_sync(0xffffffffu, v.y == s && v.w == s);
+        if (ok || kk + 2 >= pf_b0) {  // complete, or due: finish it (polling if needed)
+          if (!handoff(pf_b0, c1, v)) return false;
+          pf_next = pf_b0 + PER;
+          pf_b0 = -1;
+        } else if (c < c1 && (v.y != s || v.w != s)) {  // ask again for the missing ones
+          cp_async16(&ring_pf[wb][c & 63], a.rowbuf + c_lo + c + 1);
+          cp_async_commit();
+        }
+      }
+      if (pf_b0 < 0 && pf_next < W && pf_next <= kk + 2 * PER) {
+        const int c1 = min(W, pf_next + PER), c = pf_next + t;
+        codes(pf_next, c1);
+        if (s == 0) {
+          pf_next += PER;
+        } else {
+          if (c < c1) cp_async16(&ring_pf[wb][c & 63], a.rowbuf + c_lo + c + 1);
+          cp_async_commit();
+          pf_b0 = pf_next;
+        }
+      }
+      __syncwarp();
       return true;
     };
     // start slack (option long_start_lag, columns): tickets are taken in strip order, so the
@@ -292,30 +339,39 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
           }
         }
         if (KIND == KLOCAL) {
-          // local optimum: packed running maximum per half; strictly larger values only
-          uint32_t cm;
+          // local optimum: packed running maximum per half; strictly larger values only.
+          // cmB = max over the half's rows but its first: when the first row holds the new
+          // maximum (the common case where H falls down the rows, e.g. left of a similar
+          // pair's diagonal, where a new maximum appears at every step) its row is known
+          // without searching the others.
+          uint32_t cm, cmB;
           if (CHK) {
-            uint32_t mx = Hq[0];
+            const uint32_t keep = (act0 ? 1u : 0u) | (act1 ? 2u : 0u);
+            uint32_t mx = Hq[1];
 #pragma unroll
-            for (int r = 1; r + 1 < NR; r += 2) mx = __vimax3_s16x2(mx, Hq[r], Hq[r + 1]);
-            if ((NR % 2) == 0) mx = __vmaxs2(mx, Hq[NR - 1]);
-            mx = VS16::select_mask(mx, (act0 ? 1u : 0u) | (act1 ? 2u : 0u), VS16::splat(-32768));
-            cm = __vmaxs2(mx, best);
+            for (int r = 2; r + 1 < NR; r += 2) mx = __vimax3_s16x2(mx, Hq[r], Hq[r + 1]);
+            if ((NR % 2) == 1) mx = __vmaxs2(mx, Hq[NR - 1]);
+            cmB = VS16::select_mask(mx, keep, VS16::splat(-32768));
+            cm = __vimax3_s16x2(VS16::select_mask(Hq[0], keep, VS16::splat(-32768)), cmB, best);
           } else {
-            cm = __vimax3_s16x2(best, Hq[0], Hq[1]);
+            cmB = Hq[1];
 #pragma unroll
-            for (int r = 2; r + 1 < NR; r += 2) cm = __vimax3_s16x2(cm, Hq[r], Hq[r + 1]);
-            if ((NR % 2) == 1) cm = __vmaxs2(cm, Hq[NR - 1]);
+            for (int r = 2; r + 1 < NR; r += 2) cmB = __vimax3_s16x2(cmB, Hq[r], Hq[r + 1]);
+            if ((NR % 2) == 1) cmB = __vmaxs2(cmB, Hq[NR - 1]);
+            cm = __vimax3_s16x2(Hq[0], cmB, best);
           }
-          if (cm != best) {  // rare: resolve (value, first row, column) of the improved half(s)
+          if (cm != best) {  // resolve (value, first row, column) of the improved half(s)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int v = h16_get(cm, h);
               if (v != h16_get(best, h)) {
-                int rr = NR - 1;
+                int rr = 0;
+                if (h16_get(Hq[0], h) != v) {  // not the first row: the first row reaching v
+                  rr = NR - 1;
 #pragma unroll
-                for (int r = NR - 1; r >= 0; --r)
-                  if (h16_get(Hq[r], h) == v) rr = r;
+                  for (int r = NR - 1; r >= 1; --r)
+                    if (h16_get(Hq[r], h) == v) rr = r;
+                }
                 if (h == 0) { bv0 = v + base; bi0 = ip0 + rr + 1; bj0 = c_lo + lc + 1; }
                 else { bv1 = v + base; bi1 = ip0 + NR + rr + 1; bj1 = c_lo + lc; }
               }
@@ -397,20 +453,13 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
       const int kA = min(K & ~1, 64);          // every virtual lane has reached column 0
       const int kB = max(kA, (W - 1) & ~1);    // no virtual lane has reached column W-1
       int k = 0;
-      auto maybe_refill = [&](int kk) -> bool {
-        if ((kk % PER) == 0 && kk > 0 && kk + PER < W) {
-          if (!refill(kk + PER, min(W, kk + 2 * PER))) return false;
-          __syncwarp();
-        }
-        return true;
-      };
       for (; k < kA; k += 2) {
-        if (!maybe_refill(k)) return false;
+        if (!pump(k)) return false;
         step(ON, k);
         step(ON, k + 1);
       }
       for (; k < kB; k += 2) {
-        if (!maybe_refill(k)) return false;
+        if (!pump(k)) return false;
         if ((k % PER) == 0) {
           reframe();
           convert(k);
@@ -421,7 +470,7 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
       }
       he_nx = ring_he[wb][k & (RING - 1)];  // the CHK path's lane-0 input again
       for (; k + 1 < K; k += 2) {
-        if (!maybe_refill(k)) return false;
+        if (!pump(k)) return false;
         if ((k % PER) == 0 && k >= 64) flush(min(W, k - 63));
         step(ON, k);
         step(ON, k + 1);
