@@ -50,8 +50,12 @@ __device__ __forceinline__ uint32_t h16_pack(int lo, int hi) {
 // checkpoints the traceback's tile recompute starts from -- every ck_every-th row strip's
 // last row, (H, E) of that row (a.rowck), and every 2^kc_shift-th column, (H, F) of every
 // row (a.colck) -- in absolute 32-bit values.
+#ifndef LONG16_MINB
+#define LONG16_MINB 3  // resident blocks per SM asked of ptxas for 1024-row tasks (A/B builds: 4)
+#endif
 template <int NR, int KIND, bool CKPT = false>
-__global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs a) {
+__global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) ? 4 : 3)
+    long16_kernel(LongArgs a) {
   constexpr int HS = 64 * NR;  // rows per task: 32 lanes x 2 halves x NR
   constexpr int RING = 256;
   constexpr int PER = 32;
@@ -174,7 +178,9 @@ __global__ void __launch_bounds__(128, NR <= 12 ? 4 : 3) long16_kernel(LongArgs 
     int pf_next = 2 * PER;  // first column of the next batch to request
     int pf_b0 = -1;         // first column of the batch in flight (-1: none)
     auto pump = [&](int kk) -> bool {
-      if (pf_b0 >= 0) {
+      // a batch in flight is looked at every 8 steps until it is due (each look costs a
+      // shared-memory pass over the entries, a vote and possibly a new request)
+      if (pf_b0 >= 0 && ((kk & 7) == 0 || kk + 2 >= pf_b0)) {
         const int c1 = min(W, pf_b0 + PER), c = pf_b0 + t;
         cp_async_wait_all();
         int4 v = c < c1 ? ring_pf[wb][c & 63] : make_int4(0, s, 0, s);

@@ -1,6 +1,8 @@
-# A/B of long-kernel builds on one box: tools/ab/libanyseq_A.so vs the in-tree library,
-# alternating, C4 (5 Mbp local affine) kernel time.
+# A/B of long-kernel builds on one box, alternating: C4 (5 Mbp local affine) kernel time.
+# usage: bash tools/ab_long.sh tools/ab/libX.so [tools/ab/libY.so ...]   (in-tree lib = "cur")
 for r in 1 2; do
-  ANYSEQ_LIB=$PWD/tools/ab/libanyseq_A.so python tools/long_lag.py 5000000 0 2>&1 | head -1 | sed 's/^/A: /'
-  python tools/long_lag.py 5000000 0 2>&1 | head -1 | sed 's/^/B: /'
+  for lib in "$@"; do
+    ANYSEQ_LIB=$PWD/$lib python tools/long_lag.py 5000000 0 2>&1 | head -1 | sed "s#^#$(basename $lib): #"
+  done
+  python tools/long_lag.py 5000000 0 2>&1 | head -1 | sed 's/^/cur: /'
 done
