@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
     }
   }
   if (t == 0) {
-    st_rel(&a.sync[2], 1);  // helpers: no more jobs
+    if (helpers) st_rel(&a.sync[2], 1);  // helpers: no more jobs
     if (sh_run) {
       if (sh_nops < a.ops_cap) a.ops[sh_nops] = sh_run;
       ++sh_nops;
