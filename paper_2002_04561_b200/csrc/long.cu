@@ -583,9 +583,10 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
       const int64_t rows = (int64_t)(S - 1) / every, cols = (int64_t)(m - 1) >> kcs;
       return (rows * (int64_t)(m + 1) + cols * (int64_t)(n + 1)) * (int64_t)sizeof(int2);
     };
-    // finest first: the walk recomputes ~(n·KC + m·TH)/2 cells on one SM, the pass only
-    // writes the checkpoints (bytes ~ n·m·8·(1/TH + 1/KC))
-    const int cands[][2] = {{1, 8}, {1, 9}, {1, 10}, {1, 11}, {2, 11}, {2, 12}, {4, 12}, {8, 12}};
+    // the walk's tiles are recomputed by helper CTAs (~(n·KC + m·TH)/2 cells), the pass
+    // writes the checkpoints (bytes ~ n·m·8·(1/TH + 1/KC)): 512-column blocks balance the
+    // two (1 Mbp, 512-row strips: KC 256 / 512 / 1024 / 2048 -> 1095 / 726 / 728 / 876 ms)
+    const int cands[][2] = {{1, 9}, {1, 10}, {1, 11}, {2, 11}, {2, 12}, {4, 12}, {8, 12}};
     int every = 0, kcs = 0;
     for (auto& c : cands) {
       if (HS * c[0] > 4096) continue;
