@@ -11,6 +11,16 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Debug builds (-DANYSEQ_CHECKS, tools/checks_build.sh): device-side bounds checks on the
+// index computations of the long-pair kernels and the traceback walk; a failed check traps
+// the kernel (the call then reports ANYSEQ_E_CUDA).  compute-sanitizer is not available on
+// the GPU pool, so this is the memory-safety run of the test workload.
+#ifdef ANYSEQ_CHECKS
+#define ANY_CHECK(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define ANY_CHECK(c) do { } while (0)
+#endif
+
 namespace anyseq {
 
 enum Kind : int { KGLOBAL = 0, KLOCAL = 1, KSEMI = 2 };

@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
             const int h = ((jl & kcm) == 0) ? 0 : 1;
             const int jj = jl - h;
             if (jj < a.m) {
+              ANY_CHECK(jj >= (1 << a.kc_shift) && ((jj >> a.kc_shift) - 1) < ((a.m - 1) >> a.kc_shift));
               int2* dst = a.colck + (size_t)((jj >> a.kc_shift) - 1) * (a.n + 1);
 #pragma unroll
               for (int r = 0; r < NR; ++r) {
@@ -446,7 +447,9 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         const int c = flushed + t;
         if (c < c_end) {
           const int2 v = ring_out[wb][c & 63];
+          ANY_CHECK(c_lo + c + 1 <= a.m);
           st_row(a.rowbuf + c_lo + c + 1, v.x, v.y, s + 1);
+          ANY_CHECK(!CKPT || ck_slot < (a.S - 1) / a.ck_every);
           if (CKPT && ck_slot >= 0)  // row checkpoint: (H, E) of the strip's last row
             a.rowck[(size_t)ck_slot * (a.m + 1) + c_lo + c + 1] = make_int2(v.x, ring_eck[wb][c & 63]);
         }

@@ -57,6 +57,7 @@ struct WalkArgs {
   int* sync;          // [0] jobs queued (walker), [1] jobs taken (helpers), [2] done, [3] abort
   int* slot_job;      // [NSLOT]: the job whose bytes the slot holds (-1: none yet)
   int2* jobs;         // [JMAX]: tile (row block, column block) of each job
+  int32_t nrowck, ncolck;  // checkpoint rows / columns stored (bounds checks)
 };
 
 __device__ __forceinline__ int h_row0(const WalkArgs& a, int j) {  // H(0, j)
@@ -102,6 +103,8 @@ __device__ void recompute(const WalkArgs& a, int b, int kb, int R, int C, int nr
     const int ii = row0 + r + 1;
     const bool real = ii <= R + nr;
     int2 lb = make_int2(h_col0(a, ii), NEGI);  // column 0: H(i, 0), F = -inf
+    ANY_CHECK(!real || ii <= a.n);
+    ANY_CHECK(kb == 0 || kb - 1 < a.ncolck);
     if (real && kb > 0) lb = a.colck[(size_t)(kb - 1) * (a.n + 1) + ii];
     h[r] = lb.x;
     f[r] = lb.y;
@@ -117,6 +120,7 @@ __device__ void recompute(const WalkArgs& a, int b, int kb, int R, int C, int nr
   }
   const int nthreads = (nr + TR - 1) / TR;
   const int steps = nc + nthreads - 1;
+  ANY_CHECK(nc <= KC_MAX && nr <= NT * TR && (R == 0 || b - 1 < a.nrowck));
   for (int c = t; c < nc; c += NT) {
     const int jj = C + 1 + c;
     top[c] = R == 0 ? make_int2(h_row0(a, jj), NEGI) : a.rowck[(size_t)(b - 1) * (a.m + 1) + jj];
@@ -162,6 +166,7 @@ __device__ void recompute(const WalkArgs& a, int b, int kb, int R, int C, int nr
         if (a.kind == KLOCAL && H <= 0) { H = 0; src = 3; }  // nu = 0 wins ties at 0 (R9)
         word |= (src | (eext << 2) | (fext << 3)) << (8 * (r & 3));
         if ((r & 3) == 3 || r == TR - 1) {
+          ANY_CHECK(((size_t)k * NT + t) * ((TR + 3) / 4) * 4 < a.slot_bytes);
           reinterpret_cast<uint32_t*>(dirs)[((size_t)k * NT + t) * ((TR + 3) / 4) + (r >> 2)] = word;
           word = 0;
         }
@@ -348,6 +353,7 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
       int ci = i, cj = j, st = sh_st;
       auto dir_at = [&](int ii, int jj) -> uint32_t {  // direction byte of cell (ii, jj)
         const int rr = ii - R - 1, tt = rr / TR, step = (jj - C - 1) + tt;
+        ANY_CHECK(rr >= 0 && step >= 0 && ((size_t)step * NT + tt) * wpt_bytes < a.slot_bytes);
         return dirs[((size_t)step * NT + tt) * wpt_bytes + (rr % TR)];
       };
       bool done = false;
@@ -494,6 +500,8 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
   }
   a.slots = (uint8_t*)slotb.p;
   a.slot_bytes = scratch;
+  a.nrowck = (ck.S - 1) / ck.ck_every;
+  a.ncolck = (int)((m - 1) >> ck.kc_shift);
   a.sync = (int*)syncb.p;
   a.slot_job = helpers > 0 ? (int*)syncb.p + 4 : nullptr;
   a.jobs = (int2*)jobb.p;
