@@ -535,7 +535,10 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
       const int64_t cap_words = std::max<int64_t>(ctx->tb_scratch_bytes / esz, block_words);
       int64_t chunk = std::max<int64_t>(1, cap_words / block_words);
       chunk = std::min<int64_t>(chunk, nslot[v]);
-      CK(dirs.ensure((size_t)(chunk * block_words) * esz + 16));
+      // the G = 32 / L slots of a warp share one interleaved block (fill_kernel.cuh): the
+      // last warp of a launch owns a whole block even when it holds fewer slots
+      const int64_t gw = 32 / d.L;
+      CK(dirs.ensure((size_t)(((chunk + gw - 1) / gw) * gw * block_words) * esz + 16));
       fa.dirs = dirs.as<uint32_t>();
       fa.dir_block_words = block_words;
       fa.tb8 = tb8;

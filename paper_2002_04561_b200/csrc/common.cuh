@@ -178,13 +178,14 @@ struct Slot {
 
 // Per-pair traceback bookkeeping written by the fill kernel, read by the walk kernel.
 struct TbInfo {
-  int64_t dir_base;  // word offset of the pair's slot block in the direction buffer
-  int32_t slot_M;    // columns of the slot (max m of its pairs)
+  int64_t dir_base;  // element offset of the pair's warp-slot block in the H store
+  int32_t slot_M;    // columns of the warp-slot (max m over the warp's slots)
   int32_t ns;        // strips
   int16_t half, L, R, P;
   int32_t pad;       // top padding rows of this pair (0 for global)
   int32_t score;
   int32_t end_i, end_j;
+  int32_t grp;       // lane group of the slot within its warp (interleaved store)
 };
 
 }  // namespace anyseq

@@ -149,8 +149,11 @@ __global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) 
 #pragma unroll
     for (int X = 0; X < PP; ++X) pad[X] = (KIND == KGLOBAL) ? 0 : npad - nn[X];
     uint4* scr = a.strip_scratch + (int64_t)(warp * G + g) * a.strip_stride;
+    // traceback H store: one block per warp-slot, the G slots of the warp interleaved at
+    // lane-group granularity (a warp's store covers G x L contiguous elements: whole
+    // 32-byte sectors for every element size)
     int64_t dbase = 0;
-    if (TB && valid) dbase = (int64_t)sidx * a.dir_block_words;
+    if (TB) dbase = (int64_t)ws * G * a.dir_block_words;
 
     // column selectors of this slot in a 512-entry shared ring: columns [0, 384) now, then
     // 128 more every 128 steps (a lane at step k reads column k - t, t < L <= 8)
@@ -361,9 +364,11 @@ __global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) 
         // (R7-R9) from H alone (walk_kernel).  Storing H instead of direction
         // bits keeps the fill at the score-only instruction count.
         if (TB && valid && sact && k < M + L - 1) {
-          // word ((st * DK + k - r + R - 1) * R + r) * L + t: diagonal-major per lane (the
-          // walk's diagonal runs are sequential), lanes of a group contiguous (32 B/row)
-          const int64_t w0 = (((int64_t)st * (M + L - 1 + R - 1) + k + R - 1) * R) * L + t;
+          // element (((st * DK + k - r + R - 1) * R + r) * G + g) * L + t, DK from the warp's
+          // widest slot: diagonal-major (the walk's diagonal runs are sequential), the lane
+          // groups of the warp side by side, so one store instruction writes G * L
+          // contiguous elements (128 B full store, 64 B / 32 B low-byte store)
+          const int64_t w0 = ((((int64_t)st * (Mw + L - 1 + R - 1) + k + R - 1) * R) * G + g) * L + t;
           if (a.tb8) {
             // 1 B per cell: the low byte of H of each alignment (both halves of an s16x2
             // register in one 16-bit store); same element order, elements of 2 B (s16x2)
@@ -372,16 +377,16 @@ __global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) 
               uint16_t* bp = reinterpret_cast<uint16_t*>(a.dirs) + dbase + w0;
 #pragma unroll
               for (int r = 0; r < R; ++r)
-                bp[-(int64_t)r * (R - 1) * L] = (uint16_t)prmt((uint32_t)Hq[r], 0u, 0x0020u);
+                bp[-(int64_t)r * (R - 1) * G * L] = (uint16_t)prmt((uint32_t)Hq[r], 0u, 0x0020u);
             } else {
               uint8_t* bp = reinterpret_cast<uint8_t*>(a.dirs) + dbase + w0;
 #pragma unroll
-              for (int r = 0; r < R; ++r) bp[-(int64_t)r * (R - 1) * L] = (uint8_t)Hq[r];
+              for (int r = 0; r < R; ++r) bp[-(int64_t)r * (R - 1) * G * L] = (uint8_t)Hq[r];
             }
           } else {
             uint32_t* wp = a.dirs + dbase + w0;
 #pragma unroll
-            for (int r = 0; r < R; ++r) wp[-(int64_t)r * (R - 1) * L] = (uint32_t)Hq[r];
+            for (int r = 0; r < R; ++r) wp[-(int64_t)r * (R - 1) * G * L] = (uint32_t)Hq[r];
           }
         }
         diag = hin;
@@ -598,7 +603,8 @@ __global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) 
         if (TB) {
           TbInfo ti;
           ti.dir_base = dbase;
-          ti.slot_M = M;
+          ti.slot_M = Mw;
+          ti.grp = g;
           ti.ns = NS;
           ti.half = (int16_t)X;
           ti.L = (int16_t)L;

@@ -359,16 +359,27 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
       bool done = false;
       while (!done && ci > R && cj > C) {
         if (st == 0) {  // H state: a diagonal run, then the first non-DIAG cell
-          const int ii = ci - lane, jj = cj - lane;
-          const bool in = ii > R && jj > C;
-          const uint32_t d = in ? dir_at(ii, jj) : 0xFFu;
-          const uint32_t stopm = __ballot_sync(0xffffffffu, !in || (d & 3) != 0);
-          const int l = stopm ? __ffs(stopm) - 1 : 32;  // cells [0, l) are DIAG
+          // 4 x 32 cells of the diagonal are read at once (independent loads, one L2 round
+          // trip): similar sequences have DIAG runs of hundreds of cells
+          uint32_t dv[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const int ii = ci - lane - 32 * g, jj = cj - lane - 32 * g;
+            dv[g] = (ii > R && jj > C) ? dir_at(ii, jj) : 0xFFu;
+          }
+          int l = 128;
+          uint32_t d = 0;
+#pragma unroll
+          for (int g = 3; g >= 0; --g) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (dv[g] & 3) != 0);
+            if (m) { l = 32 * g + __ffs(m) - 1; d = __shfl_sync(0xffffffffu, dv[g], __ffs(m) - 1); }
+          }
+          // cells [0, l) are DIAG
           if (l > 0 && lane == 0) emit(0, (uint64_t)l);
           ci -= l;
           cj -= l;
-          if (l < 32) {
-            const uint32_t dl = __shfl_sync(0xffffffffu, d, l);
+          if (l < 128) {
+            const uint32_t dl = d;
             const bool inl = (ci > R && cj > C);
             if (inl) {
               const uint32_t src = dl & 3;

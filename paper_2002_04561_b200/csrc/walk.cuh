@@ -13,8 +13,8 @@
 namespace anyseq {
 
 // H(i, j) of a pair from the traceback H store (fill_kernel.cuh, traceback mode): one
-// element per (strip, diagonal d = step - row, row, lane) of the slot -- a diagonal run of
-// the walk reads consecutive 32-byte sectors.  Full store: 32-bit words with both
+// element per (strip, diagonal d = step - row, row, lane group, lane) of the warp-slot -- a
+// diagonal run of the walk steps back G * L elements per cell.  Full store: 32-bit words with both
 // alignments of an s16x2 slot in their halves (global/semi s16x2 values biased by 2^14).
 // Low-byte store (tb8): 16-bit elements holding the low byte of each alignment's H (s16x2)
 // or bytes (s32); the walk rebuilds exact values from neighbour differences (see below).
@@ -37,8 +37,9 @@ __device__ __forceinline__ int hraw(const DevParams& P, const uint32_t* __restri
   }
   const int k = (j - 1) + tt;                 // wavefront step of the cell
   const int DK = ti.slot_M + L - 1 + R - 1;   // diagonal index range per strip
+  const int G = 32 / L;                        // lane groups per warp (interleaved)
   const int64_t w =
-      ti.dir_base + ((((int64_t)st * DK + (k - r + R - 1)) * R + r) * L + tt);
+      ti.dir_base + (((((int64_t)st * DK + (k - r + R - 1)) * R + r) * G + ti.grp) * L + tt);
   if (tb8) {
     if (ti.P == 2)
       return (int)((__ldg(reinterpret_cast<const unsigned short*>(dirs) + w) >> (8 * ti.half)) & 0xffu);

@@ -3,11 +3,13 @@ mutated genome pairs (C4 variant a shape) and prints one JSON line per size: wal
 the call, the matrix cells n*m and GCUPS = n*m / time (the paper's long-traceback metric,
 Fig. 5a; Hirschberg relaxes about 2*n*m cells in its passes plus the leaves)."""
 import json
+import os
 import sys
 import time
 
-import paper_2002_04561_b200 as A
-from synth import c4_genomes
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2002_04561_b200 as A  # noqa: E402
+from synth import c4_genomes  # noqa: E402
 
 
 def main(sizes):
