@@ -53,8 +53,12 @@ __device__ __forceinline__ uint32_t imad_add(uint32_t x, uint32_t one, uint32_t 
 #ifndef FILL_MINB_SCORE
 #define FILL_MINB_SCORE 4  // resident 128-thread blocks per SM the score kernels are built for
 #endif
+#ifndef FILL_MINB_TBWIDE
+#define FILL_MINB_TBWIDE 3  // traceback kernels with R > 8 rows per lane: 168 registers, no spills
+#endif
 template <class V, int KIND, int GAP, int L, int R, bool TB, bool POS, int CGE = 0, int CGO = 0>
-__global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) {
+__global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_MINB_SCORE)
+    fill_kernel(FillArgs a) {
   using T = typename V::T;
   constexpr int PP = V::P;
   constexpr int G = 32 / L;
@@ -415,7 +419,35 @@ __global__ void __launch_bounds__(128, FILL_MINB_SCORE) fill_kernel(FillArgs a) 
             cm = V::select_mask(cm, keep, V::splat(0));
             uint32_t pb;
             const T nb = V::bmax(sbest, cm, pb);  // bit: sbest >= cm
-            if ((~pb) & ((1u << PP) - 1u)) {
+            if (PP == 2 && ((~pb) & 3u)) {
+              // the smallest row holding the new maximum, both alignments at once: on a
+              // kept half 0 <= Hq[r] <= cm (local), so e = max(Hq[r] + 1 - cm, 0) is 1 iff
+              // Hq[r] == cm, and key = 64 e + 63 - r is largest for the first such row
+              // (one DPX op + one IMAD per row instead of a compare-select per row and half)
+              const T om = __vsub2(V::splat(1), cm);
+              const uint32_t k64 = one << 6;
+              T kmax = 0;
+#pragma unroll
+              for (int r = 0; r < R; r += 2) {
+                const T ka = (T)imad_add((uint32_t)__viaddmax_s16x2(Hq[r], om, 0u), k64,
+                                         (uint32_t)(63 - r) * 0x10001u);
+                if (r + 1 < R) {
+                  const T kb = (T)imad_add((uint32_t)__viaddmax_s16x2(Hq[r + 1], om, 0u), k64,
+                                           (uint32_t)(62 - r) * 0x10001u);
+                  kmax = V::vmax3(kmax, ka, kb);
+                } else {
+                  kmax = V::vmax(kmax, ka);
+                }
+              }
+#pragma unroll
+              for (int X = 0; X < PP; ++X) {
+                if (!((pb >> X) & 1u)) {
+                  sv[X] = V::get(cm, X);
+                  si[X] = ip0 + (63 - (V::get(kmax, X) & 63)) - pad[X] + 1;
+                  sj[X] = col + 1;
+                }
+              }
+            } else if (PP == 1 && ((~pb) & 1u)) {
 #pragma unroll
               for (int X = 0; X < PP; ++X) {
                 if (!((pb >> X) & 1u)) {

@@ -20,6 +20,7 @@ def main():
     s, so = synth.uniform_csr(sm)
     ctx = A.Context([0])
     sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+    ctx.set_option("force_variant", int(os.environ.get("FORCE_VARIANT", "-1")))
     for t8 in modes:
         ctx.set_option("tb8", t8)
         ctx.traceback(sch, q, qo, s, so)
