@@ -16,10 +16,10 @@
 //  * sigma comes from one PRMT per register: per-row query profile bytes sigma(q_i, .)
 //    selected (with sign replication) by a per-column selector built from the subject
 //    symbol(s) -- one instruction for two cells in VS16.
-//  * Cell ops per register: PRMT, VIADDMNMX (E), VIADDMNMX (F), VIMNMX (E|F), VIADDMNMX (H,
-//    .RELU for local: nu = 0) on the integer pipe, and Hop = H - Go - Ge (shared by E below
-//    and F right) as an IMAD on the FMA pipe: VS16 global/semi scores are stored with a
-//    +2^14 bias so that the packed subtraction can never borrow across the halves.
+//  * Cell ops per register: PRMT, VIADDMNMX (E), VIADDMNMX (F), VIMNMX (E|F), VIADDMNMX (H;
+//    local: a 3-input max with the floor nu = 0) on the integer pipe, and Hop = H - Go - Ge
+//    (shared by E below and F right) as an IMAD on the FMA pipe: VS16 scores are stored with
+//    a +2^14 bias so that the packed subtraction can never borrow across the halves.
 //  * H lives in two register arrays used in ping-pong across steps (step k reads HA and
 //    writes HB, step k+1 the reverse), so the diagonal value H(i-1,j-1) never needs a copy.
 //  * Rows longer than one strip are handled strip after strip; the bottom row (H, E) of a
@@ -63,8 +63,10 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
   constexpr int PP = V::P;
   constexpr int G = 32 / L;
   constexpr int HS = L * R;  // strip height
-  // biased VS16 representation (global/semi): stored = value + 2^14
-  constexpr bool BIAS = (PP == 2) && (KIND != KLOCAL);
+  // biased VS16 representation (every kind): stored = value + 2^14, so every H stays above
+  // Go + Ge and Hop = H - Go - Ge is one packed IMAD (FMA pipe) without a borrow between
+  // the halves; local's floor nu = 0 (Eq. 1) becomes the biased zero ZB
+  constexpr bool BIAS = (PP == 2);
   constexpr int B0 = BIAS ? (1 << 14) : 0;
   const int lane = threadIdx.x & 31;
   const int g = lane / L, t = lane % L;
@@ -77,7 +79,6 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
   const DevParams& P = a.P;
   constexpr bool pos = TB || POS;
   constexpr bool FAST = (GAP == GAFFINE);  // reassociated affine recurrence (score and TB)
-  // VS16 local scores are unbiased; their Hop uses VIADD.16x2 (see hop) -- fine.
   const uint32_t one = (uint32_t)a.one;
   constexpr bool SPEC = CGE > 0;
   const int cop = SPEC ? ((GAP == GAFFINE) ? CGO + CGE : CGE)
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
     return V::add(h, NOC);
   };
   auto enc = [&](int v0, int v1) -> T { return V::make(v0 + B0, v1 + B0); };
+  const T ZB = V::splat(B0);  // the local floor (biased zero)
   // H(., m) of every lane at its last column (odd row stride R keeps banks distinct)
   __shared__ uint32_t capbuf[KIND != KLOCAL ? PP : 1][128][KIND != KLOCAL ? R : 1];
   // rarely touched per-lane state lives in shared memory, not in registers
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
       int sv[PP], si[PP], sj[PP];
 #pragma unroll
       for (int X = 0; X < PP; ++X) { sv[X] = 0; si[X] = 0; sj[X] = 0; }
-      T sbest = V::splat(0);
+      T sbest = ZB;
 
       const int K = Mw + L - 1;
       // H(i, 0) of row ip (initial column, P:259 / P:262)
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
             Ff[r] = NEG;  // F(i,0) = -inf
           }
           diag = (KIND == KGLOBAL && ip0 >= 1) ? init_col(ip0 - 1) : enc(0, 0);
-          if (KIND == KLOCAL && !pos) sbest = V::splat(0);
+          if (KIND == KLOCAL && !pos) sbest = ZB;
           if (KIND == KSEMI) {
             best = enc(0, 0);  // H(n,0) = 0 (first row candidate)
 #pragma unroll
@@ -346,7 +348,8 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
             const T sig = V::sigma(p0[r], p1[r], sel);
             Ff[r] = V::addmax(Ff[r], NGE, hop(Hi[r]));
             const T df = V::addmax(hd, sig, Ff[r]);
-            const T h = (KIND == KLOCAL) ? V::vmax_relu(df, e) : V::vmax(df, e);
+            const T h = (KIND != KLOCAL) ? V::vmax(df, e)
+                                         : (BIAS ? V::vmax3(df, e, ZB) : V::vmax_relu(df, e));
             e = V::addmax(e, NGE, hop(df));
             Hq[r] = h;
           }
@@ -356,8 +359,9 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
             const T hd = (r == 0) ? diag : Hi[r - 1];
             const T sig = V::sigma(p0[r], p1[r], sel);
             const T hleft = hop(Hi[r]);  // Hop(i, j-1), recomputed on the FMA pipe
-            const T tm = V::vmax(hup, hleft);  // Eqs. (2)-(3): H_up - g, H_left - g
-            const T h = (KIND == KLOCAL) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
+            // Eqs. (2)-(3): H_up - g, H_left - g (biased local: and the floor)
+            const T tm = (KIND == KLOCAL && BIAS) ? V::vmax3(hup, hleft, ZB) : V::vmax(hup, hleft);
+            const T h = (KIND == KLOCAL && !BIAS) ? V::addmax_relu(hd, sig, tm) : V::addmax(hd, sig, tm);
             Hq[r] = h;
             hup = hop(h);
           }
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
 #pragma unroll
               for (int X = 0; X < PP; ++X) keep |= (uni || col < mm[X] ? 1u : 0u) << X;
             }
-            cm = V::select_mask(cm, keep, V::splat(0));
+            cm = V::select_mask(cm, keep, ZB);
             uint32_t pb;
             const T nb = V::bmax(sbest, cm, pb);  // bit: sbest >= cm
             if (PP == 2 && ((~pb) & 3u)) {
@@ -442,7 +446,7 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
 #pragma unroll
               for (int X = 0; X < PP; ++X) {
                 if (!((pb >> X) & 1u)) {
-                  sv[X] = V::get(cm, X);
+                  sv[X] = dec(cm, X);
                   si[X] = ip0 + (63 - (V::get(kmax, X) & 63)) - pad[X] + 1;
                   sj[X] = col + 1;
                 }
@@ -597,7 +601,7 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
 #pragma unroll
     for (int X = 0; X < PP; ++X) {
       if (KIND == KLOCAL) {
-        int v = pos ? bv[X] : V::get(best, X), i = bi[X], j = bj[X];
+        int v = pos ? bv[X] : dec(best, X), i = bi[X], j = bj[X];
 #pragma unroll
         for (int o = L / 2; o > 0; o >>= 1) {
           const int v2 = __shfl_xor_sync(0xffffffffu, v, o, L);

@@ -15,7 +15,7 @@ namespace anyseq {
 // H(i, j) of a pair from the traceback H store (fill_kernel.cuh, traceback mode): one
 // element per (strip, diagonal d = step - row, row, lane group, lane) of the warp-slot -- a
 // diagonal run of the walk steps back G * L elements per cell.  Full store: 32-bit words with both
-// alignments of an s16x2 slot in their halves (global/semi s16x2 values biased by 2^14).
+// alignments of an s16x2 slot in their halves (s16x2 values biased by 2^14).
 // Low-byte store (tb8): 16-bit elements holding the low byte of each alignment's H (s16x2)
 // or bytes (s32); the walk rebuilds exact values from neighbour differences (see below).
 // Row 0 / column 0 are the initial values of P:259-264, always exact.
@@ -48,7 +48,7 @@ __device__ __forceinline__ int hraw(const DevParams& P, const uint32_t* __restri
   const uint32_t word = dirs[w];
   if (ti.P == 2) {
     const int v = (int)(int16_t)(uint16_t)(ti.half ? (word >> 16) : (word & 0xffffu));
-    return P.kind == KLOCAL ? v : v - (1 << 14);
+    return v - (1 << 14);  // every kind's s16x2 values carry the +2^14 bias
   }
   return (int)word;
 }
