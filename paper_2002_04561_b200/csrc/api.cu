@@ -1599,8 +1599,14 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
     LongResult r;
     std::string err;
     uint64_t launches = 0;
+    const auto tl0 = std::chrono::steady_clock::now();
+    auto tl_ms = [&]() {
+      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count();
+    };
     int rc = run_long(one, dp, q, n, s, m, ctx->long_opt, &r, &err, &launches, &ck);
     ctx->launches += launches;
+    if (ctx->timing >= 2)
+      fprintf(stderr, "[tb-long] pass done %.1f ms (kernel %.1f ms)\n", tl_ms(), r.kernel_ms);
     if (rc == ANYSEQ_E_UNSUPPORTED && prm->gap == ANYSEQ_GAP_LINEAR) {
       ctx->tb_method = 2;
       return run_traceback_long_hirschberg(ctx, prm, q, n, s, m, out, cigar, cap, used);
@@ -1619,7 +1625,11 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
     launches = 0;
     int64_t tiles = 0, hits = 0;
     rc = run_long_traceback(ld, dp, sig, ck, r.end_i, r.end_j, (int64_t)n, (int64_t)m, &ops, &bi,
-                            &bj, &wms, &err, &launches, (int)ctx->walk_helpers, &tiles, &hits);
+                            &bj, &wms, &err, &launches, (int)ctx->walk_helpers, &tiles, &hits,
+                            ctx->timing >= 2);
+    if (ctx->timing >= 2)
+      fprintf(stderr, "[tb-long] walk done %.1f ms (kernel %.1f ms, tiles %lld)\n", tl_ms(), wms,
+              (long long)tiles);
     ctx->tb_tiles = (double)tiles;
     ctx->tb_hits = (double)hits;
     ctx->launches += launches;

@@ -426,9 +426,6 @@ cudaError_t get_buf(Buf& b, LongWs* ws, int slot, size_t bytes) {
   b.own = true;
   return cudaMalloc(&b.p, bytes < 256 ? 256 : bytes);
 }
-enum { WS_QA, WS_SA, WS_QC, WS_SC, WS_SUM, WS_FLG, WS_OFF, WS_ROWBUF, WS_PROG, WS_TICKET,
-       WS_ABORT, WS_CB, WS_BPTR, WS_FPTR, WS_BCOL, WS_FLAGS, WS_PARTS, WS_PROF, WS_KEY,
-       WS_ROWCK, WS_COLCK };
 #define LK(call)                                                      \
   do {                                                                \
     cudaError_t e_ = (call);                                          \

@@ -23,8 +23,14 @@ struct LongOptions {
 // Device buffers of the long-pair path kept across calls (a context owns one per device):
 // slot k grows on demand, so repeated calls skip cudaMalloc / cudaFree of the row buffer,
 // the boundary columns and the traceback checkpoints (tens of GB for 1 Mbp pairs).
+enum { WS_QA, WS_SA, WS_QC, WS_SC, WS_SUM, WS_FLG, WS_OFF, WS_ROWBUF, WS_PROG, WS_TICKET,
+       WS_ABORT, WS_CB, WS_BPTR, WS_FPTR, WS_BCOL, WS_FLAGS, WS_PARTS, WS_PROF, WS_KEY,
+       WS_ROWCK, WS_COLCK,
+       // long traceback walk (long_tb.cu)
+       WS_TB_SCRATCH, WS_TB_OPS, WS_TB_OUT, WS_TB_SLOTS, WS_TB_SYNC, WS_TB_JOBS, WS_COUNT };
+
 struct LongWs {
-  static constexpr int kSlots = 24;
+  static constexpr int kSlots = WS_COUNT;
   void* p[kSlots] = {};
   size_t cap[kSlots] = {};
   cudaError_t get(int slot, size_t bytes, void** out) {

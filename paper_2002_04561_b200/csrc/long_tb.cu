@@ -18,7 +18,9 @@
 // slot (one barrier per step).  Direction bytes go to a global scratch in step-major order
 // (word (step * 256 + t) holds the thread's TR rows), so every step's stores are one
 // coalesced row of words and the walk reads a diagonal run as consecutive words.
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -441,9 +443,17 @@ __global__ void __launch_bounds__(NT) tile_walk_kernel(WalkArgs a) {
   }
 }
 
+// a walk buffer: from the context's persistent workspace when there is one (repeated calls
+// skip cudaMalloc / cudaFree), else allocated for this call
 struct DBuf {
   void* p = nullptr;
-  ~DBuf() { if (p) cudaFree(p); }
+  bool own = false;
+  cudaError_t get(LongWs* ws, int slot, size_t bytes) {
+    if (ws) return ws->get(slot, bytes, &p);
+    own = true;
+    return cudaMalloc(&p, bytes);
+  }
+  ~DBuf() { if (own && p) cudaFree(p); }
 };
 
 }  // namespace
@@ -461,7 +471,13 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
                        const LongCkpt& ck, int64_t end_i, int64_t end_j, int64_t n, int64_t m,
                        std::vector<uint32_t>* ops, int64_t* begin_i, int64_t* begin_j,
                        double* walk_ms, std::string* err, uint64_t* launches, int walk_helpers,
-                       int64_t* tiles, int64_t* hits) {
+                       int64_t* tiles, int64_t* hits, bool trace) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (trace)
+      fprintf(stderr, "[tb-walk] %s %.1f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  };
   TK(cudaSetDevice(dev.id));
   cudaStream_t st = dev.stream;
   ops->clear();
@@ -495,19 +511,19 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
   a.end_j = (int)end_j;
   const size_t scratch = ((size_t)(1 << ck.kc_shift) + NT) * NT * (((TR + 3) / 4) * 4);
   DBuf sb, ob, outb, slotb, syncb, jobb;
-  TK(cudaMalloc(&sb.p, scratch));
+  TK(sb.get(dev.ws, WS_TB_SCRATCH, scratch));
   const uint64_t cap = (uint64_t)(n + m + 2);
-  TK(cudaMalloc(&ob.p, cap * sizeof(uint32_t)));
-  TK(cudaMalloc(&outb.p, 8 * sizeof(unsigned long long)));
+  TK(ob.get(dev.ws, WS_TB_OPS, cap * sizeof(uint32_t)));
+  TK(outb.get(dev.ws, WS_TB_OUT, 8 * sizeof(unsigned long long)));
   TK(cudaMemsetAsync(outb.p, 0, 8 * sizeof(unsigned long long), st));
   // helper CTAs: whole-tile recomputes of the predicted next tiles (option walk_helpers)
   const int helpers = std::max(0, std::min(walk_helpers, dev.num_sms - 1));
   if (helpers > 0) {
-    TK(cudaMalloc(&slotb.p, (size_t)NSLOT * scratch));
-    TK(cudaMalloc(&syncb.p, (4 + NSLOT) * sizeof(int)));
+    TK(slotb.get(dev.ws, WS_TB_SLOTS, (size_t)NSLOT * scratch));
+    TK(syncb.get(dev.ws, WS_TB_SYNC, (4 + NSLOT) * sizeof(int)));
     TK(cudaMemsetAsync(syncb.p, 0, 4 * sizeof(int), st));
     TK(cudaMemsetAsync((int*)syncb.p + 4, 0xFF, NSLOT * sizeof(int), st));
-    TK(cudaMalloc(&jobb.p, (size_t)JMAX * sizeof(int2)));
+    TK(jobb.get(dev.ws, WS_TB_JOBS, (size_t)JMAX * sizeof(int2)));
   }
   a.slots = (uint8_t*)slotb.p;
   a.slot_bytes = scratch;
@@ -520,6 +536,7 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
   a.ops = (uint32_t*)ob.p;
   a.ops_cap = cap;
   a.out = (unsigned long long*)outb.p;
+  mark("buffers");
   cudaEvent_t e0, e1;
   TK(cudaEventCreate(&e0));
   TK(cudaEventCreate(&e1));
@@ -549,6 +566,7 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
   unsigned long long out[8];
   TK(cudaMemcpyAsync(out, outb.p, sizeof(out), cudaMemcpyDeviceToHost, st));
   TK(cudaStreamSynchronize(st));
+  mark("kernel synced");
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
@@ -562,6 +580,7 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
   if (out[0]) TK(cudaMemcpy(ops->data(), ob.p, out[0] * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   // walk order is end -> begin: reverse into alignment order
   for (size_t x = 0, y = ops->size(); x + 1 < y; ++x, --y) std::swap((*ops)[x], (*ops)[y - 1]);
+  mark("ops copied");
   *begin_i = (int64_t)out[1];
   *begin_j = (int64_t)out[2];
   if (tiles) *tiles = (int64_t)out[3];

@@ -17,6 +17,7 @@ int run_long_traceback(const LongDevice& dev, const DevParams& P, const int8_t s
                        const LongCkpt& ck, int64_t end_i, int64_t end_j, int64_t n, int64_t m,
                        std::vector<uint32_t>* ops, int64_t* begin_i, int64_t* begin_j,
                        double* walk_ms, std::string* err, uint64_t* launches,
-                       int walk_helpers = 96, int64_t* tiles = nullptr, int64_t* hits = nullptr);
+                       int walk_helpers = 96, int64_t* tiles = nullptr, int64_t* hits = nullptr,
+                       bool trace = false);
 
 }  // namespace anyseq
