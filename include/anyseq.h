@@ -129,25 +129,32 @@ anyseq_status anyseq_traceback(anyseq_ctx* ctx, const anyseq_params* params,
 
 /* Long-pair score-only alignment (tiled wavefront) of host
    sequences q[0..n) and s[0..m).  out receives score and end cell (cigar_len = 0).
-   32-bit arithmetic; ANYSEQ_E_UNSUPPORTED if the score range could exceed it (R11);
-   ANYSEQ_E_TIMEOUT if a bounded inter-warp wait expires (device state stays valid). */
+   Every kind and gap model runs the 16-bit differential kernel (reading
+   R21/R24: values relative to a per-warp frame, exact by the Lipschitz bound) unless the
+   subject holds N or option "long_narrow" = 0; those take the 32-bit kernel.
+   ANYSEQ_E_UNSUPPORTED if the score range could exceed int32 (R11); ANYSEQ_E_TIMEOUT if a
+   bounded inter-warp wait expires (device state stays valid). */
 anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, const char* q,
                                 uint64_t n, const char* s, uint64_t m, anyseq_alignment* out);
 
 /* Long-pair alignment WITH traceback in linear space (the paper's long
-   genome traceback workload, Fig. 5a).  Hirschberg's divide and conquer:
-   GPU forward / reverse last-row score passes (Eqs. (1)-(3)) cut the matrix at
-   the middle row of every sub-problem until a piece has <= 2^20 cells; the pieces run as
-   one batched global traceback (anyseq_traceback's kernels) and their CIGARs are joined.
-   LOCAL and SEMIGLOBAL first find the end cell with anyseq_align_long and the begin cell
-   with an anchored reverse pass (best over all cells, resp. over row 0 / column 0).  Device memory O(n + m); host inputs as anyseq_align_long.
+   genome traceback workload, Fig. 5a), every kind, linear and affine gaps.
+   Default method: one forward pass of the 16-bit long kernel (Eqs. (1)-(5),
+   P:224-255) that also writes checkpoints -- (H, E) of every ck_every-th strip's last row
+   and (H, F) of every 2^kc_shift-th column -- within the "tb_ckpt_bytes" budget (default:
+   a share of free device memory); then a walk kernel that starts at the optimum's cell,
+   recomputes one checkpoint tile at a time in shared memory (helper CTAs recompute the
+   predicted next tiles ahead of it) and re-derives every decision of the relax listing
+   (readings R7-R9) -- the same tie rules as anyseq_traceback, so the CIGAR is
+   the oracle's bit for bit.  Fallback when no 16-bit pass applies (subject with N, range
+   guard): Hirschberg's divide and conquer with GPU last-row passes for linear gaps.
    out receives score, begin/end cells, cigar_offset 0 and cigar_len; cigar[] (host)
-   receives the ops.  Among co-optimal paths the one returned may differ from
-   anyseq_traceback's tie rule (the split takes the smallest crossing column); the
-   score, end cell (LOCAL) and the path's rescored value are what is fixed.
-   Errors: ANYSEQ_E_UNSUPPORTED for affine gaps (Myers-Miller, not built) and when the
-   score range could exceed int32; ANYSEQ_E_CAPACITY with *cigar_used = words required;
-   ANYSEQ_E_BADSEQ for a byte outside ACGTNacgtn. */
+   receives the ops.  Host inputs as anyseq_align_long.
+   Errors: ANYSEQ_E_UNSUPPORTED for affine gaps on the fallback path and when the score
+   range could exceed int32; ANYSEQ_E_NOMEM if even the coarsest checkpoint geometry
+   exceeds the budget; ANYSEQ_E_CAPACITY with *cigar_used = words required;
+   ANYSEQ_E_BADSEQ for a byte outside ACGTNacgtn; ANYSEQ_E_TIMEOUT if a bounded wait
+   expires. */
 anyseq_status anyseq_traceback_long(anyseq_ctx* ctx, const anyseq_params* params, const char* q,
                                     uint64_t n, const char* s, uint64_t m, anyseq_alignment* out,
                                     uint32_t* cigar, uint64_t cigar_capacity,
@@ -166,9 +173,12 @@ uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx);
    clears them.  "timing" = 2 also prints a per-chunk event timeline of the host API to
    stderr (debug).  After anyseq_align_long: "long_kernel_ms" (device time of the long
    kernel, max over devices) and "long_narrow" (1 if the 16-bit differential kernel ran).
-   After anyseq_traceback_long: "tb_pass_ms" (device time of the Hirschberg last-row
-   passes, summed over levels), "tb_pass_cells" (cells those passes relaxed) and
-   "tb_leaf_ms" (host time of the batched leaf traceback).
+   After anyseq_traceback_long: "tb_method" (1 checkpoints, 2 Hirschberg), "tb_pass_ms"
+   (device time of the forward pass; Hirschberg: of the last-row passes summed over
+   levels), "tb_pass_cells" (cells those passes relaxed), "tb_walk_ms" (device time of the
+   walk kernel), "tb_ckpt_bytes", "tb_tiles" / "tb_hits" (tiles walked / found
+   precomputed by the helper CTAs) and "tb_leaf_ms" (Hirschberg: host time of the batched
+   leaf traceback).
    "h2d_bytes" / "d2h_bytes": bytes the host API copied host -> device (sequences as
    2-bit codes or ASCII, offsets) and device -> host (results) since the last reset.
    Returns ANYSEQ_E_INVALID for unknown names. */
@@ -185,7 +195,8 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
      "pack2_percent"     share (by bytes) of the chunks that are packed; the rest go up as
                          ASCII DMA in parallel (0 = 100, the default)
      "tb_scratch_bytes"  traceback: device bytes of the per-cell H store per fill/walk
-                         chunk (default 16 GiB; 2 B per cell for s16x2 slots)
+                         chunk (default 16 GiB; 1 B per cell with "tb8", else 2 B per cell
+                         for s16x2 slots and 4 B for s32)
      "allow16"           0 forces 32-bit arithmetic (debug); "force_variant" (debug)
      "long_strips"       long pairs on one device: column passes (0 = automatic from the
                          round count; > 0 also exercises the multi-GPU boundary protocol)
