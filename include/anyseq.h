@@ -208,6 +208,11 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
      "long_band_rows"    long pairs, rows per warp task: 32-bit kernel 512 (default) or
                          384; 16-bit kernel 1024 (default), 768 or 512
      "long_sleep_ns"     long pairs (16-bit kernel): back-off of the row hand-off poll
+     "long_spin_limit"   long pairs: poll iterations (each with a short back-off) before a
+                         bounded wait raises the abort flag -> ANYSEQ_E_TIMEOUT (default
+                         2^28; <= 0 restores it)
+     "long_stall_task"   fault injection (tests): the warp that draws this task index skips
+                         it, so every task depending on it must time out (default -1)
      "tb_leaf_cells"     long traceback, Hirschberg fallback: recursion stops at <= this
                          many cells per sub-problem (default 2^20)
      "tb_ckpt_bytes"     long traceback: device memory budget of the checkpoints (default

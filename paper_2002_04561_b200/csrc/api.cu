@@ -25,6 +25,7 @@
 #include "long.h"
 #include "hirschberg.h"
 #include "hostpack.h"
+#include "nvtx.h"
 #include "long_tb.h"
 
 using namespace anyseq;
@@ -312,6 +313,7 @@ struct DeviceJob {
 
 anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, DeviceJob& J,
                          uint32_t* d_cigar_out_or_null, uint64_t cigar_cap) {
+  NvtxRange nvtx(J.tb ? "enqueue traceback chunk" : "enqueue score chunk");
   cudaStream_t st = D.stream;
   const uint64_t B = J.B;
   const DevParams P = dev_params(prm);
@@ -762,6 +764,7 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
   anyseq_alignment* h_al =
       stage_a ? (anyseq_alignment*)((char*)D.h_stage.p + st_a_off) - k0 : aln;
   auto copy_out = [&](int c) {  // chunk c's results are complete on the host side
+    NvtxRange nvtx("copy out chunk");
     const uint64_t a0 = cb[c], B = cb[c + 1] - a0;
     if (stage_s) memcpy(scores + a0, h_sc + a0, B * 4);
     if (stage_a) memcpy(aln + a0, h_al + a0, B * sizeof(anyseq_alignment));
@@ -846,6 +849,7 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
         uint8_t* hp = (uint8_t*)D.h_pack[slot].p;
         bool ok2 = false;
         const double tp0 = ms_since();
+        NvtxRange nvtx("pack2 chunk");
         try {
           ok2 = pool->pack2(b->q + q0, b->q_off[cb[c + 1]] - q0, hp) &&
                 pool->pack2(b->s + s0, b->s_off[cb[c + 1]] - s0, hp + qb);
@@ -1603,7 +1607,11 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
     auto tl_ms = [&]() {
       return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl0).count();
     };
-    int rc = run_long(one, dp, q, n, s, m, ctx->long_opt, &r, &err, &launches, &ck);
+    int rc;
+    {
+      NvtxRange nvtx("checkpointed forward pass");
+      rc = run_long(one, dp, q, n, s, m, ctx->long_opt, &r, &err, &launches, &ck);
+    }
     ctx->launches += launches;
     if (ctx->timing >= 2)
       fprintf(stderr, "[tb-long] pass done %.1f ms (kernel %.1f ms)\n", tl_ms(), r.kernel_ms);
@@ -1624,6 +1632,7 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
     double wms = 0;
     launches = 0;
     int64_t tiles = 0, hits = 0;
+    NvtxRange nvtx_walk("checkpoint tile walk");
     rc = run_long_traceback(ld, dp, sig, ck, r.end_i, r.end_j, (int64_t)n, (int64_t)m, &ops, &bi,
                             &bj, &wms, &err, &launches, (int)ctx->walk_helpers, &tiles, &hits,
                             ctx->timing >= 2);
@@ -1776,6 +1785,7 @@ anyseq_status anyseq_align_batch(anyseq_ctx* ctx, const anyseq_params* params,
                                  anyseq_alignment* ends) {
   if (!ctx) return ANYSEQ_E_INVALID;
   return abi_guard(ctx, [&]() -> anyseq_status {
+    NvtxRange nvtx("anyseq_align_batch");
     anyseq_status s = validate_params(ctx, params);
     if (s != ANYSEQ_OK) return s;
     if ((s = check_batch_host(ctx, batch)) != ANYSEQ_OK) return s;
@@ -1790,6 +1800,7 @@ anyseq_status anyseq_traceback(anyseq_ctx* ctx, const anyseq_params* params,
                                uint64_t cigar_capacity, uint64_t* cigar_used) {
   if (!ctx) return ANYSEQ_E_INVALID;
   return abi_guard(ctx, [&]() -> anyseq_status {
+    NvtxRange nvtx("anyseq_traceback");
     anyseq_status s = validate_params(ctx, params);
     if (s != ANYSEQ_OK) return s;
     if ((s = check_batch_host(ctx, batch)) != ANYSEQ_OK) return s;
@@ -1808,6 +1819,7 @@ anyseq_status anyseq_align_batch_device(anyseq_ctx* ctx, const anyseq_params* pa
                                         anyseq_alignment* d_ends, void* stream) {
   if (!ctx) return ANYSEQ_E_INVALID;
   return abi_guard(ctx, [&]() -> anyseq_status {
+    NvtxRange nvtx("anyseq_align_batch_device");
     anyseq_status s = validate_params(ctx, params);
     if (s != ANYSEQ_OK) return s;
     if (!d_batch) return fail(ctx, ANYSEQ_E_INVALID, "batch is NULL");
@@ -1902,6 +1914,11 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
     if (n == "long_start_lag") { ctx->long_opt.start_lag = (int)value; return ANYSEQ_OK; }
     if (n == "long_sleep_ns") { ctx->long_opt.sleep_ns = (int)value; return ANYSEQ_OK; }
     if (n == "long_narrow") { ctx->long_opt.narrow = (int)value; return ANYSEQ_OK; }
+    if (n == "long_spin_limit") {
+      ctx->long_opt.spin_limit = value > 0 ? (long long)value : (1ll << 28);
+      return ANYSEQ_OK;
+    }
+    if (n == "long_stall_task") { ctx->long_opt.stall_task = (int)value; return ANYSEQ_OK; }
     if (n == "long_chunk_cols") { ctx->long_opt.chunk_cols = (int)value; return ANYSEQ_OK; }
     return fail(ctx, ANYSEQ_E_INVALID, "unknown option %s", name);
   });
@@ -1911,6 +1928,7 @@ anyseq_status anyseq_align_long(anyseq_ctx* ctx, const anyseq_params* params, co
                                 uint64_t n, const char* s, uint64_t m, anyseq_alignment* out) {
   if (!ctx) return ANYSEQ_E_INVALID;
   return abi_guard(ctx, [&]() -> anyseq_status {
+    NvtxRange nvtx("anyseq_align_long");
     anyseq_status st = validate_params(ctx, params);
     if (st != ANYSEQ_OK) return st;
     if (!out) return fail(ctx, ANYSEQ_E_INVALID, "out is NULL");
@@ -1949,6 +1967,7 @@ anyseq_status anyseq_traceback_long(anyseq_ctx* ctx, const anyseq_params* params
                                     uint64_t* cigar_used) {
   if (!ctx) return ANYSEQ_E_INVALID;
   return abi_guard(ctx, [&]() -> anyseq_status {
+    NvtxRange nvtx("anyseq_traceback_long");
     anyseq_status st = validate_params(ctx, params);
     if (st != ANYSEQ_OK) return st;
     if (cigar_used) *cigar_used = 0;

@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(128) long_kernel(LongArgs a) {
     task = __shfl_sync(0xffffffffu, task, 0);
     if (task >= a.S * a.g_count) break;
     if (*(volatile int*)a.abort_flag) break;
+    if (task == a.stall_task) continue;  // fault injection (option long_stall_task)
     const long long task_t0 = (a.prof && t == 0) ? clock64() : 0;
     // column-strip major: task (s, g) waits on (s-1, g) (row hand-off) and (s, g-1) (left
     // edge, finished a whole pass earlier) -- both lower tickets held by resident warps
@@ -768,7 +769,8 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
       LK(cudaMemset(D.profbuf.p, 0, 64));
       a.prof = (unsigned long long*)D.profbuf.p;
     }
-    a.spin_limit = 1ll << 28;
+    a.spin_limit = opt.spin_limit;
+    a.stall_task = opt.stall_task;
     LK(cudaEventCreate(&D.e0));
     LK(cudaEventCreate(&D.e1));
     LK(cudaEventRecord(D.e0, gdev[d].stream));

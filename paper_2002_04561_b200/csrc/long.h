@@ -18,6 +18,9 @@ struct LongOptions {
   int profile = 0;         // print wait/task cycle counters to stderr
   int sleep_ns = 64;       // long16: row hand-off poll back-off
   int narrow = 1;          // 1: 16-bit differential kernel where eligible (local affine)
+  long long spin_limit = 1ll << 28;  // poll iterations before a wait gives up (E_TIMEOUT)
+  int stall_task = -1;     // fault injection (tests): the warp that draws this task skips
+                           // it, so the tasks that depend on it must time out
 };
 
 // Device buffers of the long-pair path kept across calls (a context owns one per device):

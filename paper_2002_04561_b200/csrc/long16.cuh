@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
     task = __shfl_sync(0xffffffffu, task, 0);
     if (task >= a.S * a.g_count) break;
     if (*(volatile int*)a.abort_flag) break;
+    if (task == a.stall_task) continue;  // fault injection (option long_stall_task)
     const long long task_t0 = (a.prof && t == 0) ? clock64() : 0;
     const int s = task % a.S;
     const int g = a.g_first + task / a.S;

@@ -47,6 +47,7 @@ struct LongArgs {
   int32_t ck_every, kc_shift;
   unsigned long long* prof;  // optional: [0] cycles waiting, [1] cycles in tasks, [2] tasks
   long long spin_limit;
+  int32_t stall_task;  // fault injection: this task is skipped (-1: none)
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {

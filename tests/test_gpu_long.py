@@ -136,3 +136,36 @@ def test_long_matrix_scoring(ctx):
             r = ctx.align_long(A.Scheme(kind, gap, 0, 0, go, 1, matrix=m), q, s)
             o = O.score_rolling(O.Scheme(kind, gap, 0, 0, go, 1, matrix=m), q, s)
             assert (r["score"], r["q_end"], r["s_end"]) == (o.score, o.q_end, o.s_end), (kind, gap)
+
+
+@pytest.mark.parametrize("narrow", [1, 0])
+def test_long_stalled_task_times_out(ctx, narrow):
+    """Fault injection (every spin-wait bounded -> E_TIMEOUT): a warp skips one
+    row-strip task, the tasks that depend on it exhaust their poll bound, the call returns
+    ANYSEQ_E_TIMEOUT (score-only and traceback), and the same context then aligns
+    correctly (C4 variant c closed form)."""
+    import paper_2002_04561_b200 as A
+    from synth import c4_genomes
+    g1, g2 = c4_genomes(300_000, "c", seed=4)
+    sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+    ctx.set_option("long_narrow", narrow)
+    try:
+        ctx.set_option("long_spin_limit", 1 << 14)
+        ctx.set_option("long_stall_task", 2)
+        with pytest.raises(A.AnyseqError) as e:
+            ctx.align_long(sch, g1, g2)
+        assert e.value.status_name == "E_TIMEOUT"
+        if narrow:
+            with pytest.raises(A.AnyseqError) as e:
+                ctx.traceback_long(sch, g1, g2)
+            assert e.value.status_name == "E_TIMEOUT"
+    finally:
+        ctx.set_option("long_stall_task", -1)
+        ctx.set_option("long_spin_limit", 0)
+    r = ctx.align_long(sch, g1, g2)
+    assert (r["score"], r["q_end"], r["s_end"]) == (600_000, 300_000, 300_000)
+    if narrow:
+        t = ctx.traceback_long(sch, g1, g2)
+        assert (t["score"], t["q_begin"], t["s_begin"]) == (600_000, 0, 0)
+        assert t["cigar"] == [(300_000, "M")]
+    ctx.set_option("long_narrow", 1)
