@@ -85,69 +85,76 @@ struct RunWriter {
 // The walk keeps the exact H of its current cell (starting from the optimum's score) and
 // takes every other value either as a test against an expected value (hmatch) or rebuilt
 // from the adjacent cell just visited (hnear): both exact for either store format.
-static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t* __restrict__ dirs,
-                                       const TbInfo& ti, const uint8_t* qc, const uint8_t* sc,
-                                       uint32_t* ops_out, int32_t* n_ops, int32_t* beg_i,
-                                       int32_t* beg_j, bool tb8) {
+//
+// Decisions, in the relax listing's order (readings R7-R9, R16):
+//   (i, j) on row 0 / column 0: global -> boundary runs (R16), else stop; local H <= 0: stop;
+//   DIAG iff H(i-1, j-1) = H - sigma (tested for up to 8 diagonal cells per batch);
+//   linear: UP iff H(i-1, j) = H + g, else LEFT;
+//   affine: UP iff H = E(i, j) = max_k H(i-k, j) - Go - k Ge, the gap being the LARGEST such k
+//   (extension wins ties, R8), scanned 8 rows per batch while match * min(i-k, j) - Go - k Ge
+//   could still reach H; else LEFT likewise along the row.
+// One thread walks one pair, and the warp's 32 walks are kept convergent: every iteration of
+// the loop is one batch of at most 8 loads in the thread's current mode (diagonal run, linear
+// up-test, up scan, left scan), so threads in different modes only split inside one short
+// batch body instead of running whole walks one after another.
+__device__ __forceinline__ void walk_pair(const DevParams& P, const uint32_t* __restrict__ dirs,
+                                          const TbInfo& ti, const uint8_t* qc, const uint8_t* sc,
+                                          uint32_t* ops_out, int32_t* n_ops, int32_t* beg_i,
+                                          int32_t* beg_j, bool tb8) {
+  constexpr int B = 8;  // cells per batch
+  enum { TOP = 0, LINUP = 1, UP = 2, LEFT = 3, DONE = 4 };
   const int go = P.go, ge = P.ge;
   const int kind = P.kind;
+  const bool linear = P.gap == GLINEAR;
+  const int mt = max(P.smax, 0);
   RunWriter rw{ops_out, 0, 0, 0};
   int i = ti.end_i, j = ti.end_j;
   int h = ti.score;
-  const bool linear = P.gap == GLINEAR;
-  // the exact value of (i2, j2) given the exact value ref of an adjacent cell
-  auto hget = [&](int i2, int j2, int ref) -> int {
-    if (i2 == 0 || j2 == 0) return hbound(P, i2, j2);
-    return hnear(hraw(P, dirs, ti, i2, j2, tb8), ref, tb8);
-  };
-  // does (i2, j2) hold `want`
-  auto hhas = [&](int i2, int j2, int want) -> bool {
-    if (i2 == 0 || j2 == 0) return hbound(P, i2, j2) == want;
-    return hmatch(hraw(P, dirs, ti, i2, j2, tb8), want, tb8);
-  };
-  for (;;) {
-    if (i == 0 || j == 0) {
-      if (kind == KGLOBAL) {  // reading R16: boundary runs
-        rw.push(1u, (uint32_t)i);
-        rw.push(2u, (uint32_t)j);
-        i = 0; j = 0;
+  int mode = TOP;
+  int k0 = 1, ref = 0, kb = 0, hb = 0;  // gap scans: next k, exact value of the last cell, best
+  while (mode != DONE) {
+    if (mode == TOP) {
+      if (i == 0 || j == 0) {
+        if (kind == KGLOBAL) {  // reading R16: boundary runs
+          rw.push(1u, (uint32_t)i);
+          rw.push(2u, (uint32_t)j);
+          i = 0; j = 0;
+        }
+        mode = DONE;
+        continue;
       }
-      break;
-    }
-    if (kind == KLOCAL && h <= 0) break;  // STOP (reading R9)
-    {  // diagonal runs: the next DW diagonal cells are loaded together (memory-level
-       // parallelism for the dependent walk), then verified in order
-      constexpr int DW = 8;
-      const int lim = min(DW, min(i, j));
-      int hv[DW], sg[DW];
-      // the 8 query / subject codes of the run: two aligned 8-byte loads each (the code
-      // buffers carry 16 bytes of slack), instead of 16 scattered byte loads
+      if (kind == KLOCAL && h <= 0) { mode = DONE; continue; }  // STOP (reading R9)
+      // diagonal run: the next B diagonal cells are loaded together, then verified in order
+      const int lim = min(B, min(i, j));
+      int hv[B], sg[B];
       uint64_t vq = 0, vs = 0;
-      const bool vec = i > DW && j > DW;
-      if (vec) {
-        auto load8 = [](const uint8_t* p) -> uint64_t {  // bytes p[0..7], p unaligned
+      const bool vec = i > B && j > B;
+      if (vec) {  // the B query / subject codes: two aligned 8-byte loads each (16 B slack)
+        auto load8 = [](const uint8_t* p) -> uint64_t {
           const uintptr_t a = (uintptr_t)p & ~(uintptr_t)7;
           const uint64_t lo = __ldg((const unsigned long long*)a);
           const uint64_t hi = __ldg((const unsigned long long*)(a + 8));
           const int sh = (int)((uintptr_t)p - a) * 8;
           return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
         };
-        vq = load8(qc + i - (DW - 1));  // byte 7 - l = code of row i - l
-        vs = load8(sc + j - (DW - 1));
+        vq = load8(qc + i - (B - 1));  // byte B-1-l = code of row i - l
+        vs = load8(sc + j - (B - 1));
       }
 #pragma unroll
-      for (int l = 0; l < DW; ++l) {
+      for (int l = 0; l < B; ++l) {
+        hv[l] = 0;
+        sg[l] = 0;
         if (l < lim) {
           const int i2 = i - 1 - l, j2 = j - 1 - l;
           hv[l] = (i2 == 0 || j2 == 0) ? hbound(P, i2, j2) : hraw(P, dirs, ti, i2, j2, tb8);
-          const uint32_t cq = vec ? (uint32_t)(vq >> (8 * (DW - 1 - l))) & 0xffu : qc[i - l];
-          const uint32_t cs = vec ? (uint32_t)(vs >> (8 * (DW - 1 - l))) & 0xffu : sc[j - l];
+          const uint32_t cq = vec ? (uint32_t)(vq >> (8 * (B - 1 - l))) & 0xffu : qc[i - l];
+          const uint32_t cs = vec ? (uint32_t)(vs >> (8 * (B - 1 - l))) & 0xffu : sc[j - l];
           sg[l] = sigma_of(P, cq, cs);
         }
       }
       int taken = 0;
 #pragma unroll
-      for (int l = 0; l < DW; ++l) {
+      for (int l = 0; l < B; ++l) {
         if (l == taken && l < lim && !(kind == KLOCAL && h <= 0)) {
           const int want = h - sg[l];  // DIAG iff H(i-1-l, j-1-l) = H - sigma
           const bool bnd = (i - 1 - l == 0) || (j - 1 - l == 0);
@@ -161,84 +168,61 @@ static __device__ __noinline__ void walk_pair(const DevParams& P, const uint32_t
         rw.push(0u, (uint32_t)taken);
         i -= taken;
         j -= taken;
-        continue;  // re-examine (i, j): boundary, STOP or the next run
+      } else if (linear) {
+        mode = LINUP;
+      } else {
+        mode = UP; k0 = 1; ref = h; kb = 0;
       }
-    }
-    const int sig = sigma_of(P, qc[i], sc[j]);
-    if (hhas(i - 1, j - 1, h - sig)) {  // DIAG
-      rw.push(0u, 1);
-      --i; --j;
-      h -= sig;
       continue;
     }
-    if (linear) {
-      if (hhas(i - 1, j, h + ge)) { rw.push(1u, 1); --i; h += ge; continue; }
-      rw.push(2u, 1);  // LEFT: H(i, j-1) = H(i, j) + g
-      --j;
+    if (mode == LINUP) {  // linear gaps: UP iff H(i-1, j) = H + g, else LEFT
+      const bool up = (i - 1 == 0) ? hbound(P, 0, j) == h + ge
+                                   : hmatch(hraw(P, dirs, ti, i - 1, j, tb8), h + ge, tb8);
+      if (up) { rw.push(1u, 1); --i; } else { rw.push(2u, 1); --j; }
       h += ge;
+      mode = TOP;
       continue;
     }
-    // UP iff E(i,j) = h, E(i,j) = max_k H(i-k,j) - Go - k Ge <= h; the gap is the largest
-    // k with H(i-k,j) - Go - k Ge = h.  H(i',j') <= match * min(i',j') bounds the scan
-    // (no k with match * min(i-k, j) - Go - k Ge < h can reach h); loads go in batches and
-    // values are rebuilt cell by cell up the column.
-    int kb = 0, hb = 0;
-    {
-      constexpr int SB = 8;
-      const int mt = max(P.smax, 0);
-      int ref = h;  // exact value of (i - k0 + 1, j)
-      for (int k0 = 1; k0 <= i; k0 += SB) {
-        if (mt * min(i - k0, j) - go - k0 * ge < h) break;
-        int hv[SB];
+    // affine gap scans (mode UP: along column j; LEFT: along row i)
+    const bool upm = mode == UP;
+    const int len = upm ? i : j;              // k runs 1..len
+    const int other = upm ? j : i;
+    bool fin = k0 > len || mt * min(len - k0, other) - go - k0 * ge < h;
+    if (!fin) {
+      int hv[B];
 #pragma unroll
-        for (int l = 0; l < SB; ++l)
-          if (k0 + l <= i) {
-            const int i2 = i - k0 - l;
-            hv[l] = (i2 == 0) ? hbound(P, 0, j) : hraw(P, dirs, ti, i2, j, tb8);
-          }
+      for (int l = 0; l < B; ++l) {
+        hv[l] = 0;
+        if (k0 + l <= len) {
+          const int x = len - k0 - l;  // i2 (UP) or j2 (LEFT)
+          hv[l] = (x == 0) ? (upm ? hbound(P, 0, j) : hbound(P, i, 0))
+                           : (upm ? hraw(P, dirs, ti, x, j, tb8) : hraw(P, dirs, ti, i, x, tb8));
+        }
+      }
 #pragma unroll
-        for (int l = 0; l < SB; ++l)
-          if (k0 + l <= i) {
-            const int i2 = i - k0 - l;
-            ref = (i2 == 0) ? hv[l] : hnear(hv[l], ref, tb8);
-            if (ref - go - (k0 + l) * ge == h) { kb = k0 + l; hb = ref; }
-          }
+      for (int l = 0; l < B; ++l) {
+        if (k0 + l <= len) {
+          const int x = len - k0 - l;
+          ref = (x == 0) ? hv[l] : hnear(hv[l], ref, tb8);
+          if (ref - go - (k0 + l) * ge == h) { kb = k0 + l; hb = ref; }
+        }
+      }
+      k0 += B;
+      fin = k0 > len || mt * min(len - k0, other) - go - k0 * ge < h;
+    }
+    if (fin) {
+      if (kb) {
+        rw.push(upm ? 1u : 2u, (uint32_t)kb);
+        if (upm) i -= kb; else j -= kb;
+        h = hb;
+        mode = TOP;
+      } else if (upm) {
+        mode = LEFT; k0 = 1; ref = h; kb = 0;
+      } else {
+        mode = DONE;  // unreachable for a consistent H store (no predecessor found)
       }
     }
-    if (kb) {
-      rw.push(1u, (uint32_t)kb);
-      i -= kb;
-      h = hb;
-      continue;
-    }
-    {  // LEFT: F(i,j) = h, the largest such k along the row
-      constexpr int SB = 8;
-      const int mt = max(P.smax, 0);
-      int ref = h;
-      for (int k0 = 1; k0 <= j; k0 += SB) {
-        if (mt * min(i, j - k0) - go - k0 * ge < h) break;
-        int hv[SB];
-#pragma unroll
-        for (int l = 0; l < SB; ++l)
-          if (k0 + l <= j) {
-            const int j2 = j - k0 - l;
-            hv[l] = (j2 == 0) ? hbound(P, i, 0) : hraw(P, dirs, ti, i, j2, tb8);
-          }
-#pragma unroll
-        for (int l = 0; l < SB; ++l)
-          if (k0 + l <= j) {
-            const int j2 = j - k0 - l;
-            ref = (j2 == 0) ? hv[l] : hnear(hv[l], ref, tb8);
-            if (ref - go - (k0 + l) * ge == h) { kb = k0 + l; hb = ref; }
-          }
-      }
-    }
-    if (!kb) break;  // unreachable for a consistent H store (no predecessor found)
-    rw.push(2u, (uint32_t)kb);
-    j -= kb;
-    h = hb;
   }
-  (void)hget;
   rw.flush();
   *n_ops = rw.n;
   *beg_i = i;
