@@ -414,8 +414,22 @@ __global__ void walk_kernel(WalkArgs a) {
     if (pair < 0) continue;
     const TbInfo ti = a.tb[pair];
     const uint64_t base = a.q_off[pair] + a.s_off[pair] + (uint64_t)pair;
-    walk_pair(a.P, a.dirs, ti, a.qcode + a.q_off[pair] - 1, a.scode + a.s_off[pair] - 1,
-              a.ops + base, a.n_ops + pair, a.beg_i + pair, a.beg_j + pair, a.tb8 != 0);
+    const uint8_t* qc = a.qcode + a.q_off[pair] - 1;
+    const uint8_t* sc = a.scode + a.s_off[pair] - 1;
+    switch (ti.R) {  // the traceback variants' rows per lane (plan.cuh)
+      case 8:
+        walk_pair<8>(a.P, a.dirs, ti, qc, sc, a.ops + base, a.n_ops + pair, a.beg_i + pair,
+                     a.beg_j + pair, a.tb8 != 0);
+        break;
+      case 16:
+        walk_pair<16>(a.P, a.dirs, ti, qc, sc, a.ops + base, a.n_ops + pair, a.beg_i + pair,
+                      a.beg_j + pair, a.tb8 != 0);
+        break;
+      default:
+        walk_pair<19>(a.P, a.dirs, ti, qc, sc, a.ops + base, a.n_ops + pair, a.beg_i + pair,
+                      a.beg_j + pair, a.tb8 != 0);
+        break;
+    }
   }
 }
 

@@ -24,34 +24,44 @@ __device__ __forceinline__ int hbound(const DevParams& P, int i, int j) {
   return -(P.go + (i + j) * P.ge);
 }
 
-__device__ __forceinline__ int hraw(const DevParams& P, const uint32_t* __restrict__ dirs,
-                                    const TbInfo& ti, int i, int j, bool tb8) {
-  const int L = ti.L, R = ti.R;
-  const int ip = i - 1 + ti.pad;
-  int st, tt, r;
-  // R is one of the traceback variants' row counts: constant divisors
-  switch (R) {
-    case 19: st = ip / 152; r = ip - st * 152; tt = r / 19; r -= tt * 19; break;
-    case 16: st = ip / 128; r = ip - st * 128; tt = r / 16; r -= tt * 16; break;
-    default: st = ip / 64; r = ip - st * 64; tt = r / 8; r -= tt * 8; break;  // R = 8
+// Element addressing of one pair: R (rows per lane) and L = 8 (lanes per group, every batch
+// variant) are compile-time; the warp-slot base and the diagonal count are computed once per
+// pair.  raw(i, j) is the stored element of cell (i, j): the exact H (full store; s16x2
+// halves unbiased) or its low byte (tb8).
+template <int R>
+struct HView {
+  static constexpr int L = 8, G = 4, HS = L * R;
+  const uint8_t* base;  // byte address of the warp-slot block's element 0
+  int DK, pad, grp, half;
+  bool p2, tb8;
+  __device__ __forceinline__ HView(const uint32_t* dirs, const TbInfo& ti, bool t8) {
+    p2 = ti.P == 2;
+    tb8 = t8;
+    const int esz = tb8 ? (p2 ? 2 : 1) : 4;
+    base = reinterpret_cast<const uint8_t*>(dirs) + ti.dir_base * esz;
+    DK = ti.slot_M + L - 1 + R - 1;
+    pad = ti.pad;
+    grp = ti.grp;
+    half = ti.half;
   }
-  const int k = (j - 1) + tt;                 // wavefront step of the cell
-  const int DK = ti.slot_M + L - 1 + R - 1;   // diagonal index range per strip
-  const int G = 32 / L;                        // lane groups per warp (interleaved)
-  const int64_t w =
-      ti.dir_base + (((((int64_t)st * DK + (k - r + R - 1)) * R + r) * G + ti.grp) * L + tt);
-  if (tb8) {
-    if (ti.P == 2)
-      return (int)((__ldg(reinterpret_cast<const unsigned short*>(dirs) + w) >> (8 * ti.half)) & 0xffu);
-    return (int)__ldg(reinterpret_cast<const unsigned char*>(dirs) + w);
+  __device__ __forceinline__ int raw(int i, int j) const {
+    const int ip = i - 1 + pad;
+    const int st = ip / HS;
+    int r = ip - st * HS;
+    const int tt = r / R;
+    r -= tt * R;
+    const int d = (j - 1) + tt - r + R - 1;  // diagonal (wavefront step - row) of the cell
+    const uint64_t e = (uint64_t)(uint32_t)(st * DK + d) * (uint32_t)(R * G * L) +
+                       (uint32_t)((r * G + grp) * L + tt);
+    if (tb8) {
+      if (p2) return (int)((__ldg(reinterpret_cast<const unsigned short*>(base) + e) >> (8 * half)) & 0xffu);
+      return (int)__ldg(base + e);
+    }
+    const uint32_t word = __ldg(reinterpret_cast<const unsigned int*>(base) + e);
+    if (p2) return (int)(int16_t)(uint16_t)(half ? (word >> 16) : (word & 0xffffu)) - (1 << 14);
+    return (int)word;
   }
-  const uint32_t word = dirs[w];
-  if (ti.P == 2) {
-    const int v = (int)(int16_t)(uint16_t)(ti.half ? (word >> 16) : (word & 0xffffu));
-    return v - (1 << 14);  // every kind's s16x2 values carry the +2^14 bias
-  }
-  return (int)word;
-}
+};
 
 // Does cell (i, j) hold the value `want`?  Exact for the full store; for the low-byte store
 // exact whenever |H(i,j) - want| < 256 (the host admits tb8 only then).
@@ -97,11 +107,13 @@ struct RunWriter {
 // the loop is one batch of at most 8 loads in the thread's current mode (diagonal run, linear
 // up-test, up scan, left scan), so threads in different modes only split inside one short
 // batch body instead of running whole walks one after another.
+template <int R>
 __device__ __forceinline__ void walk_pair(const DevParams& P, const uint32_t* __restrict__ dirs,
                                           const TbInfo& ti, const uint8_t* qc, const uint8_t* sc,
                                           uint32_t* ops_out, int32_t* n_ops, int32_t* beg_i,
                                           int32_t* beg_j, bool tb8) {
   constexpr int B = 8;  // cells per batch
+  const HView<R> hs(dirs, ti, tb8);
   enum { TOP = 0, LINUP = 1, UP = 2, LEFT = 3, DONE = 4 };
   const int go = P.go, ge = P.ge;
   const int kind = P.kind;
@@ -146,7 +158,7 @@ __device__ __forceinline__ void walk_pair(const DevParams& P, const uint32_t* __
         sg[l] = 0;
         if (l < lim) {
           const int i2 = i - 1 - l, j2 = j - 1 - l;
-          hv[l] = (i2 == 0 || j2 == 0) ? hbound(P, i2, j2) : hraw(P, dirs, ti, i2, j2, tb8);
+          hv[l] = (i2 == 0 || j2 == 0) ? hbound(P, i2, j2) : hs.raw(i2, j2);
           const uint32_t cq = vec ? (uint32_t)(vq >> (8 * (B - 1 - l))) & 0xffu : qc[i - l];
           const uint32_t cs = vec ? (uint32_t)(vs >> (8 * (B - 1 - l))) & 0xffu : sc[j - l];
           sg[l] = sigma_of(P, cq, cs);
@@ -177,7 +189,7 @@ __device__ __forceinline__ void walk_pair(const DevParams& P, const uint32_t* __
     }
     if (mode == LINUP) {  // linear gaps: UP iff H(i-1, j) = H + g, else LEFT
       const bool up = (i - 1 == 0) ? hbound(P, 0, j) == h + ge
-                                   : hmatch(hraw(P, dirs, ti, i - 1, j, tb8), h + ge, tb8);
+                                   : hmatch(hs.raw(i - 1, j), h + ge, tb8);
       if (up) { rw.push(1u, 1); --i; } else { rw.push(2u, 1); --j; }
       h += ge;
       mode = TOP;
@@ -196,7 +208,7 @@ __device__ __forceinline__ void walk_pair(const DevParams& P, const uint32_t* __
         if (k0 + l <= len) {
           const int x = len - k0 - l;  // i2 (UP) or j2 (LEFT)
           hv[l] = (x == 0) ? (upm ? hbound(P, 0, j) : hbound(P, i, 0))
-                           : (upm ? hraw(P, dirs, ti, x, j, tb8) : hraw(P, dirs, ti, i, x, tb8));
+                           : (upm ? hs.raw(x, j) : hs.raw(i, x));
         }
       }
 #pragma unroll
