@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <functional>
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
@@ -309,6 +310,10 @@ struct DeviceJob {
   anyseq_alignment* d_aln_out;  // alignment structs (device) or null => ctx buffer
   // traceback: cigar sizing results
   uint64_t cigar_total = 0;
+  // traceback: called once the chunk's kernels are enqueued, before run_device blocks on
+  // the CIGAR total (the host API issues the next chunk's upload here, so it overlaps this
+  // chunk's fill and walk)
+  std::function<anyseq_status()> before_sync;
 };
 
 anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, DeviceJob& J,
@@ -624,6 +629,10 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     L(1);
     ctx->mark(st, "walked+scanned");
     CK(cudaMemcpyAsync(D.h_small, D.cig_off.as<uint64_t>() + B, 8, cudaMemcpyDeviceToHost, st));
+    if (J.before_sync) {
+      const anyseq_status u = J.before_sync();
+      if (u != ANYSEQ_OK) return u;
+    }
     CK(cudaStreamSynchronize(st));
     J.cigar_total = D.h_small[0];
     ctx->mark(st, "host-has-total");
@@ -976,9 +985,15 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
       CK(D.cigar.ensure(cap_words * 4));
     }
     const double tr0 = ms_since();
+    bool up_done = false;
+    if (tb && pool)  // traceback: upload chunk c+1 while chunk c's fill and walk run
+      J.before_sync = [&]() -> anyseq_status {
+        up_done = true;
+        return upload_next(c);
+      };
     s = run_device(ctx, D, prm, J, tb ? D.cigar.as<uint32_t>() : nullptr, cap_words);
     if (ctx->timing >= 2) fprintf(stderr, "[host] chunk %d run_device %.3f -> %.3f ms\n", c, tr0, ms_since());
-    if (s == ANYSEQ_OK && pool) {
+    if (s == ANYSEQ_OK && pool && !up_done) {
       const anyseq_status u = upload_next(c);
       if (u != ANYSEQ_OK) return u;
     }
