@@ -550,6 +550,12 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
       fa.dir_block_words = block_words;
       fa.tb8 = tb8;
       fa.tb = D.tb.as<TbInfo>();
+      // local optimum rows resolved by the walk: the rows of a fill lane span at most
+      // d (R - 1) below the lane's maximum, which the low byte must tell apart
+      {
+        const int64_t dl = (int64_t)P.go + P.ge + std::max(P.smax, 0);
+        fa.defer_row = (prm->kind == ANYSEQ_LOCAL && (!tb8 || dl * (d.R - 1) < 256)) ? 1 : 0;
+      }
       for (int64_t lo = 0; lo < nslot[v]; lo += chunk) {
         const int64_t hi = std::min<int64_t>(nslot[v], lo + chunk);
         fa.slot_lo = (int32_t)(sbase[v] + lo);
@@ -585,6 +591,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
         wa.n_ops = D.n_ops.as<int32_t>();
         wa.beg_i = D.beg_i.as<int32_t>();
         wa.beg_j = D.beg_j.as<int32_t>();
+        wa.end_i = D.end_i.as<int32_t>();
         std::pair<cudaEvent_t, cudaEvent_t> ew{nullptr, nullptr};
         if (ctx->timing) { ew = take_events(ctx); CK(cudaEventRecord(ew.first, vst)); }
         CK(launch_walk(wa, vst, D.num_sms));

@@ -186,6 +186,9 @@ struct TbInfo {
   int32_t score;
   int32_t end_i, end_j;
   int32_t grp;       // lane group of the slot within its warp (interleaved store)
+  int32_t end_span;  // > 0: end_i is the first row of the fill lane holding the optimum; the
+                     // end row is the first of rows end_i .. end_i + end_span - 1 whose H at
+                     // column end_j equals the score (resolved by the walk)
 };
 
 }  // namespace anyseq

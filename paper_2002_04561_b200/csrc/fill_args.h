@@ -27,6 +27,7 @@ struct FillArgs {
   TbInfo* tb;                 // TB: per pair
   int32_t tb8;                // TB: store only the low byte of H per cell (the walk rebuilds
                               // H from neighbour differences, |dH| < 128: DESIGN.md 5.3)
+  int32_t defer_row;          // TB local: the end row is resolved by the walk (TbInfo::end_span)
   int32_t one;                // = 1 at run time (keeps IMAD-based adds on the FMA pipe)
   uint32_t nge_s16;           // packed (-Ge, -Ge): read from the constant bank in the hot loop
   uint32_t koc_s16;           // -(Go+Ge)*65537 (biased VS16 Hop addend)

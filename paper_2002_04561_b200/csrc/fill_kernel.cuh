@@ -423,7 +423,18 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
             cm = V::select_mask(cm, keep, ZB);
             uint32_t pb;
             const T nb = V::bmax(sbest, cm, pb);  // bit: sbest >= cm
-            if (PP == 2 && ((~pb) & 3u)) {
+            if (TB && PP == 2 && a.defer_row && ((~pb) & 3u)) {
+              // traceback: record the lane's first row only; the walk finds the row of the
+              // lane holding the maximum in the H store (TbInfo::end_span)
+#pragma unroll
+              for (int X = 0; X < PP; ++X) {
+                if (!((pb >> X) & 1u)) {
+                  sv[X] = dec(cm, X);
+                  si[X] = ip0 - pad[X] + 1;
+                  sj[X] = col + 1;
+                }
+              }
+            } else if (PP == 2 && ((~pb) & 3u)) {
               // the smallest row holding the new maximum, both alignments at once: on a
               // kept half 0 <= Hq[r] <= cm (local), so e = max(Hq[r] + 1 - cm, 0) is 1 iff
               // Hq[r] == cm, and key = 64 e + 63 - r is largest for the first such row
@@ -650,6 +661,7 @@ __global__ void __launch_bounds__(128, (TB && R > 8) ? FILL_MINB_TBWIDE : FILL_M
           ti.score = osc[X];
           ti.end_i = oi[X];
           ti.end_j = oj[X];
+          ti.end_span = (KIND == KLOCAL && PP == 2 && a.defer_row && osc[X] > 0) ? R : 0;
           a.tb[pr[X]] = ti;
         }
       }

@@ -419,15 +419,15 @@ __global__ void walk_kernel(WalkArgs a) {
     switch (ti.R) {  // the traceback variants' rows per lane (plan.cuh)
       case 8:
         walk_pair<8>(a.P, a.dirs, ti, qc, sc, a.ops + base, a.n_ops + pair, a.beg_i + pair,
-                     a.beg_j + pair, a.tb8 != 0);
+                     a.beg_j + pair, a.end_i + pair, a.tb8 != 0);
         break;
       case 16:
         walk_pair<16>(a.P, a.dirs, ti, qc, sc, a.ops + base, a.n_ops + pair, a.beg_i + pair,
-                      a.beg_j + pair, a.tb8 != 0);
+                      a.beg_j + pair, a.end_i + pair, a.tb8 != 0);
         break;
       default:
         walk_pair<19>(a.P, a.dirs, ti, qc, sc, a.ops + base, a.n_ops + pair, a.beg_i + pair,
-                      a.beg_j + pair, a.tb8 != 0);
+                      a.beg_j + pair, a.end_i + pair, a.tb8 != 0);
         break;
     }
   }

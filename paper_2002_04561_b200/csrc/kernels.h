@@ -89,6 +89,7 @@ struct WalkArgs {
   int32_t* n_ops;
   int32_t* beg_i;
   int32_t* beg_j;
+  int32_t* end_i;  // end rows resolved by the walk (TbInfo::end_span > 0)
 };
 cudaError_t launch_walk(const WalkArgs& a, cudaStream_t st, int num_sms);
 

@@ -111,7 +111,7 @@ template <int R>
 __device__ __forceinline__ void walk_pair(const DevParams& P, const uint32_t* __restrict__ dirs,
                                           const TbInfo& ti, const uint8_t* qc, const uint8_t* sc,
                                           uint32_t* ops_out, int32_t* n_ops, int32_t* beg_i,
-                                          int32_t* beg_j, bool tb8) {
+                                          int32_t* beg_j, int32_t* end_i_out, bool tb8) {
   constexpr int B = 8;  // cells per batch
   const HView<R> hs(dirs, ti, tb8);
   enum { TOP = 0, LINUP = 1, UP = 2, LEFT = 3, DONE = 4 };
@@ -122,6 +122,21 @@ __device__ __forceinline__ void walk_pair(const DevParams& P, const uint32_t* __
   RunWriter rw{ops_out, 0, 0, 0};
   int i = ti.end_i, j = ti.end_j;
   int h = ti.score;
+  if (ti.end_span > 0) {
+    // the fill recorded the first row of the lane holding the optimum at column j: the end
+    // cell is the lane's first row with H = score (the lane's rows lie within d (R-1) < 256
+    // of the maximum, so equal low bytes mean equal values; host check)
+    int found = i;
+    bool got = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i2 = ti.end_i + r;
+      const int raw = i2 >= 1 ? hs.raw(i2, j) : -1;
+      if (!got && i2 >= 1 && hmatch(raw, h, tb8)) { found = i2; got = true; }
+    }
+    i = found;
+    *end_i_out = i;
+  }
   int mode = TOP;
   int k0 = 1, ref = 0, kb = 0, hb = 0;  // gap scans: next k, exact value of the last cell, best
   while (mode != DONE) {
