@@ -369,17 +369,34 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
             cm = __vimax3_s16x2(Hq[0], cmB, best);
           }
           if (cm != best) {  // resolve (value, first row, column) of the improved half(s)
+            // first row holding the new maximum, both halves at once (unless row 0 holds it
+            // in every improved half): t = clamp(Hq[r] + 1 - cm, 0, 1) is 1 iff Hq[r] == cm
+            // (Hq[r] <= cm), key = 64 t + 63 - r, and the largest key names the first such
+            // row -- one DPX op and one IMAD per row instead of a compare-select per row and
+            // half (the clamp keeps halves that did not improve from carrying into the other)
+            const uint32_t ne = __vcmpne2(cm, best), first = __vcmpeq2(Hq[0], cm);
+            uint32_t kmax = VS16::splat(127);  // row 0 in both halves
+            if (ne & ~first) {
+              const uint32_t om = __vsub2(VS16::splat(1), cm), k64 = one << 6;
+              kmax = 0;
+#pragma unroll
+              for (int r = 0; r < NR; r += 2) {
+                const uint32_t ka = (uint32_t)imad_add_s(
+                    (int)__viaddmin_s16x2_relu(Hq[r], om, VS16::splat(1)), k64, (63 - r) * 0x10001);
+                if (r + 1 < NR) {
+                  const uint32_t kb = (uint32_t)imad_add_s(
+                      (int)__viaddmin_s16x2_relu(Hq[r + 1], om, VS16::splat(1)), k64, (62 - r) * 0x10001);
+                  kmax = __vimax3_s16x2(kmax, ka, kb);
+                } else {
+                  kmax = __vmaxs2(kmax, ka);
+                }
+              }
+            }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int v = h16_get(cm, h);
               if (v != h16_get(best, h)) {
-                int rr = 0;
-                if (h16_get(Hq[0], h) != v) {  // not the first row: the first row reaching v
-                  rr = NR - 1;
-#pragma unroll
-                  for (int r = NR - 1; r >= 1; --r)
-                    if (h16_get(Hq[r], h) == v) rr = r;
-                }
+                const int rr = 63 - (h16_get(kmax, h) & 63);
                 if (h == 0) { bv0 = v + base; bi0 = ip0 + rr + 1; bj0 = c_lo + lc + 1; }
                 else { bv1 = v + base; bi1 = ip0 + NR + rr + 1; bj1 = c_lo + lc; }
               }
