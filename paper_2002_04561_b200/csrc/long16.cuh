@@ -62,10 +62,13 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
   __shared__ int2 ring_he[4][RING];
   // full PRMT selector of a column c for the two halves: codes of c (low half) and c - 1
   // (high half, one column behind), sign-replicating (VS16::selector)
-  __shared__ uint32_t ring_sel[4][RING];
+  // (each ring has a mirror of its first MIR entries after the end: the steady-state step
+  // reads through a pointer advanced by an IMAD and re-based once per period)
+  constexpr int MIR = 64;
+  __shared__ uint32_t ring_sel[4][RING + MIR];
   // OFF-phase steps: lane 0's input (H, E of the row above) already in the warp's relative
   // frame, packed (h | e << 16), converted once per refill period right after re-basing
-  __shared__ uint32_t ring_rel[4][RING];
+  __shared__ uint32_t ring_rel[4][RING + MIR];
   __shared__ int2 ring_out[4][64];        // the task's last row (H, E) awaiting publication
   __shared__ int ring_eck[CKPT ? 4 : 1][64];  // CKPT: E of that row itself (not of the next)
   __shared__ int4 ring_pf[4][64];  // row hand-off entries fetched (cp.async) ahead of need
@@ -82,11 +85,18 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
   const int n = a.n;
   // subject codes of columns past a task's end are read (and ignored) by the warp's last
   // steps: keep every ring entry a valid code so the active half's selector stays intact
-  for (int x = t; x < RING; x += 32) {
+  for (int x = t; x < RING + MIR; x += 32) {
     ring_sel[wb][x] = 0xC480u;
-    ring_he[wb][x] = make_int2(0, 0);
+    if (x < RING) ring_he[wb][x] = make_int2(0, 0);
     ring_rel[wb][x] = 0;
   }
+  const uint32_t sel_smem = (uint32_t)__cvta_generic_to_shared(&ring_sel[wb][0]);
+  const uint32_t rel_smem = (uint32_t)__cvta_generic_to_shared(&ring_rel[wb][0]);
+  auto lds32 = [](uint32_t addr) -> uint32_t {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+  };
   __syncwarp();
 
   LongPart part;
@@ -133,10 +143,18 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       int pcode = __shfl_up_sync(0xffffffffu, code, 1);
       if (t == 0) pcode = last_code;
       last_code = __shfl_sync(0xffffffffu, code, (c1 - 1 - c0) & 31);  // code of column c1 - 1
-      if (mine) ring_sel[wb][c & (RING - 1)] = (uint32_t)code * 0x11u + (uint32_t)pcode * 0x1100u + 0xC480u;
+      if (mine) {
+        const uint32_t v = (uint32_t)code * 0x11u + (uint32_t)pcode * 0x1100u + 0xC480u;
+        ring_sel[wb][c & (RING - 1)] = v;
+        if ((c & (RING - 1)) < MIR) ring_sel[wb][RING + (c & (RING - 1))] = v;
+      }
       // the high half relaxes column W - 1 one step after the low half left the task: its
       // selector (entry W) carries code(W - 1) in the high nibbles
-      if (c1 == W && t == 0) ring_sel[wb][W & (RING - 1)] = (uint32_t)last_code * 0x1100u + 0xC480u;
+      if (c1 == W && t == 0) {
+        const uint32_t v = (uint32_t)last_code * 0x1100u + 0xC480u;
+        ring_sel[wb][W & (RING - 1)] = v;
+        if ((W & (RING - 1)) < MIR) ring_sel[wb][RING + (W & (RING - 1))] = v;
+      }
       if (s == 0 && mine) {
         const int h0 = KIND == KGLOBAL ? -(P.go + (c_lo + c + 1) * P.ge) : 0;
         ring_he[wb][c & (RING - 1)] = make_int2(h0, h0 - cop);
@@ -254,13 +272,19 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       uint32_t sel_nx = ring_sel[wb][(0 - 2 * t) & (RING - 1)];
       int2 he_nx = ring_he[wb][0];
       uint32_t rel_nx = 0;
+      uint32_t psel = 0, prel = 0;  // OFF steps: addresses of the next selector / input entries
       auto step = [&](auto chk, const int k) {
         uint32_t (&Hi)[NR] = H;
         uint32_t (&Hq)[NR] = H;
         constexpr bool CHK = decltype(chk)::value;
         const int lc = k - 2 * t;  // low half's column (task-relative); high half: lc - 1
         const uint32_t sel = sel_nx;
-        sel_nx = ring_sel[wb][(lc + 1) & (RING - 1)];
+        if (CHK) {
+          sel_nx = ring_sel[wb][(lc + 1) & (RING - 1)];
+        } else {
+          sel_nx = lds32(psel);
+          psel = (uint32_t)imad_add_s((int)psel, one, 4);
+        }
         uint32_t hin, ein;
         int2 he = make_int2(0, 0);
         if (CHK) {
@@ -276,7 +300,8 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
           // lane 31's high half is nobody's input: it carries lane 0's input (pre-converted
           // ring entry) through the same rotating shuffle, so lane 0 needs no select
           const uint32_t rel = rel_nx;
-          rel_nx = ring_rel[wb][(k + 1) & (RING - 1)];
+          rel_nx = lds32(prel);
+          prel = (uint32_t)imad_add_s((int)prel, one, 4);
           const uint32_t vh = prmt(Hbot, rel, t == 31 ? 0x5410u : 0x3210u);
           const uint32_t ve = prmt(Ebot, rel, t == 31 ? 0x7610u : 0x3210u);
           const uint32_t hs = __shfl_sync(0xffffffffu, vh, (t + 31) & 31);
@@ -450,10 +475,17 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       };
       // lane 0's inputs of columns [c0, c0 + 32) in the current frame, packed (h | e << 16)
       auto convert = [&](int c0) {
-        const int2 v = ring_he[wb][(c0 + t) & (RING - 1)];
-        ring_rel[wb][(c0 + t) & (RING - 1)] = h16_pack(cv(v.x), cv(v.y));
+        const int x = (c0 + t) & (RING - 1);
+        const int2 v = ring_he[wb][x];
+        const uint32_t r = h16_pack(cv(v.x), cv(v.y));
+        ring_rel[wb][x] = r;
+        if (x < MIR) ring_rel[wb][RING + x] = r;
         __syncwarp();
         rel_nx = ring_rel[wb][c0 & (RING - 1)];
+        // the OFF steps from c0 on read entries c0 + 1 ... (inputs) and k - 2t + 1 ...
+        // (selectors) linearly: at most PER + 1 past the re-base, inside the mirror
+        prel = rel_smem + 4u * (uint32_t)((c0 + 1) & (RING - 1));
+        psel = sel_smem + 4u * (uint32_t)((c0 - 2 * t + 1) & (RING - 1));
       };
 
       // publish staged columns [flushed, c_end) (at most 32) to the row buffer for strip s+1
