@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
   }
   const uint32_t sel_smem = (uint32_t)__cvta_generic_to_shared(&ring_sel[wb][0]);
   const uint32_t rel_smem = (uint32_t)__cvta_generic_to_shared(&ring_rel[wb][0]);
+  const uint32_t out_smem = (uint32_t)__cvta_generic_to_shared(&ring_out[wb][0]);
   auto lds32 = [](uint32_t addr) -> uint32_t {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       int2 he_nx = ring_he[wb][0];
       uint32_t rel_nx = 0;
       uint32_t psel = 0, prel = 0;  // OFF steps: addresses of the next selector / input entries
+      uint32_t pout = 0;            // OFF steps: staging slot of the task's last row
       auto step = [&](auto chk, const int k) {
         uint32_t (&Hi)[NR] = H;
         uint32_t (&Hq)[NR] = H;
@@ -348,11 +350,20 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         diag = hin;
         Hbot = Hq[NR - 1];
         Ebot = e;
-        if (t == 31 && act1) {  // the task's last row (high half), column lc - 1: staged in
-          ring_out[wb][(lc - 1) & 63] =  // shared memory, published 32 columns at a time
-              make_int2(h16_get(Hq[NR - 1], 1) + base, h16_get(e, 1) + base);
-          if (CKPT) ring_eck[wb][(lc - 1) & 63] = h16_get(elast, 1) + base;
+        // the task's last row (high half), column c = lc - 1: staged in shared memory slot
+        // (c + 63) & 63 (= k & 63: a period's 32 steps never wrap), published 32 columns at
+        // a time; OFF steps store through a pointer advanced by an IMAD
+        if (CHK) {
+          if (t == 31 && act1)
+            ring_out[wb][(lc + 62) & 63] = make_int2(h16_get(Hq[NR - 1], 1) + base, h16_get(e, 1) + base);
+        } else {
+          if (t == 31)
+            asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(pout),
+                         "r"(h16_get(Hq[NR - 1], 1) + base), "r"(h16_get(e, 1) + base)
+                         : "memory");
+          pout = (uint32_t)imad_add_s((int)pout, one, 8);
         }
+        if (CKPT && t == 31 && act1) ring_eck[wb][(lc + 62) & 63] = h16_get(elast, 1) + base;
         if (CKPT) {  // column checkpoints: (H, F) of every real row at columns j = k 2^kc_shift
           const int kcm = (1 << a.kc_shift) - 1;
           const int jl = c_lo + lc + 1;  // the low half's column; the high half's is jl - 1
@@ -485,6 +496,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         // the OFF steps from c0 on read entries c0 + 1 ... (inputs) and k - 2t + 1 ...
         // (selectors) linearly: at most PER + 1 past the re-base, inside the mirror
         prel = rel_smem + 4u * (uint32_t)((c0 + 1) & (RING - 1));
+        pout = out_smem + 8u * (uint32_t)(c0 & 63);
         psel = sel_smem + 4u * (uint32_t)((c0 - 2 * t + 1) & (RING - 1));
       };
 
@@ -496,12 +508,12 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         __syncwarp();
         const int c = flushed + t;
         if (c < c_end) {
-          const int2 v = ring_out[wb][c & 63];
+          const int2 v = ring_out[wb][(c + 63) & 63];
           ANY_CHECK(c_lo + c + 1 <= a.m);
           st_row(a.rowbuf + c_lo + c + 1, v.x, v.y, s + 1);
           ANY_CHECK(!CKPT || ck_slot < (a.S - 1) / a.ck_every);
           if (CKPT && ck_slot >= 0)  // row checkpoint: (H, E) of the strip's last row
-            a.rowck[(size_t)ck_slot * (a.m + 1) + c_lo + c + 1] = make_int2(v.x, ring_eck[wb][c & 63]);
+            a.rowck[(size_t)ck_slot * (a.m + 1) + c_lo + c + 1] = make_int2(v.x, ring_eck[wb][(c + 63) & 63]);
         }
         flushed = c_end;
         __syncwarp();
