@@ -275,6 +275,8 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       uint32_t rel_nx = 0;
       uint32_t psel = 0, prel = 0;  // OFF steps: addresses of the next selector / input entries
       uint32_t pout = 0;            // OFF steps: staging slot of the task's last row
+      int kck = -8;  // CKPT, OFF steps: the step whose low half (this step) or high half
+                     // (next step) is at a checkpoint column, found once per period
       auto step = [&](auto chk, const int k) {
         uint32_t (&Hi)[NR] = H;
         uint32_t (&Hq)[NR] = H;
@@ -365,10 +367,16 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         }
         if (CKPT && t == 31 && act1) ring_eck[wb][(lc + 62) & 63] = h16_get(elast, 1) + base;
         if (CKPT) {  // column checkpoints: (H, F) of every real row at columns j = k 2^kc_shift
-          const int kcm = (1 << a.kc_shift) - 1;
           const int jl = c_lo + lc + 1;  // the low half's column; the high half's is jl - 1
-          if ((((jl & kcm) == 0) && act0) || ((((jl - 1) & kcm) == 0) && act1)) {
-            const int h = ((jl & kcm) == 0) ? 0 : 1;
+          int h = -1;                    // the half at a checkpoint column this step
+          if (CHK) {
+            const int kcm = (1 << a.kc_shift) - 1;
+            h = (((jl & kcm) == 0) && act0) ? 0 : ((((jl - 1) & kcm) == 0) && act1) ? 1 : -1;
+          } else {  // OFF steps: the step was found once per period (convert)
+            const unsigned dk = (unsigned)(k - kck);
+            if (dk < 2u) h = (int)dk;
+          }
+          if (h >= 0) {
             const int jj = jl - h;
             if (jj < a.m) {
               ANY_CHECK(jj >= (1 << a.kc_shift) && ((jj >> a.kc_shift) - 1) < ((a.m - 1) >> a.kc_shift));
@@ -497,6 +505,12 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         // (selectors) linearly: at most PER + 1 past the re-base, inside the mirror
         prel = rel_smem + 4u * (uint32_t)((c0 + 1) & (RING - 1));
         pout = out_smem + 8u * (uint32_t)(c0 & 63);
+        // checkpoint columns are 2^kc_shift >= 512 apart: at most one per period and half;
+        // the low half is at column c_lo + (k - 2t) + 1 (high half: one step later)
+        if (CKPT) {
+          const int kcm = (1 << a.kc_shift) - 1;
+          kck = (c0 - 1) + ((2 * t - 1 - c_lo - (c0 - 1)) & kcm);
+        }
         psel = sel_smem + 4u * (uint32_t)((c0 - 2 * t + 1) & (RING - 1));
       };
 
