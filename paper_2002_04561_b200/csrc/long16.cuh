@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       uint32_t rel_nx = 0;
       uint32_t psel = 0, prel = 0;  // OFF steps: addresses of the next selector / input entries
       uint32_t pout = 0;            // OFF steps: staging slot of the task's last row
+      uint32_t peck = 0;            // CKPT, OFF steps: staging slot of its E
       int kck = -8;  // CKPT, OFF steps: the step whose low half (this step) or high half
                      // (next step) is at a checkpoint column, found once per period
       auto step = [&](auto chk, const int k) {
@@ -359,13 +360,18 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
           if (t == 31 && act1)
             ring_out[wb][(lc + 62) & 63] = make_int2(h16_get(Hq[NR - 1], 1) + base, h16_get(e, 1) + base);
         } else {
-          if (t == 31)
+          if (t == 31) {
             asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(pout),
                          "r"(h16_get(Hq[NR - 1], 1) + base), "r"(h16_get(e, 1) + base)
                          : "memory");
+            if (CKPT)
+              asm volatile("st.shared.s32 [%0], %1;" ::"r"(peck), "r"(h16_get(elast, 1) + base)
+                           : "memory");
+          }
           pout = (uint32_t)imad_add_s((int)pout, one, 8);
+          if (CKPT) peck = (uint32_t)imad_add_s((int)peck, one, 4);
         }
-        if (CKPT && t == 31 && act1) ring_eck[wb][(lc + 62) & 63] = h16_get(elast, 1) + base;
+        if (CKPT && CHK && t == 31 && act1) ring_eck[wb][(lc + 62) & 63] = h16_get(elast, 1) + base;
         if (CKPT) {  // column checkpoints: (H, F) of every real row at columns j = k 2^kc_shift
           const int jl = c_lo + lc + 1;  // the low half's column; the high half's is jl - 1
           int h = -1;                    // the half at a checkpoint column this step
@@ -505,6 +511,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         // (selectors) linearly: at most PER + 1 past the re-base, inside the mirror
         prel = rel_smem + 4u * (uint32_t)((c0 + 1) & (RING - 1));
         pout = out_smem + 8u * (uint32_t)(c0 & 63);
+        if (CKPT) peck = (uint32_t)__cvta_generic_to_shared(&ring_eck[wb][c0 & 63]);
         // checkpoint columns are 2^kc_shift >= 512 apart: at most one per period and half;
         // the low half is at column c_lo + (k - 2t) + 1 (high half: one step later)
         if (CKPT) {
