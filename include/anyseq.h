@@ -222,6 +222,9 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
                          the scheme allows it exactly (R23); 0 = full H
      "batch_long_cells"  a batch pair with n*m >= this (and n, m >= 2048) is aligned by the
                          long-pair path instead of the batch kernel (default 2^26; 0 = never)
+     "batch_long_small"  batches of at most this many pairs send every pair with n, m >= 256
+                         to the long-pair path (default 4; 0 = never); pairs that path cannot
+                         take stay on the batch kernel
      "timing"            see above */
 anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value);
 

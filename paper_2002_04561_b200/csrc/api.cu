@@ -116,6 +116,8 @@ struct anyseq_ctx {
   int64_t force_variant = -1;
   int64_t allow16 = 1;
   int64_t batch_long_cells = 1ll << 26;  // batch pairs this large take the long-pair path
+  int64_t batch_long_small = 4;  // batches of at most this many pairs: every pair with both
+                                 // sides >= 256 takes the long-pair path
   int64_t tb8 = 1;          // traceback: 1-byte H store where the range allows
   int64_t pack2 = 1;        // host API: upload ACGT-only chunks as 2-bit codes
   int64_t pack2_percent = 0;  // share of the bytes packed (0 = all)
@@ -1156,15 +1158,32 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
 // kernel up for seconds; it goes to the long-pair path instead (the tiled wavefront over all
 // SMs, §5.4 / §5.4c), the rest of the batch to the batch path, and the results are merged in
 // pair order (both paths follow the same optimum and traceback rules, so the results are the
-// ones the batch path would give).
+// ones the batch path would give).  A batch of only a few pairs (option batch_long_small)
+// sends every pair with both sides >= 256 there too: the batch kernel gives a pair one
+// 8-lane group, the long kernel spreads it over many warps (C1, one 1000 x 1000 pair:
+// 1.3 ms instead of 5 ms with traceback).  A pair the long path cannot take (e.g. affine
+// traceback of a subject with N) falls back to the batch path on its own.
 anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const anyseq_batch* b,
                              int tb, int32_t* scores, anyseq_alignment* aln, uint32_t* cigar,
                              uint64_t cap, uint64_t* used) {
   std::vector<uint64_t> longs;
-  if (ctx->batch_long_cells > 0)
+  const bool small = b->num_pairs <= (uint64_t)ctx->batch_long_small;
+  // small-batch routing only where the long path is the checkpointed 16-bit one (its
+  // CIGARs follow the batch path's tie rules; a subject with N would take the s32 kernel
+  // and, for traceback, the Hirschberg fallback)
+  auto acgt_only = [](const char* p, uint64_t len) {
+    for (uint64_t x = 0; x < len; ++x) {
+      const char c = (char)(p[x] | 0x20);
+      if (c != 'a' && c != 'c' && c != 'g' && c != 't') return false;
+    }
+    return true;
+  };
+  if (ctx->batch_long_cells > 0 || small)
     for (uint64_t k = 0; k < b->num_pairs; ++k) {
       const uint64_t n = b->q_off[k + 1] - b->q_off[k], m = b->s_off[k + 1] - b->s_off[k];
-      if (n >= 2048 && m >= 2048 && (long double)n * m >= (long double)ctx->batch_long_cells)
+      if ((ctx->batch_long_cells > 0 && n >= 2048 && m >= 2048 &&
+           (long double)n * m >= (long double)ctx->batch_long_cells) ||
+          (small && n >= 256 && m >= 256 && acgt_only(b->s + b->s_off[k], m)))
         longs.push_back(k);
     }
   if (longs.empty()) return run_host_batch_core(ctx, prm, b, tb, scores, aln, cigar, cap, used);
@@ -1215,6 +1234,17 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
       cg3[x].resize(u);
     } else {
       r = anyseq_align_long(ctx, prm, qk, n, sk, m, &al3[x]);
+    }
+    if (r == ANYSEQ_E_UNSUPPORTED) {  // not for the long path: this pair on the batch path
+      const uint64_t qo1[2] = {0, n}, so1[2] = {0, m};
+      const anyseq_batch b1{qk, qo1, sk, so1, 1};
+      int32_t sc1 = 0;
+      uint64_t u1 = 0;
+      if (tb) cg3[x].resize(n + m + 1);
+      r = run_host_batch_core(ctx, prm, &b1, tb, &sc1, &al3[x], tb ? cg3[x].data() : nullptr,
+                              tb ? cg3[x].size() : 0, &u1);
+      if (tb) cg3[x].resize(u1);
+      if (r == ANYSEQ_OK && !tb) al3[x].score = sc1;
     }
     if (r != ANYSEQ_OK) {
       ctx->err = "pair " + std::to_string(k) + " (long-pair path): " + ctx->err;
@@ -1524,7 +1554,9 @@ anyseq_status run_traceback_long_hirschberg(anyseq_ctx* ctx, const anyseq_params
     const uint64_t lcap = cq.size() + cs.size() + B;
     lc.resize(std::max<uint64_t>(lcap, 1));
     std::vector<int32_t> lsc(B);
-    anyseq_status r = run_host_batch(ctx, &gp, &lb, 1, lsc.data(), la.data(), lc.data(), lcap, &lused);
+    // leaves stay on the batch kernel (the routing wrapper could send a few large leaves back
+    // to the long-pair path, i.e. into this recursion again)
+    anyseq_status r = run_host_batch_core(ctx, &gp, &lb, 1, lsc.data(), la.data(), lc.data(), lcap, &lused);
     if (r != ANYSEQ_OK) return r;
   }
   ctx->tb_leaf_ms =
@@ -1906,6 +1938,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
     if (n == "pack2") { ctx->pack2 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "tb8") { ctx->tb8 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "batch_long_cells") { ctx->batch_long_cells = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
+    if (n == "batch_long_small") { ctx->batch_long_small = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
     if (n == "pack2_percent") {
       if (value < 0 || value > 100) return fail(ctx, ANYSEQ_E_INVALID, "pack2_percent in [0, 100]");
       ctx->pack2_percent = value;

@@ -574,3 +574,30 @@ def test_mixed_batch_routes_long_pairs(ctx, kind):
         assert np.array_equal(aln["cigar_offset"], np.cumsum(cl) - cl)
     finally:
         ctx.set_option("batch_long_cells", 1 << 26)
+
+
+@pytest.mark.parametrize("kind", ["global", "semi", "local"])
+@pytest.mark.parametrize("gap,go", [("linear", 0), ("affine", 5)])
+def test_small_batch_takes_long_path(ctx, kind, gap, go):
+    """Batches of at most batch_long_small pairs send ACGT-only pairs with both sides >= 256
+    to the long-pair path (one pair spread over many warps); the pair whose subject holds an
+    N and the short pair stay on the batch kernel.  Scores, end/begin cells and CIGARs equal
+    the oracle's either way."""
+    import paper_2002_04561_b200 as A
+    from synth import c4_genomes, csr
+    g1, g2 = c4_genomes(4000, "a", seed=94)
+    sN = bytearray(g2[1000:1700])
+    sN[350] = ord("N")
+    qs = [g1[:1000], g1[1000:1650], b"ACGTTGCA"]
+    ss = [g2[:1050], bytes(sN), b"ACGTAGCA"]
+    q, qo = csr(qs)
+    s, so = csr(ss)
+    res, ocig = _oracle(kind, gap, go, 1, q, qo, s, so, tb=True)
+    sch = A.Scheme(kind, gap, 2, -1, go, 1)
+    for small in (4, 0):  # long path (and fallback) vs the batch kernel alone
+        ctx.set_option("batch_long_small", small)
+        try:
+            _check_scores(ctx, sch, q, qo, s, so, res)
+            _check_tb(ctx, sch, q, qo, s, so, res, ocig)
+        finally:
+            ctx.set_option("batch_long_small", 4)

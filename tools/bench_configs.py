@@ -55,8 +55,11 @@ def main():
             o = O.align(O.Scheme("global", "linear", 2, -1, 0, 1), a, b)
             ok = int(aln["score"][0]) == o.score and A.cigars_of(aln, cig)[0] == o.cigar
             cells = 1e6
+            # a one-pair batch takes the long-pair path (option batch_long_small): its
+            # device times are the checkpointed pass and the tile walk of the last call
             res.append({"config": "C1 1000x1000 NW linear traceback", "cells": cells,
                         "wall_ms": wall * 1e3, "fill_ms": fill, "walk_ms": walk,
+                        "tb_pass_ms": ctx.stat("tb_pass_ms"), "tb_walk_ms": ctx.stat("tb_walk_ms"),
                         "gcups_wall": cells / wall / 1e9, "parity": ok})
         elif c == "c3":
             qm, sm = synth.c2_reads(1_000_000, seed=2)
