@@ -276,6 +276,9 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       uint32_t psel = 0, prel = 0;  // OFF steps: addresses of the next selector / input entries
       uint32_t pout = 0;            // OFF steps: staging slot of the task's last row
       uint32_t peck = 0;            // CKPT, OFF steps: staging slot of its E
+      // LOCAL, OFF steps: track the running maximum in this period?  Skipped when no cell
+      // of the period can exceed it (see convert)
+      bool trk = true;
       int kck = -8;  // CKPT, OFF steps: the step whose low half (this step) or high half
                      // (next step) is at a checkpoint column, found once per period
       auto step = [&](auto chk, const int k) {
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
             }
           }
         }
-        if (KIND == KLOCAL) {
+        if (KIND == KLOCAL && (CHK || trk)) {
           // local optimum: packed running maximum per half; strictly larger values only.
           // cmB = max over the half's rows but its first: when the first row holds the new
           // maximum (the common case where H falls down the rows, e.g. left of a similar
@@ -505,6 +508,18 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         const uint32_t r = h16_pack(cv(v.x), cv(v.y));
         ring_rel[wb][x] = r;
         if (x < MIR) ring_rel[wb][RING + x] = r;
+        if (KIND == KLOCAL) {
+          // every H of the coming period derives from the warp's current cells (max -margin
+          // right after the re-base), the previous column's diagonal inputs and the input
+          // row of columns [c0, c0 + 32), gaining at most max(sigma) per column along a
+          // diagonal (gaps only lose, and E, F <= H): if that bound cannot pass the running
+          // maximum of either half, the period needs no tracking
+          const int top = __reduce_max_sync(
+              0xffffffffu, max((int)(int16_t)(uint16_t)(r & 0xffffu),
+                               max(h16_get(diag, 0), h16_get(diag, 1))));
+          const int bound = max(top, -a.margin) + (PER + 4) * max(P.smax, 0);
+          trk = bound > min(h16_get(best, 0), h16_get(best, 1));
+        }
         __syncwarp();
         rel_nx = ring_rel[wb][c0 & (RING - 1)];
         // the OFF steps from c0 on read entries c0 + 1 ... (inputs) and k - 2t + 1 ...
