@@ -408,8 +408,33 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   CK(launch_classify(ca, st, D.num_sms));
   L(1);
   ctx->mark(st, "classified");
-  CK(cudaStreamSynchronize(st));
-  const PlanSummary S = *D.h_sum;
+  // The plan summary normally comes back from classify (a stream synchronisation: the host
+  // waits for the previous chunk's fill).  A host-API chunk of ACGT-only pairs of one common
+  // length (2-bit upload, offsets generated on the device) has a plan the host can work out
+  // with the same plan_pair() -- then nothing waits and the host enqueues the next chunk
+  // while this one computes.
+  PlanSummary S;
+  bool host_plan = false;
+  if (J.packed2 && J.gen_q > 0 && J.gen_s > 0 && B > 0) {
+    const PairPlan pp = plan_pair(ca.cfg, J.gen_q, J.gen_s, false);
+    if (!pp.range_err && pp.v >= 0) {
+      memset(&S, 0, sizeof(S));
+      S.err_pos = ~0ull;
+      for (int v = 0; v < NV; ++v) {
+        S.kmin[v] = ~0ull;
+        S.kmax[v] = 0ull;
+      }
+      S.count[pp.v] = (int32_t)B;
+      S.maxn[pp.v] = (int32_t)J.gen_q;
+      S.maxm[pp.v] = (int32_t)J.gen_s;
+      S.kmin[pp.v] = S.kmax[pp.v] = pp.key;
+      host_plan = true;
+    }
+  }
+  if (!host_plan) {
+    CK(cudaStreamSynchronize(st));
+    S = *D.h_sum;
+  }
   ctx->mark(st, "host-planned");
   if (S.err_pos != ~0ull) {
     const bool in_s = S.err_pos >= (1ull << 62);
@@ -1006,7 +1031,12 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
       const anyseq_status u = upload_next(c);
       if (u != ANYSEQ_OK) return u;
     }
-    if (s == ANYSEQ_OK && c > 0) copy_out(c - 1);  // run_device synchronised past it
+    if (s == ANYSEQ_OK && c > 0) {
+      // chunk c-1's results have landed once its last enqueued work has (run_device no
+      // longer synchronises when the host planned chunk c itself)
+      if (stage_s || stage_a) CK(cudaEventSynchronize(D.ev_free[(c - 1) & 1]));
+      copy_out(c - 1);
+    }
     if (s != ANYSEQ_OK) {
       if (s == ANYSEQ_E_BADSEQ) describe_badseq(ctx, b, a0);
       cudaStreamSynchronize(cs);

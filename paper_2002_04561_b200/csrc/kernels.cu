@@ -237,36 +237,9 @@ __global__ void classify_kernel(ClassifyArgs a) {
         a.keys[k] = ~0ull;
         a.vals[k] = (int32_t)k;
       } else {
-        const bool hasN = a.flags[k] & 1u;
-        // range guards (reading R11): |all intermediate values| bounded by the all-gap path
-        const int64_t padded = n + 192;  // max strip padding of any variant
-        const int64_t neg = 3 * (int64_t)a.cfg.bound_go + (padded + m + 2) * (int64_t)a.cfg.bound_ge + 256;
-        const int64_t posb = (int64_t)max(a.cfg.bound_match, 0) * (padded < m ? padded : m);
-        // VS16 stores global/semi scores with a +2^14 bias; Hop = H - (Go+Ge) is a packed
-        // 32-bit IMAD that must not borrow across halves -> biased values stay >= Go+Ge.
-        const bool ok16 = a.cfg.allow16 && !hasN &&
-                          neg + a.cfg.bound_go + a.cfg.bound_ge <= 16000 && posb <= 16000;
-        const bool ok32 = neg <= (1ll << 30) - (1ll << 24) && posb <= (1ll << 30) - (1ll << 24);
-        if (!ok32) atomicExch(&a.sum->range_err, 1);
-        if (a.cfg.force_variant >= 0) {
-          v = a.cfg.force_variant;
-          if (variant_desc(v).pairs == 2 && !ok16) v = a.cfg.tb ? 5 : 4;
-        } else {
-          int best_rows = 0x7fffffff, best_R = 0;
-          for (int c = 0; c < NV; ++c) {
-            const VariantDesc d = variant_desc(c);
-            if (d.tb != a.cfg.tb) continue;
-            if (d.pairs == 2 && !ok16) continue;
-            if (d.pairs == 1 && ok16) continue;
-            const int64_t hs = (int64_t)d.L * d.R;
-            const int64_t rows = (n + hs - 1) / hs * hs;
-            if (rows < best_rows || (rows == best_rows && d.R > best_R)) {
-              best_rows = (int)(rows < 0x7fffffff ? rows : 0x7fffffff);
-              best_R = d.R;
-              v = c;
-            }
-          }
-        }
+        const PairPlan pp = plan_pair(a.cfg, n, m, (a.flags[k] & 1u) != 0);
+        v = pp.v;
+        if (pp.range_err) atomicExch(&a.sum->range_err, 1);
         // speculative slots for the uniform case (every pair in one variant, identity
         // order); the host re-forms slots from the sorted order otherwise
         if (variant_desc(v).pairs == 2) {
@@ -282,13 +255,7 @@ __global__ void classify_kernel(ClassifyArgs a) {
           sl.pair[1] = -1;
           a.slots[k] = sl;
         }
-        // plan order: by variant, then largest (m, n) first (the fill hands out slots in
-        // this order, so the tail of a launch is made of the smallest slots)
-        constexpr int64_t KM = (1 << 29) - 1;
-        const int64_t mk = m < KM ? m : KM, nk = n < KM ? n : KM;
-        key = ((unsigned long long)v << 58) |
-              ((unsigned long long)(a.cfg.ascending ? mk : KM - mk) << 29) |
-              (unsigned long long)(a.cfg.ascending ? nk : KM - nk);
+        key = pp.key;
         a.keys[k] = key;
         a.vals[k] = (int32_t)k;
       }

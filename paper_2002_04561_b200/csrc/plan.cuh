@@ -50,4 +50,55 @@ struct PlanCfg {
   int32_t ascending;   // plan order smallest-first (debug; default largest-first)
 };
 
+// The plan of one non-empty pair (n, m >= 1): its variant, its sort key and whether it
+// exceeds the 32-bit range.  Shared by the device planner (classify_kernel) and the host
+// API's plan of uniform ACGT-only chunks, so that both decide identically.
+struct PairPlan {
+  int v;
+  unsigned long long key;
+  bool range_err;
+};
+__host__ __device__ inline PairPlan plan_pair(const PlanCfg& cfg, int64_t n, int64_t m, bool hasN) {
+  PairPlan pp;
+  pp.v = -1;
+  // range guards (reading R11): |all intermediate values| bounded by the all-gap path
+  const int64_t padded = n + 192;  // max strip padding of any variant
+  const int64_t neg = 3 * (int64_t)cfg.bound_go + (padded + m + 2) * (int64_t)cfg.bound_ge + 256;
+  const int64_t posb = (int64_t)(cfg.bound_match > 0 ? cfg.bound_match : 0) * (padded < m ? padded : m);
+  // VS16 stores scores with a +2^14 bias; Hop = H - (Go+Ge) is a packed 32-bit IMAD that
+  // must not borrow across halves -> biased values stay >= Go+Ge.
+  const bool ok16 = cfg.allow16 && !hasN &&
+                    neg + cfg.bound_go + cfg.bound_ge <= 16000 && posb <= 16000;
+  const bool ok32 = neg <= (1ll << 30) - (1ll << 24) && posb <= (1ll << 30) - (1ll << 24);
+  pp.range_err = !ok32;
+  if (cfg.force_variant >= 0) {
+    pp.v = cfg.force_variant;
+    if (variant_desc(pp.v).pairs == 2 && !ok16) pp.v = cfg.tb ? 5 : 4;
+  } else {
+    int64_t best_rows = 0x7fffffff;
+    int best_R = 0;
+    for (int c = 0; c < NV; ++c) {
+      const VariantDesc d = variant_desc(c);
+      if (d.tb != cfg.tb) continue;
+      if (d.pairs == 2 && !ok16) continue;
+      if (d.pairs == 1 && ok16) continue;
+      const int64_t hs = (int64_t)d.L * d.R;
+      const int64_t rows = (n + hs - 1) / hs * hs;
+      if (rows < best_rows || (rows == best_rows && d.R > best_R)) {
+        best_rows = rows < 0x7fffffff ? rows : 0x7fffffff;
+        best_R = d.R;
+        pp.v = c;
+      }
+    }
+  }
+  // plan order: by variant, then largest (m, n) first (the fill hands out slots in this
+  // order, so the tail of a launch is made of the smallest slots)
+  constexpr int64_t KM = (1 << 29) - 1;
+  const int64_t mk = m < KM ? m : KM, nk = n < KM ? n : KM;
+  pp.key = ((unsigned long long)pp.v << 58) |
+           ((unsigned long long)(cfg.ascending ? mk : KM - mk) << 29) |
+           (unsigned long long)(cfg.ascending ? nk : KM - nk);
+  return pp;
+}
+
 }  // namespace anyseq
