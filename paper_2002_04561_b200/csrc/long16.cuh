@@ -566,7 +566,9 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         step(ON, k + 1);
       }
       for (; k < kB; k += 2) {
-        if (!pump(k)) return false;
+        // steady state: the hand-off pump runs every 8 steps and when a batch falls due (a
+        // new batch is then requested at most 6 steps later, still ~2 periods ahead)
+        if (((k & 7) == 0 || (pf_b0 >= 0 && k + 2 >= pf_b0)) && !pump(k)) return false;
         if ((k % PER) == 0) {
           reframe();
           convert(k);
