@@ -277,7 +277,10 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       uint32_t pout = 0;            // OFF steps: staging slot of the task's last row
       uint32_t peck = 0;            // CKPT, OFF steps: staging slot of its E
       // LOCAL, OFF steps: track the running maximum in this period?  Skipped when no cell
-      // of the period can exceed it (see convert)
+      // of the period can exceed it (see convert).  Only the 1024-row instances: in the
+      // 512-row ones (128 registers) the extra live state cost more than the skip saved
+      // (1 Mbp local affine 0.64 -> 0.87 s)
+      constexpr bool SKIPTRK = NR >= 16;
       bool trk = true;
       int kck = -8;  // CKPT, OFF steps: the step whose low half (this step) or high half
                      // (next step) is at a checkpoint column, found once per period
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
             }
           }
         }
-        if (KIND == KLOCAL && (CHK || trk)) {
+        if (KIND == KLOCAL && (CHK || !SKIPTRK || trk)) {
           // local optimum: packed running maximum per half; strictly larger values only.
           // cmB = max over the half's rows but its first: when the first row holds the new
           // maximum (the common case where H falls down the rows, e.g. left of a similar
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
         const uint32_t r = h16_pack(cv(v.x), cv(v.y));
         ring_rel[wb][x] = r;
         if (x < MIR) ring_rel[wb][RING + x] = r;
-        if (KIND == KLOCAL) {
+        if (KIND == KLOCAL && SKIPTRK) {
           // every H of the coming period derives from the warp's current cells (max -margin
           // right after the re-base), the previous column's diagonal inputs and the input
           // row of columns [c0, c0 + 32), gaining at most max(sigma) per column along a
