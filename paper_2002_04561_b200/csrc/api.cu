@@ -135,6 +135,10 @@ struct anyseq_ctx {
   int64_t tb_leaf_cells = 1 << 20;  // long traceback: Hirschberg leaf size (cells)
   double tb_leaf_ms = 0;            // last anyseq_traceback_long: host time of the leaves
   LongOptions long_opt;
+  int64_t long_multi = 1;  // mixed batches: long pairs share one launch (run_long_multi)
+  int64_t skip_cells = 0;  // set by run_host_batch for its batch-kernel pass (DeviceJob)
+  int64_t long_multi_pairs = 0;   // ... pairs the last batch call ran that way
+  double long_multi_ms = 0;       // ... and that launch's kernel time
   int long_narrow = 0;   // the last anyseq_align_long ran the 16-bit differential kernel
   double long_ms = 0;    // ... and its kernel time (max over devices)
   double tb_pass_ms = 0, tb_pass_cells = 0;  // last anyseq_traceback_long: forward pass(es)
@@ -307,6 +311,7 @@ struct DeviceJob {
   uint64_t rebase_q0 = 0, rebase_s0 = 0;
   int64_t gen_q = -1, gen_s = -1;   // >= 0: offsets are k * gen (not uploaded), see prep
   int packed2 = 0;                  // d_q / d_s hold 2-bit codes (host-packed ACGT-only chunk)
+  int64_t skip_cells = 0;           // score mode: pairs this large are left to the long path
   uint64_t cig_base = 0;            // traceback: added to every cigar_offset of this job
   int32_t* d_scores_out;      // score mode output (device) or null => ctx buffer
   anyseq_alignment* d_aln_out;  // alignment structs (device) or null => ctx buffer
@@ -405,6 +410,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     ca.beg_i = D.beg_i.as<int32_t>();
     ca.beg_j = D.beg_j.as<int32_t>();
   }
+  ca.skip_cells = J.skip_cells;
   CK(launch_classify(ca, st, D.num_sms));
   L(1);
   ctx->mark(st, "classified");
@@ -415,7 +421,9 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   // while this one computes.
   PlanSummary S;
   bool host_plan = false;
-  if (J.packed2 && J.gen_q > 0 && J.gen_s > 0 && B > 0) {
+  const bool skipped_all = J.skip_cells > 0 && J.gen_q >= 2048 && J.gen_s >= 2048 &&
+                           J.gen_q * J.gen_s >= J.skip_cells;
+  if (J.packed2 && J.gen_q > 0 && J.gen_s > 0 && B > 0 && !skipped_all) {
     const PairPlan pp = plan_pair(ca.cfg, J.gen_q, J.gen_s, false);
     if (!pp.range_err && pp.v >= 0) {
       memset(&S, 0, sizeof(S));
@@ -1010,6 +1018,7 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     J.q_end = qlen;
     J.s_end = slen;
     J.tb = tb;
+    J.skip_cells = tb ? 0 : ctx->skip_cells;
     J.want_ends = aln != nullptr;
     J.d_scores_out = nullptr;
     J.d_aln_out = nullptr;
@@ -1126,6 +1135,7 @@ anyseq_status run_host_batch_core(anyseq_ctx* ctx, const anyseq_params* prm, con
         local.pack2 = ctx->pack2;
         local.tb8 = ctx->tb8;
         local.pack2_percent = ctx->pack2_percent;
+        local.skip_cells = ctx->skip_cells;
         local.shared_pool = ctx->pack2 ? ctx->packer() : nullptr;
         anyseq_status s = ANYSEQ_OK;
         if (bounds[g + 1] > bounds[g])  // an exception must not escape a std::thread either
@@ -1193,6 +1203,97 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
 // 8-lane group, the long kernel spreads it over many warps (C1, one 1000 x 1000 pair:
 // 1.3 ms instead of 5 ms with traceback).  A pair the long path cannot take (e.g. affine
 // traceback of a subject with N) falls back to the batch path on its own.
+// Score mode of a mixed batch without copying it: the batch kernels skip the long pairs
+// (classify leaves pairs of >= batch_long_cells cells unplanned, ClassifyArgs::skip_cells)
+// and run while the long pairs share one launch of the long kernel (run_long_multi, one
+// device); their results are then written into the caller's outputs.  Long pairs the shared
+// launch does not take run one by one (anyseq_align_long, else the batch path alone).
+static anyseq_status run_host_batch_inplace(anyseq_ctx* ctx, const anyseq_params* prm,
+                                            const anyseq_batch* b,
+                                            const std::vector<uint64_t>& longs, int32_t* scores,
+                                            anyseq_alignment* aln) {
+  const uint64_t BL = longs.size();
+  struct SkipGuard {  // the batch pass skips the long pairs; nothing after it does
+    anyseq_ctx* c;
+    ~SkipGuard() { c->skip_cells = 0; }
+  } guard{ctx};
+  ctx->skip_cells = ctx->batch_long_cells;
+  auto run_short = [&]() -> int {
+    const anyseq_status r = run_host_batch_core(ctx, prm, b, 0, scores, aln, nullptr, 0, nullptr);
+    ctx->skip_cells = 0;
+    return r;
+  };
+  std::vector<int> done(BL, 0);
+  auto put = [&](uint64_t k, int32_t score, int64_t ei, int64_t ej) {
+    scores[k] = score;
+    if (aln) {
+      anyseq_alignment a;
+      memset(&a, 0, sizeof(a));
+      a.score = score;
+      a.q_end = a.q_begin = ei;
+      a.s_end = a.s_begin = ej;
+      aln[k] = a;
+    }
+  };
+  if (ctx->long_multi && BL >= 2 && ctx->devs.size() == 1) {
+    std::vector<LongPairIn> in(BL);
+    for (uint64_t x = 0; x < BL; ++x) {
+      const uint64_t k = longs[x];
+      in[x] = LongPairIn{b->q + b->q_off[k], b->q_off[k + 1] - b->q_off[k], b->s + b->s_off[k],
+                         b->s_off[k + 1] - b->s_off[k]};
+    }
+    const Device& D = ctx->devs[0];
+    LongDevice ld;
+    ld.id = D.id;
+    ld.stream = D.stream;
+    ld.num_sms = D.num_sms;
+    ld.ws = ctx->lws[0].get();
+    std::vector<LongResult> lr;
+    std::vector<int> took;
+    std::string err;
+    uint64_t launches = 0;
+    double kms = 0;
+    int rs = ANYSEQ_OK;
+    const int rc = run_long_multi(ld, dev_params(prm), in, ctx->long_opt, &lr, &took, &err,
+                                  &launches, &kms, [&]() { return rs = run_short(); });
+    ctx->launches += launches;
+    if (rs != ANYSEQ_OK) return (anyseq_status)rs;
+    if (rc != 0) return fail(ctx, (anyseq_status)rc, "long pairs (one launch): %s", err.c_str());
+    for (uint64_t x = 0; x < BL; ++x)
+      if (took[x]) {
+        done[x] = 1;
+        put(longs[x], lr[x].score, lr[x].end_i, lr[x].end_j);
+        ++ctx->long_multi_pairs;
+      }
+    ctx->long_multi_ms = kms;
+  } else {
+    const anyseq_status r = (anyseq_status)run_short();
+    if (r != ANYSEQ_OK) return r;
+  }
+  for (uint64_t x = 0; x < BL; ++x) {
+    if (done[x]) continue;
+    const uint64_t k = longs[x];
+    const char* qk = b->q + b->q_off[k];
+    const char* sk = b->s + b->s_off[k];
+    const uint64_t n = b->q_off[k + 1] - b->q_off[k], m = b->s_off[k + 1] - b->s_off[k];
+    anyseq_alignment a;
+    anyseq_status r = anyseq_align_long(ctx, prm, qk, n, sk, m, &a);
+    if (r == ANYSEQ_E_UNSUPPORTED) {  // not for the long path: this pair on the batch path
+      const uint64_t qo1[2] = {0, n}, so1[2] = {0, m};
+      const anyseq_batch b1{qk, qo1, sk, so1, 1};
+      r = run_host_batch_core(ctx, prm, &b1, 0, scores + k, aln ? aln + k : nullptr, nullptr, 0,
+                              nullptr);
+      if (r == ANYSEQ_OK) continue;
+    }
+    if (r != ANYSEQ_OK) {
+      ctx->err = "pair " + std::to_string(k) + " (long-pair path): " + ctx->err;
+      return r;
+    }
+    put(k, a.score, a.q_end, a.s_end);
+  }
+  return ANYSEQ_OK;
+}
+
 anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const anyseq_batch* b,
                              int tb, int32_t* scores, anyseq_alignment* aln, uint32_t* cigar,
                              uint64_t cap, uint64_t* used) {
@@ -1217,6 +1318,9 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
         longs.push_back(k);
     }
   if (longs.empty()) return run_host_batch_core(ctx, prm, b, tb, scores, aln, cigar, cap, used);
+  ctx->long_multi_pairs = 0;
+  ctx->long_multi_ms = 0;
+  if (!tb && !small) return run_host_batch_inplace(ctx, prm, b, longs, scores, aln);
   // the other pairs, compacted
   const uint64_t B = b->num_pairs, BL = longs.size(), BS = B - BL;
   std::vector<uint64_t> rest;
@@ -1241,17 +1345,69 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
   std::vector<anyseq_alignment> al2((aln || tb) ? BS : 0);
   std::vector<uint32_t> cg2;
   uint64_t used2 = 0;
-  if (BS) {
+  auto run_short = [&]() -> int {
+    if (!BS) return ANYSEQ_OK;
     if (tb) cg2.resize(std::max<uint64_t>(cq.size() + cs.size() + BS, 1));
-    const anyseq_status r = run_host_batch_core(ctx, prm, &b2, tb, sc2.data(),
-                                                al2.empty() ? nullptr : al2.data(),
-                                                tb ? cg2.data() : nullptr, cg2.size(), &used2);
-    if (r != ANYSEQ_OK) return r;
-  }
-  // the long pairs
+    return run_host_batch_core(ctx, prm, &b2, tb, sc2.data(), al2.empty() ? nullptr : al2.data(),
+                               tb ? cg2.data() : nullptr, cg2.size(), &used2);
+  };
+  // the long pairs: score-only on one device -> the bands of all of them in ONE launch
+  // (run_long_multi, the device-side queue of SURVEY 8(f) f4) on the workspace's own
+  // stream, and the short pairs' batch pipeline runs while it is in flight (its kernels
+  // take the SMs the long launch's blocks leave as its queue drains); pairs the shared
+  // launch does not take (subject with N, range guard) and traceback go one by one below
   std::vector<anyseq_alignment> al3(BL);
   std::vector<std::vector<uint32_t>> cg3(BL);
+  std::vector<int> done(BL, 0);
+  const bool multi = !tb && ctx->long_multi && BL >= 2 && ctx->devs.size() == 1;
+  if (!multi) {
+    const int r = run_short();
+    if (r != ANYSEQ_OK) return (anyseq_status)r;
+  } else {
+    std::vector<uint64_t> ord(BL);
+    for (uint64_t x = 0; x < BL; ++x) ord[x] = x;
+    auto cells = [&](uint64_t x) {
+      const uint64_t k = longs[x];
+      return (long double)(b->q_off[k + 1] - b->q_off[k]) * (long double)(b->s_off[k + 1] - b->s_off[k]);
+    };
+    std::stable_sort(ord.begin(), ord.end(), [&](uint64_t u, uint64_t v) { return cells(u) > cells(v); });
+    std::vector<LongPairIn> in(BL);
+    for (uint64_t y = 0; y < BL; ++y) {
+      const uint64_t k = longs[ord[y]];
+      in[y] = LongPairIn{b->q + b->q_off[k], b->q_off[k + 1] - b->q_off[k], b->s + b->s_off[k],
+                         b->s_off[k + 1] - b->s_off[k]};
+    }
+    const Device& D = ctx->devs[0];
+    LongDevice ld;
+    ld.id = D.id;
+    ld.stream = D.stream;
+    ld.num_sms = D.num_sms;
+    ld.ws = ctx->lws[0].get();
+    std::vector<LongResult> lr;
+    std::vector<int> took;
+    std::string err;
+    uint64_t launches = 0;
+    double kms = 0;
+    int rs = ANYSEQ_OK;
+    const int rc = run_long_multi(ld, dev_params(prm), in, ctx->long_opt, &lr, &took, &err,
+                                  &launches, &kms, [&]() { return rs = run_short(); });
+    ctx->launches += launches;
+    if (rs != ANYSEQ_OK) return (anyseq_status)rs;
+    if (rc != 0) return fail(ctx, (anyseq_status)rc, "long pairs (one launch): %s", err.c_str());
+    for (uint64_t y = 0; y < BL; ++y) {
+      if (!took[y]) continue;
+      const uint64_t x = ord[y];
+      done[x] = 1;
+      memset(&al3[x], 0, sizeof(al3[x]));
+      al3[x].score = lr[y].score;
+      al3[x].q_end = al3[x].q_begin = lr[y].end_i;
+      al3[x].s_end = al3[x].s_begin = lr[y].end_j;
+      ++ctx->long_multi_pairs;
+    }
+    ctx->long_multi_ms = kms;
+  }
   for (uint64_t x = 0; x < BL; ++x) {
+    if (done[x]) continue;
     const uint64_t k = longs[x];
     const char* qk = b->q + b->q_off[k];
     const char* sk = b->s + b->s_off[k];
@@ -1968,6 +2124,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
     if (n == "pack2") { ctx->pack2 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "tb8") { ctx->tb8 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "batch_long_cells") { ctx->batch_long_cells = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
+    if (n == "long_multi") { ctx->long_multi = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "batch_long_small") { ctx->batch_long_small = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
     if (n == "pack2_percent") {
       if (value < 0 || value > 100) return fail(ctx, ANYSEQ_E_INVALID, "pack2_percent in [0, 100]");
@@ -2076,6 +2233,8 @@ anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) 
     if (n == "fill_ms") { *value = ctx->fill_ms; return ANYSEQ_OK; }
     if (n == "walk_ms") { *value = ctx->walk_ms; return ANYSEQ_OK; }
     if (n == "long_narrow") { *value = ctx->long_narrow; return ANYSEQ_OK; }
+    if (n == "long_multi_pairs") { *value = (double)ctx->long_multi_pairs; return ANYSEQ_OK; }
+    if (n == "long_multi_ms") { *value = ctx->long_multi_ms; return ANYSEQ_OK; }
     if (n == "long_kernel_ms") { *value = ctx->long_ms; return ANYSEQ_OK; }
     if (n == "tb_pass_ms") { *value = ctx->tb_pass_ms; return ANYSEQ_OK; }
     if (n == "tb_pass_cells") { *value = ctx->tb_pass_cells; return ANYSEQ_OK; }

@@ -872,4 +872,321 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
   return 0;
 }
 
+
+// run_long_multi: one block per pair folds the warps' partial optima of that pair (the
+// host-side fold of run_long, on the device: K pairs x resident warps entries)
+__global__ void parts_reduce_kernel(const LongPart* __restrict__ parts, int nw, LongPart* out) {
+  __shared__ LongPart sh[256];
+  const LongPart* p = parts + (size_t)blockIdx.x * nw;
+  LongPart b;
+  memset(&b, 0, sizeof(b));
+  for (int x = threadIdx.x; x < nw; x += blockDim.x) {
+    const LongPart q = p[x];
+    if (q.lv > b.lv || (q.lv == b.lv && (q.lj < b.lj || (q.lj == b.lj && q.li < b.li)))) {
+      b.lv = q.lv; b.li = q.li; b.lj = q.lj;
+    }
+    if (q.gset) { b.gv = q.gv; b.gset = 1; }
+  }
+  sh[threadIdx.x] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int x = 1; x < (int)blockDim.x; ++x) {
+      const LongPart& q = sh[x];
+      if (q.lv > b.lv || (q.lv == b.lv && (q.lj < b.lj || (q.lj == b.lj && q.li < b.li)))) {
+        b.lv = q.lv; b.li = q.li; b.lj = q.lj;
+      }
+      if (q.gset) { b.gv = q.gv; b.gset = 1; }
+    }
+    out[blockIdx.x] = b;
+  }
+}
+
+int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPairIn>& pairs,
+                   const LongOptions& opt, std::vector<LongResult>* out, std::vector<int>* taken,
+                   std::string* err, uint64_t* launches, double* kernel_ms,
+                   const std::function<int()>& during) {
+  const size_t K0 = pairs.size();
+  out->assign(K0, LongResult{0, 0, 0, 0.0, true});
+  taken->assign(K0, 0);
+  *kernel_ms = 0;
+  // the eligibility rules of run_long's 16-bit path at 512-row tasks (NR = 8)
+  constexpr int NR = 8, HS = 64 * NR;
+  const int64_t d16 = (int64_t)P.go + P.ge + std::max(P.smax, 0);
+  const int64_t margin16 = 100 * d16 + 16;
+  const int NEG16C = -24576;
+  const int64_t bspan16 = (int64_t)(64 * NR + 66) * d16;
+  const bool fits = 2 * bspan16 + margin16 + 96 * d16 + P.go + P.ge + 256 < -NEG16C &&
+                    (int64_t)P.go + 2 * P.ge < 4096;
+  std::vector<size_t> sel;
+  for (size_t k = 0; k < K0 && fits; ++k) {
+    const uint64_t n = pairs[k].n, m = pairs[k].m;
+    if (n == 0 || m == 0 || n >= (1ull << 31) || m >= (1ull << 31)) continue;
+    const long double neg = 3.0L * P.go + ((long double)n + m + 2) * P.ge + 256;
+    const long double pos = (long double)std::max(P.smax, 0) * std::min(n, m);
+    if (neg > (1u << 30) - (1u << 24) || pos > (1u << 30) - (1u << 24)) continue;
+    bool ok = true;
+    for (uint64_t x = 0; x < m && ok; ++x) ok = (pairs[k].s[x] | 0x20) != 'n';
+    if (ok) sel.push_back(k);
+  }
+  const int K = (int)sel.size();
+  if (K == 0) return during ? during() : 0;
+  LK(cudaSetDevice(dev.id));
+  cudaStream_t st = dev.stream;
+  if (dev.ws && during) {
+    if (!dev.ws->stream) LK(cudaStreamCreateWithFlags(&dev.ws->stream, cudaStreamNonBlocking));
+    st = dev.ws->stream;
+  }
+  LongFn fn = long16_multi_fn(P.kind);
+  int nb = 0;
+  LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0));
+  int grid = dev.num_sms * std::max(nb, 1);
+  if (opt.blocks > 0) grid = std::min(grid, opt.blocks);
+  const int nw = grid * 4;
+  // column passes per pair: tasks no wider than a quarter of the launch's mean work per
+  // warp (>= 4096 columns), so the last tasks handed out are short; option long_strips
+  // forces the count.  Tickets: pass by pass over the pairs, widest tasks first (LPT).
+  std::vector<int> S(K), G(K);
+  double Tw = 0;
+  for (int x = 0; x < K; ++x) {
+    S[x] = (int)((pairs[sel[x]].n + HS - 1) / HS);
+    Tw += (double)S[x] * ((double)pairs[sel[x]].m + 64);
+  }
+  Tw /= nw;
+  const double Wt = std::max(4096.0, Tw / 4);
+  int Gmax = 1;
+  for (int x = 0; x < K; ++x) {
+    const uint64_t m = pairs[sel[x]].m;
+    const int g = opt.virtual_strips > 0 ? opt.virtual_strips
+                                         : (int)std::min(16.0, std::ceil((double)m / Wt));
+    G[x] = (int)std::min<uint64_t>((uint64_t)std::max(g, 1), m);
+    Gmax = std::max(Gmax, G[x]);
+  }
+  std::vector<int> ord(K);
+  for (int x = 0; x < K; ++x) ord[x] = x;
+  std::stable_sort(ord.begin(), ord.end(), [&](int u, int v) {
+    return (double)pairs[sel[u]].m / G[u] > (double)pairs[sel[v]].m / G[v];
+  });
+  std::vector<int2> segs;
+  std::vector<int32_t> task_end;
+  int64_t tasks = 0;
+  for (int g = 0; g < Gmax; ++g)
+    for (int x : ord)
+      if (G[x] > g) {
+        segs.push_back(make_int2(x, g));
+        tasks += S[x];
+        if (tasks >= (1ll << 31)) {
+          *err = "long pairs: too many tasks in one launch";
+          return ANYSEQ_E_UNSUPPORTED;
+        }
+        task_end.push_back((int32_t)tasks);
+      }
+  const int NS = (int)segs.size();
+  // per-pair offsets into the launch-wide buffers
+  std::vector<uint64_t> qo(K + 1, 0), so(K + 1, 0);
+  std::vector<int64_t> rowo(K + 1, 0), bco(K + 1, 0), flo(K + 1, 0), cbo(K + 1, 0);
+  for (int x = 0; x < K; ++x) {
+    const uint64_t n = pairs[sel[x]].n, m = pairs[sel[x]].m;
+    qo[x + 1] = qo[x] + n;
+    so[x + 1] = so[x] + m;
+    rowo[x + 1] = rowo[x] + (int64_t)m + 1;
+    const int extra = P.kind == KSEMI ? 1 : 0;  // SEMI keeps column m (edge G)
+    bco[x + 1] = bco[x] + (int64_t)(G[x] + extra) * (int64_t)(n + 1);
+    flo[x + 1] = flo[x] + (int64_t)G[x] * S[x];
+    cbo[x + 1] = cbo[x] + G[x] + 1;
+  }
+  LongWs* ws = dev.ws;
+  Buf qa, sa, qc, sc, sum, flg, off, rowbuf, bcol, flags, cbuf, bptr, fptr, ticket, abort_, parts,
+      mp, mt, ms_, red, kb;
+  // ASCII upload + pack (all pairs in one pack launch)
+  std::string cq, cs;
+  cq.reserve(qo[K]);
+  cs.reserve(so[K]);
+  for (int x = 0; x < K; ++x) {
+    cq.append(pairs[sel[x]].q, pairs[sel[x]].n);
+    cs.append(pairs[sel[x]].s, pairs[sel[x]].m);
+  }
+  LK(get_buf(qa, ws, WS_QA, qo[K] + 16));
+  LK(get_buf(sa, ws, WS_SA, so[K] + 16));
+  LK(get_buf(qc, ws, WS_QC, qo[K] + 16));
+  LK(get_buf(sc, ws, WS_SC, so[K] + 16));
+  LK(get_buf(sum, ws, WS_SUM, sizeof(PlanSummary)));
+  LK(get_buf(flg, ws, WS_FLG, (size_t)K * 4 + 16));
+  LK(get_buf(off, ws, WS_OFF, (size_t)2 * (K + 1) * 8));
+  LK(cudaMemcpyAsync(qa.p, cq.data(), qo[K], cudaMemcpyHostToDevice, st));
+  LK(cudaMemcpyAsync(sa.p, cs.data(), so[K], cudaMemcpyHostToDevice, st));
+  LK(cudaMemcpyAsync(off.p, qo.data(), (K + 1) * 8, cudaMemcpyHostToDevice, st));
+  LK(cudaMemcpyAsync((uint64_t*)off.p + K + 1, so.data(), (K + 1) * 8, cudaMemcpyHostToDevice, st));
+  PlanSummary hs;
+  memset(&hs, 0, sizeof(hs));
+  hs.err_pos = ~0ull;
+  LK(cudaMemcpyAsync(sum.p, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+  LK(launch_pack((const char*)qa.p, qo[K], (uint8_t*)qc.p, (const uint64_t*)off.p,
+                 (const char*)sa.p, so[K], (uint8_t*)sc.p, (const uint64_t*)off.p + K + 1,
+                 (uint64_t)K, (uint32_t*)flg.p, (PlanSummary*)sum.p, st, dev.num_sms));
+  *launches += 1;
+  LK(cudaMemcpyAsync(&hs, sum.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  LK(cudaStreamSynchronize(st));
+  if (hs.err_pos != ~0ull) {
+    *err = "invalid symbol in a long pair";
+    return ANYSEQ_E_BADSEQ;
+  }
+  // DP state of every pair
+  LK(get_buf(rowbuf, ws, WS_ROWBUF, (size_t)rowo[K] * sizeof(int4)));
+  LK(get_buf(bcol, ws, WS_BCOL, (size_t)bco[K] * sizeof(int2)));
+  LK(get_buf(flags, ws, WS_FLAGS, (size_t)flo[K] * 4));
+  LK(get_buf(cbuf, ws, WS_CB, (size_t)cbo[K] * 4));
+  LK(get_buf(bptr, ws, WS_BPTR, (size_t)cbo[K] * sizeof(int2*)));
+  LK(get_buf(fptr, ws, WS_FPTR, (size_t)cbo[K] * sizeof(int32_t*)));
+  LK(get_buf(ticket, ws, WS_TICKET, 4));
+  LK(get_buf(abort_, ws, WS_ABORT, 4));
+  LK(get_buf(parts, ws, WS_PARTS, (size_t)K * nw * sizeof(LongPart)));
+  LK(get_buf(mp, ws, WS_M_PAIRS, (size_t)K * sizeof(LongArgs)));
+  LK(get_buf(mt, ws, WS_M_TASKS, (size_t)NS * 4));
+  LK(get_buf(ms_, ws, WS_M_SEGS, (size_t)NS * sizeof(int2)));
+  LK(get_buf(red, ws, WS_M_RED, (size_t)K * sizeof(LongPart)));
+  if (P.kind == KSEMI) LK(get_buf(kb, ws, WS_KEY, (size_t)K * 8));
+  LK(cudaMemsetAsync(flags.p, 0, (size_t)flo[K] * 4, st));
+  LK(cudaMemsetAsync(ticket.p, 0, 4, st));
+  LK(cudaMemsetAsync(abort_.p, 0, 4, st));
+  LK(cudaMemsetAsync(parts.p, 0, (size_t)K * nw * sizeof(LongPart), st));
+  if (P.kind == KSEMI) LK(cudaMemsetAsync(kb.p, 0, (size_t)K * 8, st));
+  std::vector<int32_t> cb_h(cbo[K]);
+  std::vector<int2*> bp_h(cbo[K], nullptr);
+  std::vector<int32_t*> fp_h(cbo[K], nullptr);
+  std::vector<LongArgs> la(K);
+  const int c = P.go + P.ge;
+  const int32_t hopc =
+      c == 0 ? 0 : (int32_t)((((uint32_t)(-c - 1) & 0xffffu) << 16) | (uint32_t)((65536 - c) & 0xffff));
+  for (int x = 0; x < K; ++x) {
+    const uint64_t n = pairs[sel[x]].n, m = pairs[sel[x]].m;
+    const int Gx = G[x];
+    for (int g = 0; g <= Gx; ++g) cb_h[cbo[x] + g] = (int32_t)((m * (uint64_t)g) / Gx);
+    int2* bc = (int2*)bcol.p + bco[x];
+    for (int g = 0; g < Gx + (P.kind == KSEMI ? 1 : 0); ++g) bp_h[cbo[x] + g] = bc + (size_t)g * (n + 1);
+    for (int g = 0; g < Gx; ++g) fp_h[cbo[x] + g] = (int32_t*)flags.p + flo[x] + (size_t)g * S[x];
+    LongArgs& a = la[x];
+    memset(&a, 0, sizeof(a));
+    a.P = P;
+    a.qc = (const uint8_t*)qc.p + qo[x];
+    a.sc = (const uint8_t*)sc.p + so[x];
+    a.n = (int)n;
+    a.m = (int)m;
+    a.Gtot = Gx;
+    a.g_first = 0;
+    a.g_count = Gx;
+    a.cb = (const int32_t*)cbuf.p + cbo[x];
+    a.S = S[x];
+    a.ticket = (int32_t*)ticket.p;
+    a.rowprog = nullptr;
+    a.bflag = (int32_t* const*)fptr.p + cbo[x];
+    a.bcol = (int2* const*)bptr.p + cbo[x];
+    a.rowbuf = (int4*)rowbuf.p + rowo[x];
+    a.parts = (LongPart*)parts.p + (size_t)x * nw;
+    a.abort_flag = (int32_t*)abort_.p;
+    a.chunk = 256;
+    a.one = 1;
+    a.lag = opt.start_lag;
+    a.keyed = (long double)std::max(P.smax, 0) * std::min(n, m) < (long double)(1 << 25) ? 1 : 0;
+    a.hopc = hopc;
+    a.neg16 = NEG16C;
+    a.sleep_ns = opt.sleep_ns;
+    a.margin = (int32_t)margin16;
+    a.bspan = (int32_t)bspan16;
+    a.pad_top = P.kind == KSEMI ? (int)((uint64_t)S[x] * HS - n) : 0;
+    a.ck_every = 1;
+    a.kc_shift = 30;
+    a.spin_limit = opt.spin_limit;
+    a.stall_task = -1;
+  }
+  LK(cudaMemcpyAsync(cbuf.p, cb_h.data(), cb_h.size() * 4, cudaMemcpyHostToDevice, st));
+  LK(cudaMemcpyAsync(bptr.p, bp_h.data(), bp_h.size() * sizeof(int2*), cudaMemcpyHostToDevice, st));
+  LK(cudaMemcpyAsync(fptr.p, fp_h.data(), fp_h.size() * sizeof(int32_t*), cudaMemcpyHostToDevice, st));
+  LK(cudaMemcpyAsync(mp.p, la.data(), (size_t)K * sizeof(LongArgs), cudaMemcpyHostToDevice, st));
+  LK(cudaMemcpyAsync(mt.p, task_end.data(), (size_t)NS * 4, cudaMemcpyHostToDevice, st));
+  LK(cudaMemcpyAsync(ms_.p, segs.data(), (size_t)NS * sizeof(int2), cudaMemcpyHostToDevice, st));
+  for (int x = 0; x < K; ++x) {
+    const uint64_t n = pairs[sel[x]].n, m = pairs[sel[x]].m;
+    const int gi = (int)std::min<uint64_t>((std::max(n, m) + 256) / 256, (uint64_t)dev.num_sms * 4);
+    long_init_kernel<<<gi, 256, 0, st>>>(P, (int)n, (int)m, la[x].rowbuf, bp_h[cbo[x]],
+                                         la[x].bcol, la[x].cb, G[x], 0, G[x]);
+    LK(cudaGetLastError());
+    *launches += 1;
+  }
+  LongArgs a0 = la[0];
+  a0.pairs = (const LongArgs*)mp.p;
+  a0.task_end = (const int32_t*)mt.p;
+  a0.segs = (const int2*)ms_.p;
+  a0.task_total = (int32_t)tasks;
+  a0.stall_task = opt.stall_task;
+  a0.prof = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  LK(cudaEventCreate(&e0));
+  LK(cudaEventCreate(&e1));
+  LK(cudaEventRecord(e0, st));
+  fn<<<grid, 128, 0, st>>>(a0);
+  LK(cudaGetLastError());
+  LK(cudaEventRecord(e1, st));
+  *launches += 1;
+  parts_reduce_kernel<<<K, 256, 0, st>>>((const LongPart*)parts.p, nw, (LongPart*)red.p);
+  LK(cudaGetLastError());
+  *launches += 1;
+  if (P.kind == KSEMI)
+    for (int x = 0; x < K; ++x) {
+      const uint64_t n = pairs[sel[x]].n, m = pairs[sel[x]].m;
+      const int gi = (int)std::min<uint64_t>((n + m + 256) / 256, (uint64_t)dev.num_sms * 4);
+      semi_reduce_kernel<<<gi, 256, 0, st>>>((const int4*)la[x].rowbuf, 1, (int)m, (int)m,
+                                             bp_h[cbo[x] + G[x]], (int)n,
+                                             (unsigned long long*)kb.p + x);
+      LK(cudaGetLastError());
+      *launches += 1;
+    }
+  // the caller's work in the shadow of the launch (results are read after it: pageable
+  // device-to-host copies would block the host until the kernel ends)
+  const int rd = during ? during() : 0;
+  std::vector<LongPart> rp(K);
+  std::vector<unsigned long long> keys(P.kind == KSEMI ? K : 0);
+  int ab = 0;
+  LK(cudaMemcpyAsync(rp.data(), red.p, (size_t)K * sizeof(LongPart), cudaMemcpyDeviceToHost, st));
+  if (P.kind == KSEMI)
+    LK(cudaMemcpyAsync(keys.data(), kb.p, (size_t)K * 8, cudaMemcpyDeviceToHost, st));
+  LK(cudaMemcpyAsync(&ab, abort_.p, 4, cudaMemcpyDeviceToHost, st));
+  LK(cudaStreamSynchronize(st));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *kernel_ms = ms;
+  if (rd != 0) return rd;
+  if (ab) {
+    *err = "long kernel: a boundary wait exceeded its bound";
+    return ANYSEQ_E_TIMEOUT;
+  }
+  for (int x = 0; x < K; ++x) {
+    const size_t k = sel[x];
+    const int64_t n = (int64_t)pairs[k].n, m = (int64_t)pairs[k].m;
+    LongResult& r = (*out)[k];
+    r.narrow = true;
+    r.kernel_ms = ms;
+    if (P.kind == KLOCAL) {
+      r.score = rp[x].lv; r.end_i = rp[x].li; r.end_j = rp[x].lj;
+    } else if (P.kind == KSEMI) {
+      // (n, 0) = 0 is the first candidate (seq 0), as in run_long
+      unsigned long long key = ((unsigned long long)0x80000000u << 32) | 0xFFFFFFFFu;
+      key = std::max(key, keys[x]);
+      const uint32_t seq = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
+      r.score = (int32_t)((uint32_t)(key >> 32) ^ 0x80000000u);
+      if (seq < (uint64_t)m) { r.end_i = n; r.end_j = seq; }
+      else { r.end_i = (int64_t)(seq - m); r.end_j = m; }
+    } else {
+      if (!rp[x].gset) {
+        *err = "long kernel: global end cell not produced";
+        return ANYSEQ_E_CUDA;
+      }
+      r.score = rp[x].gv; r.end_i = n; r.end_j = m;
+    }
+    (*taken)[k] = 1;
+  }
+  return 0;
+}
+
 }  // namespace anyseq

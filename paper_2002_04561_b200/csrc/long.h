@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 #include "common.cuh"
@@ -30,7 +31,9 @@ enum { WS_QA, WS_SA, WS_QC, WS_SC, WS_SUM, WS_FLG, WS_OFF, WS_ROWBUF, WS_PROG, W
        WS_ABORT, WS_CB, WS_BPTR, WS_FPTR, WS_BCOL, WS_FLAGS, WS_PARTS, WS_PROF, WS_KEY,
        WS_ROWCK, WS_COLCK,
        // long traceback walk (long_tb.cu)
-       WS_TB_SCRATCH, WS_TB_OPS, WS_TB_OUT, WS_TB_SLOTS, WS_TB_SYNC, WS_TB_JOBS, WS_COUNT };
+       WS_TB_SCRATCH, WS_TB_OPS, WS_TB_OUT, WS_TB_SLOTS, WS_TB_SYNC, WS_TB_JOBS,
+       // several pairs in one launch (run_long_multi)
+       WS_M_PAIRS, WS_M_TASKS, WS_M_SEGS, WS_M_RED, WS_COUNT };
 
 struct LongWs {
   static constexpr int kSlots = WS_COUNT;
@@ -55,7 +58,11 @@ struct LongWs {
       cap[k] = 0;
     }
   }
-  ~LongWs() { release(); }
+  cudaStream_t stream = nullptr;  // run_long_multi's own stream (created on first use)
+  ~LongWs() {
+    release();
+    if (stream) cudaStreamDestroy(stream);
+  }
 };
 
 struct LongDevice {
@@ -96,5 +103,25 @@ struct LongCkpt {
 int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, uint64_t n,
              const char* s, uint64_t m, const LongOptions& opt, LongResult* out, std::string* err,
              uint64_t* launches, LongCkpt* ck = nullptr);
+
+// Several long pairs in ONE launch of the 16-bit kernel (device-side form;
+// DESIGN.md 5.4d): score-only, one device, the pairs' row-strip tasks in one ticket queue
+// (column pass by column pass; within a pass the pairs with the widest tasks first), so the
+// bands of many pairs run side by side and a pair's fill/drain is covered by the others.  A pair the
+// 16-bit kernel cannot take (subject with N, range guard, empty) is left alone: taken[k] = 0
+// and the caller runs it through run_long.  Results of taken pairs are bit-identical to
+// run_long's (same kernel body, same optimum rules).  `during` (optional) runs on the host
+// while the launch is in flight (it runs even when no pair is taken); the launch uses the
+// workspace's own non-blocking stream, so work `during` enqueues elsewhere overlaps it.
+struct LongPairIn {
+  const char* q;
+  uint64_t n;
+  const char* s;
+  uint64_t m;
+};
+int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPairIn>& pairs,
+                   const LongOptions& opt, std::vector<LongResult>* out, std::vector<int>* taken,
+                   std::string* err, uint64_t* launches, double* kernel_ms,
+                   const std::function<int()>& during = {});
 
 }  // namespace anyseq

@@ -53,9 +53,16 @@ __device__ __forceinline__ uint32_t h16_pack(int lo, int hi) {
 #ifndef LONG16_MINB
 #define LONG16_MINB 3  // resident blocks per SM asked of ptxas for 1024-row tasks (A/B builds: 4)
 #endif
-template <int NR, int KIND, bool CKPT = false>
+// MULTI: one launch over the tasks of several pairs (same
+// scheme and kind): a_.pairs[p] holds pair p's arguments; tickets run through segments
+// a_.segs[k] = (pair, column pass) -- every pair's pass 0, then every pair's pass 1, ... --
+// with a_.task_end the inclusive prefix of the segments' S, so a task is handed out only
+// after every task of the passes to its left.  A warp merges its partial optimum into the
+// pair's parts entry when its next ticket belongs to another pair.  Every task still waits
+// only on lower tickets of its own pair, so the deadlock argument of one pair carries over.
+template <int NR, int KIND, bool CKPT = false, bool MULTI = false>
 __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) ? 4 : 3)
-    long16_kernel(LongArgs a) {
+    long16_kernel(LongArgs a_) {
   constexpr int HS = 64 * NR;  // rows per task: 32 lanes x 2 halves x NR
   constexpr int RING = 256;
   constexpr int PER = 32;
@@ -75,14 +82,13 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
   const int t = threadIdx.x & 31;
   const int wb = threadIdx.x >> 5;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const DevParams P = a.P;
+  const DevParams P = a_.P;
   const int cop = P.go + P.ge;
   const uint32_t NGE2 = VS16::splat(-P.ge);
-  const uint32_t one = (uint32_t)a.one;
-  const int hopc = a.hopc;  // packed (-cop, -cop) with the low half's borrow pre-compensated
+  const uint32_t one = (uint32_t)a_.one;
+  const int hopc = a_.hopc;  // packed (-cop, -cop) with the low half's borrow pre-compensated
   auto hop = [&](uint32_t h) -> uint32_t { return (uint32_t)imad_add_s((int)h, one, hopc); };
-  const int NEGc = a.neg16;
-  const int n = a.n;
+  const int NEGc = a_.neg16;
   // subject codes of columns past a task's end are read (and ignored) by the warp's last
   // steps: keep every ring entry a valid code so the active half's selector stays intact
   for (int x = t; x < RING + MIR; x += 32) {
@@ -104,13 +110,50 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
   part.lv = 0; part.li = 0; part.lj = 0;
   part.rv = 0; part.rj = 0; part.cv = 0; part.ci = 0; part.gv = 0; part.gset = 0; part.pad_ = 0;
 
+  // the warp's partial optimum -> its entry in parts (warp-collective)
+  auto flush_part = [&](LongPart* parts, bool merge) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int lv = __shfl_xor_sync(0xffffffffu, part.lv, o);
+      const int li = __shfl_xor_sync(0xffffffffu, part.li, o);
+      const int lj = __shfl_xor_sync(0xffffffffu, part.lj, o);
+      if (lkey_better(lv, li, lj, part.lv, part.li, part.lj)) { part.lv = lv; part.li = li; part.lj = lj; }
+      const int gv = __shfl_xor_sync(0xffffffffu, part.gv, o);
+      const int gs = __shfl_xor_sync(0xffffffffu, part.gset, o);
+      if (gs && !part.gset) { part.gv = gv; part.gset = 1; }
+    }
+    if (t == 0) {
+      if (merge) {  // MULTI: the warp's earlier passes over the same pair
+        const LongPart q = parts[wg];
+        if (lkey_better(q.lv, q.li, q.lj, part.lv, part.li, part.lj)) { part.lv = q.lv; part.li = q.li; part.lj = q.lj; }
+        if (q.gset && !part.gset) { part.gv = q.gv; part.gset = 1; }
+      }
+      parts[wg] = part;
+    }
+  };
+  int cur = 0;     // MULTI: segment of the warp's last ticket
+  int cpair = -1;  // MULTI: pair of the warp's last task
   for (;;) {
     int task = 0;
-    if (t == 0) task = atomicAdd(a.ticket, 1);
+    if (t == 0) task = atomicAdd(a_.ticket, 1);
     task = __shfl_sync(0xffffffffu, task, 0);
-    if (task >= a.S * a.g_count) break;
-    if (*(volatile int*)a.abort_flag) break;
-    if (task == a.stall_task) continue;  // fault injection (option long_stall_task)
+    if (task >= (MULTI ? a_.task_total : a_.S * a_.g_count)) break;
+    if (*(volatile int*)a_.abort_flag) break;
+    if (task == a_.stall_task) continue;  // fault injection (option long_stall_task)
+    LongArgs am;  // MULTI: this task's pair
+    if constexpr (MULTI) {
+      while (task >= a_.task_end[cur]) ++cur;
+      const int2 sg = a_.segs[cur];  // (pair, column pass)
+      if (sg.x != cpair) {
+        if (cpair >= 0) flush_part(a_.pairs[cpair].parts, true);
+        part.lv = 0; part.li = 0; part.lj = 0; part.gv = 0; part.gset = 0;
+        cpair = sg.x;
+      }
+      am = a_.pairs[sg.x];
+      task = sg.y * am.S + task - (cur > 0 ? a_.task_end[cur - 1] : 0);
+    }
+    const LongArgs& a = MULTI ? am : a_;
+    const int n = a.n;
     const long long task_t0 = (a.prof && t == 0) ? clock64() : 0;
     const int s = task % a.S;
     const int g = a.g_first + task / a.S;
@@ -129,8 +172,8 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const int iA = ip0 + r + 1, iB = ip0 + NR + r + 1;  // real rows (1-based)
-      p0[r] = (iA >= 1 && iA <= n) ? prof4(a.P, a.qc[iA - 1]) : 0u;  // sigma rows, low half
-      p1[r] = (iB >= 1 && iB <= n) ? prof4(a.P, a.qc[iB - 1]) : 0u;  // ... and high half
+      p0[r] = (iA >= 1 && iA <= n) ? prof4(a_.P, a.qc[iA - 1]) : 0u;  // sigma rows, low half
+      p1[r] = (iB >= 1 && iB <= n) ? prof4(a_.P, a.qc[iB - 1]) : 0u;  // ... and high half
       H[r] = VS16::splat(NEGc);
       Ff[r] = VS16::splat(NEGc);
     }
@@ -609,16 +652,9 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       }
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const int lv = __shfl_xor_sync(0xffffffffu, part.lv, o);
-    const int li = __shfl_xor_sync(0xffffffffu, part.li, o);
-    const int lj = __shfl_xor_sync(0xffffffffu, part.lj, o);
-    if (lkey_better(lv, li, lj, part.lv, part.li, part.lj)) { part.lv = lv; part.li = li; part.lj = lj; }
-    const int gv = __shfl_xor_sync(0xffffffffu, part.gv, o);
-    const int gs = __shfl_xor_sync(0xffffffffu, part.gset, o);
-    if (gs && !part.gset) { part.gv = gv; part.gset = 1; }
+if (MULTI) {
+    if (cpair >= 0) flush_part(a_.pairs[cpair].parts, true);
+  } else {
+    flush_part(a_.parts, false);
   }
-  if (t == 0) a.parts[wg] = part;
 }
-

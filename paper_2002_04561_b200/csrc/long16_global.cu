@@ -12,4 +12,7 @@ LongFn long16_fn_global(int nr, bool ckpt) {
   return nr == 8 ? long16_kernel<8, KGLOBAL> : long16_kernel<16, KGLOBAL>;
 }
 
+// several pairs in one launch (MULTI, 512-row tasks, score-only)
+LongFn long16_fn_global_multi() { return long16_kernel<8, KGLOBAL, false, true>; }
+
 }  // namespace anyseq

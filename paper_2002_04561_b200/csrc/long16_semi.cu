@@ -12,4 +12,7 @@ LongFn long16_fn_semi(int nr, bool ckpt) {
   return nr == 8 ? long16_kernel<8, KSEMI> : long16_kernel<16, KSEMI>;
 }
 
+// several pairs in one launch (MULTI, 512-row tasks, score-only)
+LongFn long16_fn_semi_multi() { return long16_kernel<8, KSEMI, false, true>; }
+
 }  // namespace anyseq

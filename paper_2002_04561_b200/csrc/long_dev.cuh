@@ -48,6 +48,12 @@ struct LongArgs {
   unsigned long long* prof;  // optional: [0] cycles waiting, [1] cycles in tasks, [2] tasks
   long long spin_limit;
   int32_t stall_task;  // fault injection: this task is skipped (-1: none)
+  // long16 MULTI instances (several pairs in one launch): per-pair arguments (device array),
+  // ticket segments (pair, column pass) and the inclusive prefix of their task counts
+  const LongArgs* pairs;
+  const int2* segs;
+  const int32_t* task_end;
+  int32_t task_total;
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -141,5 +147,6 @@ __device__ __forceinline__ int imad_add_s(int x, uint32_t one, int k) {
 typedef void (*LongFn)(LongArgs);
 // long16_*.cu: the 16-bit differential kernel instance for (rows per lane, kind, checkpoints)
 LongFn long16_fn(int nr, int kind, bool ckpt);
+LongFn long16_multi_fn(int kind);  // MULTI instances (512-row tasks, score-only)
 
 }  // namespace anyseq
