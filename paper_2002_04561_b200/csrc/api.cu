@@ -115,7 +115,8 @@ struct anyseq_ctx {
   int64_t chunk_bytes = 64ll << 20;  // host-API upload/compute pipelining granularity
   int64_t force_variant = -1;
   int64_t allow16 = 1;
-  int64_t batch_long_cells = 1ll << 26;  // batch pairs this large take the long-pair path
+  int64_t batch_long_cells = 1ll << 22;  // batch pairs this large take the long-pair path
+  int64_t batch_long_min = 2048;         // ... when both sides are at least this long
   int64_t batch_long_small = 4;  // batches of at most this many pairs: every pair with both
                                  // sides >= 256 takes the long-pair path
   int64_t tb8 = 1;          // traceback: 1-byte H store where the range allows
@@ -312,6 +313,7 @@ struct DeviceJob {
   int64_t gen_q = -1, gen_s = -1;   // >= 0: offsets are k * gen (not uploaded), see prep
   int packed2 = 0;                  // d_q / d_s hold 2-bit codes (host-packed ACGT-only chunk)
   int64_t skip_cells = 0;           // score mode: pairs this large are left to the long path
+  int64_t skip_min = 2048;          // ... when both sides have at least this many bases
   uint64_t cig_base = 0;            // traceback: added to every cigar_offset of this job
   int32_t* d_scores_out;      // score mode output (device) or null => ctx buffer
   anyseq_alignment* d_aln_out;  // alignment structs (device) or null => ctx buffer
@@ -411,6 +413,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
     ca.beg_j = D.beg_j.as<int32_t>();
   }
   ca.skip_cells = J.skip_cells;
+  ca.skip_min = J.skip_min;
   CK(launch_classify(ca, st, D.num_sms));
   L(1);
   ctx->mark(st, "classified");
@@ -421,7 +424,7 @@ anyseq_status run_device(anyseq_ctx* ctx, Device& D, const anyseq_params* prm, D
   // while this one computes.
   PlanSummary S;
   bool host_plan = false;
-  const bool skipped_all = J.skip_cells > 0 && J.gen_q >= 2048 && J.gen_s >= 2048 &&
+  const bool skipped_all = J.skip_cells > 0 && J.gen_q >= J.skip_min && J.gen_s >= J.skip_min &&
                            J.gen_q * J.gen_s >= J.skip_cells;
   if (J.packed2 && J.gen_q > 0 && J.gen_s > 0 && B > 0 && !skipped_all) {
     const PairPlan pp = plan_pair(ca.cfg, J.gen_q, J.gen_s, false);
@@ -1019,6 +1022,7 @@ anyseq_status run_host_shard(anyseq_ctx* ctx, Device& D, const anyseq_params* pr
     J.s_end = slen;
     J.tb = tb;
     J.skip_cells = tb ? 0 : ctx->skip_cells;
+    J.skip_min = ctx->batch_long_min;
     J.want_ends = aln != nullptr;
     J.d_scores_out = nullptr;
     J.d_aln_out = nullptr;
@@ -1136,6 +1140,7 @@ anyseq_status run_host_batch_core(anyseq_ctx* ctx, const anyseq_params* prm, con
         local.tb8 = ctx->tb8;
         local.pack2_percent = ctx->pack2_percent;
         local.skip_cells = ctx->skip_cells;
+        local.batch_long_min = ctx->batch_long_min;
         local.shared_pool = ctx->pack2 ? ctx->packer() : nullptr;
         anyseq_status s = ANYSEQ_OK;
         if (bounds[g + 1] > bounds[g])  // an exception must not escape a std::thread either
@@ -1312,7 +1317,8 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
   if (ctx->batch_long_cells > 0 || small)
     for (uint64_t k = 0; k < b->num_pairs; ++k) {
       const uint64_t n = b->q_off[k + 1] - b->q_off[k], m = b->s_off[k + 1] - b->s_off[k];
-      if ((ctx->batch_long_cells > 0 && n >= 2048 && m >= 2048 &&
+      if ((ctx->batch_long_cells > 0 && n >= (uint64_t)ctx->batch_long_min &&
+           m >= (uint64_t)ctx->batch_long_min &&
            (long double)n * m >= (long double)ctx->batch_long_cells) ||
           (small && n >= 256 && m >= 256 && acgt_only(b->s + b->s_off[k], m)))
         longs.push_back(k);
@@ -2124,6 +2130,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
     if (n == "pack2") { ctx->pack2 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "tb8") { ctx->tb8 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "batch_long_cells") { ctx->batch_long_cells = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
+    if (n == "batch_long_min") { ctx->batch_long_min = std::max<int64_t>(value, 1); return ANYSEQ_OK; }
     if (n == "long_multi") { ctx->long_multi = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "batch_long_small") { ctx->batch_long_small = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
     if (n == "pack2_percent") {

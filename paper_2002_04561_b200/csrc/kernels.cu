@@ -236,7 +236,7 @@ __global__ void classify_kernel(ClassifyArgs a) {
         if (a.beg_i) { a.beg_i[k] = 0; a.beg_j[k] = 0; }
         a.keys[k] = ~0ull;
         a.vals[k] = (int32_t)k;
-      } else if (a.skip_cells > 0 && n >= 2048 && m >= 2048 && n * m >= a.skip_cells) {
+      } else if (a.skip_cells > 0 && n >= a.skip_min && m >= a.skip_min && n * m >= a.skip_cells) {
         a.keys[k] = ~0ull;  // left to the long-pair path
         a.vals[k] = (int32_t)k;
       } else {

@@ -51,9 +51,10 @@ struct ClassifyArgs {
   int32_t* n_ops;
   int32_t* beg_i;
   int32_t* beg_j;
-  // > 0: pairs with n, m >= 2048 and n * m >= skip_cells are not planned (key ~0, outputs
-  // untouched): the host API aligns them on the long-pair path (api.cu run_host_batch)
+  // > 0: pairs with n, m >= skip_min and n * m >= skip_cells are not planned (key ~0,
+  // outputs untouched): the host API aligns them on the long-pair path (run_host_batch)
   int64_t skip_cells;
+  int64_t skip_min;
 };
 // a2: plan -- variant choice, range guard, sort keys; finishes empty pairs.
 cudaError_t launch_classify(const ClassifyArgs& a, cudaStream_t st, int num_sms);

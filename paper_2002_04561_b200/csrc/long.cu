@@ -901,6 +901,65 @@ __global__ void parts_reduce_kernel(const LongPart* __restrict__ parts, int nw, 
   }
 }
 
+// run_long_multi: long_init_kernel for every pair of the launch in one grid (y = pair)
+__global__ void long_init_multi_kernel(DevParams P, const LongArgs* __restrict__ pairs, int K) {
+  const int NEG = NEG32;
+  const bool glob = P.kind == KGLOBAL;
+  for (int p = blockIdx.y; p < K; p += gridDim.y) {
+    const LongArgs& a = pairs[p];
+    const int n = a.n, m = a.m, G = a.Gtot;
+    int4* rowbuf = a.rowbuf;
+    int2* bcol0 = a.bcol[0];
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x <= max(n, m); x += gridDim.x * blockDim.x) {
+      if (x <= m) rowbuf[x] = make_int4(0, 0, NEG, 0);  // tag 0: no strip has written yet
+      if (x <= n) bcol0[x] = make_int2(glob && x > 0 ? -(P.go + x * P.ge) : 0, NEG);
+      if (x == 0)  // the pair's inner edges, and column m (edge G) when it keeps it (SEMI)
+        for (int g = 1; g <= G; ++g) {
+          int2* bc = a.bcol[g];
+          if (g == G && (P.kind != KSEMI || !bc)) continue;
+          bc[0] = make_int2(glob ? -(P.go + a.cb[g] * P.ge) : 0, NEG);  // H(0, c_g)
+        }
+    }
+  }
+}
+
+// run_long_multi: semi_reduce_kernel for every pair of the launch in one grid (y = pair)
+__global__ void semi_reduce_multi_kernel(const LongArgs* __restrict__ pairs, int K,
+                                         unsigned long long* out) {
+  for (int p = blockIdx.y; p < K; p += gridDim.y) {
+    const LongArgs& a = pairs[p];
+    const int n = a.n, m = a.m;
+    const int4* rowbuf = a.rowbuf;
+    const int2* colm = a.bcol[a.Gtot];
+    unsigned long long best = 0;
+    const int64_t nrow = m > 1 ? m - 1 : 0;  // j in [1, m - 1]
+    const int64_t tot = nrow + (int64_t)n + 1;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot;
+         x += (int64_t)gridDim.x * blockDim.x) {
+      int v;
+      uint32_t seq;
+      if (x < nrow) {
+        const int j = 1 + (int)x;
+        v = rowbuf[j].x;
+        seq = (uint32_t)j;
+      } else {
+        const int i = (int)(x - nrow);
+        v = colm[i].x;
+        seq = (uint32_t)m + (uint32_t)i;
+      }
+      const unsigned long long key =
+          ((unsigned long long)((uint32_t)v ^ 0x80000000u) << 32) | (0xFFFFFFFFu - seq);
+      best = key > best ? key : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+      best = y > best ? y : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(out + p, best);
+  }
+}
+
 int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPairIn>& pairs,
                    const LongOptions& opt, std::vector<LongResult>* out, std::vector<int>* taken,
                    std::string* err, uint64_t* launches, double* kernel_ms,
@@ -1104,14 +1163,12 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
   LK(cudaMemcpyAsync(mp.p, la.data(), (size_t)K * sizeof(LongArgs), cudaMemcpyHostToDevice, st));
   LK(cudaMemcpyAsync(mt.p, task_end.data(), (size_t)NS * 4, cudaMemcpyHostToDevice, st));
   LK(cudaMemcpyAsync(ms_.p, segs.data(), (size_t)NS * sizeof(int2), cudaMemcpyHostToDevice, st));
-  for (int x = 0; x < K; ++x) {
-    const uint64_t n = pairs[sel[x]].n, m = pairs[sel[x]].m;
-    const int gi = (int)std::min<uint64_t>((std::max(n, m) + 256) / 256, (uint64_t)dev.num_sms * 4);
-    long_init_kernel<<<gi, 256, 0, st>>>(P, (int)n, (int)m, la[x].rowbuf, bp_h[cbo[x]],
-                                         la[x].bcol, la[x].cb, G[x], 0, G[x]);
-    LK(cudaGetLastError());
-    *launches += 1;
-  }
+  uint64_t maxnm = 0;
+  for (int x = 0; x < K; ++x) maxnm = std::max(maxnm, std::max(pairs[sel[x]].n, pairs[sel[x]].m));
+  const dim3 gi((unsigned)std::min<uint64_t>((maxnm + 256) / 256, 64), (unsigned)std::min(K, 65535));
+  long_init_multi_kernel<<<gi, 256, 0, st>>>(P, (const LongArgs*)mp.p, K);
+  LK(cudaGetLastError());
+  *launches += 1;
   LongArgs a0 = la[0];
   a0.pairs = (const LongArgs*)mp.p;
   a0.task_end = (const int32_t*)mt.p;
@@ -1130,16 +1187,12 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
   parts_reduce_kernel<<<K, 256, 0, st>>>((const LongPart*)parts.p, nw, (LongPart*)red.p);
   LK(cudaGetLastError());
   *launches += 1;
-  if (P.kind == KSEMI)
-    for (int x = 0; x < K; ++x) {
-      const uint64_t n = pairs[sel[x]].n, m = pairs[sel[x]].m;
-      const int gi = (int)std::min<uint64_t>((n + m + 256) / 256, (uint64_t)dev.num_sms * 4);
-      semi_reduce_kernel<<<gi, 256, 0, st>>>((const int4*)la[x].rowbuf, 1, (int)m, (int)m,
-                                             bp_h[cbo[x] + G[x]], (int)n,
-                                             (unsigned long long*)kb.p + x);
-      LK(cudaGetLastError());
-      *launches += 1;
-    }
+  if (P.kind == KSEMI) {
+    const dim3 gs((unsigned)std::min<uint64_t>((2 * maxnm + 256) / 256, 64), (unsigned)std::min(K, 65535));
+    semi_reduce_multi_kernel<<<gs, 256, 0, st>>>((const LongArgs*)mp.p, K, (unsigned long long*)kb.p);
+    LK(cudaGetLastError());
+    *launches += 1;
+  }
   // the caller's work in the shadow of the launch (results are read after it: pageable
   // device-to-host copies would block the host until the kernel ends)
   const int rd = during ? during() : 0;

@@ -90,7 +90,7 @@ def test_long_pairs_one_launch(ctx, kind, gap, go):
         assert np.array_equal(ends1["s_end"], ends["s_end"])
     finally:
         ctx.set_option("long_multi", 1)
-        ctx.set_option("batch_long_cells", 1 << 26)
+        ctx.set_option("batch_long_cells", 1 << 22)
 
 
 def test_long_pairs_one_launch_column_passes(ctx):
@@ -110,7 +110,7 @@ def test_long_pairs_one_launch_column_passes(ctx):
             assert np.array_equal(ends["q_end"], oqe) and np.array_equal(ends["s_end"], ose), vs
     finally:
         ctx.set_option("long_strips", 0)
-        ctx.set_option("batch_long_cells", 1 << 26)
+        ctx.set_option("batch_long_cells", 1 << 22)
 
 
 def test_long_pairs_one_launch_timeout(ctx):
@@ -132,7 +132,7 @@ def test_long_pairs_one_launch_timeout(ctx):
     sc = ctx.align_batch(sch, q, qo, s, so)
     osc, _, _ = _oracle_scores("global", "linear", 0, q, qo, s, so)
     assert np.array_equal(sc, osc)
-    ctx.set_option("batch_long_cells", 1 << 26)
+    ctx.set_option("batch_long_cells", 1 << 22)
 
 
 @pytest.mark.parametrize("kind", ["global", "semi", "local"])
@@ -160,4 +160,4 @@ def test_batch_of_only_long_pairs(ctx, kind):
             assert np.array_equal(ends["q_begin"], oqe) and np.array_equal(ends["s_begin"], ose)
     finally:
         ctx.set_option("long_multi", 1)
-        ctx.set_option("batch_long_cells", 1 << 26)
+        ctx.set_option("batch_long_cells", 1 << 22)

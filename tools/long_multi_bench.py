@@ -24,6 +24,9 @@ def main():
     ap.add_argument("--short", type=int, default=100000)
     ap.add_argument("--kind", default="local")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--cells", type=int, default=1 << 22, help="option batch_long_cells")
+    ap.add_argument("--min", type=int, default=2048, help="option batch_long_min")
+    ap.add_argument("--only", type=int, default=-1, help="run only long_multi = this")
     args = ap.parse_args()
     import paper_2002_04561_b200 as A
     from synth import c4_genomes, random_pairs, csr
@@ -47,9 +50,12 @@ def main():
     out = {"long_pairs": args.long, "lengths": [args.lo, args.hi], "short_pairs": args.short,
            "kind": args.kind, "cells": cells}
     with A.Context([0]) as ctx:
-        ctx.set_option("batch_long_cells", 1 << 22)
+        ctx.set_option("batch_long_cells", args.cells)
+        out["batch_long_cells"] = args.cells
+        ctx.set_option("batch_long_min", args.min)
+        out["batch_long_min"] = args.min
         res = {}
-        for multi in (1, 0):
+        for multi in ((1, 0) if args.only < 0 else (args.only,)):
             ctx.set_option("long_multi", multi)
             sc = ctx.align_batch(sch, q, qo, s, so)  # warm-up
             best = 1e30
@@ -62,7 +68,8 @@ def main():
                                     "gcups": round(cells / best / 1e9, 1),
                                     "kernel_ms": round(ctx.stat("long_multi_ms"), 2),
                                     "pairs_in_shared_launch": int(ctx.stat("long_multi_pairs"))}
-        out["same_scores"] = bool(np.array_equal(res[0], res[1]))
+        if len(res) == 2:
+            out["same_scores"] = bool(np.array_equal(res[0], res[1]))
     print(json.dumps(out))
 
 
