@@ -173,6 +173,8 @@ uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx);
    clears them.  "timing" = 2 also prints a per-chunk event timeline of the host API to
    stderr (debug).  After anyseq_align_long: "long_kernel_ms" (device time of the long
    kernel, max over devices) and "long_narrow" (1 if the 16-bit differential kernel ran).
+   After anyseq_align_batch: "long_multi_pairs" (long pairs the shared launch aligned) and
+   "long_multi_ms" (its device time).
    After anyseq_traceback_long: "tb_method" (1 checkpoints, 2 Hirschberg), "tb_pass_ms"
    (device time of the forward pass; Hirschberg: of the last-row passes summed over
    levels), "tb_pass_cells" (cells those passes relaxed), "tb_walk_ms" (device time of the
@@ -220,8 +222,14 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
                          (1..8) force the column / row checkpoint spacing (tests)
      "tb8"               batch traceback: 1 (default) stores the low byte of H per cell when
                          the scheme allows it exactly (R23); 0 = full H
-     "batch_long_cells"  a batch pair with n*m >= this (and n, m >= 2048) is aligned by the
-                         long-pair path instead of the batch kernel (default 2^26; 0 = never)
+     "batch_long_cells"  a batch pair with n*m >= this (and n, m >= batch_long_min) is
+                         aligned by the long-pair path instead of the batch kernel (default
+                         2^22; 0 = never).  Score mode, one device: all such pairs of the call
+                         share ONE launch of the long kernel (their row-strip tasks in one
+                         device queue) while the batch kernels
+                         align the other pairs in place; traceback: one pair at a time
+     "batch_long_min"    minimum length of both sides for that routing (default 2048)
+     "long_multi"        1 (default): the shared launch above; 0: one long-pair call per pair
      "batch_long_small"  batches of at most this many pairs send every pair with n, m >= 256
                          to the long-pair path (default 4; 0 = never); pairs that path cannot
                          take stay on the batch kernel
