@@ -237,6 +237,64 @@ def long_pair_leg(ctx, A, n, n_sm, f_mhz, n_gpus=1):
             "score": r["score"], "end": [r["q_end"], r["s_end"]]}
 
 
+def mixed_sizes_leg(ctx, A, n_long, n_short, n_sm, f_mhz, reps=3):
+    """a score-only batch of n_long similar pairs of
+    2-20 kbp (windows of a mutated genome pair) mixed into n_short random 100-300 bp pairs,
+    local affine 5/1, through the host API (anyseq_align_batch, pageable buffers): the long
+    pairs share ONE launch of the 16-bit long kernel while the batch kernels align the short
+    pairs in place.  value = all cells / best wall time of `reps` calls; the shared launch's
+    own rate is over the long pairs' cells.  Checked against the one-long-call-per-pair path
+    (option long_multi = 0) on the same batch."""
+    import numpy as np
+    from synth import c4_genomes, random_pairs, csr
+    rng = np.random.default_rng(5)
+    g1, g2 = c4_genomes(2_000_000, "a", seed=6)
+    q0, qo0, s0, so0 = random_pairs(n_short, 100, 300, seed=7)
+    qs = [q0[qo0[k]:qo0[k + 1]].tobytes() for k in range(n_short)]
+    ss = [s0[so0[k]:so0[k + 1]].tobytes() for k in range(n_short)]
+    short_cells = float(np.sum(np.diff(qo0).astype(np.float64) * np.diff(so0)))
+    long_cells = 0.0
+    for _ in range(n_long):
+        n = int(rng.integers(2048, 20001))
+        m = int(rng.integers(2048, 20001))
+        a = int(rng.integers(0, len(g1) - max(n, m)))
+        pos = int(rng.integers(0, len(qs) + 1))
+        qs.insert(pos, g1[a:a + n])
+        ss.insert(pos, g2[a:a + m])
+        long_cells += float(n) * m
+    q, qo = csr(qs)
+    s, so = csr(ss)
+    sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+    sc = ctx.align_batch(sch, q, qo, s, so)  # warm-up (workspace growth)
+    best = 1e30
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        sc = ctx.align_batch(sch, q, qo, s, so)
+        best = min(best, time.perf_counter() - t0)
+    kms = ctx.stat("long_multi_ms")
+    taken = int(ctx.stat("long_multi_pairs"))
+    ctx.set_option("long_multi", 0)
+    t0 = time.perf_counter()
+    sc1 = ctx.align_batch(sch, q, qo, s, so)
+    per_pair = time.perf_counter() - t0
+    ctx.set_option("long_multi", 1)
+    cells = short_cells + long_cells
+    kg = long_cells / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+    peak = n_sm * f_mhz * 1e6 * (64 * 2 / 5.5) / 1e9
+    return {"workload": f"{n_long} pairs of 2-20 kbp (mutated genome windows) + {n_short} pairs of "
+                        "100-300 bp, local affine open 5 / extend 1, match 2 / mismatch -1, "
+                        "score-only, host API from pageable buffers, 1 GPU",
+            "value": round(cells / best / 1e9, 1), "unit": "GCUPS", "wall_ms": round(best * 1e3, 2),
+            "long_pairs_in_shared_launch": taken,
+            "shared_launch": {"kernel": "long16_kernel<8, LOCAL, MULTI>", "kernel_ms": round(kms, 2),
+                              "gcups": round(kg, 1),
+                              "roofline": {"bound": "alu", "achieved": round(kg, 1),
+                                           "peak": round(peak, 1), "unit": "GCUPS",
+                                           "frac": round(kg / peak, 4)}},
+            "one_call_per_long_pair_wall_ms": round(per_pair * 1e3, 1),
+            "same_scores_as_one_call_per_pair": bool(np.array_equal(sc, sc1))}
+
+
 def long_traceback_leg(ctx, A, n, kind="global", gap="linear", go=0):
     """linear-space traceback of a C4-shaped pair (n-bp genomes, G2 =
     mutated copy of G1), once, through anyseq_traceback_long with host buffers: one
@@ -292,6 +350,9 @@ def main():
                     help="linear-space long traceback leg (8(f) f1) genome length; 0 skips it")
     ap.add_argument("--long-bp", type=int, default=5_000_000,
                     help="C4 long pair (second half of the metric) genome length; 0 skips it")
+    ap.add_argument("--mixed-long", type=int, default=200,
+                    help="mixed-size leg (8(f) f4): long pairs of 2-20 kbp; 0 skips it")
+    ap.add_argument("--mixed-short", type=int, default=100_000)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -478,6 +539,8 @@ def main():
                 lctx.close()
         if ws > 1:
             dist.barrier(group=cpu_group)
+    if rank == 0 and args.mixed_long > 0:
+        line["mixed_sizes"] = mixed_sizes_leg(ctx, A, args.mixed_long, args.mixed_short, n_sm, f_mhz)
     if rank == 0 and args.long_tb_bp > 0:
         line["long_traceback"] = long_traceback_leg(ctx, A, args.long_tb_bp)
         line["long_traceback_local_affine"] = long_traceback_leg(ctx, A, args.long_tb_bp,

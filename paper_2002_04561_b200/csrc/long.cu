@@ -968,14 +968,14 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
   out->assign(K0, LongResult{0, 0, 0, 0.0, true});
   taken->assign(K0, 0);
   *kernel_ms = 0;
-  // the eligibility rules of run_long's 16-bit path at 512-row tasks (NR = 8)
-  constexpr int NR = 8, HS = 64 * NR;
+  // the eligibility rules of run_long's 16-bit path (at 512-row tasks, NR = 8)
   const int64_t d16 = (int64_t)P.go + P.ge + std::max(P.smax, 0);
   const int64_t margin16 = 100 * d16 + 16;
   const int NEG16C = -24576;
-  const int64_t bspan16 = (int64_t)(64 * NR + 66) * d16;
-  const bool fits = 2 * bspan16 + margin16 + 96 * d16 + P.go + P.ge + 256 < -NEG16C &&
-                    (int64_t)P.go + 2 * P.ge < 4096;
+  auto fits16 = [&](int nr) {
+    return 2 * (int64_t)(64 * nr + 66) * d16 + margin16 + 96 * d16 + P.go + P.ge + 256 < -NEG16C;
+  };
+  const bool fits = fits16(8) && (int64_t)P.go + 2 * P.ge < 4096;
   std::vector<size_t> sel;
   for (size_t k = 0; k < K0 && fits; ++k) {
     const uint64_t n = pairs[k].n, m = pairs[k].m;
@@ -995,7 +995,21 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
     if (!dev.ws->stream) LK(cudaStreamCreateWithFlags(&dev.ws->stream, cudaStreamNonBlocking));
     st = dev.ws->stream;
   }
-  LongFn fn = long16_multi_fn(P.kind);
+  // 1024-row tasks (NR = 16, the faster step) when the pairs give at least one task per
+  // resident warp at that height, else 512-row tasks (twice the tasks, shorter ramps);
+  // measured: 200 pairs of 2-20 kbp (1.2 tasks per warp) 14.5 -> 12.5 ms, 100 such pairs
+  // (0.6 per warp) 9.7 -> 10.7 ms (tools/long_multi_bench.py --rows)
+  int NR = 8;
+  if (fits16(16) && opt.band_rows != 512) {
+    int nb16 = 0;
+    LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb16, long16_multi_fn(P.kind, 16), 128, 0));
+    double T16 = 0;
+    for (size_t k : sel) T16 += (double)((pairs[k].n + 1023) / 1024);
+    if (T16 >= 4.0 * dev.num_sms * std::max(nb16, 1) || opt.band_rows == 1024) NR = 16;
+  }
+  const int HS = 64 * NR;
+  const int64_t bspan16 = (int64_t)(64 * NR + 66) * d16;
+  LongFn fn = long16_multi_fn(P.kind, NR);
   int nb = 0;
   LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0));
   int grid = dev.num_sms * std::max(nb, 1);

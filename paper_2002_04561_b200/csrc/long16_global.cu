@@ -12,7 +12,9 @@ LongFn long16_fn_global(int nr, bool ckpt) {
   return nr == 8 ? long16_kernel<8, KGLOBAL> : long16_kernel<16, KGLOBAL>;
 }
 
-// several pairs in one launch (MULTI, 512-row tasks, score-only)
-LongFn long16_fn_global_multi() { return long16_kernel<8, KGLOBAL, false, true>; }
+// several pairs in one launch (MULTI, score-only)
+LongFn long16_fn_global_multi(int nr) {
+  return nr == 8 ? long16_kernel<8, KGLOBAL, false, true> : long16_kernel<16, KGLOBAL, false, true>;
+}
 
 }  // namespace anyseq

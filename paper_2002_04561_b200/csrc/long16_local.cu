@@ -12,7 +12,9 @@ LongFn long16_fn_local(int nr, bool ckpt) {
   return nr == 8 ? long16_kernel<8, KLOCAL> : long16_kernel<16, KLOCAL>;
 }
 
-// several pairs in one launch (MULTI, 512-row tasks, score-only)
-LongFn long16_fn_local_multi() { return long16_kernel<8, KLOCAL, false, true>; }
+// several pairs in one launch (MULTI, score-only)
+LongFn long16_fn_local_multi(int nr) {
+  return nr == 8 ? long16_kernel<8, KLOCAL, false, true> : long16_kernel<16, KLOCAL, false, true>;
+}
 
 }  // namespace anyseq

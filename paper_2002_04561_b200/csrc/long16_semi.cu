@@ -12,7 +12,9 @@ LongFn long16_fn_semi(int nr, bool ckpt) {
   return nr == 8 ? long16_kernel<8, KSEMI> : long16_kernel<16, KSEMI>;
 }
 
-// several pairs in one launch (MULTI, 512-row tasks, score-only)
-LongFn long16_fn_semi_multi() { return long16_kernel<8, KSEMI, false, true>; }
+// several pairs in one launch (MULTI, score-only)
+LongFn long16_fn_semi_multi(int nr) {
+  return nr == 8 ? long16_kernel<8, KSEMI, false, true> : long16_kernel<16, KSEMI, false, true>;
+}
 
 }  // namespace anyseq

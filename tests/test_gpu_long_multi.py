@@ -93,6 +93,25 @@ def test_long_pairs_one_launch(ctx, kind, gap, go):
         ctx.set_option("batch_long_cells", 1 << 22)
 
 
+@pytest.mark.parametrize("kind", ["global", "semi", "local"])
+def test_long_pairs_one_launch_1024_rows(ctx, kind):
+    """The 1024-row MULTI instance (chosen automatically for batches with many long pairs;
+    long_band_rows = 1024 forces it here) gives the oracle's results too."""
+    import paper_2002_04561_b200 as A
+    q, qo, s, so, nl = _batch(500 + len(kind), with_n=False)
+    osc, oqe, ose = _oracle_scores(kind, "affine", 5, q, qo, s, so)
+    sch = A.Scheme(kind, "affine", 2, -1, 5, 1)
+    ctx.set_option("batch_long_cells", 1 << 22)
+    ctx.set_option("long_band_rows", 1024)
+    try:
+        sc, ends = ctx.align_batch(sch, q, qo, s, so, ends=True)
+        assert ctx.stat("long_multi_pairs") == nl
+        assert np.array_equal(sc, osc)
+        assert np.array_equal(ends["q_end"], oqe) and np.array_equal(ends["s_end"], ose)
+    finally:
+        ctx.set_option("long_band_rows", 0)
+
+
 def test_long_pairs_one_launch_column_passes(ctx):
     """Forced column passes (long_strips) inside the shared launch: every pair's
     tasks then wait on the pass to their left as well."""

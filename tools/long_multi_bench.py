@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--cells", type=int, default=1 << 22, help="option batch_long_cells")
     ap.add_argument("--min", type=int, default=2048, help="option batch_long_min")
+    ap.add_argument("--rows", type=int, default=0, help="option long_band_rows (512/1024 force)")
     ap.add_argument("--only", type=int, default=-1, help="run only long_multi = this")
     args = ap.parse_args()
     import paper_2002_04561_b200 as A
@@ -54,6 +55,8 @@ def main():
         out["batch_long_cells"] = args.cells
         ctx.set_option("batch_long_min", args.min)
         out["batch_long_min"] = args.min
+        ctx.set_option("long_band_rows", args.rows)
+        out["rows"] = args.rows
         res = {}
         for multi in ((1, 0) if args.only < 0 else (args.only,)):
             ctx.set_option("long_multi", multi)
