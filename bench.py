@@ -273,6 +273,7 @@ def mixed_sizes_leg(ctx, A, n_long, n_short, n_sm, f_mhz, reps=3):
         best = min(best, time.perf_counter() - t0)
     kms = ctx.stat("long_multi_ms")
     taken = int(ctx.stat("long_multi_pairs"))
+    rows = int(ctx.stat("long_multi_rows"))
     ctx.set_option("long_multi", 0)
     t0 = time.perf_counter()
     sc1 = ctx.align_batch(sch, q, qo, s, so)
@@ -286,7 +287,8 @@ def mixed_sizes_leg(ctx, A, n_long, n_short, n_sm, f_mhz, reps=3):
                         "score-only, host API from pageable buffers, 1 GPU",
             "value": round(cells / best / 1e9, 1), "unit": "GCUPS", "wall_ms": round(best * 1e3, 2),
             "long_pairs_in_shared_launch": taken,
-            "shared_launch": {"kernel": "long16_kernel<8, LOCAL, MULTI>", "kernel_ms": round(kms, 2),
+            "shared_launch": {"kernel": f"long16_kernel<{rows // 64}, LOCAL, MULTI> ({rows}-row tasks)",
+                              "kernel_ms": round(kms, 2),
                               "gcups": round(kg, 1),
                               "roofline": {"bound": "alu", "achieved": round(kg, 1),
                                            "peak": round(peak, 1), "unit": "GCUPS",

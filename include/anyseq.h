@@ -174,7 +174,7 @@ uint64_t anyseq_kernel_launches(const anyseq_ctx* ctx);
    stderr (debug).  After anyseq_align_long: "long_kernel_ms" (device time of the long
    kernel, max over devices) and "long_narrow" (1 if the 16-bit differential kernel ran).
    After anyseq_align_batch: "long_multi_pairs" (long pairs the shared launch aligned) and
-   "long_multi_ms" (its device time).
+   "long_multi_ms" (its device time), "long_multi_rows" (rows per warp task, 512 or 1024).
    After anyseq_traceback_long: "tb_method" (1 checkpoints, 2 Hirschberg), "tb_pass_ms"
    (device time of the forward pass; Hirschberg: of the last-row passes summed over
    levels), "tb_pass_cells" (cells those passes relaxed), "tb_walk_ms" (device time of the

@@ -140,6 +140,7 @@ struct anyseq_ctx {
   int64_t skip_cells = 0;  // set by run_host_batch for its batch-kernel pass (DeviceJob)
   int64_t long_multi_pairs = 0;   // ... pairs the last batch call ran that way
   double long_multi_ms = 0;       // ... and that launch's kernel time
+  int long_multi_rows = 0;        // ... and its rows per warp task (512 or 1024)
   int long_narrow = 0;   // the last anyseq_align_long ran the 16-bit differential kernel
   double long_ms = 0;    // ... and its kernel time (max over devices)
   double tb_pass_ms = 0, tb_pass_cells = 0;  // last anyseq_traceback_long: forward pass(es)
@@ -1260,7 +1261,8 @@ static anyseq_status run_host_batch_inplace(anyseq_ctx* ctx, const anyseq_params
     double kms = 0;
     int rs = ANYSEQ_OK;
     const int rc = run_long_multi(ld, dev_params(prm), in, ctx->long_opt, &lr, &took, &err,
-                                  &launches, &kms, [&]() { return rs = run_short(); });
+                                  &launches, &kms, [&]() { return rs = run_short(); },
+                                  &ctx->long_multi_rows);
     ctx->launches += launches;
     if (rs != ANYSEQ_OK) return (anyseq_status)rs;
     if (rc != 0) return fail(ctx, (anyseq_status)rc, "long pairs (one launch): %s", err.c_str());
@@ -2242,6 +2244,7 @@ anyseq_status anyseq_get_stat(anyseq_ctx* ctx, const char* name, double* value) 
     if (n == "long_narrow") { *value = ctx->long_narrow; return ANYSEQ_OK; }
     if (n == "long_multi_pairs") { *value = (double)ctx->long_multi_pairs; return ANYSEQ_OK; }
     if (n == "long_multi_ms") { *value = ctx->long_multi_ms; return ANYSEQ_OK; }
+    if (n == "long_multi_rows") { *value = ctx->long_multi_rows; return ANYSEQ_OK; }
     if (n == "long_kernel_ms") { *value = ctx->long_ms; return ANYSEQ_OK; }
     if (n == "tb_pass_ms") { *value = ctx->tb_pass_ms; return ANYSEQ_OK; }
     if (n == "tb_pass_cells") { *value = ctx->tb_pass_cells; return ANYSEQ_OK; }

@@ -963,7 +963,7 @@ __global__ void semi_reduce_multi_kernel(const LongArgs* __restrict__ pairs, int
 int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPairIn>& pairs,
                    const LongOptions& opt, std::vector<LongResult>* out, std::vector<int>* taken,
                    std::string* err, uint64_t* launches, double* kernel_ms,
-                   const std::function<int()>& during) {
+                   const std::function<int()>& during, int* rows_out) {
   const size_t K0 = pairs.size();
   out->assign(K0, LongResult{0, 0, 0, 0.0, true});
   taken->assign(K0, 0);
@@ -1008,6 +1008,7 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
     if (T16 >= 4.0 * dev.num_sms * std::max(nb16, 1) || opt.band_rows == 1024) NR = 16;
   }
   const int HS = 64 * NR;
+  if (rows_out) *rows_out = HS;
   const int64_t bspan16 = (int64_t)(64 * NR + 66) * d16;
   LongFn fn = long16_multi_fn(P.kind, NR);
   int nb = 0;

@@ -122,6 +122,6 @@ struct LongPairIn {
 int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPairIn>& pairs,
                    const LongOptions& opt, std::vector<LongResult>* out, std::vector<int>* taken,
                    std::string* err, uint64_t* launches, double* kernel_ms,
-                   const std::function<int()>& during = {});
+                   const std::function<int()>& during = {}, int* rows_out = nullptr);
 
 }  // namespace anyseq
