@@ -228,6 +228,9 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
                          share ONE launch of the long kernel (their row-strip tasks in one
                          device queue) while the batch kernels
                          align the other pairs in place; traceback: one pair at a time
+     "batch_long_cells_tb"  the same threshold for anyseq_traceback (default 2^26: long pairs
+                         there are aligned one at a time, so medium pairs stay in the batch
+                         traceback kernel)
      "batch_long_min"    minimum length of both sides for that routing (default 2048)
      "long_multi"        1 (default): the shared launch above; 0: one long-pair call per pair
      "batch_long_small"  batches of at most this many pairs send every pair with n, m >= 256

@@ -117,6 +117,8 @@ struct anyseq_ctx {
   int64_t allow16 = 1;
   int64_t batch_long_cells = 1ll << 22;  // batch pairs this large take the long-pair path
   int64_t batch_long_min = 2048;         // ... when both sides are at least this long
+  int64_t batch_long_cells_tb = 1ll << 26;  // traceback mode's threshold (long pairs there
+                                            // run one at a time)
   int64_t batch_long_small = 4;  // batches of at most this many pairs: every pair with both
                                  // sides >= 256 takes the long-pair path
   int64_t tb8 = 1;          // traceback: 1-byte H store where the range allows
@@ -1316,12 +1318,12 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
     }
     return true;
   };
-  if (ctx->batch_long_cells > 0 || small)
+  const int64_t thr = tb ? ctx->batch_long_cells_tb : ctx->batch_long_cells;
+  if (thr > 0 || small)
     for (uint64_t k = 0; k < b->num_pairs; ++k) {
       const uint64_t n = b->q_off[k + 1] - b->q_off[k], m = b->s_off[k + 1] - b->s_off[k];
-      if ((ctx->batch_long_cells > 0 && n >= (uint64_t)ctx->batch_long_min &&
-           m >= (uint64_t)ctx->batch_long_min &&
-           (long double)n * m >= (long double)ctx->batch_long_cells) ||
+      if ((thr > 0 && n >= (uint64_t)ctx->batch_long_min && m >= (uint64_t)ctx->batch_long_min &&
+           (long double)n * m >= (long double)thr) ||
           (small && n >= 256 && m >= 256 && acgt_only(b->s + b->s_off[k], m)))
         longs.push_back(k);
     }
@@ -2132,6 +2134,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
     if (n == "pack2") { ctx->pack2 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "tb8") { ctx->tb8 = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "batch_long_cells") { ctx->batch_long_cells = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
+    if (n == "batch_long_cells_tb") { ctx->batch_long_cells_tb = std::max<int64_t>(value, 0); return ANYSEQ_OK; }
     if (n == "batch_long_min") { ctx->batch_long_min = std::max<int64_t>(value, 1); return ANYSEQ_OK; }
     if (n == "long_multi") { ctx->long_multi = value ? 1 : 0; return ANYSEQ_OK; }
     if (n == "batch_long_small") { ctx->batch_long_small = std::max<int64_t>(value, 0); return ANYSEQ_OK; }

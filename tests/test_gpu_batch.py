@@ -566,6 +566,7 @@ def test_mixed_batch_routes_long_pairs(ctx, kind):
     res, ocig = _oracle(kind, "affine", 5, 1, q, qo, s, so, tb=True)
     sch = A.Scheme(kind, "affine", 2, -1, 5, 1)
     ctx.set_option("batch_long_cells", 1 << 22)
+    ctx.set_option("batch_long_cells_tb", 1 << 22)
     try:
         _check_scores(ctx, sch, q, qo, s, so, res)
         _check_tb(ctx, sch, q, qo, s, so, res, ocig)
@@ -574,6 +575,7 @@ def test_mixed_batch_routes_long_pairs(ctx, kind):
         assert np.array_equal(aln["cigar_offset"], np.cumsum(cl) - cl)
     finally:
         ctx.set_option("batch_long_cells", 1 << 22)
+        ctx.set_option("batch_long_cells_tb", 1 << 26)
 
 
 @pytest.mark.parametrize("kind", ["global", "semi", "local"])
