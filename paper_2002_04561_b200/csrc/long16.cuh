@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(128, (NR <= 12 || (LONG16_MINB > 3 && !CKPT)) 
       }
       am = a_.pairs[sg.x];
       task = sg.y * am.S + task - (cur > 0 ? a_.task_end[cur - 1] : 0);
+      ANY_CHECK(sg.y < am.g_count && task >= sg.y * am.S && task < (sg.y + 1) * am.S);
     }
     const LongArgs& a = MULTI ? am : a_;
     const int n = a.n;
