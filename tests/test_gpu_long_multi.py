@@ -180,3 +180,20 @@ def test_batch_of_only_long_pairs(ctx, kind):
     finally:
         ctx.set_option("long_multi", 1)
         ctx.set_option("batch_long_cells", 1 << 22)
+
+
+def test_mixed_batch_two_entry_context():
+    """A context naming GPU 0 twice: the batch kernels' pass shards the batch over the two
+    entries with the long pairs skipped in each shard (ClassifyArgs::skip_cells copied into
+    the per-entry contexts), and the long pairs run one at a time over the two-entry long
+    path (one launch, two column strips).  Results equal the oracle's."""
+    import paper_2002_04561_b200 as A
+    q, qo, s, so, nl = _batch(611, with_n=True)
+    osc, oqe, ose = _oracle_scores("local", "affine", 5, q, qo, s, so)
+    sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+    with A.Context([0, 0]) as c:
+        c.set_option("batch_long_cells", 1 << 22)
+        sc, ends = c.align_batch(sch, q, qo, s, so, ends=True)
+        assert c.stat("long_multi_pairs") == 0  # the shared launch is one-device only
+        assert np.array_equal(sc, osc)
+        assert np.array_equal(ends["q_end"], oqe) and np.array_equal(ends["s_end"], ose)
