@@ -1201,16 +1201,6 @@ anyseq_status run_traceback_long(anyseq_ctx* ctx, const anyseq_params* prm, cons
                                  uint64_t n, const char* s, uint64_t m, anyseq_alignment* out,
                                  uint32_t* cigar, uint64_t cap, uint64_t* used);
 
-// Mixed batches (host-side form): a pair whose matrix is large (n·m >=
-// option batch_long_cells, both sides >= 2048) would tie one 8-lane group of the batch
-// kernel up for seconds; it goes to the long-pair path instead (the tiled wavefront over all
-// SMs, §5.4 / §5.4c), the rest of the batch to the batch path, and the results are merged in
-// pair order (both paths follow the same optimum and traceback rules, so the results are the
-// ones the batch path would give).  A batch of only a few pairs (option batch_long_small)
-// sends every pair with both sides >= 256 there too: the batch kernel gives a pair one
-// 8-lane group, the long kernel spreads it over many warps (C1, one 1000 x 1000 pair:
-// 1.3 ms instead of 5 ms with traceback).  A pair the long path cannot take (e.g. affine
-// traceback of a subject with N) falls back to the batch path on its own.
 // Score mode of a mixed batch without copying it: the batch kernels skip the long pairs
 // (classify leaves pairs of >= batch_long_cells cells unplanned, ClassifyArgs::skip_cells)
 // and run while the long pairs share one launch of the long kernel (run_long_multi, one
@@ -1303,6 +1293,17 @@ static anyseq_status run_host_batch_inplace(anyseq_ctx* ctx, const anyseq_params
   return ANYSEQ_OK;
 }
 
+// Mixed batches: a pair whose matrix is large (n·m >= option
+// batch_long_cells -- batch_long_cells_tb in traceback mode -- both sides >= batch_long_min) would tie one 8-lane group of the batch
+// kernel up for seconds; it goes to the long-pair path instead (the tiled wavefront over all
+// SMs, §5.4 / §5.4c), the rest of the batch to the batch path, and the results are merged in
+// pair order (both paths follow the same optimum and traceback rules, so the results are the
+// ones the batch path would give).  A batch of only a few pairs (option batch_long_small)
+// sends every pair with both sides >= 256 there too: the batch kernel gives a pair one
+// 8-lane group, the long kernel spreads it over many warps (C1, one 1000 x 1000 pair:
+// 1.3 ms instead of 5 ms with traceback).  A pair the long path cannot take (e.g. affine
+// traceback of a subject with N) falls back to the batch path on its own.  Score mode
+// (not a small batch) takes run_host_batch_inplace above.
 anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const anyseq_batch* b,
                              int tb, int32_t* scores, anyseq_alignment* aln, uint32_t* cigar,
                              uint64_t cap, uint64_t* used) {
