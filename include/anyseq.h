@@ -122,7 +122,10 @@ anyseq_status anyseq_align_batch_device(anyseq_ctx* ctx, const anyseq_params* pa
 /* Full alignment with traceback (predecessor walk) for a batch.
    out[num_pairs] (host), cigar[cigar_capacity] (host).  cigar_capacity >= sum(n_k + m_k)
    always suffices; if smaller, returns ANYSEQ_E_CAPACITY with *cigar_used = words
-   required.  Otherwise *cigar_used = words written. */
+   required.  Otherwise *cigar_used = words written.  Pairs of >= "batch_long_cells_tb"
+   cells (both sides >= "batch_long_min") take the long-pair traceback (SURVEY 8(f) f1/f4:
+   one shared checkpointing pass on one device, then a tile walk per pair); the results are
+   the same alignments (same optimum and tie rules). */
 anyseq_status anyseq_traceback(anyseq_ctx* ctx, const anyseq_params* params,
                                const anyseq_batch* batch, anyseq_alignment* out,
                                uint32_t* cigar, uint64_t cigar_capacity, uint64_t* cigar_used);
@@ -227,10 +230,10 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
                          2^22; 0 = never).  Score mode, one device: all such pairs of the call
                          share ONE launch of the long kernel (their row-strip tasks in one
                          device queue) while the batch kernels
-                         align the other pairs in place; traceback: one pair at a time
-     "batch_long_cells_tb"  the same threshold for anyseq_traceback (default 2^26: long pairs
-                         there are aligned one at a time, so medium pairs stay in the batch
-                         traceback kernel)
+                         align the other pairs in place
+     "batch_long_cells_tb"  the same threshold for anyseq_traceback (default 2^22): one
+                         device -> one shared checkpointing forward pass over all such pairs,
+                         then each pair's tile walk
      "batch_long_min"    minimum length of both sides for that routing (default 2048)
      "long_multi"        1 (default): the shared launch above; 0: one long-pair call per pair
      "batch_long_small"  batches of at most this many pairs send every pair with n, m >= 256

@@ -117,8 +117,7 @@ struct anyseq_ctx {
   int64_t allow16 = 1;
   int64_t batch_long_cells = 1ll << 22;  // batch pairs this large take the long-pair path
   int64_t batch_long_min = 2048;         // ... when both sides are at least this long
-  int64_t batch_long_cells_tb = 1ll << 26;  // traceback mode's threshold (long pairs there
-                                            // run one at a time)
+  int64_t batch_long_cells_tb = 1ll << 22;  // traceback mode's threshold
   int64_t batch_long_small = 4;  // batches of at most this many pairs: every pair with both
                                  // sides >= 256 takes the long-pair path
   int64_t tb8 = 1;          // traceback: 1-byte H store where the range allows
@@ -1370,7 +1369,7 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
   std::vector<anyseq_alignment> al3(BL);
   std::vector<std::vector<uint32_t>> cg3(BL);
   std::vector<int> done(BL, 0);
-  const bool multi = !tb && ctx->long_multi && BL >= 2 && ctx->devs.size() == 1;
+  const bool multi = ctx->long_multi && BL >= 2 && ctx->devs.size() == 1;
   if (!multi) {
     const int r = run_short();
     if (r != ANYSEQ_OK) return (anyseq_status)r;
@@ -1400,19 +1399,44 @@ anyseq_status run_host_batch(anyseq_ctx* ctx, const anyseq_params* prm, const an
     uint64_t launches = 0;
     double kms = 0;
     int rs = ANYSEQ_OK;
-    const int rc = run_long_multi(ld, dev_params(prm), in, ctx->long_opt, &lr, &took, &err,
-                                  &launches, &kms, [&]() { return rs = run_short(); });
+    // traceback: the shared launch is the checkpointing forward pass of every pair, then
+    // each pair's tile walk (run_long_traceback) from its checkpoints
+    std::vector<LongCkpt> cks;
+    const DevParams dp = dev_params(prm);
+    const int rc = run_long_multi(ld, dp, in, ctx->long_opt, &lr, &took, &err, &launches, &kms,
+                                  [&]() { return rs = run_short(); }, &ctx->long_multi_rows,
+                                  tb ? &cks : nullptr, ctx->tb_budget);
     ctx->launches += launches;
     if (rs != ANYSEQ_OK) return (anyseq_status)rs;
     if (rc != 0) return fail(ctx, (anyseq_status)rc, "long pairs (one launch): %s", err.c_str());
+    int8_t sig[25];
+    for (int a = 0; a < 5; ++a)
+      for (int c = 0; c < 5; ++c)
+        sig[5 * a + c] = (int8_t)(prm->has_subst ? prm->subst[5 * a + c]
+                                                 : ((a == c && a < 4) ? prm->match : prm->mismatch));
     for (uint64_t y = 0; y < BL; ++y) {
       if (!took[y]) continue;
       const uint64_t x = ord[y];
-      done[x] = 1;
       memset(&al3[x], 0, sizeof(al3[x]));
       al3[x].score = lr[y].score;
       al3[x].q_end = al3[x].q_begin = lr[y].end_i;
       al3[x].s_end = al3[x].s_begin = lr[y].end_j;
+      if (tb) {
+        int64_t bi = 0, bj = 0;
+        double wms = 0;
+        uint64_t wl = 0;
+        const int rw = run_long_traceback(ld, dp, sig, cks[y], lr[y].end_i, lr[y].end_j,
+                                          (int64_t)in[y].n, (int64_t)in[y].m, &cg3[x], &bi, &bj,
+                                          &wms, &err, &wl, (int)ctx->walk_helpers);
+        ctx->launches += wl;
+        if (rw != 0)
+          return fail(ctx, (anyseq_status)rw, "pair %llu (long-pair walk): %s",
+                      (unsigned long long)longs[x], err.c_str());
+        al3[x].q_begin = bi;
+        al3[x].s_begin = bj;
+        al3[x].cigar_len = (uint32_t)cg3[x].size();
+      }
+      done[x] = 1;
       ++ctx->long_multi_pairs;
     }
     ctx->long_multi_ms = kms;

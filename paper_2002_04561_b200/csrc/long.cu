@@ -963,10 +963,17 @@ __global__ void semi_reduce_multi_kernel(const LongArgs* __restrict__ pairs, int
 int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPairIn>& pairs,
                    const LongOptions& opt, std::vector<LongResult>* out, std::vector<int>* taken,
                    std::string* err, uint64_t* launches, double* kernel_ms,
-                   const std::function<int()>& during, int* rows_out) {
+                   const std::function<int()>& during, int* rows_out,
+                   std::vector<LongCkpt>* cks, int64_t ck_budget) {
   const size_t K0 = pairs.size();
   out->assign(K0, LongResult{0, 0, 0, 0.0, true});
   taken->assign(K0, 0);
+  const bool want_ck = cks != nullptr;
+  if (want_ck) {
+    cks->clear();
+    cks->resize(K0);
+    for (LongCkpt& c : *cks) c.owns = false;
+  }
   *kernel_ms = 0;
   // the eligibility rules of run_long's 16-bit path (at 512-row tasks, NR = 8)
   const int64_t d16 = (int64_t)P.go + P.ge + std::max(P.smax, 0);
@@ -1002,7 +1009,7 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
   int NR = 8;
   if (fits16(16) && opt.band_rows != 512) {
     int nb16 = 0;
-    LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb16, long16_multi_fn(P.kind, 16), 128, 0));
+    LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb16, long16_multi_fn(P.kind, 16, want_ck), 128, 0));
     double T16 = 0;
     for (size_t k : sel) T16 += (double)((pairs[k].n + 1023) / 1024);
     if (T16 >= 4.0 * dev.num_sms * std::max(nb16, 1) || opt.band_rows == 1024) NR = 16;
@@ -1010,7 +1017,7 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
   const int HS = 64 * NR;
   if (rows_out) *rows_out = HS;
   const int64_t bspan16 = (int64_t)(64 * NR + 66) * d16;
-  LongFn fn = long16_multi_fn(P.kind, NR);
+  LongFn fn = long16_multi_fn(P.kind, NR, want_ck);
   int nb = 0;
   LK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 128, 0));
   int grid = dev.num_sms * std::max(nb, 1);
@@ -1068,9 +1075,23 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
     flo[x + 1] = flo[x] + (int64_t)G[x] * S[x];
     cbo[x + 1] = cbo[x] + G[x] + 1;
   }
+  // traceback: checkpoint rows after every strip, columns every 2^9 (the single-pair
+  // path's finest geometry), one workspace buffer for all pairs
+  constexpr int kCkShift = 9;
+  std::vector<int64_t> cko(K + 1, 0);
+  if (want_ck) {
+    for (int x = 0; x < K; ++x) {
+      const int64_t n = (int64_t)pairs[sel[x]].n, m = (int64_t)pairs[sel[x]].m;
+      cko[x + 1] = cko[x] + (int64_t)(S[x] - 1) * (m + 1) + ((m - 1) >> kCkShift) * (n + 1);
+    }
+    size_t fr = 0, tot = 0;
+    LK(cudaMemGetInfo(&fr, &tot));
+    const int64_t budget = ck_budget > 0 ? ck_budget : (int64_t)(0.4 * (double)fr);
+    if (cko[K] * (int64_t)sizeof(int2) > budget) return during ? during() : 0;  // none taken
+  }
   LongWs* ws = dev.ws;
   Buf qa, sa, qc, sc, sum, flg, off, rowbuf, bcol, flags, cbuf, bptr, fptr, ticket, abort_, parts,
-      mp, mt, ms_, red, kb;
+      mp, mt, ms_, red, kb, ckb;
   // ASCII upload + pack (all pairs in one pack launch)
   std::string cq, cs;
   cq.reserve(qo[K]);
@@ -1119,6 +1140,7 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
   LK(get_buf(ms_, ws, WS_M_SEGS, (size_t)NS * sizeof(int2)));
   LK(get_buf(red, ws, WS_M_RED, (size_t)K * sizeof(LongPart)));
   if (P.kind == KSEMI) LK(get_buf(kb, ws, WS_KEY, (size_t)K * 8));
+  if (want_ck) LK(get_buf(ckb, ws, WS_ROWCK, (size_t)std::max<int64_t>(cko[K], 1) * sizeof(int2)));
   LK(cudaMemsetAsync(flags.p, 0, (size_t)flo[K] * 4, st));
   LK(cudaMemsetAsync(ticket.p, 0, 4, st));
   LK(cudaMemsetAsync(abort_.p, 0, 4, st));
@@ -1169,6 +1191,12 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
     a.pad_top = P.kind == KSEMI ? (int)((uint64_t)S[x] * HS - n) : 0;
     a.ck_every = 1;
     a.kc_shift = 30;
+    if (want_ck) {
+      int2* base = (int2*)ckb.p + cko[x];
+      a.rowck = S[x] > 1 ? base : nullptr;
+      a.colck = ((m - 1) >> kCkShift) > 0 ? base + (size_t)(S[x] - 1) * (m + 1) : nullptr;
+      a.kc_shift = kCkShift;
+    }
     a.spin_limit = opt.spin_limit;
     a.stall_task = -1;
   }
@@ -1253,6 +1281,20 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
       r.score = rp[x].gv; r.end_i = n; r.end_j = m;
     }
     (*taken)[k] = 1;
+    if (want_ck) {
+      LongCkpt& c = (*cks)[k];
+      c.owns = false;
+      c.qc = (uint8_t*)la[x].qc;
+      c.sc = (uint8_t*)la[x].sc;
+      c.rowck = la[x].rowck;
+      c.colck = la[x].colck;
+      c.HS = HS;
+      c.ck_every = 1;
+      c.kc_shift = kCkShift;
+      c.PT = la[x].pad_top;
+      c.S = S[x];
+      c.bytes = (size_t)(cko[x + 1] - cko[x]) * sizeof(int2);
+    }
   }
   return 0;
 }

@@ -113,6 +113,10 @@ int run_long(std::vector<LongDevice>& devs, const DevParams& P, const char* q, u
 // run_long's (same kernel body, same optimum rules).  `during` (optional) runs on the host
 // while the launch is in flight (it runs even when no pair is taken); the launch uses the
 // workspace's own non-blocking stream, so work `during` enqueues elsewhere overlaps it.
+// cks (optional): the pass is the traceback's checkpointing forward pass (CKPT instances,
+// 512-column blocks, a row checkpoint after every strip) and (*cks)[k] receives pair k's
+// checkpoint view (buffers in the workspace, owns = false) for run_long_traceback; when the
+// checkpoints of all pairs exceed ck_budget (0 = 40 % of free memory) no pair is taken.
 struct LongPairIn {
   const char* q;
   uint64_t n;
@@ -122,6 +126,7 @@ struct LongPairIn {
 int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPairIn>& pairs,
                    const LongOptions& opt, std::vector<LongResult>* out, std::vector<int>* taken,
                    std::string* err, uint64_t* launches, double* kernel_ms,
-                   const std::function<int()>& during = {}, int* rows_out = nullptr);
+                   const std::function<int()>& during = {}, int* rows_out = nullptr,
+                   std::vector<LongCkpt>* cks = nullptr, int64_t ck_budget = 0);
 
 }  // namespace anyseq

@@ -12,8 +12,9 @@ LongFn long16_fn_global(int nr, bool ckpt) {
   return nr == 8 ? long16_kernel<8, KGLOBAL> : long16_kernel<16, KGLOBAL>;
 }
 
-// several pairs in one launch (MULTI, score-only)
-LongFn long16_fn_global_multi(int nr) {
+// several pairs in one launch (MULTI; CKPT: the traceback's forward pass)
+LongFn long16_fn_global_multi(int nr, bool ckpt) {
+  if (ckpt) return nr == 8 ? long16_kernel<8, KGLOBAL, true, true> : long16_kernel<16, KGLOBAL, true, true>;
   return nr == 8 ? long16_kernel<8, KGLOBAL, false, true> : long16_kernel<16, KGLOBAL, false, true>;
 }
 

@@ -12,8 +12,9 @@ LongFn long16_fn_local(int nr, bool ckpt) {
   return nr == 8 ? long16_kernel<8, KLOCAL> : long16_kernel<16, KLOCAL>;
 }
 
-// several pairs in one launch (MULTI, score-only)
-LongFn long16_fn_local_multi(int nr) {
+// several pairs in one launch (MULTI; CKPT: the traceback's forward pass)
+LongFn long16_fn_local_multi(int nr, bool ckpt) {
+  if (ckpt) return nr == 8 ? long16_kernel<8, KLOCAL, true, true> : long16_kernel<16, KLOCAL, true, true>;
   return nr == 8 ? long16_kernel<8, KLOCAL, false, true> : long16_kernel<16, KLOCAL, false, true>;
 }
 

@@ -12,8 +12,9 @@ LongFn long16_fn_semi(int nr, bool ckpt) {
   return nr == 8 ? long16_kernel<8, KSEMI> : long16_kernel<16, KSEMI>;
 }
 
-// several pairs in one launch (MULTI, score-only)
-LongFn long16_fn_semi_multi(int nr) {
+// several pairs in one launch (MULTI; CKPT: the traceback's forward pass)
+LongFn long16_fn_semi_multi(int nr, bool ckpt) {
+  if (ckpt) return nr == 8 ? long16_kernel<8, KSEMI, true, true> : long16_kernel<16, KSEMI, true, true>;
   return nr == 8 ? long16_kernel<8, KSEMI, false, true> : long16_kernel<16, KSEMI, false, true>;
 }
 

@@ -147,6 +147,6 @@ __device__ __forceinline__ int imad_add_s(int x, uint32_t one, int k) {
 typedef void (*LongFn)(LongArgs);
 // long16_*.cu: the 16-bit differential kernel instance for (rows per lane, kind, checkpoints)
 LongFn long16_fn(int nr, int kind, bool ckpt);
-LongFn long16_multi_fn(int kind, int nr);  // MULTI instances (score-only; nr 8 or 16)
+LongFn long16_multi_fn(int kind, int nr, bool ckpt = false);  // MULTI instances (nr 8 or 16)
 
 }  // namespace anyseq

@@ -575,7 +575,7 @@ def test_mixed_batch_routes_long_pairs(ctx, kind):
         assert np.array_equal(aln["cigar_offset"], np.cumsum(cl) - cl)
     finally:
         ctx.set_option("batch_long_cells", 1 << 22)
-        ctx.set_option("batch_long_cells_tb", 1 << 26)
+        ctx.set_option("batch_long_cells_tb", 1 << 22)
 
 
 @pytest.mark.parametrize("kind", ["global", "semi", "local"])

@@ -197,3 +197,54 @@ def test_mixed_batch_two_entry_context():
         assert c.stat("long_multi_pairs") == 0  # the shared launch is one-device only
         assert np.array_equal(sc, osc)
         assert np.array_equal(ends["q_end"], oqe) and np.array_equal(ends["s_end"], ose)
+
+
+def _tb_batch(seed, with_n):
+    from synth import c4_genomes, random_pairs, csr
+    g1, g2 = c4_genomes(12000, "a", seed=seed)
+    q0, qo0, s0, so0 = random_pairs(20, 0, 250, seed=seed + 1)
+    qs = [q0[qo0[k]:qo0[k + 1]].tobytes() for k in range(20)]
+    ss = [s0[so0[k]:so0[k + 1]].tobytes() for k in range(20)]
+    shapes = [(2048, 2900), (2700, 2100), (2300, 2400), (2049, 2050), (2600, 2500)]
+    longs = [(g1[k * 1500:k * 1500 + n], g2[k * 1500 + 20:k * 1500 + 20 + m])
+             for k, (n, m) in enumerate(shapes)]
+    if with_n:
+        sN = bytearray(g2[9000:11100])
+        sN[700] = ord("N")
+        longs.append((g1[9000:11200], bytes(sN)))
+    for x, (a, b) in enumerate(longs):
+        pos = (5 * x + 2) % (len(qs) + 1)
+        qs.insert(pos, a)
+        ss.insert(pos, b)
+    q, qo = csr(qs)
+    s, so = csr(ss)
+    return q, qo, s, so, len(shapes)
+
+
+@pytest.mark.parametrize("kind", ["global", "semi", "local"])
+@pytest.mark.parametrize("gap,go", [("linear", 0), ("affine", 5)])
+def test_traceback_long_pairs_one_pass(ctx, kind, gap, go):
+    """Traceback batches: the long pairs' checkpointing forward passes share one launch
+    (MULTI + CKPT instance), then each pair's tile walk runs from its checkpoints.  Scores,
+    begin/end cells and CIGARs equal the oracle's; cigar offsets stay contiguous."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    q, qo, s, so, nl = _tb_batch(700 + len(kind) + go, with_n=(kind == "global" and gap == "linear"))
+    osch = O.Scheme(kind, gap, 2, -1, go, 1)
+    res, cig = O.batch(osch, q, qo, s, so, traceback=True)
+    ocig = O.batch_cigars(res, cig, qo, so)
+    sch = A.Scheme(kind, gap, 2, -1, go, 1)
+    ctx.set_option("batch_long_cells_tb", 1 << 22)
+    try:
+        aln, words = ctx.traceback(sch, q, qo, s, so)
+        assert ctx.stat("long_multi_pairs") == nl
+        assert np.array_equal(aln["score"], res["score"].astype(np.int32))
+        for f in ("q_begin", "s_begin", "q_end", "s_end"):
+            assert np.array_equal(aln[f], res[f]), f
+        got = A.cigars_of(aln, words)
+        bad = [k for k in range(len(got)) if got[k] != ocig[k]]
+        assert not bad, f"CIGAR mismatches at {bad[:5]}"
+        cl = aln["cigar_len"].astype(np.uint64)
+        assert np.array_equal(aln["cigar_offset"], np.cumsum(cl) - cl)
+    finally:
+        ctx.set_option("batch_long_cells_tb", 1 << 22)

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--cells", type=int, default=1 << 22, help="option batch_long_cells")
     ap.add_argument("--min", type=int, default=2048, help="option batch_long_min")
     ap.add_argument("--rows", type=int, default=0, help="option long_band_rows (512/1024 force)")
+    ap.add_argument("--tb", action="store_true", help="traceback mode (anyseq_traceback)")
     ap.add_argument("--only", type=int, default=-1, help="run only long_multi = this")
     args = ap.parse_args()
     import paper_2002_04561_b200 as A
@@ -52,6 +53,8 @@ def main():
            "kind": args.kind, "cells": cells}
     with A.Context([0]) as ctx:
         ctx.set_option("batch_long_cells", args.cells)
+        ctx.set_option("batch_long_cells_tb", args.cells)
+        out["mode"] = "traceback" if args.tb else "score"
         out["batch_long_cells"] = args.cells
         ctx.set_option("batch_long_min", args.min)
         out["batch_long_min"] = args.min
@@ -60,11 +63,18 @@ def main():
         res = {}
         for multi in ((1, 0) if args.only < 0 else (args.only,)):
             ctx.set_option("long_multi", multi)
-            sc = ctx.align_batch(sch, q, qo, s, so)  # warm-up
+            def call():
+                if args.tb:
+                    aln, words = ctx.traceback(sch, q, qo, s, so)
+                    return np.concatenate([aln["score"].astype(np.int64), aln["q_begin"],
+                                           aln["s_begin"], aln["cigar_len"].astype(np.int64),
+                                           words.astype(np.int64)])
+                return ctx.align_batch(sch, q, qo, s, so)
+            sc = call()  # warm-up
             best = 1e30
             for _ in range(args.reps):
                 t0 = time.perf_counter()
-                sc = ctx.align_batch(sch, q, qo, s, so)
+                sc = call()
                 best = min(best, time.perf_counter() - t0)
             res[multi] = sc
             out[f"multi{multi}"] = {"wall_ms": round(best * 1e3, 2),
