@@ -1033,7 +1033,15 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
     Tw += (double)S[x] * ((double)pairs[sel[x]].m + 64);
   }
   Tw /= nw;
-  const double Wt = std::max(4096.0, Tw / 4);
+  static const double wmin = [] {  // tuning: ANYSEQ_MULTI_WMIN (columns), ANYSEQ_MULTI_WDIV
+    const char* e = getenv("ANYSEQ_MULTI_WMIN");
+    return e ? atof(e) : 4096.0;
+  }();
+  static const double wdiv = [] {
+    const char* e = getenv("ANYSEQ_MULTI_WDIV");
+    return e ? atof(e) : 4.0;
+  }();
+  const double Wt = std::max(wmin, Tw / wdiv);
   int Gmax = 1;
   for (int x = 0; x < K; ++x) {
     const uint64_t m = pairs[sel[x]].m;
