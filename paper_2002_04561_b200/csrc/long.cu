@@ -1129,8 +1129,14 @@ int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPa
   *launches += 1;
   LK(cudaMemcpyAsync(&hs, sum.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
   LK(cudaStreamSynchronize(st));
-  if (hs.err_pos != ~0ull) {
-    *err = "invalid symbol in a long pair";
+  if (hs.err_pos != ~0ull) {  // offsets into the concatenated sequences -> pair and offset
+    const bool in_s = hs.err_pos >= (1ull << 62);
+    const uint64_t pos = in_s ? hs.err_pos - (1ull << 62) : hs.err_pos;
+    const std::vector<uint64_t>& o = in_s ? so : qo;
+    int x = 0;
+    while (x + 1 < K && o[x + 1] <= pos) ++x;
+    *err = std::string("invalid symbol at ") + (in_s ? "s" : "q") + " offset " +
+           std::to_string(pos - o[x]) + " of long pair " + std::to_string(sel[x]);
     return ANYSEQ_E_BADSEQ;
   }
   // DP state of every pair

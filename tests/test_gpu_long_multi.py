@@ -248,3 +248,32 @@ def test_traceback_long_pairs_one_pass(ctx, kind, gap, go):
         assert np.array_equal(aln["cigar_offset"], np.cumsum(cl) - cl)
     finally:
         ctx.set_option("batch_long_cells_tb", 1 << 22)
+
+
+@pytest.mark.parametrize("tb", [False, True])
+def test_bad_symbol_in_long_pair(ctx, tb):
+    """An invalid byte inside a long pair of a mixed batch is reported as E_BADSEQ (no
+    result is returned), and the context aligns the next batch normally."""
+    import paper_2002_04561_b200 as A
+    from synth import csr
+    q, qo, s, so, nl = _batch(901, with_n=False)
+    qs = [q[qo[k]:qo[k + 1]].tobytes() for k in range(len(qo) - 1)]
+    ss = [s[so[k]:so[k + 1]].tobytes() for k in range(len(so) - 1)]
+    k = max(range(len(qs)), key=lambda i: len(qs[i]) * len(ss[i]))  # a long pair
+    bad = bytearray(ss[k])
+    bad[1500] = ord("X")
+    ss2 = list(ss)
+    ss2[k] = bytes(bad)
+    sb, sob = csr(ss2)
+    sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+    ctx.set_option("batch_long_cells", 1 << 22)
+    ctx.set_option("batch_long_cells_tb", 1 << 22)
+    with pytest.raises(A.AnyseqError) as e:
+        if tb:
+            ctx.traceback(sch, q, qo, sb, sob)
+        else:
+            ctx.align_batch(sch, q, qo, sb, sob)
+    assert e.value.status_name == "E_BADSEQ"
+    sc = ctx.align_batch(sch, q, qo, s, so)
+    osc, _, _ = _oracle_scores("local", "affine", 5, q, qo, s, so)
+    assert np.array_equal(sc, osc)
