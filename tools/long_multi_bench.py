@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--min", type=int, default=2048, help="option batch_long_min")
     ap.add_argument("--rows", type=int, default=0, help="option long_band_rows (512/1024 force)")
     ap.add_argument("--tb", action="store_true", help="traceback mode (anyseq_traceback)")
+    ap.add_argument("--helpers", type=int, default=96, help="option walk_helpers")
     ap.add_argument("--only", type=int, default=-1, help="run only long_multi = this")
     args = ap.parse_args()
     import paper_2002_04561_b200 as A
@@ -55,6 +56,8 @@ def main():
         ctx.set_option("batch_long_cells", args.cells)
         ctx.set_option("batch_long_cells_tb", args.cells)
         out["mode"] = "traceback" if args.tb else "score"
+        ctx.set_option("walk_helpers", args.helpers)
+        out["walk_helpers"] = args.helpers
         out["batch_long_cells"] = args.cells
         ctx.set_option("batch_long_min", args.min)
         out["batch_long_min"] = args.min
