@@ -297,6 +297,55 @@ def mixed_sizes_leg(ctx, A, n_long, n_short, n_sm, f_mhz, reps=3):
             "same_scores_as_one_call_per_pair": bool(np.array_equal(sc, sc1))}
 
 
+def mixed_sizes_traceback_leg(ctx, A, n_long=200, n_short=10_000, reps=3):
+    """SURVEY 8(f) f4 in traceback mode: n_long similar pairs of 2-10 kbp
+    mixed into n_short random 100-300 bp pairs, local affine 5/1, anyseq_traceback through
+    the host API (pageable buffers): the long pairs' checkpointing forward passes share one
+    launch (overlapped with the short pairs' batch traceback), then each long pair is walked
+    from its checkpoints.  value = all cells / best wall time; checked (scores, cells and
+    CIGARs) against the one-long-traceback-per-pair path (option long_multi = 0)."""
+    import numpy as np
+    from synth import c4_genomes, random_pairs, csr
+    rng = np.random.default_rng(8)
+    g1, g2 = c4_genomes(1_000_000, "a", seed=9)
+    q0, qo0, s0, so0 = random_pairs(n_short, 100, 300, seed=10)
+    qs = [q0[qo0[k]:qo0[k + 1]].tobytes() for k in range(n_short)]
+    ss = [s0[so0[k]:so0[k + 1]].tobytes() for k in range(n_short)]
+    cells = float(np.sum(np.diff(qo0).astype(np.float64) * np.diff(so0)))
+    for _ in range(n_long):
+        n = int(rng.integers(2048, 10001))
+        m = int(rng.integers(2048, 10001))
+        a = int(rng.integers(0, len(g1) - max(n, m)))
+        pos = int(rng.integers(0, len(qs) + 1))
+        qs.insert(pos, g1[a:a + n])
+        ss.insert(pos, g2[a:a + m])
+        cells += float(n) * m
+    q, qo = csr(qs)
+    s, so = csr(ss)
+    sch = A.Scheme("local", "affine", 2, -1, 5, 1)
+    aln, words = ctx.traceback(sch, q, qo, s, so)  # warm-up
+    best = 1e30
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        aln, words = ctx.traceback(sch, q, qo, s, so)
+        best = min(best, time.perf_counter() - t0)
+    taken = int(ctx.stat("long_multi_pairs"))
+    kms = ctx.stat("long_multi_ms")
+    ctx.set_option("long_multi", 0)
+    t0 = time.perf_counter()
+    aln1, words1 = ctx.traceback(sch, q, qo, s, so)
+    per_pair = time.perf_counter() - t0
+    ctx.set_option("long_multi", 1)
+    same = bool(np.array_equal(aln, aln1) and np.array_equal(words, words1))
+    return {"workload": f"{n_long} pairs of 2-10 kbp (mutated genome windows) + {n_short} pairs of "
+                        "100-300 bp, local affine open 5 / extend 1, match 2 / mismatch -1, "
+                        "traceback + CIGAR, host API from pageable buffers, 1 GPU",
+            "value": round(cells / best / 1e9, 1), "unit": "GCUPS", "wall_ms": round(best * 1e3, 2),
+            "long_pairs_in_shared_pass": taken, "shared_pass_ms": round(kms, 2),
+            "one_traceback_per_long_pair_wall_ms": round(per_pair * 1e3, 1),
+            "same_alignments_as_one_per_pair": same}
+
+
 def long_traceback_leg(ctx, A, n, kind="global", gap="linear", go=0):
     """linear-space traceback of a C4-shaped pair (n-bp genomes, G2 =
     mutated copy of G1), once, through anyseq_traceback_long with host buffers: one
@@ -543,6 +592,7 @@ def main():
             dist.barrier(group=cpu_group)
     if rank == 0 and args.mixed_long > 0:
         line["mixed_sizes"] = mixed_sizes_leg(ctx, A, args.mixed_long, args.mixed_short, n_sm, f_mhz)
+        line["mixed_sizes_traceback"] = mixed_sizes_traceback_leg(ctx, A)
     if rank == 0 and args.long_tb_bp > 0:
         line["long_traceback"] = long_traceback_leg(ctx, A, args.long_tb_bp)
         line["long_traceback_local_affine"] = long_traceback_leg(ctx, A, args.long_tb_bp,
