@@ -236,6 +236,8 @@ anyseq_status anyseq_reset_stats(anyseq_ctx* ctx);
                          then each pair's tile walk
      "batch_long_min"    minimum length of both sides for that routing (default 2048)
      "long_multi"        1 (default): the shared launch above; 0: one long-pair call per pair
+     "long_multi_group"  pairs per shared launch (default 2048; more pairs: several launches
+                         in score mode, the rest one at a time in traceback mode)
      "batch_long_small"  batches of at most this many pairs send every pair with n, m >= 256
                          to the long-pair path (default 4; 0 = never); pairs that path cannot
                          take stay on the batch kernel

@@ -2197,6 +2197,7 @@ anyseq_status anyseq_set_option(anyseq_ctx* ctx, const char* name, int64_t value
       ctx->long_opt.spin_limit = value > 0 ? (long long)value : (1ll << 28);
       return ANYSEQ_OK;
     }
+    if (n == "long_multi_group") { ctx->long_opt.multi_group = (int)std::max<int64_t>(value, 1); return ANYSEQ_OK; }
     if (n == "long_stall_task") { ctx->long_opt.stall_task = (int)value; return ANYSEQ_OK; }
     if (n == "long_chunk_cols") { ctx->long_opt.chunk_cols = (int)value; return ANYSEQ_OK; }
     return fail(ctx, ANYSEQ_E_INVALID, "unknown option %s", name);

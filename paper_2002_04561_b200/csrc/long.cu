@@ -960,11 +960,68 @@ __global__ void semi_reduce_multi_kernel(const LongArgs* __restrict__ pairs, int
   }
 }
 
+static int run_long_multi_group(LongDevice& dev, const DevParams& P,
+                                const std::vector<LongPairIn>& pairs, const LongOptions& opt,
+                                std::vector<LongResult>* out, std::vector<int>* taken,
+                                std::string* err, uint64_t* launches, double* kernel_ms,
+                                const std::function<int()>& during, int* rows_out,
+                                std::vector<LongCkpt>* cks, int64_t ck_budget);
+
+// Launches of at most opt.multi_group pairs each (per-launch device state, e.g. the per-warp
+// optimum slots of every pair, stays bounded: 2048 pairs x resident warps x 40 B ~ 0.2 GB).  With
+// checkpoints (traceback) only the first group is taken: its checkpoints live in the
+// workspace until the caller has walked them; the rest are left to the caller.
 int run_long_multi(LongDevice& dev, const DevParams& P, const std::vector<LongPairIn>& pairs,
                    const LongOptions& opt, std::vector<LongResult>* out, std::vector<int>* taken,
                    std::string* err, uint64_t* launches, double* kernel_ms,
                    const std::function<int()>& during, int* rows_out,
                    std::vector<LongCkpt>* cks, int64_t ck_budget) {
+  const size_t kGroup = (size_t)std::max(1, opt.multi_group);
+  const size_t K0 = pairs.size();
+  if (K0 <= kGroup)
+    return run_long_multi_group(dev, P, pairs, opt, out, taken, err, launches, kernel_ms, during,
+                                rows_out, cks, ck_budget);
+  out->assign(K0, LongResult{0, 0, 0, 0.0, true});
+  taken->assign(K0, 0);
+  *kernel_ms = 0;
+  if (cks) {
+    cks->clear();
+    cks->resize(K0);
+    for (LongCkpt& c : *cks) c.owns = false;
+  }
+  for (size_t g0 = 0; g0 < K0; g0 += kGroup) {
+    const size_t g1 = std::min(K0, g0 + kGroup);
+    const std::vector<LongPairIn> sub(pairs.begin() + g0, pairs.begin() + g1);
+    std::vector<LongResult> so;
+    std::vector<int> st;
+    std::vector<LongCkpt> sc;
+    double ms = 0;
+    const int rc = run_long_multi_group(dev, P, sub, opt, &so, &st, err, launches, &ms,
+                                        g0 == 0 ? during : std::function<int()>(), rows_out,
+                                        cks ? &sc : nullptr, ck_budget);
+    if (rc != 0) return rc;
+    *kernel_ms += ms;
+    for (size_t k = 0; k < sub.size(); ++k) {
+      (*out)[g0 + k] = so[k];
+      (*taken)[g0 + k] = st[k];
+      if (cks && st[k]) {
+        LongCkpt& c = (*cks)[g0 + k];
+        c = sc[k];  // a view (owns = false): copying it moves no buffer
+        sc[k].qc = sc[k].sc = nullptr;
+        sc[k].rowck = sc[k].colck = nullptr;
+      }
+    }
+    if (cks) break;  // traceback: one group (see above)
+  }
+  return 0;
+}
+
+static int run_long_multi_group(LongDevice& dev, const DevParams& P,
+                                const std::vector<LongPairIn>& pairs, const LongOptions& opt,
+                                std::vector<LongResult>* out, std::vector<int>* taken,
+                                std::string* err, uint64_t* launches, double* kernel_ms,
+                                const std::function<int()>& during, int* rows_out,
+                                std::vector<LongCkpt>* cks, int64_t ck_budget) {
   const size_t K0 = pairs.size();
   out->assign(K0, LongResult{0, 0, 0, 0.0, true});
   taken->assign(K0, 0);

@@ -20,6 +20,7 @@ struct LongOptions {
   int sleep_ns = 64;       // long16: row hand-off poll back-off
   int narrow = 1;          // 1: 16-bit differential kernel where eligible (local affine)
   long long spin_limit = 1ll << 28;  // poll iterations before a wait gives up (E_TIMEOUT)
+  int multi_group = 2048;  // run_long_multi: pairs per launch
   int stall_task = -1;     // fault injection (tests): the warp that draws this task skips
                            // it, so the tasks that depend on it must time out
 };

@@ -277,3 +277,30 @@ def test_bad_symbol_in_long_pair(ctx, tb):
     sc = ctx.align_batch(sch, q, qo, s, so)
     osc, _, _ = _oracle_scores("local", "affine", 5, q, qo, s, so)
     assert np.array_equal(sc, osc)
+
+
+def test_shared_launch_in_groups(ctx):
+    """More long pairs than one launch takes (option long_multi_group, 2048 by default; 2
+    here): score mode runs several launches and takes every pair; traceback takes the first
+    group through the shared pass and the rest one by one.  Results equal the oracle's."""
+    import paper_2002_04561_b200 as A
+    from oracle import oracle as O
+    q, qo, s, so, nl = _tb_batch(977, with_n=False)
+    osch = O.Scheme("semi", "affine", 2, -1, 5, 1)
+    res, cig = O.batch(osch, q, qo, s, so, traceback=True)
+    ocig = O.batch_cigars(res, cig, qo, so)
+    sch = A.Scheme("semi", "affine", 2, -1, 5, 1)
+    ctx.set_option("long_multi_group", 2)
+    try:
+        sc, ends = ctx.align_batch(sch, q, qo, s, so, ends=True)
+        assert ctx.stat("long_multi_pairs") == nl
+        assert np.array_equal(sc, res["score"].astype(np.int32))
+        assert np.array_equal(ends["q_end"], res["q_end"]) and np.array_equal(ends["s_end"], res["s_end"])
+        aln, words = ctx.traceback(sch, q, qo, s, so)
+        assert ctx.stat("long_multi_pairs") == 2
+        assert np.array_equal(aln["score"], res["score"].astype(np.int32))
+        for f in ("q_begin", "s_begin", "q_end", "s_end"):
+            assert np.array_equal(aln[f], res[f]), f
+        assert A.cigars_of(aln, words) == ocig
+    finally:
+        ctx.set_option("long_multi_group", 2048)
